@@ -1,0 +1,135 @@
+/* mmjoin_b200.h -- C ABI of the B200 join-project engine (libmmjoin_b200.so).
+ *
+ * Every entry point takes plain device pointers, 64-bit sizes and a CUDA
+ * stream handle (cudaStream_t passed as void*), returns 0 on success or a
+ * positive MMJ_ERR_* status, and never allocates or frees caller memory.
+ * Scratch comes from caller workspaces sized by the *_bytes / *_count
+ * queries.  The message of the last failure on the calling thread is
+ * available from mmj_last_error().
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/mmjoin/):
+ *   the only native FFI of the reference is the Cython kernel
+ *     matmul_int64(a, b, out, row_start, row_end, block)   matmul/_kernel_cy.pyx:42-47
+ *   behind multiply_counts(a, b, cores, backend)            matmul/core.py:95-123;
+ *   the remaining entry points replace the numpy operators of the path:
+ *     degree split            joinproject.py:100-116, 178-180
+ *     heavy_matrices          joinproject.py:119-143
+ *     light passes 1..3       joinproject.py:183-203 (+ gather_ranges relation.py:193-204)
+ *     merge / np.unique       joinproject.py:220-225, _merge_counts 146-152
+ *     full_join_dedup         joinproject.py:228-248
+ *     star heavy part         joinproject.py:320-365
+ *     bsi_answer_batch        apps.py:314-351
+ */
+#ifndef MMJOIN_B200_H
+#define MMJOIN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MMJ_OK 0
+#define MMJ_ERR_ARG 1          /* -> ValueError                        */
+#define MMJ_ERR_CUDA 2         /* -> RuntimeError                      */
+#define MMJ_ERR_OVERFLOW 3     /* -> MatrixOverflowError (core.py:33)  */
+#define MMJ_ERR_UNSUPPORTED 4  /* -> NotImplementedError               */
+#define MMJ_ERR_CAPACITY 5     /* -> output buffer too small           */
+
+#define MMJ_MODE_BITMAP 0      /* nonzero test -> 1 bit per (row, col)  */
+#define MMJ_MODE_COUNT32 1     /* exact int32 counts                    */
+#define MMJ_MODE_ACC64 2       /* out += count << shift (int64)         */
+
+int mmj_abi_version(void);
+const char* mmj_last_error(void);
+int mmj_set_device(int device);
+int mmj_sm_count(void);
+
+/* ---- scans ------------------------------------------------------------- */
+size_t mmj_scan_workspace_bytes(int64_t n);
+/* out[i] = sum(in[0..i)), out[n] = total  (int32 in, int64 out) */
+int mmj_exclusive_scan_i32(const int32_t* in, int64_t* out, int64_t n, void* ws, void* stream);
+
+/* ---- degree split: joinproject.py:178-180 ----------------------------------
+ * hpos[y] = rank of y among heavy y (deg_R(y) > delta1 or deg_S(y) > delta1),
+ * -1 for light y.  scan_out[dom_y] receives K = number of heavy y.
+ * flag_ws: dom_y bytes; scan_out: dom_y+1 int32. */
+int mmj_heavy_y_positions(const int32_t* rdeg_y, const int32_t* sdeg_y, int64_t dom_y, int64_t delta1,
+                          uint8_t* flag_ws, int32_t* scan_out, int32_t* hpos, void* ws, void* stream);
+
+/* ---- heavy operand build: joinproject.py:119-143 ---------------------------
+ * mat[(rows[t]-row0)*kpad + hpos[cols[t]]] = 1 for every tuple t whose left id
+ * has degree > delta2 and whose right id is heavy; mat is zeroed first. */
+int mmj_build_operand(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t delta2,
+                      const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows, int64_t kpad, void* stream);
+
+/* ---- light-z CSR of S for pass 3: joinproject.py:195-203 --------------------
+ * lz_ptr[dom_y+1]/lz_idx: S.rev(y) restricted to z with deg_S(z) <= delta2.
+ * flag_ws: n bytes; pos_ws: n+1 int32. */
+int mmj_light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, int64_t dom_y,
+                    const int32_t* left_deg, int64_t delta2, uint8_t* flag_ws, int32_t* pos_ws, int32_t* lz_ptr,
+                    int32_t* lz_idx, void* ws, void* stream);
+
+/* ---- light passes: joinproject.py:183-203 ----------------------------------
+ * Tuples t0 .. t0+ntup-1 of R in forward (x-sorted) order each expand one
+ * list of S partners (S.rev(y) if y light or x light, else the light-z list).
+ * hpos == NULL selects the FULL_JOIN strategy (every y light).
+ * mmj_light_lengths writes len[ntup] and offs[ntup+1] (exclusive scan; offs[ntup]
+ * is the light intermediate size).  mmj_light_expand sets bit (x-x0, z) of a
+ * bitmap (mode 0, ld in words) or adds 1 to count cell (x-x0, z) (mode 1, ld in
+ * int32). */
+int mmj_light_lengths(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup,
+                      const int32_t* rdeg_x, int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr,
+                      const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, int32_t* len,
+                      int64_t* offs, void* ws, void* stream);
+int mmj_light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup,
+                     const int32_t* rdeg_x, int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr,
+                     const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, const int64_t* offs,
+                     int64_t total_hint, int mode, int64_t x0, void* out, int64_t ld, void* stream);
+
+/* ---- heavy contraction on tcgen05: joinproject.py:208-216, core.py:95-123,
+ *      _kernel_cy.pyx:42-47 ------------------------------------------------
+ * A: a_rows x kpad uint8 (K-major), B: b_rows x kpad uint8 (K-major, one row
+ * per output column).  Rows [m_begin, m_begin+m_rows) of A times the K window
+ * [k_off, k_off+k_len) (multiples of 128) -> out rows 0..m_rows-1:
+ *   MMJ_MODE_BITMAP : uint32 words, ld_out words per row (multiple of 8 and
+ *                     >= ceil(b_rows/256)*8); bit j%32 of word j/32 = (C!=0)
+ *   MMJ_MODE_COUNT32: int32, ld_out per row (multiple of 4)
+ *   MMJ_MODE_ACC64  : int64, out[i][j] += C[i][j] << shift
+ * nnz (optional) accumulates the number of nonzero product cells. */
+int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_rows, int64_t kpad, int64_t k_off,
+                  int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out, int64_t ld_out,
+                  unsigned long long* nnz, int max_ctas, void* stream);
+
+/* digit plane of an int64 matrix for exact multiply_counts: dst[r][c] =
+ * (src >> 8*digit) & 255 with src = A (rows x cols) or, if transpose, the
+ * transpose of a (cols x rows) source; dst pitch kpad, zero padded. */
+int mmj_digit_plane(const int64_t* src, int64_t rows, int64_t cols, int transpose, int digit, uint8_t* dst,
+                    int64_t kpad, void* stream);
+
+/* ---- merge / emission: joinproject.py:220-225 -------------------------------
+ * Bitmap chunk of nwords words (wpr words per row, row r <-> x = x0 + r):
+ * segment popcounts + exclusive scan (seg_off[nseg+1], seg_off[nseg] = size),
+ * then sorted distinct codes x*dom_z + z. */
+int64_t mmj_bitmap_segment_count(int64_t nwords);
+int mmj_bitmap_segments(const uint32_t* bm, int64_t nwords, int32_t* segcnt, int64_t* seg_off, void* ws,
+                        void* stream);
+int mmj_bitmap_emit(const uint32_t* bm, int64_t nwords, int64_t wpr, const int64_t* seg_off, int64_t x0,
+                    int64_t dom_z, int64_t* codes, void* stream);
+/* Count chunk (nrows x ld int32, ncols valid columns): cells with count >=
+ * min_count (and col > x0+row if upper_only: the a < b filter of
+ * apps.py:57-62) -> codes + int32 counts. */
+int64_t mmj_count_segment_count(int64_t ncell);
+int mmj_count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
+                       int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws, void* stream);
+int mmj_count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
+                   int32_t min_count, int upper_only, const int64_t* seg_off, int64_t* codes, int32_t* counts,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MMJOIN_B200_H */

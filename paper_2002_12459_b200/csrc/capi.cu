@@ -1,0 +1,160 @@
+// extern "C" boundary of libmmjoin_b200.so (declared in include/mmjoin_b200.h).
+#include "../../include/mmjoin_b200.h"
+#include "mmj_common.cuh"
+
+namespace mmj {
+// twopath.cu
+int heavy_y_positions(const int32_t*, const int32_t*, int64_t, int64_t, uint8_t*, int32_t*, int32_t*, void*,
+                      cudaStream_t);
+int build_operand(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint8_t*, int64_t,
+                  int64_t, int64_t, cudaStream_t);
+int light_z_csr(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, uint8_t*, int32_t*,
+                int32_t*, int32_t*, void*, cudaStream_t);
+int light_lengths(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, const int32_t*,
+                  const int32_t*, const int32_t*, const int32_t*, const int32_t*, int32_t*, int64_t*, void*,
+                  cudaStream_t);
+int light_expand(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, const int32_t*,
+                 const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int64_t*, int64_t, int, int64_t,
+                 void*, int64_t, cudaStream_t);
+int64_t bitmap_nseg(int64_t);
+int64_t count_nseg(int64_t);
+int bitmap_segments(const uint32_t*, int64_t, int32_t*, int64_t*, void*, cudaStream_t);
+int bitmap_emit(const uint32_t*, int64_t, int64_t, const int64_t*, int64_t, int64_t, int64_t*, cudaStream_t);
+int count_segments(const int32_t*, int64_t, int64_t, int64_t, int64_t, int32_t, int, int32_t*, int64_t*, void*,
+                   cudaStream_t);
+int count_emit(const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t, int, const int64_t*, int64_t*,
+               int32_t*, cudaStream_t);
+namespace mma {
+int launch_heavy_mma(const uint8_t*, int64_t, const uint8_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                     int, int, void*, int64_t, unsigned long long*, int, cudaStream_t);
+}
+
+namespace {
+__global__ void k_digit_plane(const int64_t* __restrict__ src, int64_t rows, int64_t cols, int transpose, int digit,
+                              uint8_t* __restrict__ dst, int64_t kpad) {
+  const int64_t total = rows * kpad;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / kpad, c = i - r * kpad;
+    uint8_t v = 0;
+    if (c < cols) {
+      const int64_t x = transpose ? src[c * rows + r] : src[r * cols + c];
+      v = (uint8_t)((x >> (8 * digit)) & 255);
+    }
+    dst[i] = v;
+  }
+}
+}  // namespace
+}  // namespace mmj
+
+#define ST(s) reinterpret_cast<cudaStream_t>(s)
+
+extern "C" {
+
+int mmj_abi_version(void) { return 1; }
+
+const char* mmj_last_error(void) { return mmj::last_error(); }
+
+int mmj_set_device(int device) { return mmj::cuda_status(cudaSetDevice(device), "cudaSetDevice"); }
+
+int mmj_sm_count(void) { return mmj::sm_count(); }
+
+size_t mmj_scan_workspace_bytes(int64_t n) { return mmj::scan_ws_bytes(n); }
+
+int mmj_exclusive_scan_i32(const int32_t* in, int64_t* out, int64_t n, void* ws, void* stream) {
+  return mmj::scan_i32_i64(in, out, n, ws, ST(stream));
+}
+
+int mmj_heavy_y_positions(const int32_t* rdeg_y, const int32_t* sdeg_y, int64_t dom_y, int64_t delta1,
+                          uint8_t* flag_ws, int32_t* scan_out, int32_t* hpos, void* ws, void* stream) {
+  if (delta1 < 1) {
+    mmj::set_error("thresholds must be >= 1");
+    return MMJ_ERR_ARG;
+  }
+  return mmj::heavy_y_positions(rdeg_y, sdeg_y, dom_y, delta1, flag_ws, scan_out, hpos, ws, ST(stream));
+}
+
+int mmj_build_operand(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t delta2,
+                      const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows, int64_t kpad, void* stream) {
+  return mmj::build_operand(rows, cols, n, left_deg, delta2, hpos, mat, row0, nrows, kpad, ST(stream));
+}
+
+int mmj_light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, int64_t dom_y,
+                    const int32_t* left_deg, int64_t delta2, uint8_t* flag_ws, int32_t* pos_ws, int32_t* lz_ptr,
+                    int32_t* lz_idx, void* ws, void* stream) {
+  return mmj::light_z_csr(rev_ptr, rev_idx, n, dom_y, left_deg, delta2, flag_ws, pos_ws, lz_ptr, lz_idx, ws,
+                          ST(stream));
+}
+
+int mmj_light_lengths(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup,
+                      const int32_t* rdeg_x, int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr,
+                      const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, int32_t* len,
+                      int64_t* offs, void* ws, void* stream) {
+  return mmj::light_lengths(fwd_row, fwd_idx, t0, ntup, rdeg_x, delta2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx,
+                            len, offs, ws, ST(stream));
+}
+
+int mmj_light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup,
+                     const int32_t* rdeg_x, int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr,
+                     const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, const int64_t* offs,
+                     int64_t total_hint, int mode, int64_t x0, void* out, int64_t ld, void* stream) {
+  if (mode != 0 && mode != 1) {
+    mmj::set_error("light_expand: mode must be 0 (bitmap) or 1 (counts)");
+    return MMJ_ERR_ARG;
+  }
+  return mmj::light_expand(fwd_row, fwd_idx, t0, ntup, rdeg_x, delta2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx,
+                           offs, total_hint, mode, x0, out, ld, ST(stream));
+}
+
+int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_rows, int64_t kpad, int64_t k_off,
+                  int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out, int64_t ld_out,
+                  unsigned long long* nnz, int max_ctas, void* stream) {
+  if (mode < 0 || mode > 2) {
+    mmj::set_error("heavy_mma: unknown mode %d", mode);
+    return MMJ_ERR_ARG;
+  }
+  return mmj::mma::launch_heavy_mma(a, a_rows, b, b_rows, kpad, k_off, k_len, m_begin, m_rows, mode, shift, out,
+                                    ld_out, nnz, max_ctas, ST(stream));
+}
+
+int mmj_digit_plane(const int64_t* src, int64_t rows, int64_t cols, int transpose, int digit, uint8_t* dst,
+                    int64_t kpad, void* stream) {
+  if (digit < 0 || digit > 7 || kpad < cols) {
+    mmj::set_error("digit_plane: bad digit/pitch");
+    return MMJ_ERR_ARG;
+  }
+  const int64_t total = rows * kpad;
+  if (total == 0) return MMJ_OK;
+  int64_t g = mmj::ceil_div(total, 256);
+  if (g > (int64_t)mmj::sm_count() * 32) g = (int64_t)mmj::sm_count() * 32;
+  mmj::k_digit_plane<<<(unsigned)g, 256, 0, ST(stream)>>>(src, rows, cols, transpose, digit, dst, kpad);
+  MMJ_CHECK_LAUNCH("k_digit_plane");
+  return MMJ_OK;
+}
+
+int64_t mmj_bitmap_segment_count(int64_t nwords) { return mmj::bitmap_nseg(nwords); }
+
+int mmj_bitmap_segments(const uint32_t* bm, int64_t nwords, int32_t* segcnt, int64_t* seg_off, void* ws,
+                        void* stream) {
+  return mmj::bitmap_segments(bm, nwords, segcnt, seg_off, ws, ST(stream));
+}
+
+int mmj_bitmap_emit(const uint32_t* bm, int64_t nwords, int64_t wpr, const int64_t* seg_off, int64_t x0,
+                    int64_t dom_z, int64_t* codes, void* stream) {
+  return mmj::bitmap_emit(bm, nwords, wpr, seg_off, x0, dom_z, codes, ST(stream));
+}
+
+int64_t mmj_count_segment_count(int64_t ncell) { return mmj::count_nseg(ncell); }
+
+int mmj_count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
+                       int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws, void* stream) {
+  return mmj::count_segments(cnt, nrows, ld, ncols, x0, min_count, upper_only, segcnt, seg_off, ws, ST(stream));
+}
+
+int mmj_count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
+                   int32_t min_count, int upper_only, const int64_t* seg_off, int64_t* codes, int32_t* counts,
+                   void* stream) {
+  return mmj::count_emit(cnt, nrows, ld, ncols, x0, dom_z, min_count, upper_only, seg_off, codes, counts,
+                         ST(stream));
+}
+
+}  // extern "C"

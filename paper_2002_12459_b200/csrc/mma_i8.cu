@@ -1,0 +1,450 @@
+// Heavy-part contraction on the 5th-generation tensor cores.
+//
+// Replaces the reference's dense heavy product
+//   joinproject.py:208-216  (multiply_counts(M1, M2) -> nonzero)
+//   matmul/core.py:95-123   (float64 BLAS / int64 Cython kernel, _kernel_cy.pyx:14-47)
+// with a persistent, warp-specialised tcgen05 kernel:
+//   * operands: uint8 matrices A[rows][Kp] and B[cols][Kp], both K-major
+//     (B is "S_h transposed": one row per z), staged by TMA into 128B-swizzled
+//     shared-memory tiles through a 4-deep mbarrier ring;
+//   * math: tcgen05.mma.cta_group::1.kind::i8, M=128 N=256 K=32 per
+//     instruction, unsigned 8-bit inputs, exact s32 accumulators in TMEM
+//     (two 256-column accumulator stages so tile i's epilogue overlaps
+//     tile i+1's MMAs);
+//   * epilogue (4 warps, TMEM -> registers via tcgen05.ld):
+//       BITMAP : nonzero test, 32 cells -> one 32-bit word, 32 B per row/tile
+//                (the projection / intersection output);
+//       COUNT32: exact int32 counts (witness counts / set overlaps);
+//       ACC64  : out[i][j] += count << shift  (int64 digit recombination for
+//                the generic multiply_counts backend).
+//
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w3 idle, w4..w7 epilogue (warp w%4 owns TMEM lanes 32*(w%4) .. +31).
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "mmj_common.cuh"
+
+namespace mmj {
+namespace mma {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 128;                 // bytes (= uint8 elements) of K per stage
+constexpr int UMMA_K = 32;              // K per tcgen05.mma for kind::i8
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK;        // 16 KB
+constexpr int B_BYTES = BN * BK;        // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int ACC_STAGES = 2;
+constexpr int TMEM_COLS = 512;          // 2 x 256 s32 accumulator columns
+constexpr int NUM_THREADS = 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
+
+enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2 };
+
+struct Params {
+  int64_t m_begin;      // first A row of this launch (multiple of BM not required)
+  int64_t m_rows;       // rows of A processed / rows of the output
+  int64_t n_cols;       // columns of the product (= rows of B)
+  int num_kb;           // Kp / BK
+  int mode;
+  int shift;            // ACC64 only
+  void* out;            // BITMAP: uint32 words, COUNT32: int32, ACC64: int64
+  int64_t ld_out;       // row pitch of out in elements (words / int32 / int64)
+  unsigned long long* nnz;   // BITMAP/COUNT32: nonzero cells found (may be null)
+};
+
+// ---------------------------------------------------------------- PTX wraps
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// K-major operand tile, 128-byte rows, 128B swizzle, 8-row core groups 1 KB apart.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);   // start address
+  d |= (uint64_t)1 << 16;                    // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+  return d;
+}
+
+// kind::i8 instruction descriptor: D=s32, A=B=u8, both K-major, M=128, N=256.
+__host__ __device__ constexpr uint32_t idesc_u8_s32(int m, int n) {
+  return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+#define TMEM_LD_32x32b_X32(taddr, r)                                                            \
+  asm volatile(                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"   \
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"         \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),     \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),           \
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),           \
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])            \
+      : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TileCoord {
+  int m_blk, n_blk;
+};
+
+__device__ __forceinline__ TileCoord tile_of(int64_t t, int mt, int nt) {
+  // bands of GROUP_M M-blocks; inside a band walk N, cycling M fastest so the
+  // B tile just loaded is reused by the band from L2.
+  int64_t band_tiles = (int64_t)GROUP_M * nt;
+  int band = (int)(t / band_tiles);
+  int64_t r = t - (int64_t)band * band_tiles;
+  int first_m = band * GROUP_M;
+  int gsz = min(GROUP_M, mt - first_m);
+  TileCoord c;
+  c.m_blk = first_m + (int)(r % gsz);
+  c.n_blk = (int)(r / gsz);
+  return c;
+}
+
+// ----------------------------------------------------------------- the kernel
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    heavy_mma_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                     const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;                                   // STAGES x A_BYTES
+  uint8_t* smem_b = smem + STAGES * A_BYTES;                // STAGES x B_BYTES
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;                                    // [STAGES]
+  uint64_t* empty = bars + STAGES;                          // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;                      // [ACC_STAGES]
+  uint64_t* tempty = bars + 2 * STAGES + ACC_STAGES;        // [ACC_STAGES]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * ACC_STAGES);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int mt = (int)((p.m_rows + BM - 1) / BM);
+  const int nt = (int)((p.n_cols + BN - 1) / BN);
+  const int64_t num_tiles = (int64_t)mt * nt;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < ACC_STAGES; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_base_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        TileCoord c = tile_of(t, mt, nt);
+        const int32_t arow = (int32_t)(p.m_begin + (int64_t)c.m_blk * BM);
+        const int32_t brow = c.n_blk * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(smem_a + s * A_BYTES, &tmap_a, &full[s], kb * BK, arow);
+          tma_load_2d(smem_b + s * B_BYTES, &tmap_b, &full[s], kb * BK, brow);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_u8_s32(BM, BN);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(smem_a + s * A_BYTES);
+          const uint32_t b0 = smem_u32(smem_b + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            tc_mma_i8(d_tmem, smem_desc_sw128(a0 + k * UMMA_K), smem_desc_sw128(b0 + k * UMMA_K), idesc,
+                      (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);          // smem slot free once these MMAs retire
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        tc_commit(&tfull[acc]);          // accumulator ready for the epilogue
+        if (++acc == ACC_STAGES) { acc = 0; acc_ph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------- epilogue
+    const int q = warp & 3;              // TMEM lane quadrant
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    unsigned long long my_nnz = 0;
+    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      TileCoord c = tile_of(t, mt, nt);
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      const int64_t row = (int64_t)c.m_blk * BM + q * 32 + lane;   // local output row
+      const bool row_ok = row < p.m_rows;
+      const int64_t col0 = (int64_t)c.n_blk * BN;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (p.mode == BITMAP) {
+        uint32_t w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t r[32];
+          TMEM_LD_32x32b_X32(taddr + j * 32, r);
+          tmem_wait_ld();
+          uint32_t bits = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) bits |= (r[i] != 0u ? 1u : 0u) << i;
+          w[j] = bits;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (row_ok) {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + (col0 >> 5);
+          reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) my_nnz += __popc(w[j]);
+        }
+      } else if (p.mode == COUNT32) {
+        int32_t* dst = reinterpret_cast<int32_t*>(p.out) + row * p.ld_out + col0;
+#pragma unroll 1
+        for (int j = 0; j < 8; ++j) {
+          uint32_t r[32];
+          TMEM_LD_32x32b_X32(taddr + j * 32, r);
+          tmem_wait_ld();
+          if (row_ok) {
+            if (col0 + j * 32 + 32 <= p.ld_out) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                *reinterpret_cast<int4*>(dst + j * 32 + i) =
+                    make_int4((int)r[i], (int)r[i + 1], (int)r[i + 2], (int)r[i + 3]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (col0 + j * 32 + i < p.ld_out) dst[j * 32 + i] = (int)r[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) my_nnz += (r[i] != 0u && col0 + j * 32 + i < p.n_cols);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      } else {  // ACC64
+        int64_t* dst = reinterpret_cast<int64_t*>(p.out) + row * p.ld_out + col0;
+#pragma unroll 1
+        for (int j = 0; j < 8; ++j) {
+          uint32_t r[32];
+          TMEM_LD_32x32b_X32(taddr + j * 32, r);
+          tmem_wait_ld();
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int64_t col = col0 + j * 32 + i;
+              if (col < p.n_cols && r[i] != 0u) dst[j * 32 + i] += ((int64_t)r[i]) << p.shift;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+      if (++acc == ACC_STAGES) { acc = 0; acc_ph ^= 1; }
+    }
+    if (p.nnz != nullptr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) my_nnz += __shfl_xor_sync(0xffffffffu, my_nnz, o);
+      if (lane == 0 && my_nnz) atomicAdd(p.nnz, my_nnz);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ----------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t klen, int64_t pitch, int box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return MMJ_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)klen, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld k=%lld pitch=%lld", (int)r, (long long)rows,
+              (long long)klen, (long long)pitch);
+    return MMJ_ERR_CUDA;
+  }
+  return MMJ_OK;
+}
+
+int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_rows, int64_t kpad,
+                     int64_t k_off, int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out,
+                     int64_t ld_out, unsigned long long* nnz, int max_ctas, cudaStream_t st) {
+  if (kpad <= 0 || kpad % BK != 0 || k_off < 0 || k_len <= 0 || k_off % BK != 0 || k_len % BK != 0 ||
+      k_off + k_len > kpad) {
+    set_error("heavy_mma: K window [%lld,+%lld) of pitch %lld must be multiples of %d", (long long)k_off,
+              (long long)k_len, (long long)kpad, BK);
+    return MMJ_ERR_ARG;
+  }
+  if (m_begin < 0 || m_rows < 0 || m_begin + m_rows > a_rows) {
+    set_error("heavy_mma: row range [%lld,+%lld) outside A (%lld rows)", (long long)m_begin,
+              (long long)m_rows, (long long)a_rows);
+    return MMJ_ERR_ARG;
+  }
+  if (a_rows >= (1ll << 31) || b_rows >= (1ll << 31)) {
+    set_error("heavy_mma: operand rows must be < 2^31");
+    return MMJ_ERR_ARG;
+  }
+  if (mode == BITMAP && (ld_out % 8 != 0 || ld_out * 32 < round_up(b_rows, BN))) {
+    set_error("heavy_mma: bitmap pitch %lld words too small / unaligned", (long long)ld_out);
+    return MMJ_ERR_ARG;
+  }
+  if (mode == COUNT32 && ld_out % 4 != 0) {
+    set_error("heavy_mma: count pitch must be a multiple of 4");
+    return MMJ_ERR_ARG;
+  }
+  if (m_rows == 0 || b_rows == 0) return MMJ_OK;
+  CUtensorMap ma, mb;
+  MMJ_TRY(make_map(&ma, a + k_off, a_rows, k_len, kpad, BM));
+  MMJ_TRY(make_map(&mb, b + k_off, b_rows, k_len, kpad, BN));
+  Params p;
+  p.m_begin = m_begin;
+  p.m_rows = m_rows;
+  p.n_cols = b_rows;
+  p.num_kb = (int)(k_len / BK);
+  p.mode = mode;
+  p.shift = shift;
+  p.out = out;
+  p.ld_out = ld_out;
+  p.nnz = nnz;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MMJ_TRY(cuda_status(cudaFuncSetAttribute(heavy_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             SMEM_BYTES),
+                        "cudaFuncSetAttribute(heavy_mma)"));
+    attr_set = true;
+  }
+  const int64_t tiles = ceil_div(m_rows, BM) * ceil_div(b_rows, BN);
+  int grid = sm_count();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  if (tiles < grid) grid = (int)tiles;
+  heavy_mma_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  MMJ_CHECK_LAUNCH("heavy_mma_kernel");
+  return MMJ_OK;
+}
+
+}  // namespace mma
+}  // namespace mmj

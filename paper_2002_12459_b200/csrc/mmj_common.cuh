@@ -1,0 +1,60 @@
+// Shared helpers for the mmjoin B200 kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#define MMJ_OK 0
+#define MMJ_ERR_ARG 1
+#define MMJ_ERR_CUDA 2
+#define MMJ_ERR_OVERFLOW 3
+#define MMJ_ERR_UNSUPPORTED 4
+#define MMJ_ERR_CAPACITY 5
+
+namespace mmj {
+
+// thread-local last error message (exposed through mmj_last_error()).
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+inline int cuda_status(cudaError_t e, const char* where) {
+  if (e != cudaSuccess) {
+    set_error("%s: %s", where, cudaGetErrorString(e));
+    return MMJ_ERR_CUDA;
+  }
+  return MMJ_OK;
+}
+
+#define MMJ_CHECK_LAUNCH(where)                                   \
+  do {                                                            \
+    int _st = ::mmj::cuda_status(cudaGetLastError(), where);      \
+    if (_st) return _st;                                          \
+  } while (0)
+
+#define MMJ_TRY(expr)            \
+  do {                           \
+    int _st = (expr);            \
+    if (_st) return _st;         \
+  } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+int sm_count();
+
+// ---- exclusive scans (scan.cu) --------------------------------------------
+// out[i] = sum(in[0..i)), out[n] = total.  `ws` must hold scan_ws_bytes(n).
+size_t scan_ws_bytes(int64_t n);
+int scan_i32_i64(const int32_t* in, int64_t* out, int64_t n, void* ws, cudaStream_t st);
+int scan_u8_i32(const uint8_t* in, int32_t* out, int64_t n, void* ws, cudaStream_t st);
+int scan_i64_i64(const int64_t* in, int64_t* out, int64_t n, void* ws, cudaStream_t st);
+
+}  // namespace mmj
+
+// ---- device helpers ----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }

@@ -1,0 +1,429 @@
+// Degree split, heavy-operand build, light expansion and the merge/emission
+// kernels of the two-path join-project path.
+//
+// Reference (paths relative to /root/reference/pkg/src/mmjoin/):
+//   degree split            joinproject.py:178-180, 100-116
+//   heavy 0/1 matrices      joinproject.py:119-143
+//   light passes 1-3        joinproject.py:183-203 (gather_ranges relation.py:193-204)
+//   merge / dedup           joinproject.py:220-225, _merge_counts 146-152
+//   full join               joinproject.py:228-248
+//
+// Layout in HBM (all dense ids int32):
+//   relation CSR            fwd_ptr[dom_l+1], fwd_idx[n] (right id per tuple),
+//                           fwd_row[n] (left id per tuple), rev_ptr[dom_r+1], rev_idx[n]
+//   heavy position of y     hpos[dom_y] = rank among heavy y, -1 if light
+//   operands                A[x][Kp], B[z][Kp] uint8 0/1, K-major (row = dense id)
+//   light-z CSR of S        lz_ptr[dom_y+1], lz_idx[.]: S.rev(y) restricted to light z
+//   output chunk            bitmap rows x words (1 bit per (x, z)), or int32 counts
+//   codes                   int64 x*dom_z + z, strictly increasing (bitmap order)
+#include "mmj_common.cuh"
+
+namespace mmj {
+
+namespace {
+
+constexpr int TPB = 256;
+
+inline int grid_for(int64_t work, int per_block, int cap_waves = 32) {
+  int64_t g = ceil_div(work, per_block);
+  int64_t cap = (int64_t)sm_count() * cap_waves;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ------------------------------------------------------------------ split
+__global__ void k_heavy_y_flags(const int32_t* __restrict__ rdeg, const int32_t* __restrict__ sdeg,
+                                int64_t dom_y, int64_t d1, uint8_t* __restrict__ flag) {
+  for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < dom_y;
+       y += (int64_t)gridDim.x * blockDim.x) {
+    // joinproject.py:178: light iff deg_R(y) <= d1 and deg_S(y) <= d1
+    flag[y] = (rdeg[y] > d1 || sdeg[y] > d1) ? 1 : 0;
+  }
+}
+
+__global__ void k_heavy_y_pos(const uint8_t* __restrict__ flag, const int32_t* __restrict__ scanned,
+                              int64_t dom_y, int32_t* __restrict__ hpos) {
+  for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < dom_y;
+       y += (int64_t)gridDim.x * blockDim.x)
+    hpos[y] = flag[y] ? scanned[y] : -1;
+}
+
+// --------------------------------------------------------- operand build
+// mat[(row - row0) * kpad + hpos[col]] = 1 for every tuple whose left id is
+// heavy (deg > d2) -- joinproject.py:135-141 / 337-344.
+__global__ void k_build_operand(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                int64_t n, const int32_t* __restrict__ left_deg, int64_t d2,
+                                const int32_t* __restrict__ hpos, uint8_t* __restrict__ mat,
+                                int64_t row0, int64_t nrows, int64_t kpad) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rows[t] - row0;
+    if (r < 0 || r >= nrows) continue;
+    if (left_deg[rows[t]] <= d2) continue;
+    const int32_t k = hpos[cols[t]];
+    if (k >= 0) mat[r * kpad + k] = 1;
+  }
+}
+
+// ----------------------------------------------------------- light-z CSR
+__global__ void k_lz_flags(const int32_t* __restrict__ rev_idx, int64_t n,
+                           const int32_t* __restrict__ left_deg, int64_t d2, uint8_t* __restrict__ flag) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    flag[j] = left_deg[rev_idx[j]] <= d2 ? 1 : 0;
+}
+
+__global__ void k_lz_scatter(const int32_t* __restrict__ rev_idx, const uint8_t* __restrict__ flag,
+                             const int32_t* __restrict__ pos, int64_t n, int32_t* __restrict__ lz_idx) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    if (flag[j]) lz_idx[pos[j]] = rev_idx[j];
+}
+
+__global__ void k_lz_ptr(const int32_t* __restrict__ rev_ptr, const int32_t* __restrict__ pos, int64_t dom_y,
+                         int32_t* __restrict__ lz_ptr) {
+  for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y <= dom_y;
+       y += (int64_t)gridDim.x * blockDim.x)
+    lz_ptr[y] = pos[rev_ptr[y]];
+}
+
+// -------------------------------------------------------- light passes
+// x-driven restatement of the three witness-disjoint passes: every R tuple
+// (x, y) of the chunk expands one list of S-side partners
+//   y light                -> S.rev(y)                 (pass 1, joinproject.py:183-186)
+//   y heavy, x light       -> S.rev(y)                 (pass 2, 188-193)
+//   y heavy, x heavy       -> S.rev(y) ∩ light z       (pass 3, 195-203)
+// hpos == nullptr means "no heavy y" (FULL_JOIN plan, joinproject.py:228-248).
+struct LightArgs {
+  const int32_t* fwd_row;
+  const int32_t* fwd_idx;
+  int64_t t0;
+  const int32_t* rdeg_x;
+  int64_t d2;
+  const int32_t* hpos;
+  const int32_t* s_rev_ptr;
+  const int32_t* s_rev_idx;
+  const int32_t* lz_ptr;
+  const int32_t* lz_idx;
+};
+
+__device__ __forceinline__ void list_of(const LightArgs& a, int64_t t, int32_t& x, const int32_t*& base,
+                                        int32_t& len) {
+  x = a.fwd_row[t];
+  const int32_t y = a.fwd_idx[t];
+  const bool full_list = (a.hpos == nullptr) || (a.hpos[y] < 0) || (a.rdeg_x[x] <= a.d2);
+  if (full_list) {
+    const int32_t b = a.s_rev_ptr[y];
+    base = a.s_rev_idx + b;
+    len = a.s_rev_ptr[y + 1] - b;
+  } else {
+    const int32_t b = a.lz_ptr[y];
+    base = a.lz_idx + b;
+    len = a.lz_ptr[y + 1] - b;
+  }
+}
+
+__global__ void k_light_len(LightArgs a, int64_t ntup, int32_t* __restrict__ len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntup;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t x, l;
+    const int32_t* b;
+    list_of(a, a.t0 + i, x, b, l);
+    len[i] = l;
+  }
+}
+
+constexpr int EXP_THREADS = 256;
+constexpr int EXP_ITEMS = 8;
+constexpr int EXP_SPAN = EXP_THREADS * EXP_ITEMS;
+
+__device__ __forceinline__ int64_t upper_bound_i64(const int64_t* __restrict__ v, int64_t lo, int64_t hi,
+                                                   int64_t key) {
+  // first index in [lo, hi) with v[idx] > key
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (v[mid] <= key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// mode 0: bitmap atomicOr; mode 1: int32 counts atomicAdd
+template <int MODE>
+__global__ void __launch_bounds__(EXP_THREADS) k_light_expand(LightArgs a, const int64_t* __restrict__ offs,
+                                                              int64_t ntup, int64_t x0, void* __restrict__ out,
+                                                              int64_t ld) {
+  __shared__ int64_t s_lo, s_hi;
+  const int64_t total = offs[ntup];
+  for (int64_t span0 = (int64_t)blockIdx.x * EXP_SPAN; span0 < total; span0 += (int64_t)gridDim.x * EXP_SPAN) {
+    const int64_t span1 = min(span0 + (int64_t)EXP_SPAN, total);
+    if (threadIdx.x == 0) {
+      s_lo = upper_bound_i64(offs, 0, ntup + 1, span0) - 1;
+      s_hi = upper_bound_i64(offs, 0, ntup + 1, span1 - 1);
+    }
+    __syncthreads();
+    const int64_t lo = s_lo, hi = s_hi;
+#pragma unroll 2
+    for (int it = 0; it < EXP_ITEMS; ++it) {
+      const int64_t s = span0 + (int64_t)it * EXP_THREADS + threadIdx.x;
+      if (s >= span1) break;
+      const int64_t i = upper_bound_i64(offs, lo, hi, s) - 1;
+      int32_t x, l;
+      const int32_t* base;
+      list_of(a, a.t0 + i, x, base, l);
+      const int32_t z = base[s - offs[i]];
+      const int64_t row = (int64_t)x - x0;
+      if (MODE == 0) {
+        atomicOr(reinterpret_cast<uint32_t*>(out) + row * ld + (z >> 5), 1u << (z & 31));
+      } else {
+        atomicAdd(reinterpret_cast<int32_t*>(out) + row * ld + z, 1);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- emission
+// A segment is 32 consecutive bitmap words (1024 (x, z) cells); codes come
+// out in bitmap order = ascending code order, so the merge needs no sort.
+constexpr int SEG_WORDS = 32;
+
+__global__ void k_seg_popc(const uint32_t* __restrict__ bm, int64_t nwords, int32_t* __restrict__ segcnt,
+                           int64_t nseg) {
+  for (int64_t sgi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sgi < nseg;
+       sgi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w0 = sgi * SEG_WORDS;
+    int c = 0;
+    if (w0 + SEG_WORDS <= nwords) {
+      const uint4* p = reinterpret_cast<const uint4*>(bm + w0);
+#pragma unroll
+      for (int i = 0; i < SEG_WORDS / 4; ++i) {
+        uint4 v = p[i];
+        c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+      }
+    } else {
+      for (int64_t w = w0; w < nwords; ++w) c += __popc(bm[w]);
+    }
+    segcnt[sgi] = c;
+  }
+}
+
+constexpr int EMIT_WARPS = 4;   // 4 x 8 KB staging (static smem limit 48 KB)
+
+__global__ void __launch_bounds__(EMIT_WARPS * 32) k_bitmap_emit(const uint32_t* __restrict__ bm, int64_t nwords,
+                                                                 int64_t wpr, const int64_t* __restrict__ seg_off,
+                                                                 int64_t nseg, int64_t x0, int64_t dom_z,
+                                                                 int64_t* __restrict__ codes) {
+  __shared__ int64_t stage[EMIT_WARPS][SEG_WORDS * 32];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  int64_t* st = stage[wib];
+  for (int64_t sgi = (int64_t)blockIdx.x * EMIT_WARPS + wib; sgi < nseg; sgi += (int64_t)gridDim.x * EMIT_WARPS) {
+    const int64_t w = sgi * SEG_WORDS + lane;
+    uint32_t word = w < nwords ? bm[w] : 0u;
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int k = incl - c;
+    const int64_t row = w / wpr;
+    const int64_t code0 = (x0 + row) * dom_z + (w - row * wpr) * 32;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      st[k++] = code0 + b;
+      word &= word - 1;
+    }
+    __syncwarp();
+    const int64_t base = seg_off[sgi];
+    for (int i = lane; i < total; i += 32) codes[base + i] = st[i];
+    __syncwarp();
+  }
+}
+
+// count matrix (rows x ld int32, ncols valid): keep cells with
+// value >= min_count and (if upper_only) z > x.
+__device__ __forceinline__ bool keep_cell(int32_t v, int64_t col, int64_t x, int64_t ncols, int32_t min_count,
+                                          int upper_only) {
+  return col < ncols && v >= min_count && (!upper_only || col > x);
+}
+
+constexpr int CSEG = 1024;   // cells per count segment (32 per lane)
+
+__global__ void k_count_seg_nnz(const int32_t* __restrict__ cnt, int64_t ncell, int64_t ld, int64_t ncols,
+                                int64_t x0, int32_t min_count, int upper_only, int32_t* __restrict__ segcnt,
+                                int64_t nseg) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
+       sgi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t c0 = sgi * CSEG + (int64_t)lane * 32;
+    int n = 0;
+    for (int i = 0; i < 32; ++i) {
+      const int64_t cell = c0 + i;
+      if (cell >= ncell) break;
+      const int64_t row = cell / ld, col = cell - row * ld;
+      n += keep_cell(cnt[cell], col, x0 + row, ncols, min_count, upper_only);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) segcnt[sgi] = n;
+  }
+}
+
+__global__ void __launch_bounds__(EMIT_WARPS * 32) k_count_emit(const int32_t* __restrict__ cnt, int64_t ncell,
+                                                                int64_t ld, int64_t ncols, int64_t x0,
+                                                                int64_t dom_z, int32_t min_count, int upper_only,
+                                                                const int64_t* __restrict__ seg_off, int64_t nseg,
+                                                                int64_t* __restrict__ codes,
+                                                                int32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  for (int64_t sgi = (int64_t)blockIdx.x * EMIT_WARPS + wib; sgi < nseg; sgi += (int64_t)gridDim.x * EMIT_WARPS) {
+    const int64_t c0 = sgi * CSEG + (int64_t)lane * 32;
+    uint32_t mask = 0;
+    for (int i = 0; i < 32; ++i) {
+      const int64_t cell = c0 + i;
+      if (cell >= ncell) break;
+      const int64_t row = cell / ld, col = cell - row * ld;
+      if (keep_cell(cnt[cell], col, x0 + row, ncols, min_count, upper_only)) mask |= 1u << i;
+    }
+    const int c = __popc(mask);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int64_t k = seg_off[sgi] + incl - c;
+    while (mask) {
+      const int b = __ffs(mask) - 1;
+      const int64_t cell = c0 + b;
+      const int64_t row = cell / ld, col = cell - row * ld;
+      codes[k] = (x0 + row) * dom_z + col;
+      counts[k] = cnt[cell];
+      ++k;
+      mask &= mask - 1;
+    }
+  }
+}
+
+}  // namespace
+
+// ============================================================== host API
+int heavy_y_positions(const int32_t* rdeg_y, const int32_t* sdeg_y, int64_t dom_y, int64_t d1, uint8_t* flag_ws,
+                      int32_t* scan_ws_out /*dom_y+1*/, int32_t* hpos, void* ws, cudaStream_t st) {
+  if (dom_y == 0) return cuda_status(cudaMemsetAsync(scan_ws_out, 0, 4, st), "memset");
+  k_heavy_y_flags<<<grid_for(dom_y, TPB), TPB, 0, st>>>(rdeg_y, sdeg_y, dom_y, d1, flag_ws);
+  MMJ_CHECK_LAUNCH("k_heavy_y_flags");
+  MMJ_TRY(scan_u8_i32(flag_ws, scan_ws_out, dom_y, ws, st));
+  k_heavy_y_pos<<<grid_for(dom_y, TPB), TPB, 0, st>>>(flag_ws, scan_ws_out, dom_y, hpos);
+  MMJ_CHECK_LAUNCH("k_heavy_y_pos");
+  return MMJ_OK;
+}
+
+int build_operand(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t d2,
+                  const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows, int64_t kpad, cudaStream_t st) {
+  MMJ_TRY(cuda_status(cudaMemsetAsync(mat, 0, (size_t)(nrows * kpad), st), "memset operand"));
+  if (n == 0) return MMJ_OK;
+  k_build_operand<<<grid_for(n, TPB), TPB, 0, st>>>(rows, cols, n, left_deg, d2, hpos, mat, row0, nrows, kpad);
+  MMJ_CHECK_LAUNCH("k_build_operand");
+  return MMJ_OK;
+}
+
+int light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, int64_t dom_y, const int32_t* left_deg,
+                int64_t d2, uint8_t* flag_ws, int32_t* pos_ws /*n+1*/, int32_t* lz_ptr, int32_t* lz_idx, void* ws,
+                cudaStream_t st) {
+  if (n > 0) {
+    k_lz_flags<<<grid_for(n, TPB), TPB, 0, st>>>(rev_idx, n, left_deg, d2, flag_ws);
+    MMJ_CHECK_LAUNCH("k_lz_flags");
+  }
+  MMJ_TRY(scan_u8_i32(flag_ws, pos_ws, n, ws, st));
+  if (n > 0) {
+    k_lz_scatter<<<grid_for(n, TPB), TPB, 0, st>>>(rev_idx, flag_ws, pos_ws, n, lz_idx);
+    MMJ_CHECK_LAUNCH("k_lz_scatter");
+  }
+  k_lz_ptr<<<grid_for(dom_y + 1, TPB), TPB, 0, st>>>(rev_ptr, pos_ws, dom_y, lz_ptr);
+  MMJ_CHECK_LAUNCH("k_lz_ptr");
+  return MMJ_OK;
+}
+
+int light_lengths(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup, const int32_t* rdeg_x,
+                  int64_t d2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx,
+                  const int32_t* lz_ptr, const int32_t* lz_idx, int32_t* len, int64_t* offs, void* ws,
+                  cudaStream_t st) {
+  LightArgs a{fwd_row, fwd_idx, t0, rdeg_x, d2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx};
+  if (ntup > 0) {
+    k_light_len<<<grid_for(ntup, TPB), TPB, 0, st>>>(a, ntup, len);
+    MMJ_CHECK_LAUNCH("k_light_len");
+  }
+  return scan_i32_i64(len, offs, ntup, ws, st);
+}
+
+int light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup, const int32_t* rdeg_x,
+                 int64_t d2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx,
+                 const int32_t* lz_ptr, const int32_t* lz_idx, const int64_t* offs, int64_t total_hint, int mode,
+                 int64_t x0, void* out, int64_t ld, cudaStream_t st) {
+  if (ntup == 0 || total_hint == 0) return MMJ_OK;
+  LightArgs a{fwd_row, fwd_idx, t0, rdeg_x, d2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx};
+  const int64_t work = total_hint > 0 ? total_hint : ntup;
+  const int grid = grid_for(work, EXP_SPAN, 8);
+  if (mode == 0)
+    k_light_expand<0><<<grid, EXP_THREADS, 0, st>>>(a, offs, ntup, x0, out, ld);
+  else
+    k_light_expand<1><<<grid, EXP_THREADS, 0, st>>>(a, offs, ntup, x0, out, ld);
+  MMJ_CHECK_LAUNCH("k_light_expand");
+  return MMJ_OK;
+}
+
+int64_t bitmap_nseg(int64_t nwords) { return ceil_div(nwords, SEG_WORDS); }
+int64_t count_nseg(int64_t ncell) { return ceil_div(ncell, CSEG); }
+
+int bitmap_segments(const uint32_t* bm, int64_t nwords, int32_t* segcnt, int64_t* seg_off, void* ws,
+                    cudaStream_t st) {
+  const int64_t nseg = bitmap_nseg(nwords);
+  if (nseg > 0) {
+    k_seg_popc<<<grid_for(nseg, TPB), TPB, 0, st>>>(bm, nwords, segcnt, nseg);
+    MMJ_CHECK_LAUNCH("k_seg_popc");
+  }
+  return scan_i32_i64(segcnt, seg_off, nseg, ws, st);
+}
+
+int bitmap_emit(const uint32_t* bm, int64_t nwords, int64_t wpr, const int64_t* seg_off, int64_t x0, int64_t dom_z,
+                int64_t* codes, cudaStream_t st) {
+  const int64_t nseg = bitmap_nseg(nwords);
+  if (nseg == 0) return MMJ_OK;
+  k_bitmap_emit<<<grid_for(nseg, EMIT_WARPS, 16), EMIT_WARPS * 32, 0, st>>>(bm, nwords, wpr, seg_off, nseg, x0,
+                                                                            dom_z, codes);
+  MMJ_CHECK_LAUNCH("k_bitmap_emit");
+  return MMJ_OK;
+}
+
+int count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
+                   int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws, cudaStream_t st) {
+  const int64_t ncell = nrows * ld;
+  const int64_t nseg = count_nseg(ncell);
+  if (nseg > 0) {
+    k_count_seg_nnz<<<grid_for(nseg * 32, TPB), TPB, 0, st>>>(cnt, ncell, ld, ncols, x0, min_count, upper_only,
+                                                              segcnt, nseg);
+    MMJ_CHECK_LAUNCH("k_count_seg_nnz");
+  }
+  return scan_i32_i64(segcnt, seg_off, nseg, ws, st);
+}
+
+int count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
+               int32_t min_count, int upper_only, const int64_t* seg_off, int64_t* codes, int32_t* counts,
+               cudaStream_t st) {
+  const int64_t ncell = nrows * ld;
+  const int64_t nseg = count_nseg(ncell);
+  if (nseg == 0) return MMJ_OK;
+  k_count_emit<<<grid_for(nseg, EMIT_WARPS, 16), EMIT_WARPS * 32, 0, st>>>(cnt, ncell, ld, ncols, x0, dom_z, min_count,
+                                                                           upper_only, seg_off, nseg, codes, counts);
+  MMJ_CHECK_LAUNCH("k_count_emit");
+  return MMJ_OK;
+}
+
+}  // namespace mmj

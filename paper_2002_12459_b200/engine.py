@@ -1,0 +1,236 @@
+"""Device pipeline of the two-path join-project operator.
+
+One call = degree split -> heavy operand build -> per x-chunk
+{tcgen05 heavy product -> light expansion -> segment scan -> emission}.
+Reference: joinproject.py:155-225 (two_path_join) and 228-248
+(full_join_dedup); every step is a kernel of libmmjoin_b200.so.
+
+Per x-chunk [x0, x1) the output lives in HBM as
+  * a bitmap (rows x wpr uint32 words, wpr = ceil(dom_z/256)*8): bit (x, z)
+    set iff the pair is in the projection; the heavy product writes every
+    word of the chunk (light x / light z rows and columns of the operands are
+    zero), the light witnesses are OR-ed in afterwards, or
+  * an int32 count matrix (rows x ldc, ldc = ceil(dom_z/256)*256) when exact
+    witness counts are requested (heavy counts stored, light counts added).
+Both are compacted into strictly increasing int64 codes x*dom_z + z, which is
+the reference's OutputSet.codes order (np.unique sorts), so no sort runs.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _native as nat
+from .device import DeviceRelation, Workspace
+from .optimizer import FULL_JOIN, PARTITIONED
+
+BM = 128          # MMA tile rows
+BN = 256          # MMA tile columns
+BK = 128          # K block (bytes)
+
+DEFAULT_BITMAP_CHUNK_BYTES = 1 << 30
+DEFAULT_COUNT_CHUNK_BYTES = 4 << 30
+
+
+def _rup(a: int, b: int) -> int:
+    return -(-a // b) * b
+
+
+@dataclass
+class ChunkResult:
+    x0: int
+    x1: int
+    n: int
+    codes: object            # torch int64 view (device)
+    counts: Optional[object]  # torch int32 view (device) or None
+    light: int
+
+
+@dataclass
+class EngineStats:
+    light_intermediate: int = 0
+    heavy_pairs: int = 0
+    k_heavy: int = 0
+    kpad: int = 0
+    chunks: int = 0
+    out_size: int = 0
+    launches: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+class TwoPathEngine:
+    """Device state for one (R, S, plan) two-path evaluation."""
+
+    def __init__(self, dr: DeviceRelation, ds: DeviceRelation, strategy: str, delta1: int, delta2: int,
+                 want_counts: bool, *, min_count: int = 1, upper_only: bool = False,
+                 chunk_rows: Optional[int] = None, ws: Optional[Workspace] = None,
+                 host_left_deg_r=None, host_left_deg_s=None):
+        import torch
+        self.torch = torch
+        self.lib = nat.load()
+        self.dr, self.ds = dr, ds
+        if dr.dom_right != ds.dom_right:
+            raise ValueError("relations must share the right (y) dictionary")
+        self.strategy = strategy
+        self.d1, self.d2 = int(delta1), int(delta2)
+        self.counts = bool(want_counts)
+        self.min_count = int(min_count)
+        self.upper_only = bool(upper_only)
+        self.dom_x, self.dom_z, self.dom_y = dr.dom_left, ds.dom_left, dr.dom_right
+        self.wpr = _rup(max(self.dom_z, 1), BN) // 32
+        self.ldc = _rup(max(self.dom_z, 1), BN)
+        self.ws = ws or Workspace()
+        self.stats = EngineStats()
+        self.hpos = None
+        self.A = None
+        self.B = None
+        self.kpad = 0
+        self.lz_ptr = None
+        self.lz_idx = None
+        self._host_ldeg_r = host_left_deg_r
+        self._host_ldeg_s = host_left_deg_s
+        row_bytes = (self.ldc * 4) if self.counts else (self.wpr * 4)
+        if chunk_rows is None:
+            budget = DEFAULT_COUNT_CHUNK_BYTES if self.counts else DEFAULT_BITMAP_CHUNK_BYTES
+            chunk_rows = max(BM, (budget // max(row_bytes, 1)) // BM * BM)
+        self.chunk_rows = max(BM, _rup(int(chunk_rows), BM))
+        self.nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self._prepared = False
+
+    # ------------------------------------------------------------ prepare
+    def _st(self):
+        return nat.stream_handle()
+
+    def prepare(self):
+        if self._prepared:
+            return
+        torch = self.torch
+        st = self._st()
+        dr, ds = self.dr, self.ds
+        self.nnz.zero_()
+        if self.strategy == PARTITIONED:
+            dom_y = self.dom_y
+            flag = self.ws.get("yflag", dom_y, torch.uint8)
+            scan = self.ws.get("yscan", dom_y + 1, torch.int32)
+            self.hpos = torch.empty(max(dom_y, 1), dtype=torch.int32, device="cuda")
+            nat.call("mmj_heavy_y_positions", nat.ptr(dr.right_deg), nat.ptr(ds.right_deg), dom_y, self.d1,
+                     nat.ptr(flag), nat.ptr(scan), nat.ptr(self.hpos), nat.ptr(self.ws.scan_ws(dom_y)), st)
+            k = int(scan[dom_y].item())
+            self.stats.k_heavy = k
+            heavy_x = self._any_heavy(self._host_ldeg_r, dr)
+            heavy_z = self._any_heavy(self._host_ldeg_s, ds)
+            if k > 0 and heavy_x and heavy_z:
+                kpad = _rup(k, BK)
+                self.kpad = kpad
+                arows = _rup(max(self.dom_x, 1), BN)
+                brows = _rup(max(self.dom_z, 1), BN)
+                self.A = torch.empty((arows, kpad), dtype=torch.uint8, device="cuda")
+                self.B = torch.empty((brows, kpad), dtype=torch.uint8, device="cuda")
+                nat.call("mmj_build_operand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n, nat.ptr(dr.left_deg),
+                         self.d2, nat.ptr(self.hpos), nat.ptr(self.A), 0, arows, kpad, st)
+                nat.call("mmj_build_operand", nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n, nat.ptr(ds.left_deg),
+                         self.d2, nat.ptr(self.hpos), nat.ptr(self.B), 0, brows, kpad, st)
+            self.stats.kpad = self.kpad
+            # light-z lists of S for pass 3
+            n = ds.n
+            lflag = self.ws.get("lzflag", n, torch.uint8)
+            lpos = self.ws.get("lzpos", n + 1, torch.int32)
+            self.lz_ptr = torch.empty(dom_y + 1, dtype=torch.int32, device="cuda")
+            self.lz_idx = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+            nat.call("mmj_light_z_csr", nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), n, dom_y, nat.ptr(ds.left_deg),
+                     self.d2, nat.ptr(lflag), nat.ptr(lpos), nat.ptr(self.lz_ptr), nat.ptr(self.lz_idx),
+                     nat.ptr(self.ws.scan_ws(n)), st)
+        self._prepared = True
+
+    def _any_heavy(self, host_deg, d: DeviceRelation) -> bool:
+        if host_deg is not None:
+            return bool((np.asarray(host_deg) > self.d2).any())
+        return bool((d.left_deg > self.d2).any().item())
+
+    # ------------------------------------------------------------ chunks
+    def chunk_bounds(self, x_begin: int = 0, x_end: Optional[int] = None):
+        x_end = self.dom_x if x_end is None else x_end
+        x = x_begin
+        while x < x_end:
+            nx = min(x_end, x + self.chunk_rows)
+            yield x, nx
+            x = nx
+
+    def run_chunk(self, x0: int, x1: int) -> ChunkResult:
+        torch = self.torch
+        st = self._st()
+        dr, ds = self.dr, self.ds
+        rows = x1 - x0
+        if self.counts:
+            buf = self.ws.get("cnt", rows * self.ldc, torch.int32)
+            ld = self.ldc
+            mode = nat.MODE_COUNT32
+        else:
+            buf = self.ws.get("bm", rows * self.wpr, torch.int32)
+            ld = self.wpr
+            mode = nat.MODE_BITMAP
+        # heavy part (writes every cell of the chunk) or zero fill
+        if self.A is not None:
+            nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
+                     self.kpad, 0, self.kpad, x0, rows, mode, 0, nat.ptr(buf), ld, nat.ptr(self.nnz), 0, st)
+        else:
+            buf.zero_()
+        # light passes (x-driven; FULL_JOIN when hpos is None)
+        t0 = int(dr.fwd_ptr_host[x0])
+        t1 = int(dr.fwd_ptr_host[x1])
+        ntup = t1 - t0
+        lens = self.ws.get("len", ntup, torch.int32)
+        offs = self.ws.get("offs", ntup + 1, torch.int64)
+        hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
+        lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
+        lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
+        nat.call("mmj_light_lengths", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), t0, ntup, nat.ptr(dr.left_deg),
+                 self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(lens), nat.ptr(offs),
+                 nat.ptr(self.ws.scan_ws(ntup)), st)
+        nat.call("mmj_light_expand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), t0, ntup, nat.ptr(dr.left_deg),
+                 self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(offs), -1,
+                 1 if self.counts else 0, x0, nat.ptr(buf), ld, st)
+        # merge: segment sizes -> offsets -> codes
+        if self.counts:
+            ncell = rows * self.ldc
+            nseg = int(self.lib.mmj_count_segment_count(ncell))
+            segcnt = self.ws.get("segcnt", nseg, torch.int32)
+            segoff = self.ws.get("segoff", nseg + 1, torch.int64)
+            nat.call("mmj_count_segments", nat.ptr(buf), rows, self.ldc, self.dom_z, x0, self.min_count,
+                     int(self.upper_only), nat.ptr(segcnt), nat.ptr(segoff), nat.ptr(self.ws.scan_ws(nseg)), st)
+        else:
+            nwords = rows * self.wpr
+            nseg = int(self.lib.mmj_bitmap_segment_count(nwords))
+            segcnt = self.ws.get("segcnt", nseg, torch.int32)
+            segoff = self.ws.get("segoff", nseg + 1, torch.int64)
+            nat.call("mmj_bitmap_segments", nat.ptr(buf), nwords, nat.ptr(segcnt), nat.ptr(segoff),
+                     nat.ptr(self.ws.scan_ws(nseg)), st)
+        sizes = torch.stack([segoff[nseg], offs[ntup]]).cpu()
+        total, light = int(sizes[0]), int(sizes[1])
+        codes = self.ws.get("codes", total, torch.int64)
+        counts = None
+        if self.counts:
+            counts = self.ws.get("counts", total, torch.int32)
+            if total:
+                nat.call("mmj_count_emit", nat.ptr(buf), rows, self.ldc, self.dom_z, x0, self.dom_z, self.min_count,
+                         int(self.upper_only), nat.ptr(segoff), nat.ptr(codes), nat.ptr(counts), st)
+        elif total:
+            nat.call("mmj_bitmap_emit", nat.ptr(buf), rows * self.wpr, self.wpr, nat.ptr(segoff), x0, self.dom_z,
+                     nat.ptr(codes), st)
+        self.stats.light_intermediate += light
+        self.stats.out_size += total
+        self.stats.chunks += 1
+        return ChunkResult(x0, x1, total, codes[:total], None if counts is None else counts[:total], light)
+
+    def finish(self):
+        self.stats.heavy_pairs = int(self.nnz.item())
+        return self.stats
+
+    def run(self, consumer: Callable[[ChunkResult], None], x_begin: int = 0, x_end: Optional[int] = None):
+        self.prepare()
+        for x0, x1 in self.chunk_bounds(x_begin, x_end):
+            consumer(self.run_chunk(x0, x1))
+        return self.finish()

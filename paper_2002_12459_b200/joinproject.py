@@ -1,0 +1,229 @@
+"""Join-project operators on the B200 (drop-in for ``mmjoin.joinproject``).
+
+Same entry points, signatures, result type and errors as the reference
+(joinproject.py:28-378); the work runs in libmmjoin_b200.so kernels:
+
+  two_path_join      joinproject.py:155-225   -> engine.TwoPathEngine
+  full_join_dedup    joinproject.py:228-248   -> engine (every y light)
+  partition_two_path joinproject.py:100-116   (split of the input tuples)
+  heavy_matrices     joinproject.py:119-143   (heavy operands, returned dense)
+
+Inputs are ``IndexedRelation`` objects (this package's or the reference's);
+dense ids, hence codes, are the reference's by construction.  Outputs that
+cannot fit in host memory are produced chunk by chunk with
+``two_path_join_chunks``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Iterator, Optional, Sequence
+
+import numpy as np
+
+from .device import Workspace, device_relation
+from .engine import ChunkResult, TwoPathEngine
+from .errors import StarResourceError
+from .matmul import CountMatrix, multiply_counts
+from .optimizer import FULL_JOIN, PARTITIONED, ThresholdPlan, default_plan
+from .relation import IndexedRelation, Relation, build_indexed, semi_join_reduce_many
+
+__all__ = ["OutputSet", "Partition", "StarResourceError", "two_path_join", "two_path_join_chunks",
+           "full_join_dedup", "partition_two_path", "heavy_matrices", "CountMatrix"]
+
+
+@dataclass
+class Partition:
+    """joinproject.py:32-37."""
+    light: Relation
+    heavy: Relation
+    delta1: int
+    delta2: int
+
+
+class OutputSet:
+    """Deduplicated projected tuples, optionally with witness counts
+    (joinproject.py:40-77): ``codes`` are strictly increasing int64 mixed-radix
+    codes over ``dims``."""
+
+    def __init__(self, codes: np.ndarray, dims: Sequence[int], counts: Optional[np.ndarray] = None,
+                 stats: Optional[dict] = None):
+        self.codes = codes
+        self.dims = tuple(int(d) for d in dims)
+        self.counts = counts
+        self.stats = stats or {}
+
+    @property
+    def arity(self) -> int:
+        return len(self.dims)
+
+    def __len__(self) -> int:
+        return len(self.codes)
+
+    def tuples(self) -> np.ndarray:
+        out = np.empty((len(self.codes), self.arity), dtype=np.int64)
+        rem = self.codes
+        for i in range(self.arity - 1, -1, -1):
+            rem, out[:, i] = np.divmod(rem, self.dims[i])
+        return out
+
+    def as_set(self) -> set:
+        return set(map(tuple, self.tuples().tolist()))
+
+    def counts_dict(self) -> dict:
+        if self.counts is None:
+            raise ValueError("counts were not requested")
+        return dict(zip(map(tuple, self.tuples().tolist()), self.counts.tolist()))
+
+    def total_count(self) -> int:
+        if self.counts is None:
+            raise ValueError("counts were not requested")
+        return int(self.counts.sum())
+
+
+def _check_code_space(dims: Sequence[int]) -> None:
+    """joinproject.py:87-89."""
+    if math.prod(max(int(d), 1) for d in dims) >= 2 ** 62:
+        raise StarResourceError("combined domain too large to encode")
+
+
+def _shares(a, b) -> bool:
+    return a.rel.right_values is b.rel.right_values
+
+
+def _ensure_reduced_many(idxs: Sequence) -> list:
+    """joinproject.py:92-97: re-encode over a shared right dictionary unless
+    the inputs already share one."""
+    first = idxs[0]
+    if all(_shares(first, o) for o in idxs[1:]):
+        return list(idxs)
+    red = semi_join_reduce_many([i.rel for i in idxs])
+    return [build_indexed(r) for r in red]
+
+
+def _engine(r, s, plan: ThresholdPlan, want_counts: bool, *, min_count: int = 1, upper_only: bool = False,
+            chunk_rows: Optional[int] = None, ws: Optional[Workspace] = None) -> TwoPathEngine:
+    dr = device_relation(r)
+    ds = dr if s is r else device_relation(s)
+    if plan.strategy == FULL_JOIN:
+        d1 = d2 = max(r.n, s.n, 1)
+    else:
+        d1, d2 = plan.delta1, plan.delta2
+    return TwoPathEngine(dr, ds, plan.strategy, d1, d2, want_counts, min_count=min_count,
+                         upper_only=upper_only, chunk_rows=chunk_rows, ws=ws,
+                         host_left_deg_r=r.left_deg, host_left_deg_s=s.left_deg)
+
+
+def _collect(eng: TwoPathEngine):
+    codes, counts = [], []
+
+    def sink(ch: ChunkResult):
+        codes.append(ch.codes.cpu().numpy())
+        if ch.counts is not None:
+            counts.append(ch.counts.cpu().numpy().astype(np.int64))
+
+    stats = eng.run(sink)
+    c = np.concatenate(codes) if codes else np.empty(0, dtype=np.int64)
+    n = (np.concatenate(counts) if counts else np.empty(0, dtype=np.int64)) if eng.counts else None
+    return c, n, stats
+
+
+def two_path_join(r, s, plan: Optional[ThresholdPlan] = None, want_counts: bool = False,
+                  cores: int = 1, chunk_rows: Optional[int] = None) -> OutputSet:
+    """pi_{x,z}(R(x,y) join S(z,y)) via heavy/light partitioning
+    (joinproject.py:155-225).  ``cores`` is accepted and ignored, as on the
+    reference's BLAS path (matmul/core.py:110-116)."""
+    r, s = _ensure_reduced_many([r, s])
+    if plan is None:
+        plan = default_plan(r, s)
+    plan.validate()
+    dims = (r.rel.dom_left, s.rel.dom_left)
+    _check_code_space(dims)
+    eng = _engine(r, s, plan, want_counts, chunk_rows=chunk_rows)
+    codes, counts, st = _collect(eng)
+    if plan.strategy == FULL_JOIN:
+        return OutputSet(codes, dims, counts, {"intermediate": st.light_intermediate, "plan": plan})
+    stats = {"light_intermediate": st.light_intermediate, "plan": plan, "heavy_pairs": st.heavy_pairs}
+    return OutputSet(codes, dims, counts, stats)
+
+
+def two_path_join_chunks(r, s, plan: Optional[ThresholdPlan] = None, want_counts: bool = False,
+                         chunk_rows: Optional[int] = None, device_output: bool = False) -> Iterator[OutputSet]:
+    """Chunked form of ``two_path_join`` for outputs larger than host memory:
+    yields one ``OutputSet`` per contiguous dense-x range, in code order (the
+    concatenation equals ``two_path_join(...).codes``).  With
+    ``device_output=True`` the codes/counts are torch CUDA tensors that stay
+    valid until the next chunk is requested."""
+    r, s = _ensure_reduced_many([r, s])
+    if plan is None:
+        plan = default_plan(r, s)
+    plan.validate()
+    dims = (r.rel.dom_left, s.rel.dom_left)
+    _check_code_space(dims)
+    eng = _engine(r, s, plan, want_counts, chunk_rows=chunk_rows)
+    eng.prepare()
+    for x0, x1 in eng.chunk_bounds():
+        ch = eng.run_chunk(x0, x1)
+        if device_output:
+            codes, counts = ch.codes, ch.counts
+        else:
+            codes = ch.codes.cpu().numpy()
+            counts = None if ch.counts is None else ch.counts.cpu().numpy().astype(np.int64)
+        yield OutputSet(codes, dims, counts, {"x_range": (x0, x1), "light_intermediate": ch.light, "plan": plan})
+    eng.finish()
+
+
+def full_join_dedup(r, s, want_counts: bool = False) -> OutputSet:
+    """joinproject.py:228-248: enumerate every witness, then deduplicate."""
+    r, s = _ensure_reduced_many([r, s])
+    dims = (r.rel.dom_left, s.rel.dom_left)
+    _check_code_space(dims)
+    n = max(r.n, s.n, 1)
+    eng = _engine(r, s, ThresholdPlan(FULL_JOIN, n, n), want_counts)
+    codes, counts, st = _collect(eng)
+    return OutputSet(codes, dims, counts, {"intermediate": st.light_intermediate})
+
+
+def partition_two_path(r, s, delta1: int, delta2: int):
+    """joinproject.py:100-116: a tuple is light iff its own left value has
+    degree <= delta2, or its y has degree <= delta1 in both relations."""
+    if delta1 < 1 or delta2 < 1:
+        raise ValueError("thresholds must be >= 1")
+    r, s = _ensure_reduced_many([r, s])
+    light_y = (np.asarray(r.right_deg) <= delta1) & (np.asarray(s.right_deg) <= delta1)
+    parts = []
+    for idx, name in ((r, "R"), (s, "S")):
+        left, right = idx.rel.pairs[:, 0], idx.rel.pairs[:, 1]
+        light = (np.asarray(idx.left_deg)[left] <= delta2) | light_y[right]
+        parts.append(Partition(Relation.from_encoded(name + "-", idx.rel.pairs[light], idx.rel),
+                               Relation.from_encoded(name + "+", idx.rel.pairs[~light], idx.rel),
+                               delta1, delta2))
+    return parts[0], parts[1]
+
+
+def heavy_matrices(r, s, delta1: int, delta2: int):
+    """joinproject.py:119-143: (M1, M2) dense 0/1 matrices of the heavy parts
+    (rows/cols keyed by heavy ids), or None if a heavy side is empty.  Built
+    by the same device kernels that feed the tensor-core product."""
+    import torch
+
+    from . import _native as nat
+    r, s = _ensure_reduced_many([r, s])
+    dr = device_relation(r)
+    ds = dr if s is r else device_relation(s)
+    light_y = (np.asarray(r.right_deg) <= delta1) & (np.asarray(s.right_deg) <= delta1)
+    heavy_a = np.nonzero(np.asarray(r.left_deg) > delta2)[0]
+    heavy_b = np.nonzero(~light_y)[0]
+    heavy_c = np.nonzero(np.asarray(s.left_deg) > delta2)[0]
+    if not (len(heavy_a) and len(heavy_b) and len(heavy_c)):
+        return None
+    eng = TwoPathEngine(dr, ds, PARTITIONED, delta1, delta2, False, host_left_deg_r=r.left_deg,
+                        host_left_deg_s=s.left_deg)
+    eng.prepare()
+    k = eng.stats.k_heavy
+    a = eng.A[: r.rel.dom_left, :k].cpu().numpy()[heavy_a].astype(np.int64)
+    b = eng.B[: s.rel.dom_left, :k].cpu().numpy()[heavy_c].astype(np.int64)
+    del torch, nat
+    return (CountMatrix(a, row_keys=heavy_a, col_keys=heavy_b),
+            CountMatrix(np.ascontiguousarray(b.T), row_keys=heavy_b, col_keys=heavy_c))

@@ -1,0 +1,136 @@
+"""GPU parity: two-path join / full join / multiply_counts vs the CPU oracle.
+
+Bit-exact: identical code arrays (sorted distinct int64 mixed-radix codes),
+identical int64 counts and identical ``stats`` counters, for every plan --
+the output is plan-independent but the stats are not, so each
+plan is checked as given.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import random_pairs, zipf_pairs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2002_12459_b200 as p
+    from paper_2002_12459_b200 import joinproject, matmul  # noqa: F401
+    return p
+
+
+def _mine(pkg, r_pairs, s_pairs, self_join=False):
+    from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce
+    R = Relation.from_raw_pairs("R", np.asarray(r_pairs, dtype=np.int64).reshape(-1, 2))
+    if self_join:
+        r = build_indexed(R)
+        return r, r
+    S = Relation.from_raw_pairs("S", np.asarray(s_pairs, dtype=np.int64).reshape(-1, 2))
+    R, S = semi_join_reduce(R, S)
+    return build_indexed(R), build_indexed(S)
+
+
+def _oracle_rels(oracle, r_pairs, s_pairs, self_join=False):
+    R = oracle.encode(np.asarray(r_pairs, dtype=np.int64).reshape(-1, 2))
+    if self_join:
+        return R, R
+    S = oracle.encode(np.asarray(s_pairs, dtype=np.int64).reshape(-1, 2))
+    return tuple(oracle.semi_join_many([R, S]))
+
+
+def _check(pkg, oracle, r_pairs, s_pairs, plans, self_join=False, chunk_rows=None):
+    from paper_2002_12459_b200.joinproject import two_path_join
+    from paper_2002_12459_b200.optimizer import ThresholdPlan
+    r, s = _mine(pkg, r_pairs, s_pairs, self_join)
+    orr, oss = _oracle_rels(oracle, r_pairs, s_pairs, self_join)
+    for strategy, d1, d2 in plans:
+        for counts in (False, True):
+            got = two_path_join(r, s, plan=ThresholdPlan(strategy, d1, d2), want_counts=counts,
+                                chunk_rows=chunk_rows)
+            exp = oracle.two_path(orr, oss, oracle.OPlan(strategy, d1, d2), want_counts=counts)
+            assert got.dims == tuple(exp.dims)
+            assert np.array_equal(got.codes, exp.codes), (strategy, d1, d2, counts)
+            if counts:
+                assert got.counts.dtype == np.int64
+                assert np.array_equal(got.counts, exp.counts), (strategy, d1, d2)
+            for key in ("light_intermediate", "heavy_pairs", "intermediate"):
+                if key in exp.stats:
+                    assert got.stats[key] == exp.stats[key], (key, strategy, d1, d2, counts)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_two_path_random_plans(pkg, oracle, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(20, 400))
+    dom = int(rng.integers(5, 40))
+    rp = random_pairs(rng, n, dom, dom)
+    sp = random_pairs(rng, n, dom, dom)
+    nn = max(len(rp), len(sp))
+    plans = [("partitioned", 1, 1), ("partitioned", 2, 3), ("partitioned", 5, 2),
+             ("partitioned", nn, nn), ("fulljoin", nn, nn)]
+    _check(pkg, oracle, rp, sp, plans)
+
+
+@pytest.mark.parametrize("chunk_rows", [None, 128])
+def test_two_path_zipf_medium(pkg, oracle, chunk_rows):
+    rng = np.random.default_rng(11)
+    rp = zipf_pairs(rng, 20000, 1500, 3000, 1.2)
+    sp = zipf_pairs(rng, 20000, 1300, 3000, 1.1)
+    plans = [("partitioned", 10, 10), ("partitioned", 300, 1), ("partitioned", 40, 3)]
+    _check(pkg, oracle, rp, sp, plans, chunk_rows=chunk_rows)
+
+
+def test_two_path_self_join_default_plan(pkg, oracle):
+    from paper_2002_12459_b200.joinproject import two_path_join
+    rng = np.random.default_rng(3)
+    rp = zipf_pairs(rng, 30000, 2000, 2000, 1.2)
+    r, _ = _mine(pkg, rp, None, self_join=True)
+    R, _ = _oracle_rels(oracle, rp, None, self_join=True)
+    got = two_path_join(r, r, want_counts=True)
+    exp = oracle.two_path(R, R, None, want_counts=True)
+    assert got.stats["plan"].delta1 == exp.stats["plan"].delta1
+    assert got.stats["plan"].delta2 == exp.stats["plan"].delta2
+    assert np.array_equal(got.codes, exp.codes)
+    assert np.array_equal(got.counts, exp.counts)
+    assert got.stats["light_intermediate"] == exp.stats["light_intermediate"]
+    assert got.stats["heavy_pairs"] == exp.stats["heavy_pairs"]
+    assert got.total_count() == r.out_join_with(r)
+
+
+def test_full_join_dedup(pkg, oracle):
+    from paper_2002_12459_b200.joinproject import full_join_dedup
+    rng = np.random.default_rng(5)
+    rp = random_pairs(rng, 300, 25, 20)
+    sp = random_pairs(rng, 300, 25, 20)
+    r, s = _mine(pkg, rp, sp)
+    R, S = _oracle_rels(oracle, rp, sp)
+    for counts in (False, True):
+        got = full_join_dedup(r, s, want_counts=counts)
+        exp = oracle.full_join(R, S, counts)
+        assert np.array_equal(got.codes, exp.codes)
+        assert got.stats["intermediate"] == exp.stats["intermediate"] == r.out_join_with(s)
+        if counts:
+            assert np.array_equal(got.counts, exp.counts)
+
+
+@pytest.mark.parametrize("hi", [2, 5, 300, 10 ** 6])
+def test_multiply_counts_exact(pkg, hi):
+    from paper_2002_12459_b200.matmul import CountMatrix, multiply_counts
+    rng = np.random.default_rng(hi)
+    for _ in range(6):
+        u, v, w = (int(x) for x in rng.integers(1, 300, 3))
+        a = rng.integers(0, hi, (u, v)).astype(np.int64)
+        b = rng.integers(0, hi, (v, w)).astype(np.int64)
+        got = multiply_counts(CountMatrix(a), CountMatrix(b)).data
+        assert np.array_equal(got, a @ b)
+
+
+def test_multiply_counts_large_k(pkg):
+    from paper_2002_12459_b200.matmul import CountMatrix, multiply_counts
+    rng = np.random.default_rng(1)
+    a = rng.integers(0, 2, (300, 40000)).astype(np.int64)
+    b = rng.integers(0, 256, (40000, 260)).astype(np.int64)
+    got = multiply_counts(CountMatrix(a), CountMatrix(b)).data
+    assert np.array_equal(got, a @ b)
