@@ -46,6 +46,8 @@ int mmj_abi_version(void);
 const char* mmj_last_error(void);
 int mmj_set_device(int device);
 int mmj_sm_count(void);
+/* number of kernels this library has launched in the process */
+long long mmj_launch_count(void);
 
 /* ---- scans ------------------------------------------------------------- */
 size_t mmj_scan_workspace_bytes(int64_t n);

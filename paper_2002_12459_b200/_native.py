@@ -35,6 +35,7 @@ _SIGS = {
     "mmj_last_error": (C.c_char_p, []),
     "mmj_set_device": (INT, [INT]),
     "mmj_sm_count": (INT, []),
+    "mmj_launch_count": (C.c_longlong, []),
     "mmj_scan_workspace_bytes": (C.c_size_t, [I64]),
     "mmj_exclusive_scan_i32": (INT, [P, P, I64, P, P]),
     "mmj_heavy_y_positions": (INT, [P, P, I64, I64, P, P, P, P, P]),

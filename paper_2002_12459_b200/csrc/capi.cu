@@ -58,6 +58,8 @@ int mmj_set_device(int device) { return mmj::cuda_status(cudaSetDevice(device), 
 
 int mmj_sm_count(void) { return mmj::sm_count(); }
 
+long long mmj_launch_count(void) { return mmj::launch_count(); }
+
 size_t mmj_scan_workspace_bytes(int64_t n) { return mmj::scan_ws_bytes(n); }
 
 int mmj_exclusive_scan_i32(const int32_t* in, int64_t* out, int64_t n, void* ws, void* stream) {

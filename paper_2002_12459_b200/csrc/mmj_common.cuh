@@ -26,8 +26,14 @@ inline int cuda_status(cudaError_t e, const char* where) {
   return MMJ_OK;
 }
 
+// every kernel launch of the library goes through MMJ_CHECK_LAUNCH, which
+// also counts it (mmj_launch_count(): the bench's gpu_launches evidence).
+void count_launch();
+long long launch_count();
+
 #define MMJ_CHECK_LAUNCH(where)                                   \
   do {                                                            \
+    ::mmj::count_launch();                                        \
     int _st = ::mmj::cuda_status(cudaGetLastError(), where);      \
     if (_st) return _st;                                          \
   } while (0)

@@ -21,6 +21,10 @@ void set_error(const char* fmt, ...) {
 
 const char* last_error() { return g_err; }
 
+static long long g_launches = 0;
+void count_launch() { __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED); }
+long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
 int sm_count() {
   int dev = 0;
   cudaGetDevice(&dev);

@@ -99,6 +99,9 @@ class TwoPathEngine:
         self.chunk_rows = max(BM, _rup(int(chunk_rows), BM))
         self.nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
         self._prepared = False
+        self._sizes_dev = None
+        self._n_async = 0
+        self.timer = None          # optional PhaseTimer (bench instrumentation)
 
     # ------------------------------------------------------------ prepare
     def _st(self):
@@ -159,7 +162,14 @@ class TwoPathEngine:
             yield x, nx
             x = nx
 
-    def run_chunk(self, x0: int, x1: int) -> ChunkResult:
+    def _ph(self, name: str, start: bool):
+        if self.timer is not None:
+            (self.timer.start if start else self.timer.stop)(name)
+
+    def run_chunk(self, x0: int, x1: int, sync: bool = True) -> ChunkResult:
+        """Evaluate output rows [x0, x1).  With ``sync=False`` no host sync
+        happens: the code buffer is sized for the worst case (rows*dom_z) and
+        the chunk's sizes are fetched later by :meth:`finish`."""
         torch = self.torch
         st = self._st()
         dr, ds = self.dr, self.ds
@@ -173,11 +183,13 @@ class TwoPathEngine:
             ld = self.wpr
             mode = nat.MODE_BITMAP
         # heavy part (writes every cell of the chunk) or zero fill
+        self._ph("heavy_mma", True)
         if self.A is not None:
             nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
                      self.kpad, 0, self.kpad, x0, rows, mode, 0, nat.ptr(buf), ld, nat.ptr(self.nnz), 0, st)
         else:
             buf.zero_()
+        self._ph("heavy_mma", False)
         # light passes (x-driven; FULL_JOIN when hpos is None)
         t0 = int(dr.fwd_ptr_host[x0])
         t1 = int(dr.fwd_ptr_host[x1])
@@ -187,13 +199,16 @@ class TwoPathEngine:
         hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
         lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
         lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
+        self._ph("light", True)
         nat.call("mmj_light_lengths", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), t0, ntup, nat.ptr(dr.left_deg),
                  self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(lens), nat.ptr(offs),
                  nat.ptr(self.ws.scan_ws(ntup)), st)
         nat.call("mmj_light_expand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), t0, ntup, nat.ptr(dr.left_deg),
                  self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(offs), -1,
                  1 if self.counts else 0, x0, nat.ptr(buf), ld, st)
+        self._ph("light", False)
         # merge: segment sizes -> offsets -> codes
+        self._ph("segments", True)
         if self.counts:
             ncell = rows * self.ldc
             nseg = int(self.lib.mmj_count_segment_count(ncell))
@@ -208,26 +223,62 @@ class TwoPathEngine:
             segoff = self.ws.get("segoff", nseg + 1, torch.int64)
             nat.call("mmj_bitmap_segments", nat.ptr(buf), nwords, nat.ptr(segcnt), nat.ptr(segoff),
                      nat.ptr(self.ws.scan_ws(nseg)), st)
-        sizes = torch.stack([segoff[nseg], offs[ntup]]).cpu()
-        total, light = int(sizes[0]), int(sizes[1])
-        codes = self.ws.get("codes", total, torch.int64)
+        self._ph("segments", False)
+        if sync:
+            sizes = torch.stack([segoff[nseg], offs[ntup]]).cpu()
+            total, light = int(sizes[0]), int(sizes[1])
+            cap = total
+        else:
+            slot = self._async_slot()
+            slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
+            slot[1:2].copy_(offs[ntup:ntup + 1], non_blocking=True)
+            total = light = -1
+            cap = rows * self.dom_z
+        codes = self.ws.get("codes", cap, torch.int64)
         counts = None
+        self._ph("emit", True)
         if self.counts:
-            counts = self.ws.get("counts", total, torch.int32)
-            if total:
+            counts = self.ws.get("counts", cap, torch.int32)
+            if cap:
                 nat.call("mmj_count_emit", nat.ptr(buf), rows, self.ldc, self.dom_z, x0, self.dom_z, self.min_count,
                          int(self.upper_only), nat.ptr(segoff), nat.ptr(codes), nat.ptr(counts), st)
-        elif total:
+        elif cap:
             nat.call("mmj_bitmap_emit", nat.ptr(buf), rows * self.wpr, self.wpr, nat.ptr(segoff), x0, self.dom_z,
                      nat.ptr(codes), st)
+        self._ph("emit", False)
+        self.stats.chunks += 1
+        if not sync:
+            return ChunkResult(x0, x1, -1, codes, counts, -1)
         self.stats.light_intermediate += light
         self.stats.out_size += total
-        self.stats.chunks += 1
         return ChunkResult(x0, x1, total, codes[:total], None if counts is None else counts[:total], light)
 
+    def _async_slot(self):
+        """Device slot (2 x int64) receiving one async chunk's (size, light)."""
+        torch = self.torch
+        if self._sizes_dev is None or self._n_async >= self._sizes_dev.shape[0]:
+            grow = max(64, 2 * (0 if self._sizes_dev is None else self._sizes_dev.shape[0]))
+            new = torch.zeros((grow, 2), dtype=torch.int64, device="cuda")
+            if self._sizes_dev is not None:
+                new[: self._sizes_dev.shape[0]].copy_(self._sizes_dev)
+            self._sizes_dev = new
+        slot = self._sizes_dev[self._n_async]
+        self._n_async += 1
+        return slot
+
     def finish(self):
-        self.stats.heavy_pairs = int(self.nnz.item())
+        self.stats.heavy_pairs = int(self.nnz.item())     # synchronises the stream
+        if self._n_async:
+            tot = self._sizes_dev[: self._n_async].sum(dim=0).cpu()
+            self.stats.out_size += int(tot[0])
+            self.stats.light_intermediate += int(tot[1])
+            self._n_async = 0
         return self.stats
+
+    def reset_stats(self):
+        self.stats = EngineStats(k_heavy=self.stats.k_heavy, kpad=self.stats.kpad)
+        self.nnz.zero_()
+        self._n_async = 0
 
     def run(self, consumer: Callable[[ChunkResult], None], x_begin: int = 0, x_end: Optional[int] = None):
         self.prepare()

@@ -149,28 +149,56 @@ def two_path_join(r, s, plan: Optional[ThresholdPlan] = None, want_counts: bool 
 
 
 def two_path_join_chunks(r, s, plan: Optional[ThresholdPlan] = None, want_counts: bool = False,
-                         chunk_rows: Optional[int] = None, device_output: bool = False) -> Iterator[OutputSet]:
+                         chunk_rows: Optional[int] = None, device_output: bool = False,
+                         host_buffer=None, upload: str = "cached", x_range=None) -> Iterator[OutputSet]:
     """Chunked form of ``two_path_join`` for outputs larger than host memory:
     yields one ``OutputSet`` per contiguous dense-x range, in code order (the
-    concatenation equals ``two_path_join(...).codes``).  With
-    ``device_output=True`` the codes/counts are torch CUDA tensors that stay
-    valid until the next chunk is requested."""
+    concatenation equals ``two_path_join(...).codes``).
+
+    ``device_output=True`` yields torch CUDA tensors valid until the next
+    chunk is requested; ``host_buffer`` (a pinned int64 torch tensor of at
+    least chunk_rows*dom_z elements) receives each chunk's codes by an async
+    D2H copy and the yielded codes are a numpy view of it (valid until the
+    next chunk); ``upload="fresh"`` re-uploads the CSR inputs from host
+    (pinned) memory instead of using the cached device copy; ``x_range``
+    restricts the output to dense x in [lo, hi) (x-range sharding)."""
+    from .device import DeviceRelation
     r, s = _ensure_reduced_many([r, s])
     if plan is None:
         plan = default_plan(r, s)
     plan.validate()
     dims = (r.rel.dom_left, s.rel.dom_left)
     _check_code_space(dims)
-    eng = _engine(r, s, plan, want_counts, chunk_rows=chunk_rows)
+    if upload == "fresh":
+        dr = DeviceRelation.from_indexed(r, pinned=True)
+        ds = dr if s is r else DeviceRelation.from_indexed(s, pinned=True)
+        d1, d2 = ((plan.delta1, plan.delta2) if plan.strategy != FULL_JOIN else (max(r.n, s.n, 1),) * 2)
+        eng = TwoPathEngine(dr, ds, plan.strategy, d1, d2, want_counts, chunk_rows=chunk_rows,
+                            host_left_deg_r=r.left_deg, host_left_deg_s=s.left_deg)
+        eng.h2d_bytes = dr.h2d_bytes + (0 if s is r else ds.h2d_bytes)
+    else:
+        eng = _engine(r, s, plan, want_counts, chunk_rows=chunk_rows)
+        eng.h2d_bytes = 0
     eng.prepare()
-    for x0, x1 in eng.chunk_bounds():
+    lo, hi = (0, r.rel.dom_left) if x_range is None else x_range
+    for x0, x1 in eng.chunk_bounds(lo, hi):
         ch = eng.run_chunk(x0, x1)
         if device_output:
             codes, counts = ch.codes, ch.counts
+        elif host_buffer is not None:
+            import torch
+            if ch.n > host_buffer.numel():
+                raise ValueError("host_buffer smaller than a chunk's output")
+            if ch.n:
+                host_buffer[: ch.n].copy_(ch.codes, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            codes = host_buffer[: ch.n].numpy()
+            counts = None if ch.counts is None else ch.counts.cpu().numpy().astype(np.int64)
         else:
             codes = ch.codes.cpu().numpy()
             counts = None if ch.counts is None else ch.counts.cpu().numpy().astype(np.int64)
-        yield OutputSet(codes, dims, counts, {"x_range": (x0, x1), "light_intermediate": ch.light, "plan": plan})
+        yield OutputSet(codes, dims, counts, {"x_range": (x0, x1), "light_intermediate": ch.light, "plan": plan,
+                                              "h2d_bytes": eng.h2d_bytes})
     eng.finish()
 
 
