@@ -111,6 +111,24 @@ int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_
 int mmj_digit_plane(const int64_t* src, int64_t rows, int64_t cols, int transpose, int digit, uint8_t* dst,
                     int64_t kpad, void* stream);
 
+/* ---- fused light passes + merge + emission (projection, no counts):
+ *      joinproject.py:183-203 + 220-225 ---------------------------------------
+ * One CTA per group of rows_per_group rows of the chunk [x0, x0+rows): copies
+ * the heavy bitmap rows (heavy_bm, rows x wpr words; NULL = no heavy part)
+ * into shared memory, ORs every light witness of those rows in (shared-memory
+ * atomics), and writes the group's sorted codes at an offset found by a
+ * decoupled look-back over `status` (ceil(rows/rows_per_group) uint64, zeroed)
+ * with group tickets from `ticket` (zeroed).  `codes` must hold rows*dom_z
+ * entries (worst case); *total receives the chunk size and *witnesses
+ * accumulates the light intermediate size.  Fails with MMJ_ERR_UNSUPPORTED if
+ * the group's bitmap does not fit in shared memory. */
+size_t mmj_row_emit_smem_bytes(int64_t rows_per_group, int64_t wpr);
+int mmj_row_light_emit(const uint32_t* heavy_bm, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
+                       int rows_per_group, const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x,
+                       int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx,
+                       const int32_t* lz_ptr, const int32_t* lz_idx, int64_t* codes, unsigned long long* status,
+                       int* ticket, unsigned long long* witnesses, unsigned long long* total, void* stream);
+
 /* ---- merge / emission: joinproject.py:220-225 -------------------------------
  * Bitmap chunk of nwords words (wpr words per row, row r <-> x = x0 + r):
  * segment popcounts + exclusive scan (seg_off[nseg+1], seg_off[nseg] = size),

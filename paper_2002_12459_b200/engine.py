@@ -33,6 +33,7 @@ BK = 128          # K block (bytes)
 
 DEFAULT_BITMAP_CHUNK_BYTES = 1 << 30
 DEFAULT_COUNT_CHUNK_BYTES = 4 << 30
+FUSED_SMEM_LIMIT = 200 * 1024
 
 
 def _rup(a: int, b: int) -> int:
@@ -98,6 +99,11 @@ class TwoPathEngine:
             chunk_rows = max(BM, (budget // max(row_bytes, 1)) // BM * BM)
         self.chunk_rows = max(BM, _rup(int(chunk_rows), BM))
         self.nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.wit = torch.zeros(1, dtype=torch.int64, device="cuda")
+        # fused light+merge+emit kernel for the projection when a row group's
+        # bitmap fits in shared memory (dom_z up to ~1.2M)
+        self.group_rows = max(1, min(32, (48 * 1024) // (self.wpr * 4)))
+        self.fused = (not self.counts) and self.lib.mmj_row_emit_smem_bytes(1, self.wpr) <= FUSED_SMEM_LIMIT
         self._prepared = False
         self._sizes_dev = None
         self._n_async = 0
@@ -114,6 +120,7 @@ class TwoPathEngine:
         st = self._st()
         dr, ds = self.dr, self.ds
         self.nnz.zero_()
+        self.wit.zero_()
         if self.strategy == PARTITIONED:
             dom_y = self.dom_y
             flag = self.ws.get("yflag", dom_y, torch.uint8)
@@ -190,6 +197,8 @@ class TwoPathEngine:
         else:
             buf.zero_()
         self._ph("heavy_mma", False)
+        if self.fused:
+            return self._fused_tail(x0, x1, rows, buf, sync)
         # light passes (x-driven; FULL_JOIN when hpos is None)
         t0 = int(dr.fwd_ptr_host[x0])
         t1 = int(dr.fwd_ptr_host[x1])
@@ -253,6 +262,38 @@ class TwoPathEngine:
         self.stats.out_size += total
         return ChunkResult(x0, x1, total, codes[:total], None if counts is None else counts[:total], light)
 
+    def _fused_tail(self, x0, x1, rows, buf, sync):
+        torch = self.torch
+        st = self._st()
+        dr, ds = self.dr, self.ds
+        G = self.group_rows
+        ngroups = -(-rows // G)
+        status = self.ws.get("status", ngroups + 2, torch.int64)
+        status.zero_()                       # [0, ngroups): look-back words, [ngroups]: ticket, [+1]: total
+        ticket = status[ngroups:ngroups + 1]
+        total = status[ngroups + 1:ngroups + 2]
+        cap = rows * self.dom_z
+        codes = self.ws.get("codes", cap, torch.int64)
+        hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
+        lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
+        lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
+        heavy = nat.ptr(buf) if self.A is not None else 0
+        wit0 = int(self.wit.item()) if sync else 0
+        self._ph("light_emit", True)
+        nat.call("mmj_row_light_emit", heavy, x0, rows, self.wpr, self.dom_z, G, nat.ptr(dr.fwd_ptr),
+                 nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx),
+                 lzp, lzi, nat.ptr(codes), nat.ptr(status), nat.ptr(ticket), nat.ptr(self.wit), nat.ptr(total), st)
+        self._ph("light_emit", False)
+        self.stats.chunks += 1
+        if not sync:
+            slot = self._async_slot()
+            slot[0:1].copy_(total, non_blocking=True)
+            return ChunkResult(x0, x1, -1, codes, None, -1)
+        n = int(total.item())
+        light = int(self.wit.item()) - wit0
+        self.stats.out_size += n
+        return ChunkResult(x0, x1, n, codes[:n], None, light)
+
     def _async_slot(self):
         """Device slot (2 x int64) receiving one async chunk's (size, light)."""
         torch = self.torch
@@ -268,16 +309,20 @@ class TwoPathEngine:
 
     def finish(self):
         self.stats.heavy_pairs = int(self.nnz.item())     # synchronises the stream
+        if self.fused:
+            self.stats.light_intermediate = int(self.wit.item())
         if self._n_async:
             tot = self._sizes_dev[: self._n_async].sum(dim=0).cpu()
             self.stats.out_size += int(tot[0])
-            self.stats.light_intermediate += int(tot[1])
+            if not self.fused:
+                self.stats.light_intermediate += int(tot[1])
             self._n_async = 0
         return self.stats
 
     def reset_stats(self):
         self.stats = EngineStats(k_heavy=self.stats.k_heavy, kpad=self.stats.kpad)
         self.nnz.zero_()
+        self.wit.zero_()
         self._n_async = 0
 
     def run(self, consumer: Callable[[ChunkResult], None], x_begin: int = 0, x_end: Optional[int] = None):

@@ -134,3 +134,14 @@ def test_multiply_counts_large_k(pkg):
     b = rng.integers(0, 256, (40000, 260)).astype(np.int64)
     got = multiply_counts(CountMatrix(a), CountMatrix(b)).data
     assert np.array_equal(got, a @ b)
+
+
+@pytest.mark.parametrize("dom_z", [700, 30000, 300000])
+def test_fused_row_emit_wide_rows(pkg, oracle, dom_z):
+    """Row-group sizes from many rows per CTA (narrow z domain) to one
+    60 KB row per CTA; plans with and without a heavy part."""
+    rng = np.random.default_rng(dom_z)
+    rp = zipf_pairs(rng, 6000, 400, 900, 1.1)
+    sp = zipf_pairs(rng, 8000, dom_z, 900, 1.1)
+    plans = [("partitioned", 20, 1), ("partitioned", 5, 5), ("fulljoin", 1, 1)]
+    _check(pkg, oracle, rp, sp, plans)
