@@ -25,7 +25,12 @@ namespace {
 constexpr int RE_THREADS = 512;
 constexpr int RE_WARPS = RE_THREADS / 32;
 constexpr int TUP_BATCH = RE_THREADS;   // light tuples staged per round
-constexpr int STAGE = 1024;             // codes staged per warp (one segment max)
+constexpr int STAGE = 1024 + 64;        // codes staged per warp (one segment max) + bank padding
+
+// staging slot of the k-th code of a segment: one pad slot per 16 codes.
+// Lanes start ~16 codes apart (a 49%-dense word has ~16 set bits), so an
+// unpadded layout puts every lane's k-th store in the same bank.
+__device__ __forceinline__ int stage_slot(int k) { return k + (k >> 4); }
 
 constexpr unsigned long long FLAG_AGG = 1ull << 62;
 constexpr unsigned long long FLAG_INC = 2ull << 62;
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(RE_THREADS, 1) k_row_light_emit(const RowEmitA
     const int64_t code0 = (xa + row) * a.dom_z + (w - row * a.wpr) * 32;
     while (word) {
       const int b = __ffs(word) - 1;
-      stage[k++] = code0 + b;
+      stage[stage_slot(k++)] = code0 + b;
       word &= word - 1;
     }
     __syncwarp();
@@ -227,11 +232,14 @@ __global__ void __launch_bounds__(RE_THREADS, 1) k_row_light_emit(const RowEmitA
     // peel to a 16-byte boundary, then pairs, then the tail
     const int head = (int)(((reinterpret_cast<uintptr_t>(out) >> 3) & 1));
     const int h = min(head, tot);
-    if (lane < h) st_stream(out + lane, stage[lane]);
+    if (lane < h) st_stream(out + lane, stage[stage_slot(lane)]);
     const int npair = (tot - h) >> 1;
-    for (int p = lane; p < npair; p += 32) st_stream_v2(out + h + 2 * p, stage[h + 2 * p], stage[h + 2 * p + 1]);
+    for (int p = lane; p < npair; p += 32) {
+      const int i = h + 2 * p;
+      st_stream_v2(out + i, stage[stage_slot(i)], stage[stage_slot(i + 1)]);
+    }
     const int done = h + 2 * npair;
-    if (lane < tot - done) st_stream(out + done + lane, stage[done + lane]);
+    if (lane < tot - done) st_stream(out + done + lane, stage[stage_slot(done + lane)]);
     __syncwarp();
   }
 }
