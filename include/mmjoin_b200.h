@@ -113,16 +113,18 @@ int mmj_digit_plane(const int64_t* src, int64_t rows, int64_t cols, int transpos
 
 /* ---- fused light passes + merge + emission (projection, no counts):
  *      joinproject.py:183-203 + 220-225 ---------------------------------------
- * One CTA per group of rows_per_group rows of the chunk [x0, x0+rows): copies
- * the heavy bitmap rows (heavy_bm, rows x wpr words; NULL = no heavy part)
- * into shared memory, ORs every light witness of those rows in (shared-memory
- * atomics), and writes the group's sorted codes at an offset found by a
- * decoupled look-back over `status` (ceil(rows/rows_per_group) uint64, zeroed)
- * with group tickets from `ticket` (zeroed).  `codes` must hold rows*dom_z
- * entries (worst case); *total receives the chunk size and *witnesses
- * accumulates the light intermediate size.  Fails with MMJ_ERR_UNSUPPORTED if
- * the group's bitmap does not fit in shared memory. */
+ * The chunk's output bitmap [x0, x0+rows) x [0, dom_z) is cut into
+ * mmj_row_emit_tiles(rows, wpr) tiles of <= 65536 cells (whole rows when
+ * dom_z is small, else one row and a column block), one CTA each: the heavy
+ * bitmap tile (heavy_bm, rows x wpr words; NULL = no heavy part) is copied to
+ * shared memory, every light witness of the tile is OR-ed in (shared-memory
+ * atomics), and the tile's sorted codes are written at an offset found by a
+ * decoupled look-back over `status` (ntiles uint64, zeroed).  `codes` must
+ * hold rows*dom_z entries (worst case); *total receives the chunk size and
+ * *witnesses accumulates the light intermediate size.  rows_per_group and
+ * ticket are unused (ABI placeholders). */
 size_t mmj_row_emit_smem_bytes(int64_t rows_per_group, int64_t wpr);
+int64_t mmj_row_emit_tiles(int64_t rows, int64_t wpr);
 int mmj_row_light_emit(const uint32_t* heavy_bm, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                        int rows_per_group, const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x,
                        int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx,

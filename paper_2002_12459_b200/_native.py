@@ -46,6 +46,7 @@ _SIGS = {
     "mmj_heavy_mma": (INT, [P, I64, P, I64, I64, I64, I64, I64, I64, INT, INT, P, I64, P, INT, P]),
     "mmj_digit_plane": (INT, [P, I64, I64, INT, INT, P, I64, P]),
     "mmj_row_emit_smem_bytes": (C.c_size_t, [I64, I64]),
+    "mmj_row_emit_tiles": (I64, [I64, I64]),
     "mmj_row_light_emit": (INT, [P, I64, I64, I64, I64, INT, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P]),
     "mmj_bitmap_segment_count": (I64, [I64]),
     "mmj_bitmap_segments": (INT, [P, I64, P, P, P, P]),

@@ -25,6 +25,7 @@ int count_segments(const int32_t*, int64_t, int64_t, int64_t, int64_t, int32_t, 
 int count_emit(const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t, int, const int64_t*, int64_t*,
                int32_t*, cudaStream_t);
 size_t row_emit_smem(int64_t, int64_t);
+int64_t row_emit_tiles(int64_t, int64_t);
 int row_light_emit(const uint32_t*, int64_t, int64_t, int64_t, int64_t, int, const int32_t*, const int32_t*,
                    const int32_t*, int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*,
                    const int32_t*, int64_t*, unsigned long long*, int*, unsigned long long*, unsigned long long*,
@@ -141,6 +142,8 @@ int mmj_digit_plane(const int64_t* src, int64_t rows, int64_t cols, int transpos
 size_t mmj_row_emit_smem_bytes(int64_t rows_per_group, int64_t wpr) {
   return mmj::row_emit_smem(rows_per_group, wpr);
 }
+
+int64_t mmj_row_emit_tiles(int64_t rows, int64_t wpr) { return mmj::row_emit_tiles(rows, wpr); }
 
 int mmj_row_light_emit(const uint32_t* heavy_bm, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                        int rows_per_group, const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x,

@@ -1,19 +1,24 @@
-// Fused light expansion + merge + emission, one row group per CTA.
+// Fused light expansion + merge + emission over bitmap tiles.
 //
 // Replaces, for the projection (no counts) two-path path, the light passes
-// (joinproject.py:183-203) and the np.unique merge (joinproject.py:220-225):
-//   1. the heavy product's bitmap rows of the group are copied into shared
-//      memory (or zeroed when there is no heavy part);
-//   2. every light witness (x, z) of the group's rows -- R tuples of those x,
-//      each expanding its S-side list exactly as the reference's three
-//      witness-disjoint passes do -- is OR-ed into the shared bitmap with a
-//      shared-memory atomic (no global atomics, no materialised keys);
-//   3. per-32-word segment popcounts are block-scanned, the group's global
-//      output offset comes from a single-pass decoupled look-back over the
-//      groups (tickets taken in order, so predecessors are always resident);
-//   4. each warp stages a segment's codes x*dom_z + z in shared memory and
-//      writes them with coalesced 16-byte streaming stores.
-// The bitmap is read once, every code is written once: the kernel is bound by
+// (joinproject.py:183-203) and the np.unique merge (joinproject.py:220-225).
+// The chunk's output space (rows x dom_z bits) is cut into tiles of at most
+// TILE_BITS bits -- several whole rows when dom_z is small, otherwise one row
+// and a column block -- processed in row-major tile order, one CTA per tile:
+//   1. the heavy product's bitmap tile is copied into shared memory (or zeroed
+//      when there is no heavy part);
+//   2. every light witness (x, z) with x in the tile's rows and z in its
+//      column block -- R tuples of those x, each expanding its S-side list
+//      (sorted by z, so the column block is a contiguous slice) exactly as the
+//      reference's three witness-disjoint passes do -- is OR-ed into the tile
+//      with a shared-memory atomic (no global atomics, no materialised keys);
+//   3. per-32-word segment popcounts are block-scanned and the tile's global
+//      output offset comes from a single-pass decoupled look-back over tiles
+//      (blockIdx order: lower tiles are always already resident or done);
+//   4. each warp stages a segment's codes (as 32-bit offsets from the tile's
+//      first code, in an XOR-swizzled conflict-free layout) and writes them
+//      with coalesced 16-byte streaming stores.
+// The bitmap is read once and every code written once: the kernel is bound by
 // the HBM write of the sorted output (8 B per distinct (x, z)).
 #include <cub/block/block_scan.cuh>
 
@@ -22,15 +27,13 @@
 namespace mmj {
 namespace {
 
-constexpr int RE_THREADS = 512;
+constexpr int RE_THREADS = 256;
 constexpr int RE_WARPS = RE_THREADS / 32;
 constexpr int TUP_BATCH = RE_THREADS;   // light tuples staged per round
-constexpr int STAGE = 1024 + 64;        // codes staged per warp (one segment max) + bank padding
-
-// staging slot of the k-th code of a segment: one pad slot per 16 codes.
-// Lanes start ~16 codes apart (a 49%-dense word has ~16 set bits), so an
-// unpadded layout puts every lane's k-th store in the same bank.
-__device__ __forceinline__ int stage_slot(int k) { return k + (k >> 4); }
+constexpr int TILE_WORDS = 2048;        // 8 KB of bitmap per tile (65536 cells)
+constexpr int TILE_SEGS = TILE_WORDS / 32;
+constexpr int STAGE = 1024;             // codes staged per warp (one segment)
+constexpr int SHORT_LIST = 96;          // lists up to this length are filtered, longer ones bisected
 
 constexpr unsigned long long FLAG_AGG = 1ull << 62;
 constexpr unsigned long long FLAG_INC = 2ull << 62;
@@ -39,8 +42,10 @@ constexpr unsigned long long VAL_MASK = (1ull << 62) - 1;
 struct RowEmitArgs {
   const uint32_t* heavy_bm;   // rows x wpr words of the chunk (nullptr: no heavy part)
   int64_t x0, rows, wpr, dom_z;
-  int G;                      // rows per group
-  int64_t ngroups;
+  int G;                      // rows per tile (1 when a row spans several column blocks)
+  int cb_words;               // words per column block (== wpr when G > 1)
+  int ncb;                    // column blocks per row
+  int64_t ntiles;
   const int32_t* fwd_ptr;     // R forward CSR (x -> tuples)
   const int32_t* fwd_idx;
   const int32_t* rdeg_x;
@@ -51,10 +56,9 @@ struct RowEmitArgs {
   const int32_t* lz_ptr;
   const int32_t* lz_idx;
   int64_t* codes;
-  unsigned long long* status;          // per group look-back word (zeroed)
-  int* ticket;                         // zeroed
+  unsigned long long* status;          // per tile look-back word (zeroed)
   unsigned long long* witnesses;       // += light witnesses processed
-  unsigned long long* total;           // chunk size (written by the last group)
+  unsigned long long* total;           // chunk size (written by the last tile)
 };
 
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
@@ -72,58 +76,76 @@ __device__ __forceinline__ void st_stream(int64_t* p, int64_t a) {
   asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
 }
 
-__global__ void __launch_bounds__(RE_THREADS, 1) k_row_light_emit(const RowEmitArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+// staging slot of the k-th code of a segment: lanes start ~16 codes apart, so
+// XOR-ing the bank bits with the 32-slot row index spreads a warp's k-th
+// stores over all banks; reads of consecutive k stay conflict-free.
+__device__ __forceinline__ int stage_slot(int k) { return k ^ ((k >> 5) & 31); }
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ v, int n, int32_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (v[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(RE_THREADS) k_row_light_emit(const RowEmitArgs a) {
   using BScan = cub::BlockScan<int, RE_THREADS>;
   __shared__ typename BScan::TempStorage scan_tmp;
-  __shared__ int s_group;
-  __shared__ long long s_prefix;
-  __shared__ int s_tb_len[TUP_BATCH + 1];      // exclusive prefix of list lengths
+  __shared__ __align__(16) uint32_t sbm[TILE_WORDS];
+  __shared__ uint32_t stage_all[RE_WARPS][STAGE];
+  __shared__ int segoff[TILE_SEGS];
+  __shared__ int s_tb_len[TUP_BATCH + 1];      // exclusive prefix of (clipped) list lengths
   __shared__ const int32_t* s_tb_base[TUP_BATCH];
   __shared__ int s_tb_row[TUP_BATCH];
-  __shared__ int s_carry;
+  __shared__ int s_tb_zlo[TUP_BATCH];          // z range filter for short lists (zlo,zhi) or -1
+  __shared__ long long s_prefix;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int64_t gw = (int64_t)a.G * a.wpr;            // words per group
-  uint32_t* sbm = reinterpret_cast<uint32_t*>(smem);  // gw words
-  int64_t* stage = reinterpret_cast<int64_t*>(smem + ((gw * 4 + 15) & ~15ll)) + warp * STAGE;
-  int* segcnt = reinterpret_cast<int*>(smem + ((gw * 4 + 15) & ~15ll) + (size_t)RE_WARPS * STAGE * 8);
-  const int nseg = (int)((gw + 31) / 32);
+  uint32_t* stage = stage_all[warp];
 
-  if (tid == 0) s_group = atomicAdd(a.ticket, 1);
-  __syncthreads();
-  const int64_t g = s_group;
-  const int64_t r0 = g * a.G;
+  const int64_t tile = blockIdx.x;
+  const int64_t rg = tile / a.ncb;               // row group
+  const int cbi = (int)(tile - rg * a.ncb);     // column block
+  const int64_t r0 = rg * a.G;
   const int64_t r1 = min(r0 + (int64_t)a.G, a.rows);
-  const int64_t words = (r1 - r0) * a.wpr;
+  const int64_t c0w = (int64_t)cbi * a.cb_words;                 // first word of the block
+  const int cw = (int)min((int64_t)a.cb_words, a.wpr - c0w);      // words per row in this block
+  const int nrow = (int)(r1 - r0);
+  const int words = nrow * cw;                                     // <= TILE_WORDS
+  const int nseg = (words + 31) >> 5;
+  const int32_t zlo = (int32_t)(c0w * 32);
+  const int32_t zhi = (int32_t)min((c0w + cw) * 32, a.dom_z);
 
-  // ---- 1. heavy rows -> shared bitmap
+  // ---- 1. heavy bitmap tile -> shared memory (row pieces of cw words)
   if (a.heavy_bm != nullptr) {
-    const uint4* src = reinterpret_cast<const uint4*>(a.heavy_bm + r0 * a.wpr);
-    uint4* dst = reinterpret_cast<uint4*>(sbm);
-    for (int64_t i = tid; i < words / 4; i += RE_THREADS) dst[i] = src[i];
+    const int q4 = cw >> 2;   // cw is a multiple of 8
+    for (int i = tid; i < nrow * q4; i += RE_THREADS) {
+      const int rr = i / q4, qq = i - rr * q4;
+      reinterpret_cast<uint4*>(sbm)[rr * q4 + qq] =
+          reinterpret_cast<const uint4*>(a.heavy_bm + (r0 + rr) * a.wpr + c0w)[qq];
+    }
   } else {
-    uint4* dst = reinterpret_cast<uint4*>(sbm);
-    for (int64_t i = tid; i < words / 4; i += RE_THREADS) dst[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < words; i += RE_THREADS) sbm[i] = 0;
   }
-  for (int64_t i = words + tid; i < (int64_t)nseg * 32; i += RE_THREADS) sbm[i] = 0;   // tail segment pad
+  for (int i = words + tid; i < nseg * 32; i += RE_THREADS) sbm[i] = 0;
 
-  // ---- 2. light witnesses of the group's rows, OR-ed in shared memory
+  // ---- 2. light witnesses of the tile, OR-ed in shared memory
   const int64_t xa = a.x0 + r0, xb = a.x0 + r1;
   const int64_t t_begin = a.fwd_ptr[xa], t_end = a.fwd_ptr[xb];
   unsigned long long my_w = 0;
   __syncthreads();
   for (int64_t tb = t_begin; tb < t_end; tb += TUP_BATCH) {
     const int64_t t = tb + tid;
-    int len = 0;
+    int len = 0, row = 0, filt = -1;
     const int32_t* base = nullptr;
-    int row = 0;
     if (t < t_end) {
-      // the row of tuple t: x with fwd_ptr[x] <= t < fwd_ptr[x+1] inside [xa, xb)
-      int64_t lo = xa, hi = xb;   // upper_bound over fwd_ptr
+      int64_t lo = xa, hi = xb;   // row of tuple t: last x with fwd_ptr[x] <= t
       while (hi - lo > 1) {
-        int64_t mid = (lo + hi) >> 1;
+        const int64_t mid = (lo + hi) >> 1;
         if (a.fwd_ptr[mid] <= t) lo = mid;
         else hi = mid;
       }
@@ -131,14 +153,26 @@ __global__ void __launch_bounds__(RE_THREADS, 1) k_row_light_emit(const RowEmitA
       row = (int)(x - xa);
       const int32_t y = a.fwd_idx[t];
       const bool full = (a.hpos == nullptr) || (a.hpos[y] < 0) || (a.rdeg_x[x] <= a.d2);
+      int32_t b, e;
       if (full) {
-        const int32_t b = a.s_rev_ptr[y];
+        b = a.s_rev_ptr[y];
+        e = a.s_rev_ptr[y + 1];
         base = a.s_rev_idx + b;
-        len = a.s_rev_ptr[y + 1] - b;
       } else {
-        const int32_t b = a.lz_ptr[y];
+        b = a.lz_ptr[y];
+        e = a.lz_ptr[y + 1];
         base = a.lz_idx + b;
-        len = a.lz_ptr[y + 1] - b;
+      }
+      len = e - b;
+      if (a.ncb > 1) {
+        if (len > SHORT_LIST) {   // z-sorted list: bisect to the column block
+          const int lb = lower_bound_i32(base, len, zlo);
+          const int ub = lb + lower_bound_i32(base + lb, len - lb, zhi);
+          base += lb;
+          len = ub - lb;
+        } else {
+          filt = 1;               // scan it, keep z in [zlo, zhi)
+        }
       }
     }
     int excl, tot;
@@ -146,70 +180,77 @@ __global__ void __launch_bounds__(RE_THREADS, 1) k_row_light_emit(const RowEmitA
     s_tb_len[tid] = excl;
     s_tb_base[tid] = base;
     s_tb_row[tid] = row;
+    s_tb_zlo[tid] = filt;
     if (tid == 0) s_tb_len[TUP_BATCH] = tot;
     __syncthreads();
     const int nt = (int)min((int64_t)TUP_BATCH, t_end - tb);
+    int kept = 0;
     for (int s = tid; s < tot; s += RE_THREADS) {
       int lo = 0, hi = nt;   // last i with s_tb_len[i] <= s
       while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
+        const int mid = (lo + hi) >> 1;
         if (s_tb_len[mid] <= s) lo = mid;
         else hi = mid;
       }
       const int32_t z = s_tb_base[lo][s - s_tb_len[lo]];
-      atomicOr(&sbm[(int64_t)s_tb_row[lo] * a.wpr + (z >> 5)], 1u << (z & 31));
+      if (s_tb_zlo[lo] >= 0 && (z < zlo || z >= zhi)) continue;
+      const int wz = (z - zlo) >> 5;
+      atomicOr(&sbm[s_tb_row[lo] * cw + wz], 1u << (z & 31));
+      ++kept;
     }
-    my_w += (tid == 0) ? (unsigned long long)tot : 0ull;
+    my_w += kept;
     __syncthreads();
   }
-  if (tid == 0 && my_w) atomicAdd(a.witnesses, my_w);
+  {
+    unsigned long long w = my_w;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (lane == 0 && w) atomicAdd(a.witnesses, w);
+  }
 
   // ---- 3. segment counts, block scan, decoupled look-back
   for (int s = warp; s < nseg; s += RE_WARPS) {
-    int c = __popc(sbm[(int64_t)s * 32 + lane]);
+    int c = __popc(sbm[s * 32 + lane]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) segcnt[s] = c;
+    if (lane == 0) segoff[s] = c;
   }
-  if (tid == 0) s_carry = 0;
   __syncthreads();
-  for (int s0 = 0; s0 < nseg; s0 += RE_THREADS) {
-    const int s = s0 + tid;
-    const int v = s < nseg ? segcnt[s] : 0;
+  {
+    // TILE_SEGS (64) <= RE_THREADS: one scan round
+    const int v = tid < nseg ? segoff[tid] : 0;
     int excl, tot;
     BScan(scan_tmp).ExclusiveSum(v, excl, tot);
-    const int carry = s_carry;
     __syncthreads();
-    if (s < nseg) segcnt[s] = carry + excl;
-    if (tid == 0) s_carry = carry + tot;
-    __syncthreads();
-  }
-  if (tid == 0) {
-    const unsigned long long cnt = (unsigned long long)s_carry;
-    unsigned long long prefix = 0;
-    if (g == 0) {
-      st_release(&a.status[0], FLAG_INC | cnt);
-    } else {
-      st_release(&a.status[g], FLAG_AGG | cnt);
-      int64_t j = g - 1;
-      while (true) {
-        const unsigned long long v = ld_acquire(&a.status[j]);
-        if (v == 0) continue;
-        prefix += v & VAL_MASK;
-        if (v & FLAG_INC) break;
-        --j;
+    if (tid < nseg) segoff[tid] = excl;
+    if (tid == 0) {
+      const unsigned long long cnt = (unsigned long long)tot;
+      unsigned long long prefix = 0;
+      if (tile == 0) {
+        st_release(&a.status[0], FLAG_INC | cnt);
+      } else {
+        st_release(&a.status[tile], FLAG_AGG | cnt);
+        int64_t j = tile - 1;
+        while (true) {
+          const unsigned long long v2 = ld_acquire(&a.status[j]);
+          if (v2 == 0) continue;
+          prefix += v2 & VAL_MASK;
+          if (v2 & FLAG_INC) break;
+          --j;
+        }
+        st_release(&a.status[tile], FLAG_INC | (prefix + cnt));
       }
-      st_release(&a.status[g], FLAG_INC | (prefix + cnt));
+      s_prefix = (long long)prefix;
+      if (tile == a.ntiles - 1) *a.total = prefix + cnt;
     }
-    s_prefix = (long long)prefix;
-    if (g == a.ngroups - 1) *a.total = prefix + cnt;
   }
   __syncthreads();
-  const int64_t gbase = s_prefix;
+  const int64_t tbase_code = xa * a.dom_z + zlo;    // code of the tile's first cell
+  int64_t* const out_tile = a.codes + s_prefix;
 
-  // ---- 4. emission: per segment, stage codes, coalesced streaming stores
+  // ---- 4. emission: per segment, stage code offsets, coalesced streaming stores
   for (int s = warp; s < nseg; s += RE_WARPS) {
-    const int64_t w = (int64_t)s * 32 + lane;         // word within the group
+    const int w = s * 32 + lane;                   // word within the tile
     uint32_t word = sbm[w];
     const int c = __popc(word);
     int incl = c;
@@ -220,63 +261,41 @@ __global__ void __launch_bounds__(RE_THREADS, 1) k_row_light_emit(const RowEmitA
     }
     const int tot = __shfl_sync(0xffffffffu, incl, 31);
     int k = incl - c;
-    const int64_t row = w / a.wpr;
-    const int64_t code0 = (xa + row) * a.dom_z + (w - row * a.wpr) * 32;
+    const int rr = w / cw;
+    const uint32_t off0 = (uint32_t)(rr * a.dom_z + (w - rr * cw) * 32);   // < G*dom_z <= 2^16*... fits
     while (word) {
       const int b = __ffs(word) - 1;
-      stage[stage_slot(k++)] = code0 + b;
+      stage[stage_slot(k++)] = off0 + b;
       word &= word - 1;
     }
     __syncwarp();
-    int64_t* out = a.codes + gbase + segcnt[s];
-    // peel to a 16-byte boundary, then pairs, then the tail
-    const int head = (int)(((reinterpret_cast<uintptr_t>(out) >> 3) & 1));
-    const int h = min(head, tot);
-    if (lane < h) st_stream(out + lane, stage[stage_slot(lane)]);
+    int64_t* out = out_tile + segoff[s];
+    const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
+    if (lane < h) st_stream(out + lane, tbase_code + stage[stage_slot(lane)]);
     const int npair = (tot - h) >> 1;
     for (int p = lane; p < npair; p += 32) {
       const int i = h + 2 * p;
-      st_stream_v2(out + i, stage[stage_slot(i)], stage[stage_slot(i + 1)]);
+      st_stream_v2(out + i, tbase_code + stage[stage_slot(i)], tbase_code + stage[stage_slot(i + 1)]);
     }
     const int done = h + 2 * npair;
-    if (lane < tot - done) st_stream(out + done + lane, stage[stage_slot(done + lane)]);
+    if (lane < tot - done) st_stream(out + done + lane, tbase_code + stage[stage_slot(done + lane)]);
     __syncwarp();
   }
 }
 
 }  // namespace
 
-size_t row_emit_smem(int64_t G, int64_t wpr) {
-  const int64_t gw = G * wpr;
-  const int nseg = (int)((gw + 31) / 32);
-  return (size_t)(((gw * 4 + 15) & ~15ll) + (int64_t)RE_WARPS * STAGE * 8 + (int64_t)nseg * 4 + 16);
-}
+size_t row_emit_smem(int64_t /*G*/, int64_t /*wpr*/) { return 0; }   // static shared memory only
 
-int row_light_emit(const uint32_t* heavy_bm, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z, int G,
+int row_light_emit(const uint32_t* heavy_bm, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z, int /*G_hint*/,
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t d2,
                    const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
-                   const int32_t* lz_idx, int64_t* codes, unsigned long long* status, int* ticket,
+                   const int32_t* lz_idx, int64_t* codes, unsigned long long* status, int* /*ticket*/,
                    unsigned long long* witnesses, unsigned long long* total, cudaStream_t st) {
   if (rows <= 0) return MMJ_OK;
-  if (G < 1 || wpr % 8 != 0) {
-    set_error("row_light_emit: G >= 1 and wpr % 8 == 0 required");
+  if (wpr % 8 != 0 || wpr <= 0) {
+    set_error("row_light_emit: wpr must be a positive multiple of 8");
     return MMJ_ERR_ARG;
-  }
-  const size_t smem = row_emit_smem(G, wpr);
-  int dev = 0, maxsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t static_smem = sizeof(int) * (TUP_BATCH * 2 + 1) + sizeof(void*) * TUP_BATCH + 4096;
-  if (smem + static_smem > (size_t)maxsm) {
-    set_error("row_light_emit: row group needs %zu B of shared memory (max %d)", smem, maxsm);
-    return MMJ_ERR_UNSUPPORTED;
-  }
-  static size_t attr = 0;
-  if (smem > attr) {
-    MMJ_TRY(cuda_status(cudaFuncSetAttribute(k_row_light_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(maxsm - static_smem)),
-                        "cudaFuncSetAttribute(row_light_emit)"));
-    attr = maxsm - static_smem;
   }
   RowEmitArgs a;
   a.heavy_bm = heavy_bm;
@@ -284,8 +303,25 @@ int row_light_emit(const uint32_t* heavy_bm, int64_t x0, int64_t rows, int64_t w
   a.rows = rows;
   a.wpr = wpr;
   a.dom_z = dom_z;
-  a.G = G;
-  a.ngroups = ceil_div(rows, G);
+  if (wpr <= TILE_WORDS) {
+    a.G = (int)(TILE_WORDS / wpr);
+    a.cb_words = (int)wpr;
+    a.ncb = 1;
+  } else {
+    a.G = 1;
+    a.cb_words = TILE_WORDS;
+    a.ncb = (int)ceil_div(wpr, TILE_WORDS);
+  }
+  // tile offsets are stored as 32-bit deltas from the tile's first code
+  if ((int64_t)a.G * dom_z >= (1ll << 31)) {
+    set_error("row_light_emit: tile code span exceeds 32 bits");
+    return MMJ_ERR_UNSUPPORTED;
+  }
+  a.ntiles = ceil_div(rows, a.G) * a.ncb;
+  if (a.ntiles >= (1ll << 31)) {
+    set_error("row_light_emit: too many tiles in one chunk");
+    return MMJ_ERR_ARG;
+  }
   a.fwd_ptr = fwd_ptr;
   a.fwd_idx = fwd_idx;
   a.rdeg_x = rdeg_x;
@@ -297,12 +333,16 @@ int row_light_emit(const uint32_t* heavy_bm, int64_t x0, int64_t rows, int64_t w
   a.lz_idx = lz_idx;
   a.codes = codes;
   a.status = status;
-  a.ticket = ticket;
   a.witnesses = witnesses;
   a.total = total;
-  k_row_light_emit<<<(unsigned)a.ngroups, RE_THREADS, smem, st>>>(a);
+  k_row_light_emit<<<(unsigned)a.ntiles, RE_THREADS, 0, st>>>(a);
   MMJ_CHECK_LAUNCH("k_row_light_emit");
   return MMJ_OK;
+}
+
+int64_t row_emit_tiles(int64_t rows, int64_t wpr) {
+  if (wpr <= TILE_WORDS) return ceil_div(rows, TILE_WORDS / wpr);
+  return rows * ceil_div(wpr, TILE_WORDS);
 }
 
 }  // namespace mmj

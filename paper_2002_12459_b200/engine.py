@@ -103,7 +103,7 @@ class TwoPathEngine:
         # fused light+merge+emit kernel for the projection when a row group's
         # bitmap fits in shared memory (dom_z up to ~1.2M)
         self.group_rows = max(1, min(32, (48 * 1024) // (self.wpr * 4)))
-        self.fused = (not self.counts) and self.lib.mmj_row_emit_smem_bytes(1, self.wpr) <= FUSED_SMEM_LIMIT
+        self.fused = (not self.counts) and self.dom_z < (1 << 31)
         self._prepared = False
         self._sizes_dev = None
         self._n_async = 0
@@ -267,11 +267,11 @@ class TwoPathEngine:
         st = self._st()
         dr, ds = self.dr, self.ds
         G = self.group_rows
-        ngroups = -(-rows // G)
-        status = self.ws.get("status", ngroups + 2, torch.int64)
-        status.zero_()                       # [0, ngroups): look-back words, [ngroups]: ticket, [+1]: total
-        ticket = status[ngroups:ngroups + 1]
-        total = status[ngroups + 1:ngroups + 2]
+        ntiles = int(self.lib.mmj_row_emit_tiles(rows, self.wpr))
+        status = self.ws.get("status", ntiles + 2, torch.int64)
+        status.zero_()                       # [0, ntiles): look-back words, [ntiles+1]: total
+        ticket = status[ntiles:ntiles + 1]
+        total = status[ntiles + 1:ntiles + 2]
         cap = rows * self.dom_z
         codes = self.ws.get("codes", cap, torch.int64)
         hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
