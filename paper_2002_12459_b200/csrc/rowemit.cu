@@ -76,10 +76,11 @@ __device__ __forceinline__ void st_stream(int64_t* p, int64_t a) {
   asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
 }
 
-// staging slot of the k-th code of a segment: lanes start ~16 codes apart, so
-// XOR-ing the bank bits with the 32-slot row index spreads a warp's k-th
-// stores over all banks; reads of consecutive k stay conflict-free.
-__device__ __forceinline__ int stage_slot(int k) { return k ^ ((k >> 5) & 31); }
+// staging slot of the k-th code of a segment.  Lanes start their runs at
+// unrelated offsets; XOR-ing bits [2,5) with bits [5,8) spreads a warp's
+// stores over the banks while keeping each aligned quad (k & ~3) contiguous
+// and in order, so the reader can fetch four codes with one LDS.128.
+__device__ __forceinline__ int stage_slot(int k) { return k ^ ((k >> 3) & 0x1C); }
 
 __device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ v, int n, int32_t key) {
   int lo = 0, hi = n;
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(RE_THREADS) k_row_light_emit(const RowEmitArgs
   using BScan = cub::BlockScan<int, RE_THREADS>;
   __shared__ typename BScan::TempStorage scan_tmp;
   __shared__ __align__(16) uint32_t sbm[TILE_WORDS];
-  __shared__ uint32_t stage_all[RE_WARPS][STAGE];
+  __shared__ __align__(16) uint32_t stage_all[RE_WARPS][STAGE + 4];
   __shared__ int segoff[TILE_SEGS];
   __shared__ int s_tb_len[TUP_BATCH + 1];      // exclusive prefix of (clipped) list lengths
   __shared__ const int32_t* s_tb_base[TUP_BATCH];
@@ -260,25 +261,32 @@ __global__ void __launch_bounds__(RE_THREADS) k_row_light_emit(const RowEmitArgs
       if (lane >= o) incl += v;
     }
     const int tot = __shfl_sync(0xffffffffu, incl, 31);
-    int k = incl - c;
     const int rr = w / cw;
-    const uint32_t off0 = (uint32_t)(rr * a.dom_z + (w - rr * cw) * 32);   // < G*dom_z <= 2^16*... fits
+    const uint32_t off0 = (uint32_t)(rr * a.dom_z + (w - rr * cw) * 32);   // G*dom_z < 2^31 (checked)
+    int64_t* out = out_tile + segoff[s];
+    // stage index of code i is i + h with h = (out / 8) % 2, so that stage
+    // quads [4q, 4q+4) map to 16-byte aligned output slots out + 4q - h
+    const int h = (int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1);
+    // MSB-first: FLO gives the bit, the lane's run is filled from its end
+    int k = incl - 1 + h;
     while (word) {
-      const int b = __ffs(word) - 1;
-      stage[stage_slot(k++)] = off0 + b;
-      word &= word - 1;
+      const int b = 31 - __clz(word);
+      stage[stage_slot(k)] = off0 + (uint32_t)b;
+      --k;
+      word ^= 1u << b;
     }
     __syncwarp();
-    int64_t* out = out_tile + segoff[s];
-    const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
-    if (lane < h) st_stream(out + lane, tbase_code + stage[stage_slot(lane)]);
-    const int npair = (tot - h) >> 1;
-    for (int p = lane; p < npair; p += 32) {
-      const int i = h + 2 * p;
-      st_stream_v2(out + i, tbase_code + stage[stage_slot(i)], tbase_code + stage[stage_slot(i + 1)]);
+    const int endk = tot + h;                       // staged indices [h, endk)
+    if (lane >= h && lane < 4 && lane < endk) st_stream(out + lane - h, tbase_code + stage[stage_slot(lane)]);
+    const int nq = endk >> 2;
+    for (int q = 1 + lane; q < nq; q += 32) {
+      const uint4 v = *reinterpret_cast<const uint4*>(&stage[stage_slot(4 * q)]);
+      int64_t* o = out + 4 * q - h;
+      st_stream_v2(o, tbase_code + v.x, tbase_code + v.y);
+      st_stream_v2(o + 2, tbase_code + v.z, tbase_code + v.w);
     }
-    const int done = h + 2 * npair;
-    if (lane < tot - done) st_stream(out + done + lane, tbase_code + stage[stage_slot(done + lane)]);
+    const int tail = max(4, nq << 2);
+    if (tail + lane < endk) st_stream(out + tail + lane - h, tbase_code + stage[stage_slot(tail + lane)]);
     __syncwarp();
   }
 }
