@@ -345,7 +345,7 @@ def run_b200(args):
                         padded_ops=2.0 * (x_hi - x_lo) * stats.kpad * s.rel.dom_left)
             if int8_peak:
                 info.update(peak_measured_cublaslt=int8_peak / 1e12, frac_measured=ops / int8_peak)
-        if name == "light" and t > 0:
+        if name in ("light", "light_merge") and t > 0:
             info.update(witnesses=stats.light_intermediate, witness_rate=stats.light_intermediate / t)
         phase_info[name] = info
     dominant = max(phases, key=lambda k: phases[k]) if phases else "emit"
@@ -360,7 +360,8 @@ def run_b200(args):
                     "unit": "TOPS", "frac": dom.get("frac_datasheet"), "traffic": traffic,
                     "kernel": "heavy_mma_kernel", "peak_kind": "datasheet int8 dense"}
     else:
-        kern = {"emit": "k_bitmap_emit", "light": "k_light_expand", "segments": "k_seg_popc"}.get(dominant)
+        kern = {"emit": "k_emit", "light": "k_light_expand", "light_merge": "k_tile_merge",
+                "segments": "tile_scan"}.get(dominant)
         ach = dom.get("achieved")
         roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                     "frac": (ach / hbm) if ach else None, "traffic": traffic, "kernel": kern,

@@ -111,25 +111,24 @@ int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_
 int mmj_digit_plane(const int64_t* src, int64_t rows, int64_t cols, int transpose, int digit, uint8_t* dst,
                     int64_t kpad, void* stream);
 
-/* ---- fused light passes + merge + emission (projection, no counts):
- *      joinproject.py:183-203 + 220-225 ---------------------------------------
- * The chunk's output bitmap [x0, x0+rows) x [0, dom_z) is cut into
- * mmj_row_emit_tiles(rows, wpr) tiles of <= 65536 cells (whole rows when
- * dom_z is small, else one row and a column block), one CTA each: the heavy
- * bitmap tile (heavy_bm, rows x wpr words; NULL = no heavy part) is copied to
- * shared memory, every light witness of the tile is OR-ed in (shared-memory
- * atomics), and the tile's sorted codes are written at an offset found by a
- * decoupled look-back over `status` (ntiles uint64, zeroed).  `codes` must
- * hold rows*dom_z entries (worst case); *total receives the chunk size and
- * *witnesses accumulates the light intermediate size.  rows_per_group and
- * ticket are unused (ABI placeholders). */
-size_t mmj_row_emit_smem_bytes(int64_t rows_per_group, int64_t wpr);
-int64_t mmj_row_emit_tiles(int64_t rows, int64_t wpr);
-int mmj_row_light_emit(const uint32_t* heavy_bm, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
-                       int rows_per_group, const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x,
-                       int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx,
-                       const int32_t* lz_ptr, const int32_t* lz_idx, int64_t* codes, unsigned long long* status,
-                       int* ticket, unsigned long long* witnesses, unsigned long long* total, void* stream);
+/* ---- light passes merged into the bitmap + emission (projection, no
+ *      counts): joinproject.py:183-203 + 220-225 ------------------------------
+ * Chunk bitmap [x0, x0+rows) x [0, dom_z): rows x wpr words, wpr a multiple
+ * of 32 (rows start on 1024-cell segments).  mmj_tile_merge runs one CTA per
+ * tile (mmj_tile_count(rows, wpr) tiles of <= 65536 cells): the heavy bits
+ * (has_heavy) or zeros are staged in shared memory, every light witness of
+ * the tile is OR-ed in (shared-memory atomics), the merged tile is written
+ * back and segcnt[rows*wpr/32] receives each 32-word segment's popcount;
+ * *witnesses accumulates the light intermediate size.  After an exclusive
+ * scan of segcnt (mmj_exclusive_scan_i32 -> seg_off), mmj_emit_codes writes
+ * the chunk's sorted codes x*dom_z + z to codes[0 .. seg_off[nseg]). */
+int64_t mmj_tile_count(int64_t rows, int64_t wpr);
+int mmj_tile_merge(uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
+                   const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
+                   const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
+                   const int32_t* lz_idx, int32_t* segcnt, unsigned long long* witnesses, void* stream);
+int mmj_emit_codes(const uint32_t* bitmap, const int64_t* seg_off, int64_t rows, int64_t wpr, int64_t x0,
+                   int64_t dom_z, int64_t* codes, void* stream);
 
 /* ---- merge / emission: joinproject.py:220-225 -------------------------------
  * Bitmap chunk of nwords words (wpr words per row, row r <-> x = x0 + r):

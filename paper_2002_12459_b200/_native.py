@@ -45,9 +45,9 @@ _SIGS = {
     "mmj_light_expand": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P, I64, INT, I64, P, I64, P]),
     "mmj_heavy_mma": (INT, [P, I64, P, I64, I64, I64, I64, I64, I64, INT, INT, P, I64, P, INT, P]),
     "mmj_digit_plane": (INT, [P, I64, I64, INT, INT, P, I64, P]),
-    "mmj_row_emit_smem_bytes": (C.c_size_t, [I64, I64]),
-    "mmj_row_emit_tiles": (I64, [I64, I64]),
-    "mmj_row_light_emit": (INT, [P, I64, I64, I64, I64, INT, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P]),
+    "mmj_tile_count": (I64, [I64, I64]),
+    "mmj_tile_merge": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P]),
+    "mmj_emit_codes": (INT, [P, P, I64, I64, I64, I64, P, P]),
     "mmj_bitmap_segment_count": (I64, [I64]),
     "mmj_bitmap_segments": (INT, [P, I64, P, P, P, P]),
     "mmj_bitmap_emit": (INT, [P, I64, I64, P, I64, I64, P, P]),

@@ -24,12 +24,11 @@ int count_segments(const int32_t*, int64_t, int64_t, int64_t, int64_t, int32_t, 
                    cudaStream_t);
 int count_emit(const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t, int, const int64_t*, int64_t*,
                int32_t*, cudaStream_t);
-size_t row_emit_smem(int64_t, int64_t);
 int64_t row_emit_tiles(int64_t, int64_t);
-int row_light_emit(const uint32_t*, int64_t, int64_t, int64_t, int64_t, int, const int32_t*, const int32_t*,
-                   const int32_t*, int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*,
-                   const int32_t*, int64_t*, unsigned long long*, int*, unsigned long long*, unsigned long long*,
-                   cudaStream_t);
+int tile_merge(uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t*, const int32_t*, const int32_t*,
+               int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int32_t*,
+               unsigned long long*, cudaStream_t);
+int emit_codes(const uint32_t*, const int64_t*, int64_t, int64_t, int64_t, int64_t, int64_t*, cudaStream_t);
 namespace mma {
 int launch_heavy_mma(const uint8_t*, int64_t, const uint8_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                      int, int, void*, int64_t, unsigned long long*, int, cudaStream_t);
@@ -139,20 +138,19 @@ int mmj_digit_plane(const int64_t* src, int64_t rows, int64_t cols, int transpos
   return MMJ_OK;
 }
 
-size_t mmj_row_emit_smem_bytes(int64_t rows_per_group, int64_t wpr) {
-  return mmj::row_emit_smem(rows_per_group, wpr);
+int64_t mmj_tile_count(int64_t rows, int64_t wpr) { return mmj::row_emit_tiles(rows, wpr); }
+
+int mmj_tile_merge(uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
+                   const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
+                   const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
+                   const int32_t* lz_idx, int32_t* segcnt, unsigned long long* witnesses, void* stream) {
+  return mmj::tile_merge(bitmap, has_heavy, x0, rows, wpr, dom_z, fwd_ptr, fwd_idx, rdeg_x, delta2, hpos, s_rev_ptr,
+                         s_rev_idx, lz_ptr, lz_idx, segcnt, witnesses, ST(stream));
 }
 
-int64_t mmj_row_emit_tiles(int64_t rows, int64_t wpr) { return mmj::row_emit_tiles(rows, wpr); }
-
-int mmj_row_light_emit(const uint32_t* heavy_bm, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
-                       int rows_per_group, const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x,
-                       int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx,
-                       const int32_t* lz_ptr, const int32_t* lz_idx, int64_t* codes, unsigned long long* status,
-                       int* ticket, unsigned long long* witnesses, unsigned long long* total, void* stream) {
-  return mmj::row_light_emit(heavy_bm, x0, rows, wpr, dom_z, rows_per_group, fwd_ptr, fwd_idx, rdeg_x, delta2, hpos,
-                             s_rev_ptr, s_rev_idx, lz_ptr, lz_idx, codes, status, ticket, witnesses, total,
-                             ST(stream));
+int mmj_emit_codes(const uint32_t* bitmap, const int64_t* seg_off, int64_t rows, int64_t wpr, int64_t x0,
+                   int64_t dom_z, int64_t* codes, void* stream) {
+  return mmj::emit_codes(bitmap, seg_off, rows, wpr, x0, dom_z, codes, ST(stream));
 }
 
 int64_t mmj_bitmap_segment_count(int64_t nwords) { return mmj::bitmap_nseg(nwords); }

@@ -81,7 +81,7 @@ class TwoPathEngine:
         self.min_count = int(min_count)
         self.upper_only = bool(upper_only)
         self.dom_x, self.dom_z, self.dom_y = dr.dom_left, ds.dom_left, dr.dom_right
-        self.wpr = _rup(max(self.dom_z, 1), BN) // 32
+        self.wpr = _rup(max(self.dom_z, 1), 1024) // 32     # rows start on 1024-cell segments
         self.ldc = _rup(max(self.dom_z, 1), BN)
         self.ws = ws or Workspace()
         self.stats = EngineStats()
@@ -263,36 +263,45 @@ class TwoPathEngine:
         return ChunkResult(x0, x1, total, codes[:total], None if counts is None else counts[:total], light)
 
     def _fused_tail(self, x0, x1, rows, buf, sync):
+        """Light witnesses merged into the bitmap tile by tile, segment scan,
+        emission (mmj_tile_merge -> mmj_exclusive_scan_i32 -> mmj_emit_codes)."""
         torch = self.torch
         st = self._st()
         dr, ds = self.dr, self.ds
-        G = self.group_rows
-        ntiles = int(self.lib.mmj_row_emit_tiles(rows, self.wpr))
-        status = self.ws.get("status", ntiles + 2, torch.int64)
-        status.zero_()                       # [0, ntiles): look-back words, [ntiles+1]: total
-        ticket = status[ntiles:ntiles + 1]
-        total = status[ntiles + 1:ntiles + 2]
-        cap = rows * self.dom_z
-        codes = self.ws.get("codes", cap, torch.int64)
+        nseg = rows * self.wpr // 32
+        segcnt = self.ws.get("segcnt", nseg, torch.int32)
+        segoff = self.ws.get("segoff", nseg + 1, torch.int64)
         hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
         lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
         lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
-        heavy = nat.ptr(buf) if self.A is not None else 0
         wit0 = int(self.wit.item()) if sync else 0
-        self._ph("light_emit", True)
-        nat.call("mmj_row_light_emit", heavy, x0, rows, self.wpr, self.dom_z, G, nat.ptr(dr.fwd_ptr),
-                 nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx),
-                 lzp, lzi, nat.ptr(codes), nat.ptr(status), nat.ptr(ticket), nat.ptr(self.wit), nat.ptr(total), st)
-        self._ph("light_emit", False)
+        self._ph("light_merge", True)
+        nat.call("mmj_tile_merge", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
+                 nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp, nat.ptr(ds.rev_ptr),
+                 nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(self.wit), st)
+        self._ph("light_merge", False)
+        self._ph("segments", True)
+        nat.call("mmj_exclusive_scan_i32", nat.ptr(segcnt), nat.ptr(segoff), nseg, nat.ptr(self.ws.scan_ws(nseg)), st)
+        self._ph("segments", False)
+        if sync:
+            total = int(segoff[nseg].item())
+            cap = total
+        else:
+            cap = rows * self.dom_z
+        codes = self.ws.get("codes", cap, torch.int64)
+        self._ph("emit", True)
+        if cap:
+            nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dom_z,
+                     nat.ptr(codes), st)
+        self._ph("emit", False)
         self.stats.chunks += 1
         if not sync:
             slot = self._async_slot()
-            slot[0:1].copy_(total, non_blocking=True)
+            slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
             return ChunkResult(x0, x1, -1, codes, None, -1)
-        n = int(total.item())
         light = int(self.wit.item()) - wit0
-        self.stats.out_size += n
-        return ChunkResult(x0, x1, n, codes[:n], None, light)
+        self.stats.out_size += total
+        return ChunkResult(x0, x1, total, codes[:total], None, light)
 
     def _async_slot(self):
         """Device slot (2 x int64) receiving one async chunk's (size, light)."""
