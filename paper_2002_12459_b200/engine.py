@@ -82,7 +82,7 @@ class TwoPathEngine:
         self.upper_only = bool(upper_only)
         self.dom_x, self.dom_z, self.dom_y = dr.dom_left, ds.dom_left, dr.dom_right
         self.wpr = _rup(max(self.dom_z, 1), 1024) // 32     # rows start on 1024-cell segments
-        self.ldc = _rup(max(self.dom_z, 1), BN)
+        self.ldc = _rup(max(self.dom_z, 1), 1024)
         self.ws = ws or Workspace()
         self.stats = EngineStats()
         self.hpos = None
@@ -136,7 +136,7 @@ class TwoPathEngine:
                 kpad = _rup(k, BK)
                 self.kpad = kpad
                 arows = _rup(max(self.dom_x, 1), BN)
-                brows = _rup(max(self.dom_z, 1), BN)
+                brows = _rup(max(self.dom_z, 1), 1024)   # product covers every word of the padded rows
                 self.A = torch.empty((arows, kpad), dtype=torch.uint8, device="cuda")
                 self.B = torch.empty((brows, kpad), dtype=torch.uint8, device="cuda")
                 nat.call("mmj_build_operand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n, nat.ptr(dr.left_deg),
