@@ -18,8 +18,10 @@
 //       ACC64  : out[i][j] += count << shift  (int64 digit recombination for
 //                the generic multiply_counts backend).
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w3 idle, w4..w7 epilogue (warp w%4 owns TMEM lanes 32*(w%4) .. +31).
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w3 idle, w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4) .. +31 and the
+// 128-column half (w-4)/4 of the accumulator; the four 32-column loads of a
+// half are all in flight before one tcgen05.wait::ld).
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -39,7 +41,8 @@ constexpr int B_BYTES = BN * BK;        // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int ACC_STAGES = 2;
 constexpr int TMEM_COLS = 512;          // 2 x 256 s32 accumulator columns
-constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARPS = 8;            // two warps per TMEM lane quadrant, one per 128-column half
+constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < ACC_STAGES; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -261,6 +264,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------- epilogue
     const int q = warp & 3;              // TMEM lane quadrant
+    const int half = (warp - 4) >> 2;    // 128-column half of the 256-column tile
     int acc = 0;
     uint32_t acc_ph = 0;
     unsigned long long my_nnz = 0;
@@ -270,34 +274,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int64_t row = (int64_t)c.m_blk * BM + q * 32 + lane;   // local output row
       const bool row_ok = row < p.m_rows;
-      const int64_t col0 = (int64_t)c.n_blk * BN;
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const int64_t col0 = (int64_t)c.n_blk * BN + half * 128;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * 128;
       if (p.mode == BITMAP) {
-        uint32_t w[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint32_t r[32];
-          TMEM_LD_32x32b_X32(taddr + j * 32, r);
-          tmem_wait_ld();
-          uint32_t bits = 0;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) bits |= (r[i] != 0u ? 1u : 0u) << i;
-          w[j] = bits;
-        }
+        uint32_t r0[32], r1[32], r2[32], r3[32];
+        TMEM_LD_32x32b_X32(taddr, r0);
+        TMEM_LD_32x32b_X32(taddr + 32, r1);
+        TMEM_LD_32x32b_X32(taddr + 64, r2);
+        TMEM_LD_32x32b_X32(taddr + 96, r3);
+        tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
+        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          w0 |= (r0[i] != 0u ? 1u : 0u) << i;
+          w1 |= (r1[i] != 0u ? 1u : 0u) << i;
+          w2 |= (r2[i] != 0u ? 1u : 0u) << i;
+          w3 |= (r3[i] != 0u ? 1u : 0u) << i;
+        }
         if (row_ok) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + (col0 >> 5);
-          reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) my_nnz += __popc(w[j]);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
+          my_nnz += __popc(w0) + __popc(w1) + __popc(w2) + __popc(w3);
         }
       } else if (p.mode == COUNT32) {
         int32_t* dst = reinterpret_cast<int32_t*>(p.out) + row * p.ld_out + col0;
 #pragma unroll 1
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 4; ++j) {
           uint32_t r[32];
           TMEM_LD_32x32b_X32(taddr + j * 32, r);
           tmem_wait_ld();
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {  // ACC64
         int64_t* dst = reinterpret_cast<int64_t*>(p.out) + row * p.ld_out + col0;
 #pragma unroll 1
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 4; ++j) {
           uint32_t r[32];
           TMEM_LD_32x32b_X32(taddr + j * 32, r);
           tmem_wait_ld();
