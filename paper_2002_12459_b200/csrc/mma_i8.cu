@@ -145,6 +145,20 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(int m, int n) {
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])            \
       : "r"(taddr))
 
+// 32 lanes x 64 columns, adjacent column pairs packed into one register as
+// two 16-bit halves (low half = even column).  The accumulators are exact
+// counts < 2^16 here (K windows <= 32768 with 0/1 operands in BITMAP mode).
+#define TMEM_LD_32x32b_X32_PACK16(taddr, r)                                                     \
+  asm volatile(                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"  \
+      "%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];" \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),     \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),           \
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),           \
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])            \
+      : "r"(taddr))
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -277,22 +291,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int64_t col0 = (int64_t)c.n_blk * BN + half * 128;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * 128;
       if (p.mode == BITMAP) {
-        uint32_t r0[32], r1[32], r2[32], r3[32];
-        TMEM_LD_32x32b_X32(taddr, r0);
-        TMEM_LD_32x32b_X32(taddr + 32, r1);
-        TMEM_LD_32x32b_X32(taddr + 64, r2);
-        TMEM_LD_32x32b_X32(taddr + 96, r3);
+        uint32_t r0[32], r1[32];
+        TMEM_LD_32x32b_X32_PACK16(taddr, r0);        // columns [0, 64) of the half
+        TMEM_LD_32x32b_X32_PACK16(taddr + 64, r1);   // columns [64, 128)
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
         uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          w0 |= (r0[i] != 0u ? 1u : 0u) << i;
-          w1 |= (r1[i] != 0u ? 1u : 0u) << i;
-          w2 |= (r2[i] != 0u ? 1u : 0u) << i;
-          w3 |= (r3[i] != 0u ? 1u : 0u) << i;
+        for (int i = 0; i < 16; ++i) {
+          w0 |= ((r0[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+          w0 |= ((r0[i] >> 16) ? 1u : 0u) << (2 * i + 1);
+          w1 |= ((r0[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+          w1 |= ((r0[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
+          w2 |= ((r1[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+          w2 |= ((r1[i] >> 16) ? 1u : 0u) << (2 * i + 1);
+          w3 |= ((r1[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+          w3 |= ((r1[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
         }
         if (row_ok) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + (col0 >> 5);
@@ -419,6 +435,10 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   }
   if (mode == COUNT32 && ld_out % 4 != 0) {
     set_error("heavy_mma: count pitch must be a multiple of 4");
+    return MMJ_ERR_ARG;
+  }
+  if (mode == BITMAP && k_len > 65535) {
+    set_error("heavy_mma: BITMAP mode packs 16-bit counts; K window must be < 65536");
     return MMJ_ERR_ARG;
   }
   if (m_rows == 0 || b_rows == 0) return MMJ_OK;
