@@ -5,9 +5,10 @@
 // The chunk's output space (rows x dom_z cells, bitmap rows padded to whole
 // 1024-bit segments) is processed in two kernels:
 //
-//   k_tile_merge  one CTA per tile of <= 65536 cells (several whole rows when
-//                 dom_z is small, otherwise one row and a 2048-word column
-//                 block): the heavy product's bitmap tile is staged in shared
+//   k_tile_merge  one CTA per tile of <= 2^19 cells (whole rows up to 64 KB
+//                 of bitmap, several when dom_z is small, otherwise one row and
+//                 a 16384-word column block): the heavy product's bitmap tile
+//                 is staged in shared
 //                 memory, every light witness (x, z) of the tile -- R tuples
 //                 of its rows, each expanding its z-sorted S-side list (so a
 //                 column block is a contiguous slice) exactly as the
@@ -32,7 +33,7 @@ namespace {
 
 constexpr int TM_THREADS = 256;
 constexpr int TUP_BATCH = TM_THREADS;   // light tuples staged per round
-constexpr int TILE_WORDS = 2048;        // 8 KB of bitmap per tile (65536 cells)
+constexpr int TILE_WORDS = 16384;       // up to 64 KB of bitmap per tile (whole rows up to 524288 cells)
 constexpr int SHORT_LIST = 96;          // lists up to this length are filtered, longer ones bisected
 constexpr int EM_WARPS = 8;
 constexpr int EM_SEGS = 64;             // segments per emission CTA
@@ -75,7 +76,7 @@ struct TileArgs {
 __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   using BScan = cub::BlockScan<int, TM_THREADS>;
   __shared__ typename BScan::TempStorage scan_tmp;
-  __shared__ __align__(16) uint32_t sbm[TILE_WORDS];
+  extern __shared__ __align__(16) uint32_t sbm[];     // tile words (dynamic)
   __shared__ int s_tb_len[TUP_BATCH + 1];
   __shared__ const int32_t* s_tb_base[TUP_BATCH];
   __shared__ int s_tb_row[TUP_BATCH];
@@ -303,7 +304,15 @@ int tile_merge(uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int64_t wp
   a.lz_idx = lz_idx;
   a.segcnt = segcnt;
   a.witnesses = witnesses;
-  k_tile_merge<<<(unsigned)ntiles, TM_THREADS, 0, st>>>(a);
+  const size_t smem = (size_t)a.G * a.cb_words * 4;
+  static bool attr = false;
+  if (!attr) {
+    MMJ_TRY(cuda_status(cudaFuncSetAttribute(k_tile_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             TILE_WORDS * 4),
+                        "cudaFuncSetAttribute(k_tile_merge)"));
+    attr = true;
+  }
+  k_tile_merge<<<(unsigned)ntiles, TM_THREADS, smem, st>>>(a);
   MMJ_CHECK_LAUNCH("k_tile_merge");
   return MMJ_OK;
 }
