@@ -57,6 +57,7 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-slice-x", type=int, default=32, help="x values per reference-arm sample")
     ap.add_argument("--x-limit", type=int, default=0, help="debug: only the first X output rows")
+    ap.add_argument("--serial", action="store_true", help="one stream (no emission/compute overlap)")
     return ap.parse_args()
 
 
@@ -145,14 +146,14 @@ class PhaseTimer:
         self.open = {}
         self.done = []
 
-    def start(self, name):
+    def start(self, name, stream=None):
         e = self.torch.cuda.Event(enable_timing=True)
-        e.record()
+        e.record(stream)
         self.open[name] = e
 
-    def stop(self, name):
+    def stop(self, name, stream=None):
         e = self.torch.cuda.Event(enable_timing=True)
-        e.record()
+        e.record(stream)
         self.done.append((name, self.open.pop(name), e))
 
     def totals(self):
@@ -280,10 +281,13 @@ def run_b200(args):
 
     def step(timer=None):
         eng = make_engine()
-        eng.timer = timer
-        eng.prepare()
-        for a, b in eng.chunk_bounds(x_lo, x_hi):
-            eng.run_chunk(a, b, sync=False)
+        if args.serial:
+            eng.timer = timer
+            eng.prepare()
+            for a, b in eng.chunk_bounds(x_lo, x_hi):
+                eng.run_chunk(a, b, sync=False)
+        else:
+            eng.run_pipelined(x_lo, x_hi, timer=timer)
         return eng.finish()
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")

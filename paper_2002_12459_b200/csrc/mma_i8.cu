@@ -18,10 +18,11 @@
 //       ACC64  : out[i][j] += count << shift  (int64 digit recombination for
 //                the generic multiply_counts backend).
 //
-// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w3 idle, w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4) .. +31 and the
-// 128-column half (w-4)/4 of the accumulator; the four 32-column loads of a
-// half are all in flight before one tcgen05.wait::ld).
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w3 idle, w4..w7 epilogue (warp w owns TMEM lanes 32*(w%4) .. +31).  The
+// ring depth is chosen per launch (2 stages when a tile has <= 2 K blocks), so
+// a short-K launch leaves shared memory and registers for a co-resident
+// emission kernel on another stream.
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -35,15 +36,15 @@ constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 128;                 // bytes (= uint8 elements) of K per stage
 constexpr int UMMA_K = 32;              // K per tcgen05.mma for kind::i8
-constexpr int STAGES = 4;
+constexpr int STAGES = 4;                // maximum ring depth (the launch picks 2..4)
 constexpr int A_BYTES = BM * BK;        // 16 KB
 constexpr int B_BYTES = BN * BK;        // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int ACC_STAGES = 2;
 constexpr int TMEM_COLS = 512;          // 2 x 256 s32 accumulator columns
-constexpr int EPI_WARPS = 8;            // two warps per TMEM lane quadrant, one per 128-column half
+constexpr int EPI_WARPS = 4;            // one warp per TMEM lane quadrant
 constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int smem_bytes_for(int stages) { return stages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/; }
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
 enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2 };
@@ -53,6 +54,7 @@ struct Params {
   int64_t m_rows;       // rows of A processed / rows of the output
   int64_t n_cols;       // columns of the product (= rows of B)
   int num_kb;           // Kp / BK
+  int stages;           // smem ring depth (2..STAGES)
   int mode;
   int shift;            // ACC64 only
   void* out;            // BITMAP: uint32 words, COUNT32: int32, ACC64: int64
@@ -182,14 +184,17 @@ __device__ __forceinline__ TileCoord tile_of(int64_t t, int mt, int nt) {
 }
 
 // ----------------------------------------------------------------- the kernel
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// minBlocks = 2 caps registers at 128/thread so a short-K launch (2-stage
+// ring, ~97 KB smem) leaves room for co-resident emission CTAs
+__global__ void __launch_bounds__(NUM_THREADS, 2)
     heavy_mma_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smem_a = smem;                                   // STAGES x A_BYTES
-  uint8_t* smem_b = smem + STAGES * A_BYTES;                // STAGES x B_BYTES
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  const int NST = p.stages;
+  uint8_t* smem_a = smem;                                   // NST x A_BYTES
+  uint8_t* smem_b = smem + NST * A_BYTES;                   // NST x B_BYTES
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES);
   uint64_t* full = bars;                                    // [STAGES]
   uint64_t* empty = bars + STAGES;                          // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;                      // [ACC_STAGES]
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
           tma_load_2d(smem_a + s * A_BYTES, &tmap_a, &full[s], kb * BK, arow);
           tma_load_2d(smem_b + s * B_BYTES, &tmap_b, &full[s], kb * BK, brow);
-          if (++s == STAGES) { s = 0; ph ^= 1; }
+          if (++s == NST) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       (kb > 0 || k > 0) ? 1u : 0u);
           }
           tc_commit(&empty[s]);          // smem slot free once these MMAs retire
-          if (++s == STAGES) { s = 0; ph ^= 1; }
+          if (++s == NST) { s = 0; ph ^= 1; }
         }
         tc_commit(&tfull[acc]);          // accumulator ready for the epilogue
         if (++acc == ACC_STAGES) { acc = 0; acc_ph ^= 1; }
@@ -278,7 +283,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------- epilogue
     const int q = warp & 3;              // TMEM lane quadrant
-    const int half = (warp - 4) >> 2;    // 128-column half of the 256-column tile
     int acc = 0;
     uint32_t acc_ph = 0;
     unsigned long long my_nnz = 0;
@@ -288,37 +292,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int64_t row = (int64_t)c.m_blk * BM + q * 32 + lane;   // local output row
       const bool row_ok = row < p.m_rows;
-      const int64_t col0 = (int64_t)c.n_blk * BN + half * 128;
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * 128;
+      const int64_t col0 = (int64_t)c.n_blk * BN;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (p.mode == BITMAP) {
-        uint32_t r0[32], r1[32];
-        TMEM_LD_32x32b_X32_PACK16(taddr, r0);        // columns [0, 64) of the half
-        TMEM_LD_32x32b_X32_PACK16(taddr + 64, r1);   // columns [64, 128)
-        tmem_wait_ld();
+        uint32_t w[8];
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t r0[32], r1[32];
+          TMEM_LD_32x32b_X32_PACK16(taddr + hh * 128, r0);        // columns [0, 64) of the half
+          TMEM_LD_32x32b_X32_PACK16(taddr + hh * 128 + 64, r1);   // columns [64, 128)
+          tmem_wait_ld();
+          uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            w0 |= ((r0[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+            w0 |= ((r0[i] >> 16) ? 1u : 0u) << (2 * i + 1);
+            w1 |= ((r0[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+            w1 |= ((r0[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
+            w2 |= ((r1[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+            w2 |= ((r1[i] >> 16) ? 1u : 0u) << (2 * i + 1);
+            w3 |= ((r1[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+            w3 |= ((r1[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
+          }
+          if (hh == 0) {
+            w[0] = w0; w[1] = w1; w[2] = w2; w[3] = w3;
+          } else {
+            w[4] = w0; w[5] = w1; w[6] = w2; w[7] = w3;
+          }
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
-        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          w0 |= ((r0[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-          w0 |= ((r0[i] >> 16) ? 1u : 0u) << (2 * i + 1);
-          w1 |= ((r0[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-          w1 |= ((r0[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
-          w2 |= ((r1[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-          w2 |= ((r1[i] >> 16) ? 1u : 0u) << (2 * i + 1);
-          w3 |= ((r1[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-          w3 |= ((r1[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
-        }
         if (row_ok) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + (col0 >> 5);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
-          my_nnz += __popc(w0) + __popc(w1) + __popc(w2) + __popc(w3);
+          reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) my_nnz += __popc(w[j]);
         }
       } else if (p.mode == COUNT32) {
         int32_t* dst = reinterpret_cast<int32_t*>(p.out) + row * p.ld_out + col0;
 #pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 8; ++j) {
           uint32_t r[32];
           TMEM_LD_32x32b_X32(taddr + j * 32, r);
           tmem_wait_ld();
@@ -343,7 +358,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {  // ACC64
         int64_t* dst = reinterpret_cast<int64_t*>(p.out) + row * p.ld_out + col0;
 #pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 8; ++j) {
           uint32_t r[32];
           TMEM_LD_32x32b_X32(taddr + j * 32, r);
           tmem_wait_ld();
@@ -450,6 +465,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   p.m_rows = m_rows;
   p.n_cols = b_rows;
   p.num_kb = (int)(k_len / BK);
+  p.stages = p.num_kb <= 2 ? 2 : STAGES;
   p.mode = mode;
   p.shift = shift;
   p.out = out;
@@ -458,7 +474,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   static bool attr_set = false;
   if (!attr_set) {
     MMJ_TRY(cuda_status(cudaFuncSetAttribute(heavy_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             SMEM_BYTES),
+                                             smem_bytes_for(STAGES)),
                         "cudaFuncSetAttribute(heavy_mma)"));
     attr_set = true;
   }
@@ -466,7 +482,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   int grid = sm_count();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (tiles < grid) grid = (int)tiles;
-  heavy_mma_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  heavy_mma_kernel<<<grid, NUM_THREADS, smem_bytes_for(p.stages), st>>>(ma, mb, p);
   MMJ_CHECK_LAUNCH("heavy_mma_kernel");
   return MMJ_OK;
 }

@@ -303,6 +303,77 @@ class TwoPathEngine:
         self.stats.out_size += total
         return ChunkResult(x0, x1, total, codes[:total], None, light)
 
+    def run_pipelined(self, x_begin: int = 0, x_end: Optional[int] = None, timer=None):
+        """Projection over [x_begin, x_end) with two streams: chunk i's
+        emission (HBM-write bound) runs on a side stream while chunk i+1's
+        heavy product + light merge + scan (SM bound) run on the current
+        stream.  Chunk bitmaps / segment offsets are double-buffered; codes
+        land in one device buffer (a streaming consumer).  No host sync
+        until :meth:`finish`."""
+        if not self.fused:
+            raise ValueError("run_pipelined needs the bitmap (no counts) path")
+        torch = self.torch
+        self.prepare()
+        dr, ds = self.dr, self.ds
+        main = torch.cuda.current_stream()
+        if getattr(self, "_emit_stream", None) is None:
+            self._emit_stream = torch.cuda.Stream()
+        es = self._emit_stream
+        es.wait_stream(main)
+        freed = [None, None]
+        hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
+        lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
+        lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
+        mst, est = main.cuda_stream, es.cuda_stream
+        rows_max = self.chunk_rows
+        codes = self.ws.get("codes", rows_max * self.dom_z, torch.int64)
+        for i, (x0, x1) in enumerate(self.chunk_bounds(x_begin, x_end)):
+            b = i & 1
+            rows = x1 - x0
+            nseg = rows * self.wpr // 32
+            buf = self.ws.get(f"bm{b}", rows_max * self.wpr, torch.int32)
+            segcnt = self.ws.get(f"segcnt{b}", rows_max * self.wpr // 32, torch.int32)
+            segoff = self.ws.get(f"segoff{b}", rows_max * self.wpr // 32 + 1, torch.int64)
+            if freed[b] is not None:
+                main.wait_event(freed[b])
+            if timer is not None:
+                timer.start("heavy_mma", main)
+            if self.A is not None:
+                nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
+                         self.kpad, 0, self.kpad, x0, rows, nat.MODE_BITMAP, 0, nat.ptr(buf), self.wpr,
+                         nat.ptr(self.nnz), 0, mst)
+            if timer is not None:
+                timer.stop("heavy_mma", main)
+                timer.start("light_merge", main)
+            nat.call("mmj_tile_merge", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
+                     nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp,
+                     nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(self.wit), mst)
+            if timer is not None:
+                timer.stop("light_merge", main)
+                timer.start("segments", main)
+            nat.call("mmj_exclusive_scan_i32", nat.ptr(segcnt), nat.ptr(segoff), nseg,
+                     nat.ptr(self.ws.scan_ws(rows_max * self.wpr // 32)), mst)
+            if timer is not None:
+                timer.stop("segments", main)
+            ready = torch.cuda.Event()
+            ready.record(main)
+            es.wait_event(ready)
+            if timer is not None:
+                timer.start("emit", es)
+            nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dom_z,
+                     nat.ptr(codes), est)
+            if timer is not None:
+                timer.stop("emit", es)
+            with torch.cuda.stream(es):
+                slot = self._async_slot()
+                slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(es)
+            freed[b] = ev
+            self.stats.chunks += 1
+        main.wait_stream(es)
+        return codes
+
     def _async_slot(self):
         """Device slot (2 x int64) receiving one async chunk's (size, light)."""
         torch = self.torch
