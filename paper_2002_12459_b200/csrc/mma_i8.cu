@@ -18,11 +18,10 @@
 //       ACC64  : out[i][j] += count << shift  (int64 digit recombination for
 //                the generic multiply_counts backend).
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w3 idle, w4..w7 epilogue (warp w owns TMEM lanes 32*(w%4) .. +31).  The
-// ring depth is chosen per launch (2 stages when a tile has <= 2 K blocks), so
-// a short-K launch leaves shared memory and registers for a co-resident
-// emission kernel on another stream.
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w3 idle, w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4) .. +31 and the
+// 128-column half (w-4)/4 of the accumulator).  The ring depth is chosen per
+// launch (2 stages when a tile has <= 2 K blocks).
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -42,7 +41,7 @@ constexpr int B_BYTES = BN * BK;        // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int ACC_STAGES = 2;
 constexpr int TMEM_COLS = 512;          // 2 x 256 s32 accumulator columns
-constexpr int EPI_WARPS = 4;            // one warp per TMEM lane quadrant
+constexpr int EPI_WARPS = 8;            // two warps per TMEM lane quadrant (one per 128-column half)
 constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int smem_bytes_for(int stages) { return stages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/; }
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
@@ -184,9 +183,7 @@ __device__ __forceinline__ TileCoord tile_of(int64_t t, int mt, int nt) {
 }
 
 // ----------------------------------------------------------------- the kernel
-// minBlocks = 2 caps registers at 128/thread so a short-K launch (2-stage
-// ring, ~97 KB smem) leaves room for co-resident emission CTAs
-__global__ void __launch_bounds__(NUM_THREADS, 2)
+__global__ void __launch_bounds__(NUM_THREADS, 1)
     heavy_mma_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -283,6 +280,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   } else if (warp >= 4) {
     // ------------------------------------------------------- epilogue
     const int q = warp & 3;              // TMEM lane quadrant
+    const int half = (warp - 4) >> 2;    // 128-column half of the 256-column tile
     int acc = 0;
     uint32_t acc_ph = 0;
     unsigned long long my_nnz = 0;
@@ -292,48 +290,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       tc_fence_after();
       const int64_t row = (int64_t)c.m_blk * BM + q * 32 + lane;   // local output row
       const bool row_ok = row < p.m_rows;
-      const int64_t col0 = (int64_t)c.n_blk * BN;
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const int64_t col0 = (int64_t)c.n_blk * BN + half * 128;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * 128;
       if (p.mode == BITMAP) {
-        uint32_t w[8];
-#pragma unroll 1
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t r0[32], r1[32];
-          TMEM_LD_32x32b_X32_PACK16(taddr + hh * 128, r0);        // columns [0, 64) of the half
-          TMEM_LD_32x32b_X32_PACK16(taddr + hh * 128 + 64, r1);   // columns [64, 128)
-          tmem_wait_ld();
-          uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            w0 |= ((r0[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-            w0 |= ((r0[i] >> 16) ? 1u : 0u) << (2 * i + 1);
-            w1 |= ((r0[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-            w1 |= ((r0[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
-            w2 |= ((r1[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-            w2 |= ((r1[i] >> 16) ? 1u : 0u) << (2 * i + 1);
-            w3 |= ((r1[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-            w3 |= ((r1[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
-          }
-          if (hh == 0) {
-            w[0] = w0; w[1] = w1; w[2] = w2; w[3] = w3;
-          } else {
-            w[4] = w0; w[5] = w1; w[6] = w2; w[7] = w3;
-          }
-        }
+        uint32_t r0[32], r1[32];
+        TMEM_LD_32x32b_X32_PACK16(taddr, r0);        // columns [0, 64) of the half
+        TMEM_LD_32x32b_X32_PACK16(taddr + 64, r1);   // columns [64, 128)
+        tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
+        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          w0 |= ((r0[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+          w0 |= ((r0[i] >> 16) ? 1u : 0u) << (2 * i + 1);
+          w1 |= ((r0[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+          w1 |= ((r0[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
+          w2 |= ((r1[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+          w2 |= ((r1[i] >> 16) ? 1u : 0u) << (2 * i + 1);
+          w3 |= ((r1[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
+          w3 |= ((r1[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
+        }
         if (row_ok) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + (col0 >> 5);
-          reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) my_nnz += __popc(w[j]);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
+          my_nnz += __popc(w0) + __popc(w1) + __popc(w2) + __popc(w3);
         }
       } else if (p.mode == COUNT32) {
         int32_t* dst = reinterpret_cast<int32_t*>(p.out) + row * p.ld_out + col0;
 #pragma unroll 1
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 4; ++j) {
           uint32_t r[32];
           TMEM_LD_32x32b_X32(taddr + j * 32, r);
           tmem_wait_ld();
@@ -358,7 +345,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       } else {  // ACC64
         int64_t* dst = reinterpret_cast<int64_t*>(p.out) + row * p.ld_out + col0;
 #pragma unroll 1
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 4; ++j) {
           uint32_t r[32];
           TMEM_LD_32x32b_X32(taddr + j * 32, r);
           tmem_wait_ld();

@@ -45,6 +45,37 @@ __device__ __forceinline__ void st_cs(int64_t* p, int64_t a) {
   asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
 }
 
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 1-D bulk async copies (TMA engine) between global memory and shared memory
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait0(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 __device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ v, int n, int32_t key) {
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -82,6 +113,7 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   __shared__ int s_tb_row[TUP_BATCH];
   __shared__ int s_tb_filt[TUP_BATCH];
   __shared__ int s_touched;
+  __shared__ __align__(8) uint64_t s_bar;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -98,11 +130,15 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   const int32_t zhi = (int32_t)min((c0w + cw) * 32, a.dom_z);
   const int q4 = cw >> 2;
 
+  // the tile is one contiguous range of the chunk bitmap: several whole rows
+  // (ncb == 1) or one row piece (G == 1)
+  uint32_t* gtile = a.bm + r0 * a.wpr + c0w;
+  const uint32_t tile_bytes = (uint32_t)words * 4u;
   if (a.has_heavy) {
-    for (int i = tid; i < nrow * q4; i += TM_THREADS) {
-      const int rr = i / q4, qq = i - rr * q4;
-      reinterpret_cast<uint4*>(sbm)[rr * q4 + qq] =
-          reinterpret_cast<const uint4*>(a.bm + (r0 + rr) * a.wpr + c0w)[qq];
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      bulk_g2s(sbm, gtile, tile_bytes, &s_bar);
     }
   } else {
     for (int i = tid; i < words; i += TM_THREADS) sbm[i] = 0;
@@ -113,6 +149,7 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   const int64_t t_begin = a.fwd_ptr[xa], t_end = a.fwd_ptr[xb];
   unsigned long long my_w = 0;
   __syncthreads();
+  if (a.has_heavy) bar_wait0(&s_bar);   // tile bytes landed (all threads observe the phase)
   for (int64_t tb = t_begin; tb < t_end; tb += TUP_BATCH) {
     const int64_t t = tb + tid;
     int len = 0, row = 0, filt = 0;
@@ -183,12 +220,8 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
     if (lane == 0 && w) atomicAdd(a.witnesses, w);
   }
   // write back the merged tile (skipped when the heavy bits are unchanged)
-  if (s_touched || !a.has_heavy) {
-    for (int i = tid; i < nrow * q4; i += TM_THREADS) {
-      const int rr = i / q4, qq = i - rr * q4;
-      reinterpret_cast<uint4*>(a.bm + (r0 + rr) * a.wpr + c0w)[qq] = reinterpret_cast<const uint4*>(sbm)[rr * q4 + qq];
-    }
-  }
+  __syncthreads();
+  if ((s_touched || !a.has_heavy) && tid == 0) bulk_s2g(gtile, sbm, tile_bytes);
   // segment popcounts (segments never straddle rows: wpr % 32 == 0)
   const int nseg = words >> 5;
   const int segs_per_piece = cw >> 5;
@@ -214,10 +247,12 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const uint32_t* __restri
   // XOR-ing the bank bits with the 32-slot row index spreads their stores
   auto sl = [](int k) { return k ^ ((k >> 5) & 31); };
   const int64_t s0 = (int64_t)blockIdx.x * EM_SEGS;
+  uint32_t next = (s0 + warp < nseg) ? bm[(s0 + warp) * 32 + lane] : 0u;
   for (int si = warp; si < EM_SEGS; si += EM_WARPS) {
     const int64_t s = s0 + si;
     if (s >= nseg) break;
-    uint32_t word = bm[s * 32 + lane];
+    uint32_t word = next;
+    if (si + EM_WARPS < EM_SEGS && s + EM_WARPS < nseg) next = bm[(s + EM_WARPS) * 32 + lane];   // prefetch
     const int c = __popc(word);
     int incl = c;
 #pragma unroll
