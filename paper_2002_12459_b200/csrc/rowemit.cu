@@ -197,16 +197,12 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
     __syncthreads();
     const int nt = (int)min((int64_t)TUP_BATCH, t_end - tb);
     int kept = 0;
+    int ti = 0;   // tuple of the current slot; slots grow, so the cursor only moves forward
     for (int s = tid; s < tot; s += TM_THREADS) {
-      int lo = 0, hi = nt;   // last i with s_tb_len[i] <= s
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_tb_len[mid] <= s) lo = mid;
-        else hi = mid;
-      }
-      const int32_t z = s_tb_base[lo][s - s_tb_len[lo]];
-      if (s_tb_filt[lo] && (z < zlo || z >= zhi)) continue;
-      atomicOr(&sbm[s_tb_row[lo] * cw + ((z - zlo) >> 5)], 1u << (z & 31));
+      while (ti + 1 < nt && s_tb_len[ti + 1] <= s) ++ti;
+      const int32_t z = s_tb_base[ti][s - s_tb_len[ti]];
+      if (s_tb_filt[ti] && (z < zlo || z >= zhi)) continue;
+      atomicOr(&sbm[s_tb_row[ti] * cw + ((z - zlo) >> 5)], 1u << (z & 31));
       ++kept;
     }
     my_w += kept;
@@ -222,16 +218,22 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   // write back the merged tile (skipped when the heavy bits are unchanged)
   __syncthreads();
   if ((s_touched || !a.has_heavy) && tid == 0) bulk_s2g(gtile, sbm, tile_bytes);
-  // segment popcounts (segments never straddle rows: wpr % 32 == 0)
+  // segment popcounts (segments never straddle rows: wpr % 32 == 0): a warp
+  // takes 32 segments, lane l reads word l of each (conflict-free LDS) and
+  // REDUX sums the 32 popcounts; lane j keeps the total of segment j
   const int nseg = words >> 5;
   const int segs_per_piece = cw >> 5;
-  for (int s = warp; s < nseg; s += TM_THREADS / 32) {
-    int c = __popc(sbm[s * 32 + lane]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) {
-      const int rr = s / segs_per_piece, sc = s - rr * segs_per_piece;
-      a.segcnt[((r0 + rr) * a.wpr + c0w) / 32 + sc] = c;
+  for (int sb = warp * 32; sb < nseg; sb += TM_THREADS) {
+    int mine = 0;
+    const int ns = min(32, nseg - sb);
+    for (int j = 0; j < ns; ++j) {
+      const int c = __reduce_add_sync(0xffffffffu, __popc(sbm[(sb + j) * 32 + lane]));
+      if (lane == j) mine = c;
+    }
+    if (lane < ns) {
+      const int sg = sb + lane;
+      const int rr = sg / segs_per_piece, sc = sg - rr * segs_per_piece;
+      a.segcnt[((r0 + rr) * a.wpr + c0w) / 32 + sc] = mine;
     }
   }
 }
