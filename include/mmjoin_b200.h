@@ -149,6 +149,23 @@ int mmj_count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols,
                    int32_t min_count, int upper_only, const int64_t* seg_off, int64_t* codes, int32_t* counts,
                    void* stream);
 
+/* ---- batched boolean set intersection: apps.py:314-351 ----------------------
+ * Heavy y (hpos >= 0, from mmj_heavy_y_positions) -> per-left-id bitsets of
+ * `words` uint32 (multiple of 4); the remaining (light) y of every left id's
+ * forward list -> compacted sorted light lists.  mmj_bsi_answer resolves raw
+ * query ids through each relation's sorted raw left values (r_sorted/r_order;
+ * NULL = queries are dense ids already) and writes ans[q] = 1 (intersect),
+ * 0 (disjoint) or -1 (id unknown to the unreduced relation = None). */
+int mmj_bsi_bits(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* hpos, int words, uint32_t* bits,
+                 int64_t dom_left, void* stream);
+int mmj_bsi_light_lists(const int32_t* fwd_ptr, const int32_t* fwd_idx, int64_t n, int64_t dom_left,
+                        const int32_t* hpos, uint8_t* flag_ws, int32_t* pos_ws, int32_t* lptr, int32_t* lidx,
+                        void* ws, void* stream);
+int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted, const int32_t* r_order,
+                   int64_t r_n, const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const uint32_t* r_bits,
+                   const uint32_t* s_bits, int words, const int32_t* r_lptr, const int32_t* r_lidx,
+                   const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,214 @@
+"""Host orchestration of batched boolean set intersection on the B200
+(apps.py:314-351).  See csrc/bsi.cu for the device algorithm.
+
+Steps (all kernels of libmmjoin_b200.so):
+  1. degree split of y over both relations (mmj_heavy_y_positions) with
+     delta1 chosen so that at most `heavy_bits` y are heavy;
+  2. heavy-y bitsets per left id of R and S (mmj_bsi_bits);
+  3. light lists per left id (mmj_bsi_light_lists);
+  4. per query: raw id -> dense id through each relation's own (unreduced)
+     dictionary, bitset test, light merge intersection (mmj_bsi_answer).
+If R and S do not share a right dictionary, their y ids are first mapped to
+a common raw-value space on the host (input preparation, as the reference's
+semi_join_reduce does) -- left ids, hence "known" ids, stay those of the
+unreduced relations.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .device import Workspace
+
+BITS_BLOCK = 128     # bitset width granularity (4 words)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class BsiSide:
+    """Device arrays of one relation in the shared y space."""
+    n: int
+    dom_left: int
+    fwd_ptr: object
+    fwd_idx: object
+    fwd_row: object
+    ydeg: np.ndarray          # host degrees over the shared y space
+    sorted_vals: object       # device int64 sorted raw left values (or None)
+    order: object             # device int32 dense id of each sorted value
+    h2d_bytes: int = 0
+
+
+def _left_lookup_arrays(rel):
+    """(sorted raw values, order) for int-valued dictionaries, else None."""
+    lv = rel.left_values
+    if isinstance(lv, np.ndarray) and lv.dtype.kind in "iu":
+        vals = lv.astype(np.int64)
+    else:
+        try:
+            if not all(isinstance(v, (int, np.integer)) and not isinstance(v, bool) for v in lv):
+                return None
+            vals = np.asarray(lv, dtype=np.int64)
+        except (OverflowError, TypeError, ValueError):
+            return None
+    order = np.argsort(vals, kind="stable")
+    return vals[order], order.astype(np.int32)
+
+
+def _side(idx, y_map, dom_y, pinned=False) -> BsiSide:
+    torch = _torch()
+    fptr = np.asarray(idx.fwd_indptr, dtype=np.int64)
+    fidx = np.asarray(idx.fwd_indices, dtype=np.int64)
+    ldeg = np.diff(fptr)
+    rows = np.repeat(np.arange(idx.rel.dom_left, dtype=np.int64), ldeg)
+    if y_map is not None:
+        fidx = y_map[fidx]
+        order = np.lexsort((fidx, rows))          # keep each list sorted by shared y id
+        fidx = fidx[order]
+    ydeg = np.bincount(fidx, minlength=dom_y).astype(np.int32)
+    lk = _left_lookup_arrays(idx.rel)
+    dev = {}
+    nbytes = 0
+    for name, arr in (("fwd_ptr", fptr.astype(np.int32)), ("fwd_idx", fidx.astype(np.int32)),
+                      ("fwd_row", rows.astype(np.int32))):
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        if pinned:
+            t = t.pin_memory()
+        nbytes += arr.nbytes
+        dev[name] = t.to("cuda", non_blocking=pinned)
+    sv = od = None
+    if lk is not None:
+        sv = torch.from_numpy(lk[0]).to("cuda")
+        od = torch.from_numpy(lk[1]).to("cuda")
+        nbytes += lk[0].nbytes + lk[1].nbytes
+    return BsiSide(len(fidx), idx.rel.dom_left, dev["fwd_ptr"], dev["fwd_idx"], dev["fwd_row"], ydeg, sv, od, nbytes)
+
+
+def prepare(r, s, pinned=False):
+    """Device sides of R and S over one y id space (cached on the objects)."""
+    key = (id(r), id(s))
+    cache = getattr(r, "_mmj_bsi_cache", None)
+    if cache is not None and cache[0] == key and not pinned:
+        return cache[1]
+    if r.rel.right_values is s.rel.right_values:
+        dom_y = r.rel.dom_right
+        sides = (_side(r, None, dom_y, pinned), _side(s, None, dom_y, pinned), dom_y)
+    else:
+        rv, sv = r.rel.right_values, s.rel.right_values
+        try:
+            ra = np.asarray(rv, dtype=np.int64)
+            sa = np.asarray(sv, dtype=np.int64)
+            allv = np.union1d(ra, sa)
+            rmap, smap = np.searchsorted(allv, ra), np.searchsorted(allv, sa)
+        except (TypeError, ValueError, OverflowError):
+            allv = {}
+            for v in list(rv) + list(sv):
+                allv.setdefault(v, len(allv))
+            rmap = np.array([allv[v] for v in rv], dtype=np.int64)
+            smap = np.array([allv[v] for v in sv], dtype=np.int64)
+        dom_y = len(allv)
+        sides = (_side(r, rmap, dom_y, pinned), _side(s, smap, dom_y, pinned), dom_y)
+    if not pinned:
+        try:
+            r._mmj_bsi_cache = (key, sides)
+        except AttributeError:
+            pass
+    return sides
+
+
+def _dense_queries(rel, q):
+    """Host dictionary probe for non-integer raw ids (-1 when unknown)."""
+    ids = rel.left_ids
+    return np.array([ids.get(v, -1) if ids.get(v) is not None else -1 for v in q], dtype=np.int64)
+
+
+class BsiEngine:
+    """Index build + answering for one (R, S) pair (reusable across batches)."""
+
+    def __init__(self, sR: BsiSide, sS: BsiSide, dom_y: int, heavy_bits: int = 256, ws=None):
+        self.sR, self.sS, self.dom_y = sR, sS, dom_y
+        self.heavy_bits = max(BITS_BLOCK, -(-heavy_bits // BITS_BLOCK) * BITS_BLOCK)
+        self.ws = ws or Workspace()
+        m = np.maximum(sR.ydeg, sS.ydeg)
+        # delta1 = the heavy_bits-th largest max-degree: y heavy iff max deg > delta1
+        if len(m) > self.heavy_bits:
+            self.delta1 = max(1, int(np.partition(m, len(m) - self.heavy_bits)[len(m) - self.heavy_bits]))
+        else:
+            self.delta1 = 1
+        torch = _torch()
+        self.rdeg = torch.from_numpy(sR.ydeg).to("cuda")
+        self.sdeg = torch.from_numpy(sS.ydeg).to("cuda")
+        self.k = 0
+
+    def build(self):
+        torch = _torch()
+        st = nat.stream_handle()
+        dom_y = self.dom_y
+        flag = self.ws.get("yflag", dom_y, torch.uint8)
+        scan = self.ws.get("yscan", dom_y + 1, torch.int32)
+        self.hpos = self.ws.get("hpos", max(dom_y, 1), torch.int32)
+        nat.call("mmj_heavy_y_positions", nat.ptr(self.rdeg), nat.ptr(self.sdeg), dom_y, self.delta1,
+                 nat.ptr(flag), nat.ptr(scan), nat.ptr(self.hpos), nat.ptr(self.ws.scan_ws(dom_y)), st)
+        self.words = self.heavy_bits // 32
+        self.sides = []
+        for tag, sd in (("r", self.sR), ("s", self.sS)):
+            bits = self.ws.get(f"bits_{tag}", max(sd.dom_left, 1) * self.words, torch.int32)
+            nat.call("mmj_bsi_bits", nat.ptr(sd.fwd_row), nat.ptr(sd.fwd_idx), sd.n, nat.ptr(self.hpos),
+                     self.words, nat.ptr(bits), sd.dom_left, st)
+            lflag = self.ws.get(f"lflag_{tag}", sd.n, torch.uint8)
+            lpos = self.ws.get(f"lpos_{tag}", sd.n + 1, torch.int32)
+            lptr = self.ws.get(f"lptr_{tag}", sd.dom_left + 1, torch.int32)
+            lidx = self.ws.get(f"lidx_{tag}", max(sd.n, 1), torch.int32)
+            nat.call("mmj_bsi_light_lists", nat.ptr(sd.fwd_ptr), nat.ptr(sd.fwd_idx), sd.n, sd.dom_left,
+                     nat.ptr(self.hpos), nat.ptr(lflag), nat.ptr(lpos), nat.ptr(lptr), nat.ptr(lidx),
+                     nat.ptr(self.ws.scan_ws(sd.n)), st)
+            self.sides.append((bits, lptr, lidx))
+
+    def answer(self, qa_dev, qb_dev, nq, dense_a=False, dense_b=False, out=None):
+        torch = _torch()
+        st = nat.stream_handle()
+        ans = out if out is not None else torch.empty(max(nq, 1), dtype=torch.int8, device="cuda")
+        (rb, rlp, rli), (sb, slp, sli) = self.sides
+        sR, sS = self.sR, self.sS
+        rs = 0 if dense_a else nat.ptr(sR.sorted_vals)
+        ro = 0 if dense_a else nat.ptr(sR.order)
+        ss = 0 if dense_b else nat.ptr(sS.sorted_vals)
+        so = 0 if dense_b else nat.ptr(sS.order)
+        nat.call("mmj_bsi_answer", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, rs, ro, sR.dom_left, ss, so, sS.dom_left,
+                 nat.ptr(rb), nat.ptr(sb), self.words, nat.ptr(rlp), nat.ptr(rli), nat.ptr(slp), nat.ptr(sli),
+                 nat.ptr(ans), st)
+        return ans[:nq]
+
+
+def answer_batch(r, s, batch_a, batch_b, heavy_bits: int = 256) -> np.ndarray:
+    """int8 answers (1 / 0 / -1 for None) for raw query ids."""
+    torch = _torch()
+    nat.require_cuda()
+    qa = list(batch_a) if not isinstance(batch_a, np.ndarray) else batch_a
+    qb = list(batch_b) if not isinstance(batch_b, np.ndarray) else batch_b
+    nq = len(qa)
+    if nq == 0:
+        return np.empty(0, dtype=np.int8)
+    sR, sS, dom_y = prepare(r, s)
+    eng = BsiEngine(sR, sS, dom_y, heavy_bits)
+    eng.build()
+
+    def to_dev(rel, side, q):
+        try:
+            arr = np.asarray(q, dtype=np.int64)
+            if side.sorted_vals is not None:
+                return torch.from_numpy(arr).to("cuda"), False
+            dense = _dense_queries(rel, q)
+        except (TypeError, ValueError, OverflowError):
+            dense = _dense_queries(rel, q)
+        return torch.from_numpy(dense).to("cuda"), True
+
+    da, dense_a = to_dev(r.rel, sR, qa)
+    db, dense_b = to_dev(s.rel, sS, qb)
+    return eng.answer(da, db, nq, dense_a, dense_b).cpu().numpy()

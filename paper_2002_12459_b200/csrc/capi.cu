@@ -29,6 +29,12 @@ int tile_merge(uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t
                int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int32_t*,
                unsigned long long*, cudaStream_t);
 int emit_codes(const uint32_t*, const int64_t*, int64_t, int64_t, int64_t, int64_t, int64_t*, cudaStream_t);
+int bsi_bits(const int32_t*, const int32_t*, int64_t, const int32_t*, int, uint32_t*, int64_t, cudaStream_t);
+int bsi_light_lists(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, uint8_t*, int32_t*, int32_t*,
+                    int32_t*, void*, cudaStream_t);
+int bsi_answer(const int64_t*, const int64_t*, int64_t, const int64_t*, const int32_t*, int64_t, const int64_t*,
+               const int32_t*, int64_t, const uint32_t*, const uint32_t*, int, const int32_t*, const int32_t*,
+               const int32_t*, const int32_t*, int8_t*, cudaStream_t);
 namespace mma {
 int launch_heavy_mma(const uint8_t*, int64_t, const uint8_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                      int, int, void*, int64_t, unsigned long long*, int, cudaStream_t);
@@ -151,6 +157,25 @@ int mmj_tile_merge(uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, in
 int mmj_emit_codes(const uint32_t* bitmap, const int64_t* seg_off, int64_t rows, int64_t wpr, int64_t x0,
                    int64_t dom_z, int64_t* codes, void* stream) {
   return mmj::emit_codes(bitmap, seg_off, rows, wpr, x0, dom_z, codes, ST(stream));
+}
+
+int mmj_bsi_bits(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* hpos, int words, uint32_t* bits,
+                 int64_t dom_left, void* stream) {
+  return mmj::bsi_bits(rows, cols, n, hpos, words, bits, dom_left, ST(stream));
+}
+
+int mmj_bsi_light_lists(const int32_t* fwd_ptr, const int32_t* fwd_idx, int64_t n, int64_t dom_left,
+                        const int32_t* hpos, uint8_t* flag_ws, int32_t* pos_ws, int32_t* lptr, int32_t* lidx,
+                        void* ws, void* stream) {
+  return mmj::bsi_light_lists(fwd_ptr, fwd_idx, n, dom_left, hpos, flag_ws, pos_ws, lptr, lidx, ws, ST(stream));
+}
+
+int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted, const int32_t* r_order,
+                   int64_t r_n, const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const uint32_t* r_bits,
+                   const uint32_t* s_bits, int words, const int32_t* r_lptr, const int32_t* r_lidx,
+                   const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, void* stream) {
+  return mmj::bsi_answer(qa, qb, nq, r_sorted, r_order, r_n, s_sorted, s_order, s_n, r_bits, s_bits, words, r_lptr,
+                         r_lidx, s_lptr, s_lidx, ans, ST(stream));
 }
 
 int64_t mmj_bitmap_segment_count(int64_t nwords) { return mmj::bitmap_nseg(nwords); }
