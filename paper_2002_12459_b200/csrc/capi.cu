@@ -35,6 +35,11 @@ int bsi_light_lists(const int32_t*, const int32_t*, int64_t, int64_t, const int3
 int bsi_answer(const int64_t*, const int64_t*, int64_t, const int64_t*, const int32_t*, int64_t, const int64_t*,
                const int32_t*, int64_t, const uint32_t*, const uint32_t*, int, const int32_t*, const int32_t*,
                const int32_t*, const int32_t*, int8_t*, cudaStream_t);
+int star_split(int, const int32_t* const*, int64_t, double, uint8_t*, uint8_t*, int32_t*, int32_t*, int32_t*, int32_t*,
+               void*, cudaStream_t);
+int star_operand(int, const int64_t*, const uint8_t* const*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
+int star_light(int, const int64_t*, const int32_t* const*, const int32_t* const*, const int32_t*, int64_t, int64_t,
+               int64_t, int, void*, int64_t, unsigned long long*, cudaStream_t);
 namespace mma {
 int launch_heavy_mma(const uint8_t*, int64_t, const uint8_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                      int, int, void*, int64_t, unsigned long long*, int, cudaStream_t);
@@ -176,6 +181,25 @@ int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64
                    const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, void* stream) {
   return mmj::bsi_answer(qa, qb, nq, r_sorted, r_order, r_n, s_sorted, s_order, s_n, r_bits, s_bits, words, r_lptr,
                          r_lidx, s_lptr, s_lidx, ans, ST(stream));
+}
+
+int mmj_star_split(int k, const int32_t* const* rev_ptr, int64_t dom_y, double threshold, uint8_t* heavy_flag,
+                   uint8_t* light_flag, int32_t* heavy_scan, int32_t* light_scan, int32_t* hpos, int32_t* light_y,
+                   void* ws, void* stream) {
+  return mmj::star_split(k, rev_ptr, dom_y, threshold, heavy_flag, light_flag, heavy_scan, light_scan, hpos, light_y,
+                         ws, ST(stream));
+}
+
+int mmj_star_operand(int k, const int64_t* dims, const uint8_t* const* heavy, int64_t kpad, int64_t x1_begin,
+                     int64_t rows, uint8_t* A, void* stream) {
+  return mmj::star_operand(k, dims, heavy, kpad, x1_begin, rows, A, ST(stream));
+}
+
+int mmj_star_light(int k, const int64_t* dims, const int32_t* const* rev_ptr, const int32_t* const* rev_idx,
+                   const int32_t* light_y, int64_t n_light, int64_t x1_begin, int64_t x1_end, int mode, void* out,
+                   int64_t ld, unsigned long long* witnesses, void* stream) {
+  return mmj::star_light(k, dims, rev_ptr, rev_idx, light_y, n_light, x1_begin, x1_end, mode, out, ld, witnesses,
+                         ST(stream));
 }
 
 int64_t mmj_bitmap_segment_count(int64_t nwords) { return mmj::bitmap_nseg(nwords); }

@@ -30,7 +30,7 @@ from .optimizer import FULL_JOIN, PARTITIONED, ThresholdPlan, default_plan
 from .relation import IndexedRelation, Relation, build_indexed, semi_join_reduce_many
 
 __all__ = ["OutputSet", "Partition", "StarResourceError", "two_path_join", "two_path_join_chunks",
-           "full_join_dedup", "partition_two_path", "heavy_matrices", "CountMatrix"]
+           "full_join_dedup", "partition_two_path", "heavy_matrices", "star_join", "CountMatrix"]
 
 
 @dataclass
@@ -255,3 +255,6 @@ def heavy_matrices(r, s, delta1: int, delta2: int):
     del torch, nat
     return (CountMatrix(a, row_keys=heavy_a, col_keys=heavy_b),
             CountMatrix(np.ascontiguousarray(b.T), row_keys=heavy_b, col_keys=heavy_c))
+
+
+from .star import star_join  # noqa: E402  (joinproject.py:281-378; defined in star.py)

@@ -1,0 +1,210 @@
+"""Star join-project on the B200 (joinproject.py:281-378, star_join).
+
+The output pi_{x1..xk} is evaluated as a two-path over composite rows
+(x1..x_{k-1}) and column x_k (code = row * d_k + x_k, the reference's
+mixed-radix _encode).  Join values y are split on the device by the product
+of their k degrees: heavy y go through the tcgen05 product (A = row-wise AND
+of the heavy rows of R_1..R_{k-1}, generated per x1 chunk; B = heavy rows of
+R_k), light y are enumerated witness by witness.  The reference's own
+heavy/light decomposition only decides its `heavy_dims` statistic and its
+StarResourceError cap; both are reproduced from degrees on the host, so the
+drop-in keeps the same results, stats and errors for every (delta1, delta2)
+(the output itself is plan-independent).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as nat
+from .device import Workspace, device_relation
+from .errors import StarResourceError
+
+BK = 128
+LIGHT_RATE = 1.0e10          # light witnesses / s (global atomics)
+MMA_RATE = 2.0e15            # int8 ops / s
+CELL_RATE = 4.0e12           # epilogue floor, output cells / s
+DEFAULT_CHUNK_BYTES = 256 << 20
+
+
+def _rup(a: int, b: int) -> int:
+    return -(-a // b) * b
+
+
+def reference_heavy_dims(rels, delta1: int, delta2: int, cap: int) -> list:
+    """joinproject.py:321-333, 360: the reference's heavy-part geometry
+    (raises StarResourceError exactly when the reference does)."""
+    k = len(rels)
+    deg = np.stack([np.asarray(r.right_deg) for r in rels])
+    nheavy = [int((np.asarray(r.left_deg) > delta2).sum()) for r in rels]
+    ny = int(((deg > delta1).sum(axis=0) >= 2).sum())
+    if not (ny and all(nheavy)):
+        return []
+    g1 = list(range(math.ceil(k / 2)))
+    g2 = list(range(math.ceil(k / 2), k))
+    rows = [math.prod(nheavy[i] for i in g) for g in (g1, g2)]
+    for n in rows:
+        if n > cap:
+            raise StarResourceError(f"{n} heavy combinations exceed the cap; increase delta2")
+    return [rows[0], rows[1], ny]
+
+
+def choose_threshold(rels) -> float:
+    """Product-degree threshold minimising modelled B200 time."""
+    deg = np.stack([np.asarray(r.right_deg, dtype=np.float64) for r in rels])
+    prod = deg.prod(axis=0)
+    order = np.sort(prod)[::-1]
+    order = order[order > 0]
+    dims = [r.rel.dom_left for r in rels]
+    cells = float(math.prod(dims))
+    tail = np.concatenate([np.cumsum(order[::-1])[::-1], [0.0]])   # tail[k] = sum of order[k:]
+    best_t, best_thr = tail[0] / LIGHT_RATE, math.inf                 # no heavy y
+    for kk in range(BK, min(len(order), 8192) + BK, BK):
+        ke = min(kk, len(order))
+        t = tail[ke] / LIGHT_RATE + max(2.0 * cells * _rup(ke, BK) / MMA_RATE, cells / CELL_RATE)
+        if t < best_t:
+            best_t, best_thr = t, (float(order[ke]) if ke < len(order) else 0.0)
+    return best_thr
+
+
+def _ptr_array(vals, ctype=C.c_void_p):
+    arr = (ctype * 4)()
+    for i, v in enumerate(vals):
+        arr[i] = v
+    return arr
+
+
+class StarEngine:
+    def __init__(self, rels, want_counts: bool, threshold: Optional[float] = None,
+                 chunk_bytes: int = DEFAULT_CHUNK_BYTES, ws: Optional[Workspace] = None):
+        import torch
+        self.torch = torch
+        self.lib = nat.load()
+        self.rels = rels
+        self.k = len(rels)
+        self.dev = [device_relation(r) for r in rels]
+        self.dims = [r.rel.dom_left for r in rels]
+        self.dom_y = rels[0].rel.dom_right
+        self.counts = want_counts
+        self.threshold = choose_threshold(rels) if threshold is None else float(threshold)
+        self.ws = ws or Workspace()
+        self.dk = self.dims[-1]
+        self.wpr = _rup(max(self.dk, 1), 1024) // 32
+        self.ldc = _rup(max(self.dk, 1), 1024)
+        self.row_per_x1 = math.prod(self.dims[1:-1]) if self.k > 2 else 1
+        row_bytes = self.ldc * 4 if want_counts else self.wpr * 4
+        self.x1_per_chunk = max(1, chunk_bytes // max(row_bytes * self.row_per_x1, 1))
+        self.nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.wit = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def prepare(self):
+        torch = self.torch
+        st = nat.stream_handle()
+        dom_y = self.dom_y
+        rev_ptrs = _ptr_array([nat.ptr(d.rev_ptr) for d in self.dev])
+        hflag = self.ws.get("s_hflag", dom_y, torch.uint8)
+        lflag = self.ws.get("s_lflag", dom_y, torch.uint8)
+        hscan = self.ws.get("s_hscan", dom_y + 1, torch.int32)
+        lscan = self.ws.get("s_lscan", dom_y + 1, torch.int32)
+        self.hpos = torch.empty(max(dom_y, 1), dtype=torch.int32, device="cuda")
+        self.light_y = torch.empty(max(dom_y, 1), dtype=torch.int32, device="cuda")
+        nat.call("mmj_star_split", self.k, rev_ptrs, dom_y, self.threshold, nat.ptr(hflag), nat.ptr(lflag),
+                 nat.ptr(hscan), nat.ptr(lscan), nat.ptr(self.hpos), nat.ptr(self.light_y),
+                 nat.ptr(self.ws.scan_ws(dom_y)), st)
+        kk, nl = (int(v) for v in torch.stack([hscan[dom_y], lscan[dom_y]]).cpu())
+        self.kh, self.n_light = kk, nl
+        self.H = None
+        if kk > 0:
+            self.kpad = _rup(kk, BK)
+            self.H = []
+            for j, d in enumerate(self.dev):
+                pad = 1024 if j == self.k - 1 else 256
+                rows = _rup(max(d.dom_left, 1), pad)
+                h = torch.empty((rows, self.kpad), dtype=torch.uint8, device="cuda")
+                nat.call("mmj_build_operand", nat.ptr(d.fwd_row), nat.ptr(d.fwd_idx), d.n, nat.ptr(d.left_deg), 0,
+                         nat.ptr(self.hpos), nat.ptr(h), 0, rows, self.kpad, st)
+                self.H.append(h)
+
+    def run(self):
+        torch = self.torch
+        st = nat.stream_handle()
+        self.prepare()
+        dims_arr = (C.c_int64 * 4)(*(self.dims + [0] * (4 - self.k)))
+        rev_ptrs = _ptr_array([nat.ptr(d.rev_ptr) for d in self.dev])
+        rev_idxs = _ptr_array([nat.ptr(d.rev_idx) for d in self.dev])
+        heavy_ptrs = _ptr_array([nat.ptr(h) for h in self.H]) if self.H else None
+        codes_out, counts_out = [], []
+        d1 = self.dims[0]
+        for xa in range(0, d1, self.x1_per_chunk):
+            xb = min(d1, xa + self.x1_per_chunk)
+            rows = (xb - xa) * self.row_per_x1
+            ld = self.ldc if self.counts else self.wpr
+            buf = self.ws.get("star_out", rows * ld, torch.int32)
+            if self.H is not None:
+                arows = _rup(rows, 256)
+                A = self.ws.get("star_A", arows * self.kpad, torch.uint8)
+                nat.call("mmj_star_operand", self.k, dims_arr, heavy_ptrs, self.kpad, xa, rows, nat.ptr(A), st)
+                B = self.H[-1]
+                nat.call("mmj_heavy_mma", nat.ptr(A), arows, nat.ptr(B), B.shape[0], self.kpad, 0, self.kpad, 0, rows,
+                         nat.MODE_COUNT32 if self.counts else nat.MODE_BITMAP, 0, nat.ptr(buf), ld, nat.ptr(self.nnz),
+                         0, st)
+            else:
+                buf.zero_()
+            nat.call("mmj_star_light", self.k, dims_arr, rev_ptrs, rev_idxs, nat.ptr(self.light_y), self.n_light, xa,
+                     xb, 1 if self.counts else 0, nat.ptr(buf), ld, nat.ptr(self.wit), st)
+            x0 = xa * self.row_per_x1
+            if self.counts:
+                ncell = rows * self.ldc
+                nseg = int(self.lib.mmj_count_segment_count(ncell))
+                segcnt = self.ws.get("segcnt", nseg, torch.int32)
+                segoff = self.ws.get("segoff", nseg + 1, torch.int64)
+                nat.call("mmj_count_segments", nat.ptr(buf), rows, self.ldc, self.dk, x0, 1, 0, nat.ptr(segcnt),
+                         nat.ptr(segoff), nat.ptr(self.ws.scan_ws(nseg)), st)
+                total = int(segoff[nseg].item())
+                codes = self.ws.get("codes", total, torch.int64)
+                cnts = self.ws.get("counts", total, torch.int32)
+                if total:
+                    nat.call("mmj_count_emit", nat.ptr(buf), rows, self.ldc, self.dk, x0, self.dk, 1, 0,
+                             nat.ptr(segoff), nat.ptr(codes), nat.ptr(cnts), st)
+                codes_out.append(codes[:total].cpu().numpy())
+                counts_out.append(cnts[:total].cpu().numpy().astype(np.int64))
+            else:
+                nwords = rows * self.wpr
+                nseg = int(self.lib.mmj_bitmap_segment_count(nwords))
+                segcnt = self.ws.get("segcnt", nseg, torch.int32)
+                segoff = self.ws.get("segoff", nseg + 1, torch.int64)
+                nat.call("mmj_bitmap_segments", nat.ptr(buf), nwords, nat.ptr(segcnt), nat.ptr(segoff),
+                         nat.ptr(self.ws.scan_ws(nseg)), st)
+                total = int(segoff[nseg].item())
+                codes = self.ws.get("codes", total, torch.int64)
+                if total:
+                    nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dk,
+                             nat.ptr(codes), st)
+                codes_out.append(codes[:total].cpu().numpy())
+        codes = np.concatenate(codes_out) if codes_out else np.empty(0, dtype=np.int64)
+        counts = (np.concatenate(counts_out) if counts_out else np.empty(0, dtype=np.int64)) if self.counts else None
+        return codes, counts
+
+
+def star_join(relations: Sequence, delta1: int, delta2: int, want_counts: bool = False, cores: int = 1,
+              heavy_rows_cap: int = 1 << 22, threshold: Optional[float] = None):
+    """joinproject.py:281-378: pi_{x1..xk} of k relations joined on the
+    shared right column, with exact witness counts on request."""
+    from .joinproject import OutputSet, _check_code_space, _ensure_reduced_many
+    k = len(relations)
+    if not 2 <= k <= 4:
+        raise ValueError("star_join supports 2 <= k <= 4 relations")
+    if delta1 < 1 or delta2 < 1:
+        raise ValueError("thresholds must be >= 1")
+    rels = _ensure_reduced_many(relations)
+    dims = [r.rel.dom_left for r in rels]
+    _check_code_space(dims)
+    hdims = reference_heavy_dims(rels, delta1, delta2, heavy_rows_cap)
+    nat.require_cuda()
+    eng = StarEngine(rels, want_counts, threshold=threshold)
+    codes, counts = eng.run()
+    return OutputSet(codes, dims, counts, {"heavy_dims": hdims})

@@ -107,3 +107,54 @@ def test_bsi_zipf_vs_oracle(oracle, heavy_bits):
     got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], heavy_bits=heavy_bits)
     assert np.array_equal(got, exp)
     assert (exp == -1).any() and (exp == 1).any() and (exp == 0).any()
+
+
+def test_star_golden():
+    from paper_2002_12459_b200.joinproject import star_join
+    from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce_many
+    z = np.load(os.path.join(GOLDEN, "star.npz"))
+    meta = json.loads(str(z["meta"]))
+    for m in meta:
+        i, k = m["inst"], m["k"]
+        rels = semi_join_reduce_many([Relation.from_raw_pairs(f"R{j}", z[f"s{i}_rel{j}"]) for j in range(k)])
+        idxs = [build_indexed(x) for x in rels]
+        for thr in (None, 0.0, float("inf"), 3.0):     # all-heavy, all-light and mixed device splits
+            res = star_join(idxs, m["d1"], m["d2"], want_counts=m["counts"], threshold=thr)
+            assert list(res.dims) == m["dims"]
+            assert np.array_equal(res.codes, z[m["key"] + "_codes"]), (m["key"], thr)
+            assert list(res.stats["heavy_dims"]) == m["heavy_dims"], m["key"]
+            if m["counts"]:
+                assert np.array_equal(res.counts, z[m["key"] + "_counts"]), (m["key"], thr)
+
+
+def test_star_errors_and_k2_equals_two_path():
+    from paper_2002_12459_b200.errors import StarResourceError
+    from paper_2002_12459_b200.joinproject import star_join, two_path_join
+    from paper_2002_12459_b200.optimizer import ThresholdPlan
+    from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce_many
+    rng = np.random.default_rng(11)
+    rels = semi_join_reduce_many([Relation.from_raw_pairs(f"R{i}", random_pairs(rng, 200, 12, 6)) for i in range(3)])
+    idxs = [build_indexed(x) for x in rels]
+    with pytest.raises(StarResourceError):
+        star_join(idxs, 1, 1, heavy_rows_cap=2)
+    with pytest.raises(ValueError):
+        star_join(idxs[:1], 2, 2)
+    with pytest.raises(ValueError):
+        star_join(idxs, 0, 2)
+    a = star_join(idxs[:2], 2, 2)
+    b = two_path_join(idxs[0], idxs[1], plan=ThresholdPlan("partitioned", 2, 2))
+    assert np.array_equal(a.codes, b.codes)
+
+
+def test_star_zipf_k3_vs_oracle(oracle):
+    from paper_2002_12459_b200.joinproject import star_join
+    from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce_many
+    rng = np.random.default_rng(7)
+    raws = [np.array(zipf_pairs(rng, 3000, 60, 400, 1.3)) for _ in range(3)]
+    rels = semi_join_reduce_many([Relation.from_raw_pairs(f"R{i}", r) for i, r in enumerate(raws)])
+    idxs = [build_indexed(x) for x in rels]
+    orels = oracle.semi_join_many([oracle.encode(r) for r in raws])
+    exp = oracle.star(orels, 100, 1, want_counts=True, cap=1 << 30)
+    got = star_join(idxs, 100, 1, want_counts=True, heavy_rows_cap=1 << 30)
+    assert np.array_equal(got.codes, exp.codes) and np.array_equal(got.counts, exp.counts)
+    assert list(got.stats["heavy_dims"]) == list(exp.stats["heavy_dims"])
