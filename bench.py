@@ -8,9 +8,9 @@ on [0,200k), seeds 2/3; output = sorted distinct packed int64 (x,z) codes,
 One step = the whole device path from HBM-resident CSR inputs: degree split,
 heavy operand build, tcgen05 heavy product, light expansion, merge/emission
 of every chunk's sorted codes into HBM.  Multi-GPU: contiguous dense-x
-ranges balanced by witness work, S replicated (weak sharding of independent
-output rows, no data-path collective); value = all ranks' |OUT| / max rank
-time.
+ranges balanced by witness work, S replicated, no data-path collective (the
+one join's output rows are split across ranks: strong scaling); value = all
+ranks' |OUT| / max rank time.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -234,7 +234,7 @@ def run_reference(args):
     line = {
         "metric": METRIC, "impl": "reference", "value": v, "unit": "tuples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(args.steps, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"{args.config} x-slices of {nx} dense x (two_path_join, default plan)",
                    "config_name": args.config},
         "cpu_baseline": {"value": v, "unit": "tuples/s", "cores": cores, "kind": "port",
@@ -357,7 +357,8 @@ def run_b200(args):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(dominant)
+            t = json.load(f).get(dominant)
+        traffic = t.get("dram_bytes_per_launch") if isinstance(t, dict) else t
     dom = phase_info.get(dominant, {})
     if dominant == "heavy_mma":
         roofline = {"bound": "tensor", "achieved": dom.get("achieved"), "peak": dom.get("peak_datasheet"),
@@ -390,7 +391,7 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_step_g, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": wl.description + " (BASELINE configs[1])", "config_name": args.config,
                        "out_tuples_per_step": out_total, "plan": [plan.strategy, d1, d2],
                        "k_heavy": stats.k_heavy, "kpad": stats.kpad, "chunk_rows": args.chunk_rows,
