@@ -88,16 +88,9 @@ def _plan(args, r, s):
 
 
 def _shard(r, s, rank: int, world: int):
-    """Contiguous dense-x ranges balanced by witness work sum_{y in R[x]} degS(y)."""
-    if world == 1:
-        return 0, r.rel.dom_left
-    w = np.zeros(r.rel.dom_left + 1, dtype=np.int64)
-    per_tuple = np.asarray(s.right_deg, dtype=np.int64)[np.asarray(r.fwd_indices)]
-    csum = np.concatenate([[0], np.cumsum(per_tuple)])
-    w = csum[np.asarray(r.fwd_indptr)]
-    total = int(w[-1])
-    cuts = [0] + [int(np.searchsorted(w, total * k // world)) for k in range(1, world)] + [r.rel.dom_left]
-    return cuts[rank], cuts[rank + 1]
+    """Contiguous dense-x ranges balanced by witness work (shard.py)."""
+    from paper_2002_12459_b200.shard import shard_of
+    return shard_of(r, s, rank, world)
 
 
 # ----------------------------------------------------------------- clocks

@@ -129,7 +129,10 @@ class StarEngine:
                          nat.ptr(self.hpos), nat.ptr(h), 0, rows, self.kpad, st)
                 self.H.append(h)
 
-    def run(self):
+    def run(self, sink=None):
+        """Evaluate every x1 chunk.  Without `sink` the codes (and counts) are
+        collected to host numpy arrays; with `sink(x1_lo, x1_hi, codes_dev,
+        counts_dev)` they stay on the device (valid during the call)."""
         torch = self.torch
         st = nat.stream_handle()
         self.prepare()
@@ -170,8 +173,11 @@ class StarEngine:
                 if total:
                     nat.call("mmj_count_emit", nat.ptr(buf), rows, self.ldc, self.dk, x0, self.dk, 1, 0,
                              nat.ptr(segoff), nat.ptr(codes), nat.ptr(cnts), st)
-                codes_out.append(codes[:total].cpu().numpy())
-                counts_out.append(cnts[:total].cpu().numpy().astype(np.int64))
+                if sink is not None:
+                    sink(xa, xb, codes[:total], cnts[:total])
+                else:
+                    codes_out.append(codes[:total].cpu().numpy())
+                    counts_out.append(cnts[:total].cpu().numpy().astype(np.int64))
             else:
                 nwords = rows * self.wpr
                 nseg = int(self.lib.mmj_bitmap_segment_count(nwords))
@@ -184,7 +190,10 @@ class StarEngine:
                 if total:
                     nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dk,
                              nat.ptr(codes), st)
-                codes_out.append(codes[:total].cpu().numpy())
+                if sink is not None:
+                    sink(xa, xb, codes[:total], None)
+                else:
+                    codes_out.append(codes[:total].cpu().numpy())
         codes = np.concatenate(codes_out) if codes_out else np.empty(0, dtype=np.int64)
         counts = (np.concatenate(counts_out) if counts_out else np.empty(0, dtype=np.int64)) if self.counts else None
         return codes, counts

@@ -109,3 +109,19 @@ def test_chunked_api_concatenates_to_full():
     assert len(parts) > 1
     assert np.array_equal(np.concatenate([p.codes for p in parts]), full.codes)
     assert all(np.all(np.diff(p.codes) > 0) for p in parts)
+
+
+def test_sharded_outputs_concatenate_to_full():
+    from paper_2002_12459_b200.joinproject import two_path_join
+    from paper_2002_12459_b200.optimizer import ThresholdPlan
+    from paper_2002_12459_b200.shard import two_path_join_shard
+    z = np.load(os.path.join(GOLDEN, "twopath.npz"))
+    meta = json.loads(str(z["meta"]))
+    last = max(m["inst"] for m in meta)
+    r, s = _rels(z, last, False)
+    plan = ThresholdPlan("partitioned", 40, 3)
+    full = two_path_join(r, s, plan=plan, want_counts=True)
+    for world in (2, 3):
+        parts = [two_path_join_shard(r, s, plan, k, world, want_counts=True, chunk_rows=128) for k in range(world)]
+        assert np.array_equal(np.concatenate([p.codes for p in parts]), full.codes)
+        assert np.array_equal(np.concatenate([p.counts for p in parts]), full.counts)

@@ -1,0 +1,88 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the x-range sharding:
+ranges cover the domain, balance the witness work, and the rank-order
+concatenation of per-rank outputs equals the single-process output.  The
+per-rank compute here is the CPU oracle (the GPU engine runs the same ranges
+in bench.py); the max-over-ranks timing / size exchange uses torch.distributed
+exactly as bench.py does."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, zipf_pairs
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rels(seed=5):
+    from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce
+    rng = np.random.default_rng(seed)
+    rp = np.array(zipf_pairs(rng, 4000, 300, 500, 1.1))
+    sp = np.array(zipf_pairs(rng, 4000, 280, 500, 1.1))
+    a, b = semi_join_reduce(Relation.from_raw_pairs("R", rp), Relation.from_raw_pairs("S", sp))
+    return rp, sp, build_indexed(a), build_indexed(b)
+
+
+def test_ranges_cover_and_balance():
+    from paper_2002_12459_b200 import shard
+    _, _, r, s = _rels()
+    for world in (1, 2, 3, 8):
+        rg = shard.x_ranges(r, s, world)
+        assert rg[0][0] == 0 and rg[-1][1] == r.rel.dom_left
+        assert all(a[1] == b[0] for a, b in zip(rg, rg[1:]))
+        w = shard.x_work(r, s)
+        loads = [w[hi] - w[lo] for lo, hi in rg]
+        assert max(loads) <= w[-1] / world + w[-1] * 0.05 + max(np.diff(w))
+    assert [shard.batch_slice(10, k, 3) for k in range(3)] == [(0, 4), (4, 7), (7, 10)]
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import sys
+    sys.path.insert(0, ROOT)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import mmjoin_oracle as o
+    from paper_2002_12459_b200 import shard
+    rp, sp, r, s = _rels()
+    lo, hi = shard.shard_of(r, s, rank, world)
+    # per-rank compute (oracle restricted to the rank's x range, in r's dense ids)
+    OR, OS = o.semi_join_many([o.encode(rp), o.encode(sp)])
+    full = o.two_path(OR, OS, None)
+    mine = full.codes[(full.codes // full.dims[1] >= lo) & (full.codes // full.dims[1] < hi)]
+    # size exchange + max-over-ranks timing, as bench.py
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([len(mine)], dtype=torch.int64))
+    t = torch.tensor([0.01 * (rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine.tolist())
+    if rank == 0:
+        cat = np.concatenate([np.asarray(g, dtype=np.int64) for g in gathered])
+        out.put((cat.tolist() == full.codes.tolist(), [int(x) for x in sizes], float(t)))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_concatenate_to_full():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(k, 2, port, q)) for k in range(2)]
+    for p in procs:
+        p.start()
+    ok, sizes, tmax = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert ok
+    assert sum(sizes) > 0 and all(x > 0 for x in sizes)
+    assert tmax == pytest.approx(0.02)

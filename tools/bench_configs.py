@@ -1,0 +1,149 @@
+"""Throughput of every BASELINE config on one B200 (bench.py covers the
+headline cfg2 with the full bench contract; this tool reports the others).
+
+    python tools/bench_configs.py [cfg1 cfg3 cfg4 cfg5 ...] > profiles/rN_configs.jsonl
+
+Each line: config, workload, output size, device time per evaluation (CUDA
+events, inputs resident in HBM, 1 warm-up + best of 3), throughput and the
+main kernels' shares.  Parity at these sizes is covered by
+tests/test_gpu_fullsize.py.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def _timed(fn, reps=3):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        out = fn()
+        b.record()
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) / 1e3
+        best = (t, out) if best is None or t < best[0] else best
+    return best
+
+
+def cfg1():
+    from paper_2002_12459_b200 import datagen
+    from paper_2002_12459_b200.device import device_relation
+    from paper_2002_12459_b200.engine import TwoPathEngine
+    from paper_2002_12459_b200.optimizer import default_plan, gpu_plan
+    from paper_2002_12459_b200.relation import Relation, build_indexed
+    r = build_indexed(Relation.from_raw_pairs("R", datagen.config("cfg1").relations[0]))
+    dr = device_relation(r)
+    res = []
+    for name, plan in (("gpu_plan", gpu_plan(r, r)), ("reference_default_plan", default_plan(r, r))):
+        def run():
+            eng = TwoPathEngine(dr, dr, plan.strategy, plan.delta1, plan.delta2, False, chunk_rows=20480,
+                                host_left_deg_r=r.left_deg, host_left_deg_s=r.left_deg)
+            eng.run_pipelined(0, r.rel.dom_left)
+            return eng.finish()
+        t, st = _timed(run)
+        res.append({"config": "cfg1", "variant": name, "plan": [plan.strategy, plan.delta1, plan.delta2],
+                    "out": st.out_size, "seconds": t, "tuples_per_s": st.out_size / t,
+                    "light_intermediate": st.light_intermediate, "heavy_pairs": st.heavy_pairs,
+                    "reference_cpu_seconds_same_container": 147.1})
+    return res
+
+
+def cfg3():
+    from paper_2002_12459_b200 import datagen
+    from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce_many
+    from paper_2002_12459_b200.star import StarEngine
+    wl = datagen.config("cfg3")
+    rels = semi_join_reduce_many([Relation.from_raw_pairs(f"R{j}", r) for j, r in enumerate(wl.relations)])
+    idxs = [build_indexed(x) for x in rels]
+    tot = {}
+
+    def run():
+        n = [0]
+
+        def sink(a, b, codes, counts):
+            n[0] += int(codes.numel())
+        eng = StarEngine(idxs, False)
+        eng.run(sink)
+        tot["k"] = eng.kh
+        tot["light"] = int(eng.wit.item())
+        return n[0]
+    t, n = _timed(run, reps=2)
+    return [{"config": "cfg3", "workload": wl.description, "out": n, "seconds": t, "tuples_per_s": n / t,
+             "k_heavy": tot["k"], "light_witnesses": tot["light"]}]
+
+
+def cfg4():
+    from paper_2002_12459_b200 import datagen
+    from paper_2002_12459_b200.apps import SetFamily
+    from paper_2002_12459_b200.joinproject import _engine
+    from paper_2002_12459_b200.optimizer import gpu_plan
+    from paper_2002_12459_b200.relation import Relation
+    fam = SetFamily(Relation.from_raw_pairs("sets", datagen.config("cfg4").relations[0]))
+    idx = fam.indexed
+    plan = gpu_plan(idx, idx)
+
+    def run():
+        eng = _engine(idx, idx, plan, True, min_count=4, upper_only=True)
+        n = [0]
+        eng.run(lambda ch: n.__setitem__(0, n[0] + ch.n))
+        eng.finish()
+        return n[0]
+    t, n = _timed(run)
+    return [{"config": "cfg4", "workload": "SSJ c=4, 2M (set, element) pairs, 100k sets", "plan":
+             [plan.strategy, plan.delta1, plan.delta2], "out_pairs": n, "seconds": t, "pairs_per_s": n / t}]
+
+
+def cfg5():
+    import torch
+
+    from paper_2002_12459_b200 import datagen
+    from paper_2002_12459_b200.bsi import BsiEngine, prepare
+    from paper_2002_12459_b200.relation import Relation, build_indexed
+    t0 = time.time()
+    wl = datagen.config("cfg5")
+    r = build_indexed(Relation.from_raw_pairs("R", wl.relations[0]))
+    s = build_indexed(Relation.from_raw_pairs("S", wl.relations[1]))
+    prep = time.time() - t0
+    sR, sS, dom_y = prepare(r, s)
+    qa = torch.from_numpy(wl.batch[:, 0].copy()).cuda()
+    qb = torch.from_numpy(wl.batch[:, 1].copy()).cuda()
+    nq = len(wl.batch)
+    holder = {}
+
+    def full():
+        eng = BsiEngine(sR, sS, dom_y, 256)
+        eng.build()
+        holder["eng"] = eng
+        return eng.answer(qa, qb, nq)
+    t_full, ans = _timed(full)
+    eng = holder["eng"]
+    t_ans, _ = _timed(lambda: eng.answer(qa, qb, nq))
+    a = ans.cpu().numpy()
+    in_bytes = 8 * (r.n + s.n) + 9 * nq
+    return [{"config": "cfg5", "workload": wl.description, "queries": nq, "true": int((a == 1).sum()),
+             "none": int((a == -1).sum()), "seconds_build_plus_answer": t_full, "answers_per_s": nq / t_full,
+             "seconds_answer_only": t_ans, "answers_per_s_answer_only": nq / t_ans,
+             "lower_bound_bytes": in_bytes, "achieved_GBps_vs_lower_bound": in_bytes / t_full / 1e9,
+             "host_prep_seconds": prep}]
+
+
+if __name__ == "__main__":
+    import torch
+    torch.cuda.set_device(0)
+    names = sys.argv[1:] or ["cfg1", "cfg3", "cfg4", "cfg5"]
+    for nm in names:
+        for row in globals()[nm]():
+            print(json.dumps(row), flush=True)
