@@ -36,7 +36,7 @@ constexpr int TUP_BATCH = TM_THREADS;   // light tuples staged per round
 constexpr int TILE_WORDS = 16384;       // up to 64 KB of bitmap per tile (whole rows up to 524288 cells)
 constexpr int SHORT_LIST = 96;          // lists up to this length are filtered, longer ones bisected
 constexpr int EM_WARPS = 8;
-constexpr int EM_SEGS = 64;             // segments per emission CTA
+constexpr int EM_SEGS = EM_WARPS;       // one segment per warp: short-lived CTAs balance best (emit_lab)
 
 __device__ __forceinline__ void st_cs2(int64_t* p, int64_t a, int64_t b) {
   asm volatile("st.global.cs.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
@@ -249,12 +249,10 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const uint32_t* __restri
   // XOR-ing the bank bits with the 32-slot row index spreads their stores
   auto sl = [](int k) { return k ^ ((k >> 5) & 31); };
   const int64_t s0 = (int64_t)blockIdx.x * EM_SEGS;
-  uint32_t next = (s0 + warp < nseg) ? bm[(s0 + warp) * 32 + lane] : 0u;
   for (int si = warp; si < EM_SEGS; si += EM_WARPS) {
     const int64_t s = s0 + si;
     if (s >= nseg) break;
-    uint32_t word = next;
-    if (si + EM_WARPS < EM_SEGS && s + EM_WARPS < nseg) next = bm[(s + EM_WARPS) * 32 + lane];   // prefetch
+    uint32_t word = bm[s * 32 + lane];
     const int c = __popc(word);
     int incl = c;
 #pragma unroll

@@ -22,6 +22,16 @@ __device__ __forceinline__ void st_wb2(int64_t* p, int64_t a, int64_t b) {
   asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
+__device__ __forceinline__ void st_cs4(int64_t* p, int64_t a, int64_t b, int64_t c, int64_t d) {
+  asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+__device__ __forceinline__ void st_wb4(int64_t* p, int64_t a, int64_t b, int64_t c, int64_t d) {
+  asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+__device__ __forceinline__ void st_na4(int64_t* p, int64_t a, int64_t b, int64_t c, int64_t d) {
+  asm volatile("st.global.L1::no_allocate.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
 __device__ __forceinline__ int warp_incl(int c, int lane) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -32,14 +42,15 @@ __device__ __forceinline__ int warp_incl(int c, int lane) {
 }
 
 // V: variant id
-template <int V>
+template <int V, int SEGS = SEGS_PER_CTA, int ORDER = 0>
 __global__ void __launch_bounds__(WARPS * 32) k_emit(const uint32_t* __restrict__ bm, const int64_t* __restrict__ segoff,
                                                      int64_t nseg, int64_t* __restrict__ out_all) {
   __shared__ __align__(16) uint32_t stage_all[WARPS][1024 + 8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* stage = stage_all[warp];
-  const int64_t s0 = (int64_t)blockIdx.x * SEGS_PER_CTA;
-  for (int si = warp; si < SEGS_PER_CTA; si += WARPS) {
+  const int64_t s0 = (int64_t)blockIdx.x * SEGS;
+  for (int j = 0; j < SEGS / WARPS; ++j) {
+    const int si = ORDER == 0 ? warp + j * WARPS : warp * (SEGS / WARPS) + j;
     const int64_t s = s0 + si;
     if (s >= nseg) break;
     uint32_t word = bm[s * 32 + lane];
@@ -106,6 +117,92 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const uint32_t* __restrict_
       }
       const int tail = max(4, nq << 2);
       if (tail + lane < endk) st_cs(out + tail + lane - h, base + stage[sl(tail + lane)]);
+    } else if (V == 8) {  // V0 staging (lsb, xor5) + 32 B quad stores
+      int k = incl - c;
+      while (word) {
+        const int b = __ffs(word) - 1;
+        stage[k ^ ((k >> 5) & 31)] = off0 + b;
+        ++k;
+        word &= word - 1;
+      }
+      __syncwarp();
+      auto sl = [](int q) { return q ^ ((q >> 5) & 31); };
+      const int h = min((int)((4 - ((reinterpret_cast<uintptr_t>(out) >> 3) & 3)) & 3), tot);
+      if (lane < h) st_cs(out + lane, base + stage[sl(lane)]);
+      const int nq = (tot - h) >> 2;
+      for (int q = lane; q < nq; q += 32) {
+        const int i = h + 4 * q;
+        st_wb4(out + i, base + stage[sl(i)], base + stage[sl(i + 1)], base + stage[sl(i + 2)], base + stage[sl(i + 3)]);
+      }
+      const int done = h + 4 * nq;
+      if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(done + lane)]);
+    } else if (V == 9) {  // two bits per iteration
+      int k = incl - c;
+      while (word) {
+        const int b0 = __ffs(word) - 1;
+        word &= word - 1;
+        const int b1 = __ffs(word) - 1;   // -1 when exhausted
+        word &= word - 1;
+        stage[k ^ ((k >> 5) & 31)] = off0 + b0;
+        if (b1 >= 0) stage[(k + 1) ^ (((k + 1) >> 5) & 31)] = off0 + b1;
+        k += 2;
+      }
+      __syncwarp();
+      const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
+      auto sl = [](int q) { return q ^ ((q >> 5) & 31); };
+      if (lane < h) st_cs(out + lane, base + stage[sl(lane)]);
+      const int np = (tot - h) >> 1;
+      for (int p = lane; p < np; p += 32) {
+        const int i = h + 2 * p;
+        st_cs2(out + i, base + stage[sl(i)], base + stage[sl(i + 1)]);
+      }
+      const int done = h + 2 * np;
+      if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(done + lane)]);
+    } else if (V == 10) {  // 16-bit offsets, two per 32-bit store; reader takes 32-bit pairs
+      uint16_t* st16 = reinterpret_cast<uint16_t*>(stage);
+      auto sl32 = [](int q) { return q ^ ((q >> 5) & 31); };   // swizzle on 32-bit word index
+      int k = incl - c;
+      if ((k & 1) && word) {          // odd start: one 16-bit store to align
+        const int b = __ffs(word) - 1;
+        word &= word - 1;
+        st16[2 * sl32(k >> 1) + 1] = (uint16_t)(off0 + b);
+        ++k;
+      }
+      while (word) {
+        const int b0 = __ffs(word) - 1;
+        word &= word - 1;
+        if (word) {
+          const int b1 = __ffs(word) - 1;
+          word &= word - 1;
+          stage[sl32(k >> 1)] = (off0 + b0) | ((off0 + b1) << 16);
+          k += 2;
+        } else {
+          st16[2 * sl32(k >> 1)] = (uint16_t)(off0 + b0);
+          ++k;
+        }
+      }
+      __syncwarp();
+      const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
+      if (lane < h) st_cs(out + lane, base + st16[2 * sl32(0)]);
+      const int np = (tot - h) >> 1;
+      for (int p = lane; p < np; p += 32) {
+        const int i = h + 2 * p;
+        uint32_t lo, hi;
+        if ((i & 1) == 0) {
+          const uint32_t w2 = stage[sl32(i >> 1)];
+          lo = w2 & 0xFFFFu;
+          hi = w2 >> 16;
+        } else {
+          lo = st16[2 * sl32(i >> 1) + 1];
+          hi = st16[2 * sl32((i + 1) >> 1)];
+        }
+        st_cs2(out + i, base + lo, base + hi);
+      }
+      const int done = h + 2 * np;
+      if (lane < tot - done) {
+        const int i = done + lane;
+        st_cs(out + i, base + st16[2 * sl32(i >> 1) + (i & 1)]);
+      }
     } else if (V == 4) {  // no staging: each lane writes its own run (uncoalesced)
       int k = incl - c;
       while (word) {
@@ -170,10 +267,49 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const uint32_t* __restrict_
   }
 }
 
-template <int V>
-float run(const uint32_t* bm, const int64_t* segoff, int64_t nseg, int64_t* out) {
-  const int grid = (int)((nseg + SEGS_PER_CTA - 1) / SEGS_PER_CTA);
-  k_emit<V><<<grid, WARPS * 32>>>(bm, segoff, nseg, out);
+// pure store kernels: the HBM write ceiling for different store shapes
+template <int W>
+__global__ void __launch_bounds__(256) k_store(int64_t* __restrict__ out, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i * 2 * W < n; i += stride) {
+    int64_t* p = out + i * 2 * W;
+    if (W == 1) {
+      st_cs2(p, i, i + 1);
+    } else if (W == 2) {   // 32 B per thread, two 16 B stores
+      st_cs2(p, i, i + 1);
+      st_cs2(p + 2, i + 2, i + 3);
+    } else if (W == 3) {
+      st_wb2(p, i, i + 1);
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_store4(int64_t* __restrict__ out, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i * 4 < n; i += stride) {
+    int64_t* p = out + i * 4;
+    if (W == 0) st_cs4(p, i, i + 1, i + 2, i + 3);
+    else if (W == 1) st_wb4(p, i, i + 1, i + 2, i + 3);
+    else st_na4(p, i, i + 1, i + 2, i + 3);
+  }
+}
+
+// block-contiguous: CTA b writes [b*CH, (b+1)*CH) with 32 B per thread per step
+template <int CH_ELEMS>
+__global__ void __launch_bounds__(256) k_store_blk(int64_t* __restrict__ out, int64_t n) {
+  const int64_t base = (int64_t)blockIdx.x * CH_ELEMS;
+#pragma unroll 4
+  for (int j = threadIdx.x * 4; j < CH_ELEMS; j += 256 * 4) {
+    const int64_t i = base + j;
+    if (i + 3 < n) st_wb4(out + i, i, i + 1, i + 2, i + 3);
+  }
+}
+
+template <int CH>
+float run_blk(int64_t* out, int64_t n) {
+  const int grid = (int)((n + CH - 1) / CH);
+  k_store_blk<CH><<<grid, 256>>>(out, n);
   CK(cudaDeviceSynchronize());
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -181,7 +317,70 @@ float run(const uint32_t* bm, const int64_t* segoff, int64_t nseg, int64_t* out)
   float best = 1e9;
   for (int r = 0; r < 5; ++r) {
     cudaEventRecord(a);
-    k_emit<V><<<grid, WARPS * 32>>>(bm, segoff, nseg, out);
+    k_store_blk<CH><<<grid, 256>>>(out, n);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+template <int W>
+float run_store4(int64_t* out, int64_t n) {
+  const int grid = 148 * 8;
+  k_store4<W><<<grid, 256>>>(out, n);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    k_store4<W><<<grid, 256>>>(out, n);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+template <int W>
+float run_store(int64_t* out, int64_t n) {
+  const int grid = 148 * 8;
+  k_store<W><<<grid, 256>>>(out, n);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    k_store<W><<<grid, 256>>>(out, n);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+template <int V, int SEGS = SEGS_PER_CTA, int ORDER = 0>
+float run(const uint32_t* bm, const int64_t* segoff, int64_t nseg, int64_t* out) {
+  const int grid = (int)((nseg + SEGS - 1) / SEGS);
+  k_emit<V, SEGS, ORDER><<<grid, WARPS * 32>>>(bm, segoff, nseg, out);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    k_emit<V, SEGS, ORDER><<<grid, WARPS * 32>>>(bm, segoff, nseg, out);
     cudaEventRecord(b);
     CK(cudaEventSynchronize(b));
     float ms;
@@ -221,6 +420,18 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(dso, so.data(), (nseg + 1) * 8, cudaMemcpyHostToDevice));
   const double bytes = acc * 8.0;
   printf("density %.2f codes %lld (%.1f GB)\n", density, (long long)acc, bytes / 1e9);
+  {
+    float a = run<0, 8>(dbm, dso, nseg, dout), b = run<0, 16>(dbm, dso, nseg, dout), c = run<0, 256>(dbm, dso, nseg, dout);
+    float d = run<0, 64, 1>(dbm, dso, nseg, dout), e = run<0, 256, 1>(dbm, dso, nseg, dout), f = run<0, 1024, 1>(dbm, dso, nseg, dout);
+    printf("V0 segs 8 / 16 / 256 (interleaved): %.1f %.1f %.1f GB/s\n", bytes / (a * 1e-3) / 1e9, bytes / (b * 1e-3) / 1e9, bytes / (c * 1e-3) / 1e9);
+    printf("V0 segs 64 / 256 / 1024 (contiguous per warp): %.1f %.1f %.1f GB/s\n", bytes / (d * 1e-3) / 1e9, bytes / (e * 1e-3) / 1e9, bytes / (f * 1e-3) / 1e9);
+  }
+  const float t8 = run<8>(dbm, dso, nseg, dout);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "V8 xor5 + 32B quads", t8, bytes / (t8 * 1e-3) / 1e9);
+  const float t9 = run<9>(dbm, dso, nseg, dout);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "V9 2 bits/iter", t9, bytes / (t9 * 1e-3) / 1e9);
+  const float t10 = run<10>(dbm, dso, nseg, dout);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "V10 16-bit staging", t10, bytes / (t10 * 1e-3) / 1e9);
   const char* names[] = {"V0 lsb xor5 pairs", "V1 msb quad LDS128", "V2 lsb quad LDS128", "V3 V2 + wb stores",
                          "V4 unstaged lane runs", "V5 store ceiling", "V6 unswizzled pairs", "V7 2-chain xor5"};
   float t[8];
@@ -233,5 +444,17 @@ int main(int argc, char** argv) {
   t[6] = run<6>(dbm, dso, nseg, dout);
   t[7] = run<7>(dbm, dso, nseg, dout);
   for (int v = 0; v < 8; ++v) printf("%-24s %8.3f ms  %7.1f GB/s\n", names[v], t[v], bytes / (t[v] * 1e-3) / 1e9);
+  const float s1 = run_store<1>(dout, acc), s2 = run_store<2>(dout, acc), s3 = run_store<3>(dout, acc);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "store 16B cs", s1, bytes / (s1 * 1e-3) / 1e9);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "store 2x16B cs", s2, bytes / (s2 * 1e-3) / 1e9);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "store 16B wb", s3, bytes / (s3 * 1e-3) / 1e9);
+  const float q0 = run_store4<0>(dout, acc), q1 = run_store4<1>(dout, acc), q2 = run_store4<2>(dout, acc);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "store 32B cs", q0, bytes / (q0 * 1e-3) / 1e9);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "store 32B wb", q1, bytes / (q1 * 1e-3) / 1e9);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "store 32B L1::no_alloc", q2, bytes / (q2 * 1e-3) / 1e9);
+  const float b1 = run_blk<4096>(dout, acc), b2 = run_blk<16384>(dout, acc), b3 = run_blk<65536>(dout, acc);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "blk 32KB", b1, bytes / (b1 * 1e-3) / 1e9);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "blk 128KB", b2, bytes / (b2 * 1e-3) / 1e9);
+  printf("%-24s %8.3f ms  %7.1f GB/s\n", "blk 512KB", b3, bytes / (b3 * 1e-3) / 1e9);
   return 0;
 }
