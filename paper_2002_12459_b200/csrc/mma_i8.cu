@@ -26,6 +26,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include "mmj_common.cuh"
 
 namespace mmj {
@@ -54,6 +56,7 @@ struct Params {
   int64_t n_cols;       // columns of the product (= rows of B)
   int num_kb;           // Kp / BK
   int stages;           // smem ring depth (2..STAGES)
+  int debug;            // 1: epilogue skips the bit packing (profiling experiment)
   int mode;
   int shift;            // ACC64 only
   void* out;            // BITMAP: uint32 words, COUNT32: int32, ACC64: int64
@@ -159,6 +162,29 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(int m, int n) {
         "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),           \
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])            \
       : "r"(taddr))
+
+// 16 pack::16b registers (32 columns, counts < 256) -> 32-bit nonzero mask
+__device__ __forceinline__ uint32_t pack_bits_u8(const uint32_t* r) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t p = __byte_perm(r[2 * j], r[2 * j + 1], 0x6420);          // [c3 c2 c1 c0]
+    const uint32_t nz = (((p & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | p) & 0x80808080u;   // byte MSB = (c != 0)
+    w |= ((nz * 0x00204081u) >> 28) << (4 * j);                                // bits 7,15,23,31 -> 4 bits
+  }
+  return w;
+}
+
+// 16 pack::16b registers (32 columns, counts < 2^16) -> 32-bit nonzero mask
+__device__ __forceinline__ uint32_t pack_bits_u16(const uint32_t* r) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t nz = (((r[i] & 0x7FFF7FFFu) + 0x7FFF7FFFu) | r[i]) & 0x80008000u;
+    w |= ((nz * 0x8001u) >> 30) << (2 * i);                                     // bits 15,31 -> 2 bits
+  }
+  return w;
+}
 
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -300,17 +326,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
-        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          w0 |= ((r0[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-          w0 |= ((r0[i] >> 16) ? 1u : 0u) << (2 * i + 1);
-          w1 |= ((r0[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-          w1 |= ((r0[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
-          w2 |= ((r1[i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-          w2 |= ((r1[i] >> 16) ? 1u : 0u) << (2 * i + 1);
-          w3 |= ((r1[16 + i] & 0xFFFFu) ? 1u : 0u) << (2 * i);
-          w3 |= ((r1[16 + i] >> 16) ? 1u : 0u) << (2 * i + 1);
+        uint32_t w0, w1, w2, w3;
+        if (p.debug) {
+          w0 = r0[0] | r0[7]; w1 = r0[16]; w2 = r1[3]; w3 = r1[31];
+        } else if (p.num_kb == 1) {
+          // K <= 128: every count < 256 -> 4 counts per register (PRMT), SWAR
+          // nonzero test, 4-flag movemask by one multiply
+          w0 = pack_bits_u8(r0);
+          w1 = pack_bits_u8(r0 + 16);
+          w2 = pack_bits_u8(r1);
+          w3 = pack_bits_u8(r1 + 16);
+        } else {
+          w0 = pack_bits_u16(r0);
+          w1 = pack_bits_u16(r0 + 16);
+          w2 = pack_bits_u16(r1);
+          w3 = pack_bits_u16(r1 + 16);
         }
         if (row_ok) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + (col0 >> 5);
@@ -453,6 +483,14 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   p.n_cols = b_rows;
   p.num_kb = (int)(k_len / BK);
   p.stages = p.num_kb <= 2 ? 2 : STAGES;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("MMJ_DEBUG_EPI");
+      dbg = (e && e[0] == '1') ? 1 : 0;
+    }
+    p.debug = dbg;
+  }
   p.mode = mode;
   p.shift = shift;
   p.out = out;

@@ -36,7 +36,7 @@ constexpr int TUP_BATCH = TM_THREADS;   // light tuples staged per round
 constexpr int TILE_WORDS = 16384;       // up to 64 KB of bitmap per tile (whole rows up to 524288 cells)
 constexpr int SHORT_LIST = 96;          // lists up to this length are filtered, longer ones bisected
 constexpr int EM_WARPS = 8;
-constexpr int EM_SEGS = EM_WARPS;       // one segment per warp: short-lived CTAs balance best (emit_lab)
+constexpr int EM_SEGS = 64;             // segments per emission CTA (8 per warp: balances uneven row densities)
 
 __device__ __forceinline__ void st_cs2(int64_t* p, int64_t a, int64_t b) {
   asm volatile("st.global.cs.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
