@@ -57,7 +57,9 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-slice-x", type=int, default=32, help="x values per reference-arm sample")
     ap.add_argument("--x-limit", type=int, default=0, help="debug: only the first X output rows")
-    ap.add_argument("--serial", action="store_true", help="one stream (no emission/compute overlap)")
+    ap.add_argument("--schedule", default="mma_ahead", choices=["serial", "mma_ahead", "pipelined"],
+                    help="chunk schedule: one stream, heavy product one chunk ahead on a side stream, "
+                         "or emission on a side stream")
     return ap.parse_args()
 
 
@@ -274,11 +276,13 @@ def run_b200(args):
 
     def step(timer=None):
         eng = make_engine()
-        if args.serial:
+        if args.schedule == "serial":
             eng.timer = timer
             eng.prepare()
             for a, b in eng.chunk_bounds(x_lo, x_hi):
                 eng.run_chunk(a, b, sync=False)
+        elif args.schedule == "mma_ahead":
+            eng.run_mma_ahead(x_lo, x_hi, timer=timer)
         else:
             eng.run_pipelined(x_lo, x_hi, timer=timer)
         return eng.finish()
@@ -387,7 +391,7 @@ def run_b200(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": wl.description + " (BASELINE configs[1])", "config_name": args.config,
                        "out_tuples_per_step": out_total, "plan": [plan.strategy, d1, d2],
-                       "k_heavy": stats.k_heavy, "kpad": stats.kpad, "chunk_rows": args.chunk_rows,
+                       "k_heavy": stats.k_heavy, "kpad": stats.kpad, "chunk_rows": args.chunk_rows, "schedule": args.schedule,
                        "chunks": stats.chunks, "light_intermediate": stats.light_intermediate,
                        "heavy_pairs": stats.heavy_pairs, "parallelism": f"x-range shards x{world}",
                        "l2": "256 MiB L2 flush before every timed step; each step writes ~1 TB of codes"},

@@ -303,6 +303,88 @@ class TwoPathEngine:
         self.stats.out_size += total
         return ChunkResult(x0, x1, total, codes[:total], None, light)
 
+    def run_mma_ahead(self, x_begin: int = 0, x_end: Optional[int] = None, timer=None):
+        """Projection with the heavy product of chunk i+1 running on a side
+        stream while chunk i's light merge, scan and emission run in order on
+        the current stream (the tensor-core kernel overlaps the HBM-bound
+        emission; the latency-bound merge keeps its SMs).  Chunk bitmaps are
+        double-buffered."""
+        if not self.fused:
+            raise ValueError("run_mma_ahead needs the bitmap (no counts) path")
+        torch = self.torch
+        self.prepare()
+        dr, ds = self.dr, self.ds
+        main = torch.cuda.current_stream()
+        if getattr(self, "_mma_stream", None) is None:
+            self._mma_stream = torch.cuda.Stream()
+        ms = self._mma_stream
+        ms.wait_stream(main)
+        hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
+        lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
+        lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
+        mst, sst = main.cuda_stream, ms.cuda_stream
+        rows_max = self.chunk_rows
+        codes = self.ws.get("codes", rows_max * self.dom_z, torch.int64)
+        bounds = list(self.chunk_bounds(x_begin, x_end))
+        bufs = [self.ws.get(f"bm{b}", rows_max * self.wpr, torch.int32) for b in (0, 1)]
+        freed = [None, None]
+        mma_done = {}
+
+        def issue_mma(i):
+            x0, x1 = bounds[i]
+            b = i & 1
+            if freed[b] is not None:
+                ms.wait_event(freed[b])
+            if timer is not None:
+                timer.start("heavy_mma", ms)
+            if self.A is not None:
+                nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
+                         self.kpad, 0, self.kpad, x0, x1 - x0, nat.MODE_BITMAP, 0, nat.ptr(bufs[b]), self.wpr,
+                         nat.ptr(self.nnz), 0, sst)
+            if timer is not None:
+                timer.stop("heavy_mma", ms)
+            ev = torch.cuda.Event()
+            ev.record(ms)
+            mma_done[i] = ev
+
+        if bounds:
+            issue_mma(0)
+        for i, (x0, x1) in enumerate(bounds):
+            if i + 1 < len(bounds):
+                issue_mma(i + 1)
+            b = i & 1
+            rows = x1 - x0
+            nseg = rows * self.wpr // 32
+            buf = bufs[b]
+            segcnt = self.ws.get("segcnt", rows_max * self.wpr // 32, torch.int32)
+            segoff = self.ws.get("segoff", rows_max * self.wpr // 32 + 1, torch.int64)
+            main.wait_event(mma_done.pop(i))
+            if timer is not None:
+                timer.start("light_merge", main)
+            nat.call("mmj_tile_merge", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
+                     nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp,
+                     nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(self.wit), mst)
+            if timer is not None:
+                timer.stop("light_merge", main)
+                timer.start("segments", main)
+            nat.call("mmj_exclusive_scan_i32", nat.ptr(segcnt), nat.ptr(segoff), nseg,
+                     nat.ptr(self.ws.scan_ws(rows_max * self.wpr // 32)), mst)
+            if timer is not None:
+                timer.stop("segments", main)
+                timer.start("emit", main)
+            nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dom_z,
+                     nat.ptr(codes), mst)
+            if timer is not None:
+                timer.stop("emit", main)
+            slot = self._async_slot()
+            slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            freed[b] = ev
+            self.stats.chunks += 1
+        main.wait_stream(ms)
+        return codes
+
     def run_pipelined(self, x_begin: int = 0, x_end: Optional[int] = None, timer=None):
         """Projection over [x_begin, x_end) with two streams: chunk i's
         emission (HBM-write bound) runs on a side stream while chunk i+1's
