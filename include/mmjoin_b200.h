@@ -41,6 +41,7 @@ extern "C" {
 #define MMJ_MODE_BITMAP 0      /* nonzero test -> 1 bit per (row, col)  */
 #define MMJ_MODE_COUNT32 1     /* exact int32 counts                    */
 #define MMJ_MODE_ACC64 2       /* out += count << shift (int64)         */
+#define MMJ_MODE_BITMAP_U8 3   /* BITMAP, caller guarantees counts < 256 (<= 255 nonzero K columns) */
 
 int mmj_abi_version(void);
 const char* mmj_last_error(void);

@@ -24,6 +24,7 @@ MMJ_ERR_CAPACITY = 5
 MODE_BITMAP = 0
 MODE_COUNT32 = 1
 MODE_ACC64 = 2
+MODE_BITMAP_U8 = 3
 
 P = C.c_void_p
 I64 = C.c_int64

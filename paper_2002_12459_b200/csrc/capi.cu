@@ -126,7 +126,7 @@ int mmj_light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0,
 int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_rows, int64_t kpad, int64_t k_off,
                   int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out, int64_t ld_out,
                   unsigned long long* nnz, int max_ctas, void* stream) {
-  if (mode < 0 || mode > 2) {
+  if (mode < 0 || mode > 3) {
     mmj::set_error("heavy_mma: unknown mode %d", mode);
     return MMJ_ERR_ARG;
   }

@@ -48,7 +48,7 @@ constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int smem_bytes_for(int stages) { return stages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/; }
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
-enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2 };
+enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3 };
 
 struct Params {
   int64_t m_begin;      // first A row of this launch (multiple of BM not required)
@@ -57,6 +57,7 @@ struct Params {
   int num_kb;           // Kp / BK
   int stages;           // smem ring depth (2..STAGES)
   int debug;            // 1: epilogue skips the bit packing (profiling experiment)
+  int small_counts;     // BITMAP: every product entry < 256 (K window <= 255 nonzero columns)
   int mode;
   int shift;            // ACC64 only
   void* out;            // BITMAP: uint32 words, COUNT32: int32, ACC64: int64
@@ -329,8 +330,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t w0, w1, w2, w3;
         if (p.debug) {
           w0 = r0[0] | r0[7]; w1 = r0[16]; w2 = r1[3]; w3 = r1[31];
-        } else if (p.num_kb == 1) {
-          // K <= 128: every count < 256 -> 4 counts per register (PRMT), SWAR
+        } else if (p.small_counts) {
+          // every count < 256 (K <= 255) -> 4 counts per register (PRMT), SWAR
           // nonzero test, 4-flag movemask by one multiply
           w0 = pack_bits_u8(r0);
           w1 = pack_bits_u8(r0 + 16);
@@ -461,7 +462,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
     set_error("heavy_mma: operand rows must be < 2^31");
     return MMJ_ERR_ARG;
   }
-  if (mode == BITMAP && (ld_out % 8 != 0 || ld_out * 32 < round_up(b_rows, BN))) {
+  if ((mode == BITMAP || mode == BITMAP_U8) && (ld_out % 8 != 0 || ld_out * 32 < round_up(b_rows, BN))) {
     set_error("heavy_mma: bitmap pitch %lld words too small / unaligned", (long long)ld_out);
     return MMJ_ERR_ARG;
   }
@@ -469,7 +470,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
     set_error("heavy_mma: count pitch must be a multiple of 4");
     return MMJ_ERR_ARG;
   }
-  if (mode == BITMAP && k_len > 65535) {
+  if ((mode == BITMAP || mode == BITMAP_U8) && k_len > 65535) {
     set_error("heavy_mma: BITMAP mode packs 16-bit counts; K window must be < 65536");
     return MMJ_ERR_ARG;
   }
@@ -483,6 +484,8 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   p.n_cols = b_rows;
   p.num_kb = (int)(k_len / BK);
   p.stages = p.num_kb <= 2 ? 2 : STAGES;
+  p.small_counts = (mode == BITMAP_U8 || k_len <= 255) ? 1 : 0;
+  if (mode == BITMAP_U8) p.mode = BITMAP;
   {
     static int dbg = -1;
     if (dbg < 0) {

@@ -155,6 +155,11 @@ class TwoPathEngine:
                      nat.ptr(self.ws.scan_ws(n)), st)
         self._prepared = True
 
+    def _bitmap_mode(self) -> int:
+        # every product entry counts <= K shared heavy y: with K <= 255 the
+        # epilogue may pack counts as bytes
+        return nat.MODE_BITMAP_U8 if 0 < self.stats.k_heavy <= 255 else nat.MODE_BITMAP
+
     def _any_heavy(self, host_deg, d: DeviceRelation) -> bool:
         if host_deg is not None:
             return bool((np.asarray(host_deg) > self.d2).any())
@@ -188,7 +193,7 @@ class TwoPathEngine:
         else:
             buf = self.ws.get("bm", rows * self.wpr, torch.int32)
             ld = self.wpr
-            mode = nat.MODE_BITMAP
+            mode = self._bitmap_mode()
         # heavy part (writes every cell of the chunk) or zero fill
         self._ph("heavy_mma", True)
         if self.A is not None:
@@ -339,7 +344,7 @@ class TwoPathEngine:
                 timer.start("heavy_mma", ms)
             if self.A is not None:
                 nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
-                         self.kpad, 0, self.kpad, x0, x1 - x0, nat.MODE_BITMAP, 0, nat.ptr(bufs[b]), self.wpr,
+                         self.kpad, 0, self.kpad, x0, x1 - x0, self._bitmap_mode(), 0, nat.ptr(bufs[b]), self.wpr,
                          nat.ptr(self.nnz), 0, sst)
             if timer is not None:
                 timer.stop("heavy_mma", ms)
@@ -422,7 +427,7 @@ class TwoPathEngine:
                 timer.start("heavy_mma", main)
             if self.A is not None:
                 nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
-                         self.kpad, 0, self.kpad, x0, rows, nat.MODE_BITMAP, 0, nat.ptr(buf), self.wpr,
+                         self.kpad, 0, self.kpad, x0, rows, self._bitmap_mode(), 0, nat.ptr(buf), self.wpr,
                          nat.ptr(self.nnz), 0, mst)
             if timer is not None:
                 timer.stop("heavy_mma", main)

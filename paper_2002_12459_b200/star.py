@@ -153,7 +153,8 @@ class StarEngine:
                 nat.call("mmj_star_operand", self.k, dims_arr, heavy_ptrs, self.kpad, xa, rows, nat.ptr(A), st)
                 B = self.H[-1]
                 nat.call("mmj_heavy_mma", nat.ptr(A), arows, nat.ptr(B), B.shape[0], self.kpad, 0, self.kpad, 0, rows,
-                         nat.MODE_COUNT32 if self.counts else nat.MODE_BITMAP, 0, nat.ptr(buf), ld, nat.ptr(self.nnz),
+                         nat.MODE_COUNT32 if self.counts else (nat.MODE_BITMAP_U8 if self.kh <= 255 else nat.MODE_BITMAP),
+                         0, nat.ptr(buf), ld, nat.ptr(self.nnz),
                          0, st)
             else:
                 buf.zero_()
