@@ -485,7 +485,6 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   p.num_kb = (int)(k_len / BK);
   p.stages = p.num_kb <= 2 ? 2 : STAGES;
   p.small_counts = (mode == BITMAP_U8 || k_len <= 255) ? 1 : 0;
-  if (mode == BITMAP_U8) p.mode = BITMAP;
   {
     static int dbg = -1;
     if (dbg < 0) {
@@ -494,7 +493,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
     }
     p.debug = dbg;
   }
-  p.mode = mode;
+  p.mode = mode == BITMAP_U8 ? BITMAP : mode;
   p.shift = shift;
   p.out = out;
   p.ld_out = ld_out;
