@@ -108,6 +108,7 @@ class TwoPathEngine:
         self._sizes_dev = None
         self._n_async = 0
         self.timer = None          # optional PhaseTimer (bench instrumentation)
+        self.mma_ctas = int(__import__("os").environ.get("MMJ_MMA_CTAS", "0"))   # 0 = one CTA per SM
 
     # ------------------------------------------------------------ prepare
     def _st(self):
@@ -319,11 +320,18 @@ class TwoPathEngine:
         torch = self.torch
         self.prepare()
         dr, ds = self.dr, self.ds
-        main = torch.cuda.current_stream()
+        caller = torch.cuda.current_stream()
+        lo_pri, hi_pri = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
         if getattr(self, "_mma_stream", None) is None:
-            self._mma_stream = torch.cuda.Stream()
+            # the in-order merge -> scan -> emit chain is the critical path: give
+            # it the high-priority stream so its CTAs are scheduled ahead of the
+            # side-stream heavy product's
+            self._mma_stream = torch.cuda.Stream(priority=0)
+            self._main_stream = torch.cuda.Stream(priority=-1)
         ms = self._mma_stream
-        ms.wait_stream(main)
+        main = self._main_stream
+        main.wait_stream(caller)
+        ms.wait_stream(caller)
         hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
         lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
         lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
@@ -345,7 +353,7 @@ class TwoPathEngine:
             if self.A is not None:
                 nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
                          self.kpad, 0, self.kpad, x0, x1 - x0, self._bitmap_mode(), 0, nat.ptr(bufs[b]), self.wpr,
-                         nat.ptr(self.nnz), 0, sst)
+                         nat.ptr(self.nnz), self.mma_ctas, sst)
             if timer is not None:
                 timer.stop("heavy_mma", ms)
             ev = torch.cuda.Event()
@@ -381,13 +389,15 @@ class TwoPathEngine:
                      nat.ptr(codes), mst)
             if timer is not None:
                 timer.stop("emit", main)
-            slot = self._async_slot()
-            slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
+            with torch.cuda.stream(main):
+                slot = self._async_slot()
+                slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(main)
             freed[b] = ev
             self.stats.chunks += 1
-        main.wait_stream(ms)
+        caller.wait_stream(ms)
+        caller.wait_stream(main)
         return codes
 
     def run_pipelined(self, x_begin: int = 0, x_end: Optional[int] = None, timer=None):
