@@ -51,7 +51,7 @@ def _args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--plan", default="gpu", help="gpu | default | d1,d2")
-    ap.add_argument("--chunk-rows", type=int, default=2048)
+    ap.add_argument("--chunk-rows", type=int, default=16384)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -414,7 +414,8 @@ def _e2e(args, r, s, plan, x_lo, x_hi, world):
 
     from paper_2002_12459_b200.joinproject import two_path_join_chunks
 
-    host_out = torch.empty(args.chunk_rows * s.rel.dom_left, dtype=torch.int64, pin_memory=True)
+    e2e_rows = min(args.chunk_rows, 2048)
+    host_out = torch.empty(e2e_rows * s.rel.dom_left, dtype=torch.int64, pin_memory=True)
     best = None
     h2d = d2h = 0
     for _ in range(args.e2e_steps):
@@ -423,7 +424,7 @@ def _e2e(args, r, s, plan, x_lo, x_hi, world):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         nout = 0
-        for part in two_path_join_chunks(r, s, plan, chunk_rows=args.chunk_rows, host_buffer=host_out,
+        for part in two_path_join_chunks(r, s, plan, chunk_rows=e2e_rows, host_buffer=host_out,
                                          upload="fresh", x_range=(x_lo, x_hi)):
             nout += len(part.codes)
             h2d = part.stats["h2d_bytes"]

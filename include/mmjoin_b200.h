@@ -42,6 +42,8 @@ extern "C" {
 #define MMJ_MODE_COUNT32 1     /* exact int32 counts                    */
 #define MMJ_MODE_ACC64 2       /* out += count << shift (int64)         */
 #define MMJ_MODE_BITMAP_U8 3   /* BITMAP, caller guarantees counts < 256 (<= 255 nonzero K columns) */
+#define MMJ_MODE_UPPER 16      /* OR-flag: self-join, skip tiles whose columns are all <= their rows
+                                  (cells there are left unwritten; consumers keep z > x only) */
 
 int mmj_abi_version(void);
 const char* mmj_last_error(void);
@@ -82,15 +84,17 @@ int mmj_light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, i
  * mmj_light_lengths writes len[ntup] and offs[ntup+1] (exclusive scan; offs[ntup]
  * is the light intermediate size).  mmj_light_expand sets bit (x-x0, z) of a
  * bitmap (mode 0, ld in words) or adds 1 to count cell (x-x0, z) (mode 1, ld in
- * int32). */
+ * int32).  min_deg > 1 (SSJ threshold c) skips rows of sets smaller than c
+ * and light-z lists when delta2 < c; upper_only skips witnesses with z <= x. */
 int mmj_light_lengths(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup,
                       const int32_t* rdeg_x, int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr,
-                      const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, int32_t* len,
-                      int64_t* offs, void* ws, void* stream);
+                      const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, int64_t min_deg,
+                      int upper_only, int32_t* len, int64_t* offs, void* ws, void* stream);
 int mmj_light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup,
                      const int32_t* rdeg_x, int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr,
-                     const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, const int64_t* offs,
-                     int64_t total_hint, int mode, int64_t x0, void* out, int64_t ld, void* stream);
+                     const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, int64_t min_deg,
+                     int upper_only, const int64_t* offs, int64_t total_hint, int mode, int64_t x0, void* out,
+                     int64_t ld, void* stream);
 
 /* ---- heavy contraction on tcgen05: joinproject.py:208-216, core.py:95-123,
  *      _kernel_cy.pyx:42-47 ------------------------------------------------

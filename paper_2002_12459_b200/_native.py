@@ -25,6 +25,7 @@ MODE_BITMAP = 0
 MODE_COUNT32 = 1
 MODE_ACC64 = 2
 MODE_BITMAP_U8 = 3
+MODE_UPPER = 16
 
 P = C.c_void_p
 I64 = C.c_int64
@@ -42,8 +43,8 @@ _SIGS = {
     "mmj_heavy_y_positions": (INT, [P, P, I64, I64, P, P, P, P, P]),
     "mmj_build_operand": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
     "mmj_light_z_csr": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P]),
-    "mmj_light_lengths": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P, P, P, P]),
-    "mmj_light_expand": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P, I64, INT, I64, P, I64, P]),
+    "mmj_light_lengths": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, I64, INT, P, P, P, P]),
+    "mmj_light_expand": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, I64, INT, P, I64, INT, I64, P, I64, P]),
     "mmj_heavy_mma": (INT, [P, I64, P, I64, I64, I64, I64, I64, I64, INT, INT, P, I64, P, INT, P]),
     "mmj_digit_plane": (INT, [P, I64, I64, INT, INT, P, I64, P]),
     "mmj_tile_count": (I64, [I64, I64]),

@@ -11,11 +11,11 @@ int build_operand(const int32_t*, const int32_t*, int64_t, const int32_t*, int64
 int light_z_csr(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, uint8_t*, int32_t*,
                 int32_t*, int32_t*, void*, cudaStream_t);
 int light_lengths(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, const int32_t*,
-                  const int32_t*, const int32_t*, const int32_t*, const int32_t*, int32_t*, int64_t*, void*,
+                  const int32_t*, const int32_t*, const int32_t*, const int32_t*, int64_t, int, int32_t*, int64_t*, void*,
                   cudaStream_t);
 int light_expand(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, const int32_t*,
-                 const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int64_t*, int64_t, int, int64_t,
-                 void*, int64_t, cudaStream_t);
+                 const int32_t*, const int32_t*, const int32_t*, const int32_t*, int64_t, int, const int64_t*, int64_t,
+                 int, int64_t, void*, int64_t, cudaStream_t);
 int64_t bitmap_nseg(int64_t);
 int64_t count_nseg(int64_t);
 int bitmap_segments(const uint32_t*, int64_t, int32_t*, int64_t*, void*, cudaStream_t);
@@ -105,29 +105,31 @@ int mmj_light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, i
 
 int mmj_light_lengths(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup,
                       const int32_t* rdeg_x, int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr,
-                      const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, int32_t* len,
-                      int64_t* offs, void* ws, void* stream) {
+                      const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, int64_t min_deg,
+                      int upper_only, int32_t* len, int64_t* offs, void* ws, void* stream) {
   return mmj::light_lengths(fwd_row, fwd_idx, t0, ntup, rdeg_x, delta2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx,
-                            len, offs, ws, ST(stream));
+                            min_deg, upper_only, len, offs, ws, ST(stream));
 }
 
 int mmj_light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup,
                      const int32_t* rdeg_x, int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr,
-                     const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, const int64_t* offs,
-                     int64_t total_hint, int mode, int64_t x0, void* out, int64_t ld, void* stream) {
+                     const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, int64_t min_deg,
+                     int upper_only, const int64_t* offs, int64_t total_hint, int mode, int64_t x0, void* out,
+                     int64_t ld, void* stream) {
   if (mode != 0 && mode != 1) {
     mmj::set_error("light_expand: mode must be 0 (bitmap) or 1 (counts)");
     return MMJ_ERR_ARG;
   }
   return mmj::light_expand(fwd_row, fwd_idx, t0, ntup, rdeg_x, delta2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx,
-                           offs, total_hint, mode, x0, out, ld, ST(stream));
+                           min_deg, upper_only, offs, total_hint, mode, x0, out, ld, ST(stream));
 }
 
 int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_rows, int64_t kpad, int64_t k_off,
                   int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out, int64_t ld_out,
                   unsigned long long* nnz, int max_ctas, void* stream) {
-  if (mode < 0 || mode > 3) {
-    mmj::set_error("heavy_mma: unknown mode %d", mode);
+  const int base_mode = mode & ~MMJ_MODE_UPPER;
+  if (base_mode < 0 || base_mode > 3 || (mode != base_mode && base_mode != MMJ_MODE_COUNT32)) {
+    mmj::set_error("heavy_mma: unknown mode %d (MMJ_MODE_UPPER combines with COUNT32 only)", mode);
     return MMJ_ERR_ARG;
   }
   return mmj::mma::launch_heavy_mma(a, a_rows, b, b_rows, kpad, k_off, k_len, m_begin, m_rows, mode, shift, out,

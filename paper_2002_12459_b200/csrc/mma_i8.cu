@@ -48,10 +48,11 @@ constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int smem_bytes_for(int stages) { return stages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/; }
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
-enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3 };
+enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, MODE_UPPER = 16 };
 
 struct Params {
   int64_t m_begin;      // first A row of this launch (multiple of BM not required)
+  int upper;            // skip tiles strictly below the x = z diagonal
   int64_t m_rows;       // rows of A processed / rows of the output
   int64_t n_cols;       // columns of the product (= rows of B)
   int num_kb;           // Kp / BK
@@ -209,6 +210,12 @@ __device__ __forceinline__ TileCoord tile_of(int64_t t, int mt, int nt) {
   return c;
 }
 
+// Self-join consumers that keep only z > x (SSJ's a < b filter) skip tiles
+// whose every column is <= every row: A row m_begin + i is x, B row j is z.
+__device__ __forceinline__ bool below_diagonal(const Params& p, TileCoord c) {
+  return p.upper && (int64_t)c.n_blk * BN + BN - 1 <= p.m_begin + (int64_t)c.m_blk * BM;
+}
+
 // ----------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     heavy_mma_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -264,6 +271,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         TileCoord c = tile_of(t, mt, nt);
+        if (below_diagonal(p, c)) continue;
         const int32_t arow = (int32_t)(p.m_begin + (int64_t)c.m_blk * BM);
         const int32_t brow = c.n_blk * BN;
         for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -284,6 +292,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int acc = 0;
       uint32_t acc_ph = 0;
       for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        if (below_diagonal(p, tile_of(t, mt, nt))) continue;
         mbar_wait(&tempty[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -313,6 +322,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     unsigned long long my_nnz = 0;
     for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       TileCoord c = tile_of(t, mt, nt);
+      if (below_diagonal(p, c)) continue;
       mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       const int64_t row = (int64_t)c.m_blk * BM + q * 32 + lane;   // local output row
@@ -447,6 +457,8 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t kl
 int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_rows, int64_t kpad,
                      int64_t k_off, int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out,
                      int64_t ld_out, unsigned long long* nnz, int max_ctas, cudaStream_t st) {
+  const int upper = (mode & MODE_UPPER) ? 1 : 0;
+  mode &= ~MODE_UPPER;
   if (kpad <= 0 || kpad % BK != 0 || k_off < 0 || k_len <= 0 || k_off % BK != 0 || k_len % BK != 0 ||
       k_off + k_len > kpad) {
     set_error("heavy_mma: K window [%lld,+%lld) of pitch %lld must be multiples of %d", (long long)k_off,
@@ -480,6 +492,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   MMJ_TRY(make_map(&mb, b + k_off, b_rows, k_len, kpad, BN));
   Params p;
   p.m_begin = m_begin;
+  p.upper = upper;
   p.m_rows = m_rows;
   p.n_cols = b_rows;
   p.num_kb = (int)(k_len / BK);

@@ -106,13 +106,16 @@ struct LightArgs {
   const int32_t* s_rev_idx;
   const int32_t* lz_ptr;
   const int32_t* lz_idx;
+  int64_t min_deg;   // SSJ c-prefilter: left ids with degree < min_deg cannot reach overlap >= c
+  int upper_only;    // SSJ: only z > x cells are ever emitted
 };
 
 __device__ __forceinline__ void list_of(const LightArgs& a, int64_t t, int32_t& x, const int32_t*& base,
-                                        int32_t& len) {
+                                        int32_t& len, bool& lz) {
   x = a.fwd_row[t];
   const int32_t y = a.fwd_idx[t];
   const bool full_list = (a.hpos == nullptr) || (a.hpos[y] < 0) || (a.rdeg_x[x] <= a.d2);
+  lz = !full_list;
   if (full_list) {
     const int32_t b = a.s_rev_ptr[y];
     base = a.s_rev_idx + b;
@@ -129,7 +132,12 @@ __global__ void k_light_len(LightArgs a, int64_t ntup, int32_t* __restrict__ len
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t x, l;
     const int32_t* b;
-    list_of(a, a.t0 + i, x, b, l);
+    bool lz;
+    list_of(a, a.t0 + i, x, b, l, lz);
+    // c-prefilter (ssj_mmjoin, apps.py:57-62): a row whose set has fewer than c
+    // elements, or a light-z list (all its z have degree <= d2 < c), cannot
+    // produce a pair with overlap >= c; skipping them leaves the output unchanged
+    if (a.min_deg > 1 && (a.rdeg_x[x] < a.min_deg || (lz && a.d2 < a.min_deg))) l = 0;
     len[i] = l;
   }
 }
@@ -171,9 +179,11 @@ __global__ void __launch_bounds__(EXP_THREADS) k_light_expand(LightArgs a, const
       const int64_t i = upper_bound_i64(offs, lo, hi, s) - 1;
       int32_t x, l;
       const int32_t* base;
-      list_of(a, a.t0 + i, x, base, l);
+      bool lz;
+      list_of(a, a.t0 + i, x, base, l, lz);
       const int32_t z = base[s - offs[i]];
       const int64_t row = (int64_t)x - x0;
+      if (a.upper_only && z <= x) continue;       // SSJ keeps a < b only (apps.py:60)
       if (MODE == 0) {
         atomicOr(reinterpret_cast<uint32_t*>(out) + row * ld + (z >> 5), 1u << (z & 31));
       } else {
@@ -353,9 +363,9 @@ int light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, int64
 
 int light_lengths(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup, const int32_t* rdeg_x,
                   int64_t d2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx,
-                  const int32_t* lz_ptr, const int32_t* lz_idx, int32_t* len, int64_t* offs, void* ws,
-                  cudaStream_t st) {
-  LightArgs a{fwd_row, fwd_idx, t0, rdeg_x, d2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx};
+                  const int32_t* lz_ptr, const int32_t* lz_idx, int64_t min_deg, int upper_only, int32_t* len,
+                  int64_t* offs, void* ws, cudaStream_t st) {
+  LightArgs a{fwd_row, fwd_idx, t0, rdeg_x, d2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx, min_deg, upper_only};
   if (ntup > 0) {
     k_light_len<<<grid_for(ntup, TPB), TPB, 0, st>>>(a, ntup, len);
     MMJ_CHECK_LAUNCH("k_light_len");
@@ -365,10 +375,10 @@ int light_lengths(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, in
 
 int light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup, const int32_t* rdeg_x,
                  int64_t d2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx,
-                 const int32_t* lz_ptr, const int32_t* lz_idx, const int64_t* offs, int64_t total_hint, int mode,
-                 int64_t x0, void* out, int64_t ld, cudaStream_t st) {
+                 const int32_t* lz_ptr, const int32_t* lz_idx, int64_t min_deg, int upper_only, const int64_t* offs,
+                 int64_t total_hint, int mode, int64_t x0, void* out, int64_t ld, cudaStream_t st) {
   if (ntup == 0 || total_hint == 0) return MMJ_OK;
-  LightArgs a{fwd_row, fwd_idx, t0, rdeg_x, d2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx};
+  LightArgs a{fwd_row, fwd_idx, t0, rdeg_x, d2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx, min_deg, upper_only};
   const int64_t work = total_hint > 0 ? total_hint : ntup;
   const int grid = grid_for(work, EXP_SPAN, 8);
   if (mode == 0)

@@ -80,6 +80,13 @@ class TwoPathEngine:
         self.counts = bool(want_counts)
         self.min_count = int(min_count)
         self.upper_only = bool(upper_only)
+        if (self.upper_only or self.min_count > 1) and not self.counts:
+            raise ValueError("min_count / upper_only filter the count path; pass want_counts=True")
+        if self.upper_only and dr.dom_left != ds.dom_left:
+            raise ValueError("upper_only needs a self-join (x and z in one dictionary)")
+        # c-prefilter only when the caller discards counts < min_count (SSJ);
+        # the light_intermediate statistic then counts the pruned witnesses only
+        self.prefilter = self.min_count if (self.counts and self.min_count > 1) else 0
         self.dom_x, self.dom_z, self.dom_y = dr.dom_left, ds.dom_left, dr.dom_right
         self.wpr = _rup(max(self.dom_z, 1), 1024) // 32     # rows start on 1024-cell segments
         self.ldc = _rup(max(self.dom_z, 1), 1024)
@@ -190,7 +197,7 @@ class TwoPathEngine:
         if self.counts:
             buf = self.ws.get("cnt", rows * self.ldc, torch.int32)
             ld = self.ldc
-            mode = nat.MODE_COUNT32
+            mode = nat.MODE_COUNT32 | (nat.MODE_UPPER if self.upper_only else 0)
         else:
             buf = self.ws.get("bm", rows * self.wpr, torch.int32)
             ld = self.wpr
@@ -216,11 +223,11 @@ class TwoPathEngine:
         lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
         self._ph("light", True)
         nat.call("mmj_light_lengths", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), t0, ntup, nat.ptr(dr.left_deg),
-                 self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(lens), nat.ptr(offs),
-                 nat.ptr(self.ws.scan_ws(ntup)), st)
+                 self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, self.prefilter, int(self.upper_only),
+                 nat.ptr(lens), nat.ptr(offs), nat.ptr(self.ws.scan_ws(ntup)), st)
         nat.call("mmj_light_expand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), t0, ntup, nat.ptr(dr.left_deg),
-                 self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(offs), -1,
-                 1 if self.counts else 0, x0, nat.ptr(buf), ld, st)
+                 self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, self.prefilter, int(self.upper_only),
+                 nat.ptr(offs), -1, 1 if self.counts else 0, x0, nat.ptr(buf), ld, st)
         self._ph("light", False)
         # merge: segment sizes -> offsets -> codes
         self._ph("segments", True)

@@ -267,6 +267,50 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const uint32_t* __restrict_
   }
 }
 
+// V12: CTA of 8 warps stages its 8 segments' int64 codes contiguously in
+// shared memory, then all 256 threads write the CTA range with 16 B stores
+__global__ void __launch_bounds__(256) k_emit_cta(const uint32_t* __restrict__ bm, const int64_t* __restrict__ segoff,
+                                                  int64_t nseg, int64_t* __restrict__ out_all) {
+  extern __shared__ __align__(16) int64_t cstage[];      // 8192 codes worst case
+  __shared__ int s_cnt[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * 8 + warp;
+  uint32_t word = s < nseg ? bm[s * 32 + lane] : 0u;
+  const int c = __popc(word);
+  const int incl = warp_incl(c, lane);
+  if (lane == 31) s_cnt[warp] = incl;
+  __syncthreads();
+  int wbase = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const int v = s_cnt[w];
+    if (w < warp) wbase += v;
+    total += v;
+  }
+  const int64_t base = s * 1024;
+  const uint32_t off0 = lane * 32;
+  int k = wbase + incl - c;
+  while (word) {
+    const int b = __ffs(word) - 1;
+    cstage[k ^ (((k >> 4) & 7) << 1)] = base + off0 + b;   // keep pairs, spread lanes over banks
+    ++k;
+    word &= word - 1;
+  }
+  __syncthreads();
+  const int64_t s0 = (int64_t)blockIdx.x * 8;
+  int64_t* out = out_all + segoff[s0];
+  const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), total);
+  auto sl = [](int q) { return q ^ (((q >> 4) & 7) << 1); };
+  if (threadIdx.x < h) st_cs(out, cstage[sl(0)]);
+  const int np = (total - h) >> 1;
+  for (int p = threadIdx.x; p < np; p += 256) {
+    const int i = h + 2 * p;
+    st_cs2(out + i, cstage[sl(i)], cstage[sl(i + 1)]);
+  }
+  const int done = h + 2 * np;
+  if (threadIdx.x < total - done) st_cs(out + done + threadIdx.x, cstage[sl(done + threadIdx.x)]);
+}
+
 // pure store kernels: the HBM write ceiling for different store shapes
 template <int W>
 __global__ void __launch_bounds__(256) k_store(int64_t* __restrict__ out, int64_t n) {
@@ -425,6 +469,26 @@ int main(int argc, char** argv) {
     float d = run<0, 64, 1>(dbm, dso, nseg, dout), e = run<0, 256, 1>(dbm, dso, nseg, dout), f = run<0, 1024, 1>(dbm, dso, nseg, dout);
     printf("V0 segs 8 / 16 / 256 (interleaved): %.1f %.1f %.1f GB/s\n", bytes / (a * 1e-3) / 1e9, bytes / (b * 1e-3) / 1e9, bytes / (c * 1e-3) / 1e9);
     printf("V0 segs 64 / 256 / 1024 (contiguous per warp): %.1f %.1f %.1f GB/s\n", bytes / (d * 1e-3) / 1e9, bytes / (e * 1e-3) / 1e9, bytes / (f * 1e-3) / 1e9);
+  }
+  {
+    cudaFuncSetAttribute(k_emit_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    const int grid = (int)((nseg + 7) / 8);
+    k_emit_cta<<<grid, 256, 65536>>>(dbm, dso, nseg, dout);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t ea, eb;
+    cudaEventCreate(&ea);
+    cudaEventCreate(&eb);
+    float best = 1e9;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(ea);
+      k_emit_cta<<<grid, 256, 65536>>>(dbm, dso, nseg, dout);
+      cudaEventRecord(eb);
+      CK(cudaEventSynchronize(eb));
+      float ms;
+      cudaEventElapsedTime(&ms, ea, eb);
+      if (ms < best) best = ms;
+    }
+    printf("%-24s %8.3f ms  %7.1f GB/s\n", "V12 CTA-staged int64", best, bytes / (best * 1e-3) / 1e9);
   }
   const float t8 = run<8>(dbm, dso, nseg, dout);
   printf("%-24s %8.3f ms  %7.1f GB/s\n", "V8 xor5 + 32B quads", t8, bytes / (t8 * 1e-3) / 1e9);
