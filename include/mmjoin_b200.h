@@ -146,7 +146,9 @@ int mmj_bitmap_emit(const uint32_t* bm, int64_t nwords, int64_t wpr, const int64
                     int64_t dom_z, int64_t* codes, void* stream);
 /* Count chunk (nrows x ld int32, ncols valid columns): cells with count >=
  * min_count (and col > x0+row if upper_only: the a < b filter of
- * apps.py:57-62) -> codes + int32 counts. */
+ * apps.py:57-62) -> codes + int32 counts.  ld must be a multiple of 1024
+ * (segments of 1024 cells never straddle rows); with upper_only, segments at
+ * or below the diagonal are not read. */
 int64_t mmj_count_segment_count(int64_t ncell);
 int mmj_count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
                        int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws, void* stream);

@@ -59,9 +59,9 @@ class SetFamily:
         return (self.raw_id(a), self.raw_id(b))
 
 
-def _ssj_plan(idx, plan: Optional[ThresholdPlan]) -> ThresholdPlan:
+def _ssj_plan(idx, plan: Optional[ThresholdPlan], c: int = 1, upper_only: bool = True) -> ThresholdPlan:
     from .optimizer import gpu_plan
-    return plan if plan is not None else gpu_plan(idx, idx)
+    return plan if plan is not None else gpu_plan(idx, idx, counts=True, min_count=c, upper_only=upper_only)
 
 
 def ssj_mmjoin_arrays(family: SetFamily, c: int, plan: Optional[ThresholdPlan] = None,
@@ -72,7 +72,7 @@ def ssj_mmjoin_arrays(family: SetFamily, c: int, plan: Optional[ThresholdPlan] =
         raise ValueError("c must be >= 1")
     from .joinproject import _engine
     idx = family.indexed
-    plan = _ssj_plan(idx, plan)
+    plan = _ssj_plan(idx, plan, int(c))
     plan.validate()
     eng = _engine(idx, idx, plan, True, min_count=int(c), upper_only=True, chunk_rows=chunk_rows)
     dz = idx.rel.dom_left
@@ -107,7 +107,7 @@ def scj_join_project(family: SetFamily) -> set:
     i.e. overlap(a, b) == |a| on the exact count path."""
     from .joinproject import two_path_join
     idx = family.indexed
-    res = two_path_join(idx, idx, plan=_ssj_plan(idx, None), want_counts=True)
+    res = two_path_join(idx, idx, plan=_ssj_plan(idx, None, upper_only=False), want_counts=True)
     t = res.tuples()
     sizes = np.asarray(idx.left_deg)
     keep = (t[:, 0] != t[:, 1]) & (res.counts == sizes[t[:, 0]])

@@ -45,7 +45,12 @@ constexpr int ACC_STAGES = 2;
 constexpr int TMEM_COLS = 512;          // 2 x 256 s32 accumulator columns
 constexpr int EPI_WARPS = 8;            // two warps per TMEM lane quadrant (one per 128-column half)
 constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
-constexpr int smem_bytes_for(int stages) { return stages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/; }
+constexpr int EPI_PITCH = 36;           // COUNT32 staging: words per row (16-B aligned, conflict-free v4)
+constexpr int EPI_STAGE_BYTES = EPI_WARPS * 32 * EPI_PITCH * 4;
+constexpr int smem_bytes_for(int stages, bool staged) {
+  return stages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + (staged ? EPI_STAGE_BYTES : 0);
+}
+static_assert(smem_bytes_for(3, true) <= smem_bytes_for(STAGES, false), "staged COUNT32 launch must fit");
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
 enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, MODE_UPPER = 16 };
@@ -231,6 +236,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = bars + 2 * STAGES;                      // [ACC_STAGES]
   uint64_t* tempty = bars + 2 * STAGES + ACC_STAGES;        // [ACC_STAGES]
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * ACC_STAGES);
+  uint32_t* epi_stage = reinterpret_cast<uint32_t*>(smem + NST * STAGE_BYTES + 256);   // COUNT32 only
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -359,26 +365,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           my_nnz += __popc(w0) + __popc(w1) + __popc(w2) + __popc(w3);
         }
       } else if (p.mode == COUNT32) {
-        int32_t* dst = reinterpret_cast<int32_t*>(p.out) + row * p.ld_out + col0;
+        // 32x32 blocks: lane (= row) stages its 32 counts in shared memory,
+        // then the warp stores 4 full rows (128 B each) per instruction.
+        uint32_t* stg = epi_stage + (warp - 4) * 32 * EPI_PITCH;
+        const int64_t row_base = (int64_t)c.m_blk * BM + q * 32;
+        const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
 #pragma unroll 1
         for (int j = 0; j < 4; ++j) {
           uint32_t r[32];
           TMEM_LD_32x32b_X32(taddr + j * 32, r);
           tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<uint4*>(stg + lane * EPI_PITCH + i) = make_uint4(r[i], r[i + 1], r[i + 2], r[i + 3]);
           if (row_ok) {
-            if (col0 + j * 32 + 32 <= p.ld_out) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 4)
-                *reinterpret_cast<int4*>(dst + j * 32 + i) =
-                    make_int4((int)r[i], (int)r[i + 1], (int)r[i + 2], (int)r[i + 3]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (col0 + j * 32 + i < p.ld_out) dst[j * 32 + i] = (int)r[i];
-            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) my_nnz += (r[i] != 0u && col0 + j * 32 + i < p.n_cols);
           }
+          __syncwarp();
+          const int64_t col = col0 + j * 32 + sub_c;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = sub_r + 4 * i;
+            const int64_t orow = row_base + rr;
+            const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * EPI_PITCH + sub_c);
+            if (orow < p.m_rows && col + 4 <= p.ld_out)
+              *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(p.out) + orow * p.ld_out + col) = v;
+          }
+          __syncwarp();
         }
         tc_fence_before();
         __syncwarp();
@@ -497,6 +511,8 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   p.n_cols = b_rows;
   p.num_kb = (int)(k_len / BK);
   p.stages = p.num_kb <= 2 ? 2 : STAGES;
+  const bool staged = (mode == COUNT32);
+  if (staged && p.stages > 3) p.stages = 3;   // room for the epilogue staging buffers
   p.small_counts = (mode == BITMAP_U8 || k_len <= 255) ? 1 : 0;
   {
     static int dbg = -1;
@@ -514,7 +530,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   static bool attr_set = false;
   if (!attr_set) {
     MMJ_TRY(cuda_status(cudaFuncSetAttribute(heavy_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem_bytes_for(STAGES)),
+                                             smem_bytes_for(STAGES, false)),   // >= smem_bytes_for(3, true)
                         "cudaFuncSetAttribute(heavy_mma)"));
     attr_set = true;
   }
@@ -522,7 +538,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   int grid = sm_count();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (tiles < grid) grid = (int)tiles;
-  heavy_mma_kernel<<<grid, NUM_THREADS, smem_bytes_for(p.stages), st>>>(ma, mb, p);
+  heavy_mma_kernel<<<grid, NUM_THREADS, smem_bytes_for(p.stages, staged), st>>>(ma, mb, p);
   MMJ_CHECK_LAUNCH("heavy_mma_kernel");
   return MMJ_OK;
 }

@@ -255,68 +255,111 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32) k_bitmap_emit(const uint32_t*
   }
 }
 
-// count matrix (rows x ld int32, ncols valid): keep cells with
-// value >= min_count and (if upper_only) z > x.
-__device__ __forceinline__ bool keep_cell(int32_t v, int64_t col, int64_t x, int64_t ncols, int32_t min_count,
-                                          int upper_only) {
-  return col < ncols && v >= min_count && (!upper_only || col > x);
+// count matrix (rows x ld int32, ld a multiple of CSEG, ncols valid): keep
+// cells with value >= min_count and (if upper_only) z > x.  One warp per
+// 1024-cell segment, which always lies inside one row; lane l loads cells
+// it*128 + 4l .. +3 (it = 0..7) as coalesced int4s.  Segments entirely at or
+// below the diagonal (upper_only) or right of ncols are never read - the
+// MMA leaves the former unwritten.
+constexpr int CSEG = 1024;   // cells per count segment
+constexpr int CIT = CSEG / 128;
+
+struct CountSeg {
+  int64_t row, col0;
+  bool live;
+};
+
+__device__ __forceinline__ CountSeg count_seg(int64_t sgi, int64_t spr, int64_t ncols, int64_t x0, int upper_only) {
+  CountSeg g;
+  g.row = sgi / spr;
+  g.col0 = (sgi - g.row * spr) * CSEG;
+  g.live = g.col0 < ncols && !(upper_only && g.col0 + CSEG - 1 <= x0 + g.row);
+  return g;
 }
 
-constexpr int CSEG = 1024;   // cells per count segment (32 per lane)
+// keep flags of one lane's 4 cells of iteration `it` as a nibble
+__device__ __forceinline__ uint32_t keep_nibble(int4 v, int64_t col, int64_t x, int64_t ncols, int32_t min_count,
+                                                int upper_only) {
+  const int64_t lo = upper_only ? x + 1 : 0;   // first kept column
+  uint32_t m = 0;
+  m |= (v.x >= min_count && col + 0 >= lo && col + 0 < ncols) ? 1u : 0u;
+  m |= (v.y >= min_count && col + 1 >= lo && col + 1 < ncols) ? 2u : 0u;
+  m |= (v.z >= min_count && col + 2 >= lo && col + 2 < ncols) ? 4u : 0u;
+  m |= (v.w >= min_count && col + 3 >= lo && col + 3 < ncols) ? 8u : 0u;
+  return m;
+}
 
-__global__ void k_count_seg_nnz(const int32_t* __restrict__ cnt, int64_t ncell, int64_t ld, int64_t ncols,
-                                int64_t x0, int32_t min_count, int upper_only, int32_t* __restrict__ segcnt,
-                                int64_t nseg) {
+__global__ void __launch_bounds__(256) k_count_seg_nnz(const int32_t* __restrict__ cnt, int64_t nseg, int64_t spr,
+                                                       int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
+                                                       int upper_only, int32_t* __restrict__ segcnt) {
   const int lane = threadIdx.x & 31;
   for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
        sgi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t c0 = sgi * CSEG + (int64_t)lane * 32;
+    const CountSeg g = count_seg(sgi, spr, ncols, x0, upper_only);
     int n = 0;
-    for (int i = 0; i < 32; ++i) {
-      const int64_t cell = c0 + i;
-      if (cell >= ncell) break;
-      const int64_t row = cell / ld, col = cell - row * ld;
-      n += keep_cell(cnt[cell], col, x0 + row, ncols, min_count, upper_only);
-    }
+    if (g.live) {
+      const int4* src = reinterpret_cast<const int4*>(cnt + g.row * ld + g.col0) + lane;
+      int4 v[CIT];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+      for (int it = 0; it < CIT; ++it) v[it] = __ldcs(src + it * 32);
+#pragma unroll
+      for (int it = 0; it < CIT; ++it)
+        n += __popc(keep_nibble(v[it], g.col0 + it * 128 + lane * 4, x0 + g.row, ncols, min_count, upper_only));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    }
     if (lane == 0) segcnt[sgi] = n;
   }
 }
 
-__global__ void __launch_bounds__(EMIT_WARPS * 32) k_count_emit(const int32_t* __restrict__ cnt, int64_t ncell,
-                                                                int64_t ld, int64_t ncols, int64_t x0,
-                                                                int64_t dom_z, int32_t min_count, int upper_only,
-                                                                const int64_t* __restrict__ seg_off, int64_t nseg,
-                                                                int64_t* __restrict__ codes,
-                                                                int32_t* __restrict__ counts) {
+__global__ void __launch_bounds__(256) k_count_emit(const int32_t* __restrict__ cnt, int64_t nseg, int64_t spr,
+                                                    int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
+                                                    int32_t min_count, int upper_only,
+                                                    const int64_t* __restrict__ seg_off,
+                                                    int64_t* __restrict__ codes, int32_t* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  for (int64_t sgi = (int64_t)blockIdx.x * EMIT_WARPS + wib; sgi < nseg; sgi += (int64_t)gridDim.x * EMIT_WARPS) {
-    const int64_t c0 = sgi * CSEG + (int64_t)lane * 32;
-    uint32_t mask = 0;
-    for (int i = 0; i < 32; ++i) {
-      const int64_t cell = c0 + i;
-      if (cell >= ncell) break;
-      const int64_t row = cell / ld, col = cell - row * ld;
-      if (keep_cell(cnt[cell], col, x0 + row, ncols, min_count, upper_only)) mask |= 1u << i;
+  for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
+       sgi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const CountSeg g = count_seg(sgi, spr, ncols, x0, upper_only);
+    if (!g.live) continue;
+    const int64_t base = seg_off[sgi];
+    if (seg_off[sgi + 1] == base) continue;
+    const int4* src = reinterpret_cast<const int4*>(cnt + g.row * ld + g.col0) + lane;
+    int4 v[CIT];
+#pragma unroll
+    for (int it = 0; it < CIT; ++it) v[it] = __ldcs(src + it * 32);
+    // 8-bit count field per iteration, packed, warp-scanned in one pass
+    uint32_t nib[CIT];
+    uint64_t packed = 0;
+#pragma unroll
+    for (int it = 0; it < CIT; ++it) {
+      nib[it] = keep_nibble(v[it], g.col0 + it * 128 + lane * 4, x0 + g.row, ncols, min_count, upper_only);
+      packed |= (uint64_t)__popc(nib[it]) << (8 * it);
     }
-    const int c = __popc(mask);
-    int incl = c;
+    uint64_t incl = packed;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+      const uint64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
     }
-    int64_t k = seg_off[sgi] + incl - c;
-    while (mask) {
-      const int b = __ffs(mask) - 1;
-      const int64_t cell = c0 + b;
-      const int64_t row = cell / ld, col = cell - row * ld;
-      codes[k] = (x0 + row) * dom_z + col;
-      counts[k] = cnt[cell];
-      ++k;
-      mask &= mask - 1;
+    const uint64_t tot = __shfl_sync(0xffffffffu, incl, 31);   // per-iteration totals
+    const uint64_t excl = incl - packed;
+    const int64_t code_row = (x0 + g.row) * dom_z + g.col0;
+    int64_t it_base = base;
+#pragma unroll
+    for (int it = 0; it < CIT; ++it) {
+      uint32_t m = nib[it];
+      int64_t k = it_base + (int64_t)((excl >> (8 * it)) & 0xff);
+      const int32_t vals[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (m & (1u << j)) {
+          __stcs(codes + k, code_row + it * 128 + lane * 4 + j);
+          __stcs(counts + k, vals[j]);
+          ++k;
+        }
+      }
+      it_base += (int64_t)((tot >> (8 * it)) & 0xff);
     }
   }
 }
@@ -412,13 +455,29 @@ int bitmap_emit(const uint32_t* bm, int64_t nwords, int64_t wpr, const int64_t* 
   return MMJ_OK;
 }
 
+static int check_count_pitch(int64_t ld, int64_t ncols) {
+  if (ld % CSEG != 0 || ld < ncols) {
+    set_error("count matrix pitch %lld must be a multiple of %d and >= %lld columns", (long long)ld, CSEG,
+              (long long)ncols);
+    return MMJ_ERR_ARG;
+  }
+  return MMJ_OK;
+}
+
+static int count_grid(int64_t nseg) {
+  // 8 warps per CTA, 8 CTAs per SM resident; grid-stride beyond that
+  const int64_t ctas = ceil_div(nseg, (int64_t)8);
+  const int64_t cap = (int64_t)sm_count() * 8;
+  return (int)(ctas < cap ? ctas : cap);
+}
+
 int count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
                    int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws, cudaStream_t st) {
-  const int64_t ncell = nrows * ld;
-  const int64_t nseg = count_nseg(ncell);
+  MMJ_TRY(check_count_pitch(ld, ncols));
+  const int64_t nseg = count_nseg(nrows * ld);
   if (nseg > 0) {
-    k_count_seg_nnz<<<grid_for(nseg * 32, TPB), TPB, 0, st>>>(cnt, ncell, ld, ncols, x0, min_count, upper_only,
-                                                              segcnt, nseg);
+    k_count_seg_nnz<<<count_grid(nseg), 256, 0, st>>>(cnt, nseg, ld / CSEG, ld, ncols, x0, min_count, upper_only,
+                                                      segcnt);
     MMJ_CHECK_LAUNCH("k_count_seg_nnz");
   }
   return scan_i32_i64(segcnt, seg_off, nseg, ws, st);
@@ -427,11 +486,11 @@ int count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols,
 int count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
                int32_t min_count, int upper_only, const int64_t* seg_off, int64_t* codes, int32_t* counts,
                cudaStream_t st) {
-  const int64_t ncell = nrows * ld;
-  const int64_t nseg = count_nseg(ncell);
+  MMJ_TRY(check_count_pitch(ld, ncols));
+  const int64_t nseg = count_nseg(nrows * ld);
   if (nseg == 0) return MMJ_OK;
-  k_count_emit<<<grid_for(nseg, EMIT_WARPS, 16), EMIT_WARPS * 32, 0, st>>>(cnt, ncell, ld, ncols, x0, dom_z, min_count,
-                                                                           upper_only, seg_off, nseg, codes, counts);
+  k_count_emit<<<count_grid(nseg), 256, 0, st>>>(cnt, nseg, ld / CSEG, ld, ncols, x0, dom_z, min_count, upper_only,
+                                                 seg_off, codes, counts);
   MMJ_CHECK_LAUNCH("k_count_emit");
   return MMJ_OK;
 }

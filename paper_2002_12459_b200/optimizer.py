@@ -113,17 +113,22 @@ def default_plan(r, s) -> ThresholdPlan:
 # per heavy y on the int8 tensor cores, and the bitmap it writes is the same
 # for every plan.  Rates are per-B200 planning constants (measured orders of
 # magnitude, refined by bench runs), not correctness parameters.
-LIGHT_WITNESS_RATE = 2.0e11        # light witnesses / s (L2 atomics)
+LIGHT_WITNESS_RATE = 2.0e11        # light witnesses / s (bitmap atomicOr, L2 resident)
+LIGHT_COUNT_RATE = 2.0e10          # light witnesses / s (int32 count atomics over a chunk larger than L2)
 MMA_OPS_RATE = 2.0e15              # int8 ops / s sustained (K is padded to 128)
 K_BLOCK = 128
 
 
-def gpu_plan(r, s, candidates=None) -> ThresholdPlan:
+def gpu_plan(r, s, candidates=None, *, counts: bool = False, min_count: int = 1,
+             upper_only: bool = False) -> ThresholdPlan:
     """Pick (delta1, delta2=1) minimising modelled B200 time.
 
     delta2 = 1 makes (almost) every x and z heavy, so the light side is pass 1
     (light y) only; delta1 then trades sum_{y light} degR*degS light
     witnesses against K = #heavy y columns of the tensor-core product.
+    The count path (``counts``) pays more per light witness; with SSJ's
+    pruning (``min_count`` > 1 drops sets smaller than c, ``upper_only``
+    keeps z > x) only the surviving witnesses and half the product count.
     """
     n = max(r.n, s.n)
     out_join = r.out_join_with(s)
@@ -132,12 +137,21 @@ def gpu_plan(r, s, candidates=None) -> ThresholdPlan:
     rdeg = np.asarray(r.right_deg, dtype=np.int64)
     sdeg = np.asarray(s.right_deg, dtype=np.int64)
     m = np.maximum(rdeg, sdeg)
-    prod = rdeg * sdeg
+    if min_count > 1:
+        def kept(idx):
+            ok = np.asarray(idx.left_deg) >= min_count
+            rows = np.repeat(ok, np.diff(idx.fwd_indptr))
+            return np.bincount(idx.fwd_indices[rows], minlength=len(idx.right_deg)).astype(np.int64)
+        prod = kept(r) * kept(s)
+    else:
+        prod = rdeg * sdeg
     order = np.argsort(m, kind="stable")
     ms = m[order]
     cum_light = np.concatenate([[0], np.cumsum(prod[order])])
     u = int((np.asarray(r.left_deg) > 1).sum())
     w = int((np.asarray(s.left_deg) > 1).sum())
+    light_rate = LIGHT_COUNT_RATE if counts else LIGHT_WITNESS_RATE
+    share = 0.5 if upper_only else 1.0
     if candidates is None:
         candidates = sorted({int(v) for v in np.unique(ms)} | {1})
     best = None
@@ -146,7 +160,7 @@ def gpu_plan(r, s, candidates=None) -> ThresholdPlan:
         k = len(ms) - n_light
         light = int(cum_light[n_light])
         kpad = -(-k // K_BLOCK) * K_BLOCK
-        t = light / LIGHT_WITNESS_RATE + 2.0 * u * w * kpad / MMA_OPS_RATE
+        t = share * (light / light_rate + 2.0 * u * w * kpad / MMA_OPS_RATE)
         if best is None or t < best[0]:
             best = (t, d1, light, 2.0 * u * w * kpad)
     _, d1, light, mma = best
