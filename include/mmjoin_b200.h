@@ -42,6 +42,9 @@ extern "C" {
 #define MMJ_MODE_COUNT32 1     /* exact int32 counts                    */
 #define MMJ_MODE_ACC64 2       /* out += count << shift (int64)         */
 #define MMJ_MODE_BITMAP_U8 3   /* BITMAP, caller guarantees counts < 256 (<= 255 nonzero K columns) */
+#define MMJ_MODE_BITMAP_PAIR 4 /* BITMAP over a z-pair B operand (mmj_build_operand_pairs): b_rows = pair
+                                  rows, 2 bits per accumulator; needs every count < 128 (a side whose
+                                  heavy degrees are <= 127); ld_out*16 >= b_rows rounded up to 256 */
 #define MMJ_MODE_UPPER 16      /* OR-flag: self-join, skip tiles whose columns are all <= their rows
                                   (cells there are left unwritten; consumers keep z > x only) */
 
@@ -69,6 +72,12 @@ int mmj_heavy_y_positions(const int32_t* rdeg_y, const int32_t* sdeg_y, int64_t 
  * has degree > delta2 and whose right id is heavy; mat is zeroed first. */
 int mmj_build_operand(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t delta2,
                       const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows, int64_t kpad, void* stream);
+/* Same, z-pair form for MMJ_MODE_BITMAP_PAIR (nrows a multiple of 32; mat has
+ * nrows/2 rows): z = row0 + 32G + k + 8j (k < 8, j < 4) lands in row
+ * 16G + 2k + j/2 with weight 1 (j even) or 128 (j odd). */
+int mmj_build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
+                            int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
+                            int64_t kpad, void* stream);
 
 /* ---- light-z CSR of S for pass 3: joinproject.py:195-203 --------------------
  * lz_ptr[dom_y+1]/lz_idx: S.rev(y) restricted to z with deg_S(z) <= delta2.

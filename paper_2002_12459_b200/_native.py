@@ -25,6 +25,7 @@ MODE_BITMAP = 0
 MODE_COUNT32 = 1
 MODE_ACC64 = 2
 MODE_BITMAP_U8 = 3
+MODE_BITMAP_PAIR = 4
 MODE_UPPER = 16
 
 P = C.c_void_p
@@ -42,6 +43,7 @@ _SIGS = {
     "mmj_exclusive_scan_i32": (INT, [P, P, I64, P, P]),
     "mmj_heavy_y_positions": (INT, [P, P, I64, I64, P, P, P, P, P]),
     "mmj_build_operand": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
+    "mmj_build_operand_pairs": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
     "mmj_light_z_csr": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P]),
     "mmj_light_lengths": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, I64, INT, P, P, P, P]),
     "mmj_light_expand": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, I64, INT, P, I64, INT, I64, P, I64, P]),

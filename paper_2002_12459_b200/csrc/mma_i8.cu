@@ -16,7 +16,10 @@
 //                (the projection / intersection output);
 //       COUNT32: exact int32 counts (witness counts / set overlaps);
 //       ACC64  : out[i][j] += count << shift  (int64 digit recombination for
-//                the generic multiply_counts backend).
+//                the generic multiply_counts backend);
+//       BITMAP_PAIR: B rows are z pairs weighted (1, 128) (mmj_build_operand_pairs),
+//                one accumulator = two cells: half the MMAs and half the TMEM
+//                read-out per output bit, 64 B per row/tile.
 //
 // Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
 // w3 idle, w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4) .. +31 and the
@@ -51,13 +54,15 @@ constexpr int smem_bytes_for(int stages, bool staged) {
   return stages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + (staged ? EPI_STAGE_BYTES : 0);
 }
 static_assert(smem_bytes_for(3, true) <= smem_bytes_for(STAGES, false), "staged COUNT32 launch must fit");
+static_assert(smem_bytes_for(STAGES, false) <= 227 * 1024, "shared memory budget");
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
-enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, MODE_UPPER = 16 };
+enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, BITMAP_PAIR = 4, MODE_UPPER = 16 };
 
 struct Params {
   int64_t m_begin;      // first A row of this launch (multiple of BM not required)
   int upper;            // skip tiles strictly below the x = z diagonal
+  int backoff;          // producer / MMA issuer sleep between barrier polls
   int64_t m_rows;       // rows of A processed / rows of the output
   int64_t n_cols;       // columns of the product (= rows of B)
   int num_kb;           // Kp / BK
@@ -86,6 +91,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "DONE:\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Same wait with a short sleep between polls: used by the single-thread TMA
+// producer and MMA issuer so their spinning does not take issue slots from
+// the epilogue warps sharing their SM sub-partitions.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  while (!ok) {
+    __nanosleep(32);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
 }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -193,6 +222,27 @@ __device__ __forceinline__ uint32_t pack_bits_u16(const uint32_t* r) {
   return w;
 }
 
+// BITMAP_PAIR: every B row holds two z cells weighted (1, 128), so an
+// accumulator is c0 + 128*c1 with c0, c1 < 128 (the caller guarantees a side
+// whose heavy degrees are <= 127).  The operand builder places z = 32G + b
+// (b = k + 8j, k < 8, j < 4) in accumulator column 16G + 2k + (j >> 1), slot
+// j & 1, so that after the per-register flag test (flags at bits 7, 15, 23,
+// 31) a right-shift-and-or chain lands every flag on its own bit:
+// 8 pack::16b registers = 16 accumulator columns = one 32-bit word.
+__device__ __forceinline__ uint32_t pair_flags(uint32_t r) {
+  const uint32_t lo = (r & 0x007F007Fu) + 0x007F007Fu;   // c0 != 0 -> bits 7, 23 (no bits above 7 per half)
+  const uint32_t hi = r + 0x7F807F80u;                   // v >= 128 (c1 != 0) -> bits 15, 31; no carry
+                                                         // out of the low half since v < 2^14
+  return (lo & 0x00800080u) | (hi & 0x80008000u);
+}
+
+__device__ __forceinline__ uint32_t pack_bits_pair(const uint32_t* r) {
+  uint32_t w = pair_flags(r[0]);
+#pragma unroll
+  for (int k = 1; k < 8; ++k) w = (w >> 1) + pair_flags(r[k]);   // disjoint bits: + == |
+  return w;   // register k's flags now sit at bits k, 8+k, 16+k, 24+k
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -203,15 +253,28 @@ struct TileCoord {
 
 __device__ __forceinline__ TileCoord tile_of(int64_t t, int mt, int nt) {
   // bands of GROUP_M M-blocks; inside a band walk N, cycling M fastest so the
-  // B tile just loaded is reused by the band from L2.
-  int64_t band_tiles = (int64_t)GROUP_M * nt;
-  int band = (int)(t / band_tiles);
-  int64_t r = t - (int64_t)band * band_tiles;
-  int first_m = band * GROUP_M;
-  int gsz = min(GROUP_M, mt - first_m);
+  // B tile just loaded is reused by the band from L2.  32-bit arithmetic when
+  // the tile count allows (the 64-bit divide is a ~40-instruction sequence).
   TileCoord c;
-  c.m_blk = first_m + (int)(r % gsz);
-  c.n_blk = (int)(r / gsz);
+  const uint32_t band_tiles = (uint32_t)GROUP_M * (uint32_t)nt;
+  if ((uint64_t)mt * (uint64_t)nt < (1ull << 31)) {
+    const uint32_t tt = (uint32_t)t;
+    const uint32_t band = tt / band_tiles;
+    const uint32_t r = tt - band * band_tiles;
+    const int first_m = (int)band * GROUP_M;
+    const uint32_t gsz = (uint32_t)min(GROUP_M, mt - first_m);
+    const uint32_t nb = r / gsz;
+    c.m_blk = first_m + (int)(r - nb * gsz);
+    c.n_blk = (int)nb;
+  } else {
+    const int64_t bt = (int64_t)GROUP_M * nt;
+    const int band = (int)(t / bt);
+    const int64_t r = t - (int64_t)band * bt;
+    const int first_m = band * GROUP_M;
+    const int gsz = min(GROUP_M, mt - first_m);
+    c.m_blk = first_m + (int)(r % gsz);
+    c.n_blk = (int)(r / gsz);
+  }
   return c;
 }
 
@@ -236,7 +299,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = bars + 2 * STAGES;                      // [ACC_STAGES]
   uint64_t* tempty = bars + 2 * STAGES + ACC_STAGES;        // [ACC_STAGES]
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * ACC_STAGES);
-  uint32_t* epi_stage = reinterpret_cast<uint32_t*>(smem + NST * STAGE_BYTES + 256);   // COUNT32 only
+  // COUNT32 int32 blocks (after the barriers)
+  uint32_t* epi_stage = reinterpret_cast<uint32_t*>(smem + NST * STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -281,7 +345,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int32_t arow = (int32_t)(p.m_begin + (int64_t)c.m_blk * BM);
         const int32_t brow = c.n_blk * BN;
         for (int kb = 0; kb < p.num_kb; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+          if (p.backoff) mbar_wait_backoff(&empty[s], ph ^ 1); else mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
           tma_load_2d(smem_a + s * A_BYTES, &tmap_a, &full[s], kb * BK, arow);
           tma_load_2d(smem_b + s * B_BYTES, &tmap_b, &full[s], kb * BK, brow);
@@ -299,7 +363,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t acc_ph = 0;
       for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         if (below_diagonal(p, tile_of(t, mt, nt))) continue;
-        mbar_wait(&tempty[acc], acc_ph ^ 1);
+        if (p.backoff) mbar_wait_backoff(&tempty[acc], acc_ph ^ 1); else mbar_wait(&tempty[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -335,7 +399,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool row_ok = row < p.m_rows;
       const int64_t col0 = (int64_t)c.n_blk * BN + half * 128;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * 128;
-      if (p.mode == BITMAP) {
+      if (p.mode == BITMAP || p.mode == BITMAP_PAIR) {
         uint32_t r0[32], r1[32];
         TMEM_LD_32x32b_X32_PACK16(taddr, r0);        // columns [0, 64) of the half
         TMEM_LD_32x32b_X32_PACK16(taddr + 64, r1);   // columns [64, 128)
@@ -343,26 +407,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
-        uint32_t w0, w1, w2, w3;
-        if (p.debug) {
-          w0 = r0[0] | r0[7]; w1 = r0[16]; w2 = r1[3]; w3 = r1[31];
-        } else if (p.small_counts) {
-          // every count < 256 (K <= 255) -> 4 counts per register (PRMT), SWAR
-          // nonzero test, 4-flag movemask by one multiply
-          w0 = pack_bits_u8(r0);
-          w1 = pack_bits_u8(r0 + 16);
-          w2 = pack_bits_u8(r1);
-          w3 = pack_bits_u8(r1 + 16);
+        // BITMAP: 128 columns -> 4 words; BITMAP_PAIR: 128 accumulators = 256 z -> 8 words
+        const bool pair = (p.mode == BITMAP_PAIR);
+        const int ow = pair ? 16 : 8;                // words per tile row
+        uint32_t w[8];
+        if (pair) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            w[k] = pack_bits_pair(r0 + 8 * k);
+            w[k + 4] = pack_bits_pair(r1 + 8 * k);
+          }
         } else {
-          w0 = pack_bits_u16(r0);
-          w1 = pack_bits_u16(r0 + 16);
-          w2 = pack_bits_u16(r1);
-          w3 = pack_bits_u16(r1 + 16);
+          if (p.debug) {
+            w[0] = r0[0] | r0[7]; w[1] = r0[16]; w[2] = r1[3]; w[3] = r1[31];
+          } else if (p.small_counts) {
+            // every count < 256 (K <= 255) -> 4 counts per register (PRMT), SWAR
+            // nonzero test, 4-flag movemask by one multiply
+            w[0] = pack_bits_u8(r0);
+            w[1] = pack_bits_u8(r0 + 16);
+            w[2] = pack_bits_u8(r1);
+            w[3] = pack_bits_u8(r1 + 16);
+          } else {
+            w[0] = pack_bits_u16(r0);
+            w[1] = pack_bits_u16(r0 + 16);
+            w[2] = pack_bits_u16(r1);
+            w[3] = pack_bits_u16(r1 + 16);
+          }
+          w[4] = w[5] = w[6] = w[7] = 0;
         }
         if (row_ok) {
-          uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + (col0 >> 5);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
-          my_nnz += __popc(w0) + __popc(w1) + __popc(w2) + __popc(w3);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) my_nnz += __popc(w[k]);
+        }
+        if (row_ok) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out +
+                                                (int64_t)c.n_blk * ow + half * (ow / 2));
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          if (pair) dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
         }
       } else if (p.mode == COUNT32) {
         // 32x32 blocks: lane (= row) stages its 32 counts in shared memory,
@@ -492,11 +573,15 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
     set_error("heavy_mma: bitmap pitch %lld words too small / unaligned", (long long)ld_out);
     return MMJ_ERR_ARG;
   }
+  if (mode == BITMAP_PAIR && (ld_out % 8 != 0 || ld_out * 16 < round_up(b_rows, BN))) {
+    set_error("heavy_mma: pair-bitmap pitch %lld words too small / unaligned", (long long)ld_out);
+    return MMJ_ERR_ARG;
+  }
   if (mode == COUNT32 && ld_out % 4 != 0) {
     set_error("heavy_mma: count pitch must be a multiple of 4");
     return MMJ_ERR_ARG;
   }
-  if ((mode == BITMAP || mode == BITMAP_U8) && k_len > 65535) {
+  if ((mode == BITMAP || mode == BITMAP_U8 || mode == BITMAP_PAIR) && k_len > 65535) {
     set_error("heavy_mma: BITMAP mode packs 16-bit counts; K window must be < 65536");
     return MMJ_ERR_ARG;
   }
@@ -504,6 +589,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   CUtensorMap ma, mb;
   MMJ_TRY(make_map(&ma, a + k_off, a_rows, k_len, kpad, BM));
   MMJ_TRY(make_map(&mb, b + k_off, b_rows, k_len, kpad, BN));
+
   Params p;
   p.m_begin = m_begin;
   p.upper = upper;
@@ -511,6 +597,14 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   p.n_cols = b_rows;
   p.num_kb = (int)(k_len / BK);
   p.stages = p.num_kb <= 2 ? 2 : STAGES;
+  {
+    static int st_env = -1;
+    if (st_env < 0) {
+      const char* e = getenv("MMJ_MMA_STAGES");
+      st_env = e ? atoi(e) : 0;
+    }
+    if (st_env >= 2 && st_env <= STAGES) p.stages = st_env;
+  }
   const bool staged = (mode == COUNT32);
   if (staged && p.stages > 3) p.stages = 3;   // room for the epilogue staging buffers
   p.small_counts = (mode == BITMAP_U8 || k_len <= 255) ? 1 : 0;
@@ -521,6 +615,12 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
       dbg = (e && e[0] == '1') ? 1 : 0;
     }
     p.debug = dbg;
+    static int bo = -1;
+    if (bo < 0) {
+      const char* e = getenv("MMJ_BACKOFF");
+      bo = (e && e[0] == '0') ? 0 : 1;
+    }
+    p.backoff = bo;
   }
   p.mode = mode == BITMAP_U8 ? BITMAP : mode;
   p.shift = shift;

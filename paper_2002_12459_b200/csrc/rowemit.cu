@@ -25,6 +25,7 @@
 // every code is written once: emission is bound by the HBM write of the
 // sorted output (8 B per distinct (x, z)).
 #include <cub/block/block_scan.cuh>
+#include <stdlib.h>
 
 #include "mmj_common.cuh"
 
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
 }
 
 // --------------------------------------------------------------- emission
+template <int SEGS>
 __global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const uint32_t* __restrict__ bm, const int64_t* __restrict__ segoff,
                                                         int64_t nseg, int64_t segs_per_row, int64_t x0, int64_t dom_z,
                                                         int64_t* __restrict__ codes) {
@@ -248,8 +250,8 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const uint32_t* __restri
   // staging slot of the k-th code: lanes' runs start at unrelated offsets, so
   // XOR-ing the bank bits with the 32-slot row index spreads their stores
   auto sl = [](int k) { return k ^ ((k >> 5) & 31); };
-  const int64_t s0 = (int64_t)blockIdx.x * EM_SEGS;
-  for (int si = warp; si < EM_SEGS; si += EM_WARPS) {
+  const int64_t s0 = (int64_t)blockIdx.x * SEGS;
+  for (int si = warp; si < SEGS; si += EM_WARPS) {
     const int64_t s = s0 + si;
     if (s >= nseg) break;
     uint32_t word = bm[s * 32 + lane];
@@ -360,7 +362,17 @@ int emit_codes(const uint32_t* bm, const int64_t* segoff, int64_t rows, int64_t 
   }
   const int64_t nseg = rows * wpr / 32;
   if (nseg == 0) return MMJ_OK;
-  k_emit<<<(unsigned)ceil_div(nseg, EM_SEGS), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes);
+  static int segs = -1;
+  if (segs < 0) {
+    const char* e = getenv("MMJ_EMIT_SEGS");
+    segs = e ? atoi(e) : EM_SEGS;
+  }
+  switch (segs) {
+    case 8: k_emit<8><<<(unsigned)ceil_div(nseg, 8), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes); break;
+    case 16: k_emit<16><<<(unsigned)ceil_div(nseg, 16), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes); break;
+    case 32: k_emit<32><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes); break;
+    default: k_emit<EM_SEGS><<<(unsigned)ceil_div(nseg, EM_SEGS), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes);
+  }
   MMJ_CHECK_LAUNCH("k_emit");
   return MMJ_OK;
 }

@@ -66,6 +66,29 @@ __global__ void k_build_operand(const int32_t* __restrict__ rows, const int32_t*
   }
 }
 
+// z-pair operand for MMJ_MODE_BITMAP_PAIR: z = 32G + b (b = k + 8j) goes to
+// row 16G + 2k + (j >> 1) with weight 1 (j even) or 128 (j odd) -- the
+// placement the heavy_mma pair epilogue unpacks (mma_i8.cu pack_bits_pair).
+// The two halves of a byte come from different tuples -> word atomicOr.
+__global__ void k_build_operand_pairs(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                      int64_t n, const int32_t* __restrict__ left_deg, int64_t d2,
+                                      const int32_t* __restrict__ hpos, uint8_t* __restrict__ mat, int64_t row0,
+                                      int64_t nrows, int64_t kpad) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rows[t] - row0;
+    if (r < 0 || r >= nrows) continue;
+    if (left_deg[rows[t]] <= d2) continue;
+    const int32_t k = hpos[cols[t]];
+    if (k < 0) continue;
+    const int b = (int)(r & 31), kk = b & 7, j = b >> 3;
+    const int64_t prow = (r >> 5) * 16 + 2 * kk + (j >> 1);
+    const int64_t off = prow * kpad + k;
+    const uint32_t v = (j & 1) ? 0x80u : 0x01u;
+    atomicOr(reinterpret_cast<unsigned int*>(mat + (off & ~int64_t(3))), v << (8 * (off & 3)));
+  }
+}
+
 // ----------------------------------------------------------- light-z CSR
 __global__ void k_lz_flags(const int32_t* __restrict__ rev_idx, int64_t n,
                            const int32_t* __restrict__ left_deg, int64_t d2, uint8_t* __restrict__ flag) {
@@ -384,6 +407,21 @@ int build_operand(const int32_t* rows, const int32_t* cols, int64_t n, const int
   if (n == 0) return MMJ_OK;
   k_build_operand<<<grid_for(n, TPB), TPB, 0, st>>>(rows, cols, n, left_deg, d2, hpos, mat, row0, nrows, kpad);
   MMJ_CHECK_LAUNCH("k_build_operand");
+  return MMJ_OK;
+}
+
+int build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t d2,
+                        const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows, int64_t kpad,
+                        cudaStream_t st) {
+  if (kpad % 4 != 0 || reinterpret_cast<uintptr_t>(mat) % 4 != 0 || nrows % 32 != 0) {
+    set_error("build_operand_pairs: kpad and mat must be 4-byte aligned, nrows a multiple of 32");
+    return MMJ_ERR_ARG;
+  }
+  MMJ_TRY(cuda_status(cudaMemsetAsync(mat, 0, (size_t)((nrows / 2) * kpad), st), "memset operand"));
+  if (n == 0) return MMJ_OK;
+  k_build_operand_pairs<<<grid_for(n, TPB), TPB, 0, st>>>(rows, cols, n, left_deg, d2, hpos, mat, row0, nrows,
+                                                          kpad);
+  MMJ_CHECK_LAUNCH("k_build_operand_pairs");
   return MMJ_OK;
 }
 

@@ -68,7 +68,7 @@ class TwoPathEngine:
     def __init__(self, dr: DeviceRelation, ds: DeviceRelation, strategy: str, delta1: int, delta2: int,
                  want_counts: bool, *, min_count: int = 1, upper_only: bool = False,
                  chunk_rows: Optional[int] = None, ws: Optional[Workspace] = None,
-                 host_left_deg_r=None, host_left_deg_s=None):
+                 host_left_deg_r=None, host_left_deg_s=None, pair_operand: bool = True):
         import torch
         self.torch = torch
         self.lib = nat.load()
@@ -95,6 +95,8 @@ class TwoPathEngine:
         self.hpos = None
         self.A = None
         self.B = None
+        self.pairs = False
+        self.allow_pairs = bool(pair_operand)   # False: B stays one z per row (heavy_matrices reads it)
         self.kpad = 0
         self.lz_ptr = None
         self.lz_idx = None
@@ -146,11 +148,22 @@ class TwoPathEngine:
                 arows = _rup(max(self.dom_x, 1), BN)
                 brows = _rup(max(self.dom_z, 1), 1024)   # product covers every word of the padded rows
                 self.A = torch.empty((arows, kpad), dtype=torch.uint8, device="cuda")
-                self.B = torch.empty((brows, kpad), dtype=torch.uint8, device="cuda")
                 nat.call("mmj_build_operand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n, nat.ptr(dr.left_deg),
                          self.d2, nat.ptr(self.hpos), nat.ptr(self.A), 0, arows, kpad, st)
-                nat.call("mmj_build_operand", nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n, nat.ptr(ds.left_deg),
-                         self.d2, nat.ptr(self.hpos), nat.ptr(self.B), 0, brows, kpad, st)
+                self.pairs = (self.allow_pairs and not self.counts
+                              and __import__("os").environ.get("MMJ_PAIR", "1") != "0"
+                              and (k <= 127 or self._max_deg(self._host_ldeg_r, dr) <= 127
+                                   or self._max_deg(self._host_ldeg_s, ds) <= 127))
+                if self.pairs:
+                    # z pairs share one accumulator (weights 1, 128): every
+                    # count is < 128 because one side's heavy degrees are
+                    self.B = torch.empty((brows // 2, kpad), dtype=torch.uint8, device="cuda")
+                    nat.call("mmj_build_operand_pairs", nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n,
+                             nat.ptr(ds.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.B), 0, brows, kpad, st)
+                else:
+                    self.B = torch.empty((brows, kpad), dtype=torch.uint8, device="cuda")
+                    nat.call("mmj_build_operand", nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n,
+                             nat.ptr(ds.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.B), 0, brows, kpad, st)
             self.stats.kpad = self.kpad
             # light-z lists of S for pass 3
             n = ds.n
@@ -166,7 +179,15 @@ class TwoPathEngine:
     def _bitmap_mode(self) -> int:
         # every product entry counts <= K shared heavy y: with K <= 255 the
         # epilogue may pack counts as bytes
+        if self.pairs:
+            return nat.MODE_BITMAP_PAIR
         return nat.MODE_BITMAP_U8 if 0 < self.stats.k_heavy <= 255 else nat.MODE_BITMAP
+
+    @staticmethod
+    def _max_deg(host_deg, d: DeviceRelation) -> int:
+        if host_deg is not None:
+            return int(np.asarray(host_deg).max(initial=0))
+        return int(d.left_deg.max().item()) if d.left_deg.numel() else 0
 
     def _any_heavy(self, host_deg, d: DeviceRelation) -> bool:
         if host_deg is not None:
@@ -367,10 +388,11 @@ class TwoPathEngine:
             ev.record(ms)
             mma_done[i] = ev
 
+        merge_first = __import__("os").environ.get("MMJ_MERGE_FIRST", "0") == "1"
         if bounds:
             issue_mma(0)
         for i, (x0, x1) in enumerate(bounds):
-            if i + 1 < len(bounds):
+            if i + 1 < len(bounds) and not merge_first:
                 issue_mma(i + 1)
             b = i & 1
             rows = x1 - x0
@@ -386,6 +408,9 @@ class TwoPathEngine:
                      nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(self.wit), mst)
             if timer is not None:
                 timer.stop("light_merge", main)
+            if i + 1 < len(bounds) and merge_first:
+                issue_mma(i + 1)
+            if timer is not None:
                 timer.start("segments", main)
             nat.call("mmj_exclusive_scan_i32", nat.ptr(segcnt), nat.ptr(segoff), nseg,
                      nat.ptr(self.ws.scan_ws(rows_max * self.wpr // 32)), mst)

@@ -247,7 +247,7 @@ def heavy_matrices(r, s, delta1: int, delta2: int):
     if not (len(heavy_a) and len(heavy_b) and len(heavy_c)):
         return None
     eng = TwoPathEngine(dr, ds, PARTITIONED, delta1, delta2, False, host_left_deg_r=r.left_deg,
-                        host_left_deg_s=s.left_deg)
+                        host_left_deg_s=s.left_deg, pair_operand=False)
     eng.prepare()
     k = eng.stats.k_heavy
     a = eng.A[: r.rel.dom_left, :k].cpu().numpy()[heavy_a].astype(np.int64)
