@@ -350,12 +350,17 @@ def run_b200(args):
             info.update(witnesses=stats.light_intermediate, witness_rate=stats.light_intermediate / t)
         phase_info[name] = info
     dominant = max(phases, key=lambda k: phases[k]) if phases else "emit"
+    # DRAM bytes per launch from the committed ncu --set full capture, scaled
+    # to this run's launches by the measured traffic/algorithmic ratio
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             t = json.load(f).get(dominant)
-        traffic = t.get("dram_bytes_per_launch") if isinstance(t, dict) else t
+        if isinstance(t, dict) and dominant == "emit" and stats.chunks:
+            traffic = t["traffic_over_algorithmic"] * 8.0 * out_local / stats.chunks
+        elif isinstance(t, dict):
+            traffic = t.get("dram_bytes_per_launch")
     dom = phase_info.get(dominant, {})
     if dominant == "heavy_mma":
         roofline = {"bound": "tensor", "achieved": dom.get("achieved"), "peak": dom.get("peak_datasheet"),
