@@ -200,6 +200,41 @@ int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64
                    const uint32_t* s_bits, int words, const int32_t* r_lptr, const int32_t* r_lidx,
                    const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, void* stream);
 
+
+/* ---- device ingest: relation.py:37-69, 119-140, 148-186 ----
+ * Raw int64 pairs (n x 2, row-major) -> deduplicated, dictionary-encoded,
+ * semi-join-reduced relations and their int32 CSR, all in HBM.  Every call
+ * takes a caller workspace of >= mmj_ingest_workspace_bytes(n) bytes; counts
+ * come back in device int64 scalars (*_out), for the caller to read before
+ * sizing the next step.  Ids match the reference's bit for bit. */
+size_t mmj_ingest_workspace_bytes(int64_t n);
+/* keep-first dedup of (left, right) tuples in input order (dict.fromkeys, relation.py:53) */
+int mmj_ingest_dedup(const int64_t* pairs, int64_t n, int64_t* out, int64_t* n_out, void* ws, size_t ws_bytes,
+                     void* stream);
+/* first-seen dense ids of vals[i*stride] (relation.py:56-66): ids[n] int32, dict[ndict] int64 */
+int mmj_ingest_first_seen(const int64_t* vals, int64_t stride, int64_t n, int32_t* ids, int64_t* dict,
+                          int64_t* ndict, void* ws, size_t ws_bytes, void* stream);
+/* ascending distinct values of vals[i*stride] */
+int mmj_ingest_distinct(const int64_t* vals, int64_t stride, int64_t n, int64_t* out, int64_t* n_out, void* ws,
+                        size_t ws_bytes, void* stream);
+/* sorted-unique a intersect sorted-unique b (relation.py:121-122) */
+int mmj_ingest_intersect(const int64_t* a, int64_t na, const int64_t* b, int64_t nb, int64_t* out, int64_t* n_out,
+                         void* ws, size_t ws_bytes, void* stream);
+/* vals (ascending) in repr() order (relation.py:123): out[j] = vals[perm[j]], rank[perm[j]] = j */
+int mmj_ingest_repr_order(const int64_t* vals, int64_t n, int64_t* out, int32_t* rank, void* ws, size_t ws_bytes,
+                          void* stream);
+/* ids[i] = id_of_sorted[p] where sorted[p] == q[i*stride] (p if id_of_sorted is NULL), -1 if absent */
+int mmj_ingest_lookup(const int64_t* sorted, const int32_t* id_of_sorted, int64_t nd, const int64_t* q,
+                      int64_t stride, int64_t nq, int32_t* ids, void* stream);
+/* keep tuples with rid >= 0 in input order (relation.py:128-130): left raw values + right ids */
+int mmj_ingest_filter(const int64_t* pairs, const int32_t* rid, int64_t n, int64_t* left_out, int32_t* rid_out,
+                      int64_t* n_out, void* ws, size_t ws_bytes, void* stream);
+/* CSR of (rows, cols) with each row's cols ascending (relation.py:148-154): ptr[dom_rows+1],
+ * idx[n], row_of[n] (may be NULL), deg[dom_rows] (may be NULL); all int32 */
+int mmj_ingest_csr(const int32_t* rows, const int32_t* cols, int64_t n, int64_t dom_rows, int64_t dom_cols,
+                   int32_t* ptr, int32_t* idx, int32_t* row_of, int32_t* deg, void* ws, size_t ws_bytes,
+                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,6 +32,7 @@ P = C.c_void_p
 I64 = C.c_int64
 I32 = C.c_int32
 INT = C.c_int
+SZ = C.c_size_t
 
 _SIGS = {
     "mmj_abi_version": (INT, []),
@@ -43,6 +44,15 @@ _SIGS = {
     "mmj_exclusive_scan_i32": (INT, [P, P, I64, P, P]),
     "mmj_heavy_y_positions": (INT, [P, P, I64, I64, P, P, P, P, P]),
     "mmj_build_operand": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
+    "mmj_ingest_workspace_bytes": (SZ, [I64]),
+    "mmj_ingest_dedup": (INT, [P, I64, P, P, P, SZ, P]),
+    "mmj_ingest_first_seen": (INT, [P, I64, I64, P, P, P, P, SZ, P]),
+    "mmj_ingest_distinct": (INT, [P, I64, I64, P, P, P, SZ, P]),
+    "mmj_ingest_intersect": (INT, [P, I64, P, I64, P, P, P, SZ, P]),
+    "mmj_ingest_repr_order": (INT, [P, I64, P, P, P, SZ, P]),
+    "mmj_ingest_lookup": (INT, [P, P, I64, P, I64, I64, P, P]),
+    "mmj_ingest_filter": (INT, [P, P, I64, P, P, P, P, SZ, P]),
+    "mmj_ingest_csr": (INT, [P, P, I64, I64, I64, P, P, P, P, P, SZ, P]),
     "mmj_build_operand_pairs": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
     "mmj_light_z_csr": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P]),
     "mmj_light_lengths": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, I64, INT, P, P, P, P]),

@@ -1,0 +1,522 @@
+// Device-side ingest: dictionary encoding of raw
+// int64 (left, right) pairs and CSR construction in HBM, replacing the host
+// preparation the reference runs before its operators:
+//   Relation.from_raw_pairs   relation.py:37-69   keep-first dedup of tuples
+//                                                 (dict.fromkeys, 53) and
+//                                                 first-seen dense ids (56-66)
+//   semi_join_reduce_many     relation.py:119-140 shared right dictionary of
+//                                                 the common values ordered by
+//                                                 repr() (123), kept tuples in
+//                                                 input order, left ids re-assigned
+//                                                 first-seen over the kept tuples
+//   _csr / IndexedRelation    relation.py:148-186 both CSR directions, rows
+//                                                 ascending within each list
+// Every step is a stable radix sort (CUB) plus flag / scan / scatter kernels,
+// so the dense ids match the reference's bit for bit (first-seen = smallest
+// position among equal keys after a stable sort).  Sizes are < 2^31.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../include/mmjoin_b200.h"
+#include "mmj_common.cuh"
+
+namespace mmj {
+namespace {
+
+constexpr int TPB = 256;
+
+inline int grid1(int64_t n) {
+  int64_t g = ceil_div(n, TPB);
+  const int64_t cap = (int64_t)sm_count() * 16;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// bump allocator over the caller's workspace (256-B aligned slices)
+struct Bump {
+  char* base;
+  size_t cap, off;
+  template <typename T>
+  T* take(int64_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += (size_t)count * sizeof(T);
+    return p;
+  }
+  bool ok() const { return off <= cap; }
+};
+
+size_t sort_temp_bytes(int64_t n) {
+  size_t a = 0, b = 0, c = 0;
+  const int ni = (int)(n < 1 ? 1 : n);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const int64_t*)nullptr, (int64_t*)nullptr, (const int32_t*)nullptr,
+                                  (int32_t*)nullptr, ni);
+  cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, ni);
+  cub::DeviceRadixSort::SortKeys(nullptr, c, (const uint64_t*)nullptr, (uint64_t*)nullptr, ni);
+  size_t m = a > b ? a : b;
+  return (m > c ? m : c) + 256;
+}
+
+size_t ws_bytes(int64_t n) {
+  const int64_t m = n + 1;
+  // 4 x int64/uint64 key arrays, 4 x int32 arrays, 2 x u8 flags, scans, CUB temp
+  return 4 * (size_t)m * 8 + 6 * (size_t)m * 4 + 2 * (size_t)m + 2 * scan_ws_bytes(m) + sort_temp_bytes(m) +
+         32 * 256;
+}
+
+int check_n(int64_t n, const char* what) {
+  if (n < 0 || n >= (1ll << 31) - 1) {
+    set_error("%s: %lld items (must be in [0, 2^31-1))", what, (long long)n);
+    return MMJ_ERR_ARG;
+  }
+  return MMJ_OK;
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void k_iota(int32_t* v, int64_t n) { GRID_STRIDE(i, n) v[i] = (int32_t)i; }
+
+__global__ void k_column(const int64_t* __restrict__ src, int64_t stride, int64_t n, int64_t* __restrict__ dst) {
+  GRID_STRIDE(i, n) dst[i] = src[i * stride];
+}
+
+__global__ void k_gather_column(const int64_t* __restrict__ src, int64_t stride, const int32_t* __restrict__ perm,
+                                int64_t n, int64_t* __restrict__ dst) {
+  GRID_STRIDE(i, n) dst[i] = src[(int64_t)perm[i] * stride];
+}
+
+// keep flag at the original position of the first tuple of every equal (a, b) run
+__global__ void k_pair_heads(const int64_t* __restrict__ pairs, const int32_t* __restrict__ perm, int64_t n,
+                             uint8_t* __restrict__ keep) {
+  GRID_STRIDE(i, n) {
+    const int64_t p = perm[i];
+    bool head = (i == 0);
+    if (!head) {
+      const int64_t q = perm[i - 1];
+      head = pairs[2 * p] != pairs[2 * q] || pairs[2 * p + 1] != pairs[2 * q + 1];
+    }
+    keep[p] = head ? 1 : 0;
+  }
+}
+
+__global__ void k_compact_pairs(const int64_t* __restrict__ pairs, const uint8_t* __restrict__ keep,
+                                const int32_t* __restrict__ pos, int64_t n, int64_t* __restrict__ out) {
+  GRID_STRIDE(i, n) {
+    if (keep[i]) {
+      const int64_t o = pos[i];
+      out[2 * o] = pairs[2 * i];
+      out[2 * o + 1] = pairs[2 * i + 1];
+    }
+  }
+}
+
+__global__ void k_heads(const int64_t* __restrict__ ks, int64_t n, uint8_t* __restrict__ head) {
+  GRID_STRIDE(i, n) head[i] = (i == 0 || ks[i] != ks[i - 1]) ? 1 : 0;
+}
+
+// head j of run r (= E[j]): first position fp[r] = pos[j]; mark it
+__global__ void k_run_first(const uint8_t* __restrict__ head, const int32_t* __restrict__ E,
+                            const int32_t* __restrict__ pos, int64_t n, int32_t* __restrict__ fp,
+                            uint8_t* __restrict__ mark) {
+  GRID_STRIDE(j, n) {
+    if (head[j]) {
+      fp[E[j]] = pos[j];
+      mark[pos[j]] = 1;
+    }
+  }
+}
+
+__global__ void k_assign_ids(const int64_t* __restrict__ ks, const uint8_t* __restrict__ head,
+                             const int32_t* __restrict__ E, const int32_t* __restrict__ pos,
+                             const int32_t* __restrict__ fp, const int32_t* __restrict__ P, int64_t n,
+                             int32_t* __restrict__ ids, int64_t* __restrict__ dict) {
+  GRID_STRIDE(j, n) {
+    const int32_t r = E[j] + head[j] - 1;   // run of j (inclusive head count - 1)
+    const int32_t id = P[fp[r]];            // rank of the run's first position
+    ids[pos[j]] = id;
+    if (head[j] && dict) dict[id] = ks[j];
+  }
+}
+
+__global__ void k_compact_heads(const int64_t* __restrict__ ks, const uint8_t* __restrict__ head,
+                                const int32_t* __restrict__ E, int64_t n, int64_t* __restrict__ out) {
+  GRID_STRIDE(j, n) if (head[j]) out[E[j]] = ks[j];
+}
+
+__device__ __forceinline__ int64_t lower_bound_i64(const int64_t* __restrict__ v, int64_t n, int64_t key) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (v[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_member(const int64_t* __restrict__ a, int64_t na, const int64_t* __restrict__ b, int64_t nb,
+                         uint8_t* __restrict__ flag) {
+  GRID_STRIDE(i, na) {
+    const int64_t p = lower_bound_i64(b, nb, a[i]);
+    flag[i] = (p < nb && b[p] == a[i]) ? 1 : 0;
+  }
+}
+
+__global__ void k_compact_flagged(const int64_t* __restrict__ a, const uint8_t* __restrict__ flag,
+                                  const int32_t* __restrict__ pos, int64_t n, int64_t* __restrict__ out) {
+  GRID_STRIDE(i, n) if (flag[i]) out[pos[i]] = a[i];
+}
+
+__global__ void k_lookup(const int64_t* __restrict__ sorted, const int32_t* __restrict__ id_of_sorted, int64_t nd,
+                         const int64_t* __restrict__ q, int64_t stride, int64_t nq, int32_t* __restrict__ out) {
+  GRID_STRIDE(i, nq) {
+    const int64_t key = q[i * stride];
+    const int64_t p = lower_bound_i64(sorted, nd, key);
+    out[i] = (p < nd && sorted[p] == key) ? (id_of_sorted ? id_of_sorted[p] : (int32_t)p) : -1;
+  }
+}
+
+// decimal-string order of int64 (Python's repr of an int): '-' sorts before
+// every digit, a proper prefix before its extensions.  Symbol per character
+// position: 0 = end of string, digit d -> d + 1; 19 positions cover |int64|.
+__global__ void k_repr_keys(const int64_t* __restrict__ v, int64_t n, uint64_t* __restrict__ hi,
+                            uint64_t* __restrict__ lo) {
+  GRID_STRIDE(i, n) {
+    const int64_t x = v[i];
+    const bool neg = x < 0;
+    uint64_t u = neg ? (uint64_t)(-(x + 1)) + 1u : (uint64_t)x;
+    int d[20];
+    int len = 0;
+    do {
+      d[len++] = (int)(u % 10u);
+      u /= 10u;
+    } while (u);
+    uint64_t h = neg ? 0 : (1ull << 63), l = 0;
+#pragma unroll
+    for (int k = 0; k < 19; ++k) {
+      const uint64_t sym = k < len ? (uint64_t)(d[len - 1 - k] + 1) : 0ull;
+      if (k < 15) h |= sym << (59 - 4 * k);
+      else l |= sym << (12 - 4 * (k - 15));
+    }
+    hi[i] = h;
+    lo[i] = l;
+  }
+}
+
+__global__ void k_permute_i64(const int64_t* __restrict__ src, const int32_t* __restrict__ perm, int64_t n,
+                              int64_t* __restrict__ out, int32_t* __restrict__ rank) {
+  GRID_STRIDE(j, n) {
+    const int32_t p = perm[j];
+    out[j] = src[p];
+    rank[p] = (int32_t)j;
+  }
+}
+
+__global__ void k_filter_flags(const int32_t* __restrict__ rid, int64_t n, uint8_t* __restrict__ keep) {
+  GRID_STRIDE(i, n) keep[i] = rid[i] >= 0 ? 1 : 0;
+}
+
+__global__ void k_compact_kept(const int64_t* __restrict__ pairs, const int32_t* __restrict__ rid,
+                               const uint8_t* __restrict__ keep, const int32_t* __restrict__ pos, int64_t n,
+                               int64_t* __restrict__ left_out, int32_t* __restrict__ rid_out) {
+  GRID_STRIDE(i, n) {
+    if (keep[i]) {
+      left_out[pos[i]] = pairs[2 * i];
+      rid_out[pos[i]] = rid[i];
+    }
+  }
+}
+
+__global__ void k_csr_keys(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols, int64_t n, int cb,
+                           uint64_t* __restrict__ key) {
+  GRID_STRIDE(i, n) key[i] = ((uint64_t)(uint32_t)rows[i] << cb) | (uint32_t)cols[i];
+}
+
+// rows are runs of the sorted keys: the run's first and last tuple write its
+// length (no atomics on hot rows)
+__global__ void k_csr_unpack(const uint64_t* __restrict__ key, int64_t n, int cb, int32_t* __restrict__ idx,
+                             int32_t* __restrict__ row_of, int32_t* __restrict__ first, int32_t* __restrict__ cnt) {
+  GRID_STRIDE(i, n) {
+    const uint64_t k = key[i];
+    const int32_t r = (int32_t)(k >> cb);
+    idx[i] = (int32_t)(k & ((1ull << cb) - 1));
+    if (row_of) row_of[i] = r;
+    if (i == 0 || (int32_t)(key[i - 1] >> cb) != r) first[r] = (int32_t)i;
+  }
+}
+
+__global__ void k_csr_counts(const uint64_t* __restrict__ key, int64_t n, int cb, const int32_t* __restrict__ first,
+                             int32_t* __restrict__ cnt) {
+  GRID_STRIDE(i, n) {
+    const int32_t r = (int32_t)(key[i] >> cb);
+    if (i == n - 1 || (int32_t)(key[i + 1] >> cb) != r) cnt[r] = (int32_t)i + 1 - first[r];
+  }
+}
+
+__global__ void k_degrees(const int32_t* __restrict__ ptr, int64_t dom, int32_t* __restrict__ deg) {
+  GRID_STRIDE(i, dom) deg[i] = ptr[i + 1] - ptr[i];
+}
+
+int bits_for(int64_t v) {   // bits to represent values in [0, v)
+  int b = 1;
+  while (b < 62 && (1ll << b) < v) ++b;
+  return b;
+}
+
+// stable sort of (int64 keys, int32 values), results in *_out
+int sort_pairs_i64(void* tmp, size_t tmp_bytes, const int64_t* k_in, int64_t* k_out, const int32_t* v_in,
+                   int32_t* v_out, int64_t n, cudaStream_t st) {
+  if (n == 0) return MMJ_OK;
+  size_t tb = tmp_bytes;
+  MMJ_TRY(cuda_status(cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, v_in, v_out, (int)n, 0, 64, st),
+                      "cub SortPairs(int64)"));
+  count_launch();
+  return MMJ_OK;
+}
+
+int sort_pairs_u64(void* tmp, size_t tmp_bytes, const uint64_t* k_in, uint64_t* k_out, const int32_t* v_in,
+                   int32_t* v_out, int64_t n, int begin_bit, int end_bit, cudaStream_t st) {
+  if (n == 0) return MMJ_OK;
+  size_t tb = tmp_bytes;
+  MMJ_TRY(cuda_status(
+      cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, v_in, v_out, (int)n, begin_bit, end_bit, st),
+      "cub SortPairs(uint64)"));
+  count_launch();
+  return MMJ_OK;
+}
+
+struct Scratch {
+  Bump w;
+  int64_t *k0, *k1, *k2, *k3;
+  int32_t *v0, *v1, *i0, *i1, *i2, *i3;
+  uint8_t *f0, *f1;
+  void *scan0, *scan1, *tmp;
+  size_t tmp_bytes;
+};
+
+int carve(void* ws, size_t ws_bytes, int64_t n, Scratch& s) {
+  s.w = Bump{static_cast<char*>(ws), ws_bytes, 0};
+  const int64_t m = n + 1;
+  s.k0 = s.w.take<int64_t>(m);
+  s.k1 = s.w.take<int64_t>(m);
+  s.k2 = s.w.take<int64_t>(m);
+  s.k3 = s.w.take<int64_t>(m);
+  s.v0 = s.w.take<int32_t>(m);
+  s.v1 = s.w.take<int32_t>(m);
+  s.i0 = s.w.take<int32_t>(m);
+  s.i1 = s.w.take<int32_t>(m);
+  s.i2 = s.w.take<int32_t>(m);
+  s.i3 = s.w.take<int32_t>(m);
+  s.f0 = s.w.take<uint8_t>(m);
+  s.f1 = s.w.take<uint8_t>(m);
+  s.scan0 = s.w.take<char>((int64_t)scan_ws_bytes(m));
+  s.scan1 = s.w.take<char>((int64_t)scan_ws_bytes(m));
+  s.tmp_bytes = sort_temp_bytes(m);
+  s.tmp = s.w.take<char>((int64_t)s.tmp_bytes);
+  if (!s.w.ok() || ws == nullptr) {
+    set_error("ingest: workspace of %zu bytes too small (need mmj_ingest_workspace_bytes(%lld) = %zu)", ws_bytes,
+              (long long)n, mmj::ws_bytes(n));
+    return MMJ_ERR_ARG;
+  }
+  return MMJ_OK;
+}
+
+}  // namespace
+
+// first-seen ids of vals[i*stride] (i < n): ids[i], dict[id] = value, *ndict
+int first_seen(const int64_t* vals, int64_t stride, int64_t n, int32_t* ids, int64_t* dict, int64_t* ndict,
+               Scratch& s, cudaStream_t st) {
+  if (n == 0) return cuda_status(cudaMemsetAsync(ndict, 0, 8, st), "memset");
+  k_column<<<grid1(n), TPB, 0, st>>>(vals, stride, n, s.k0);
+  MMJ_CHECK_LAUNCH("k_column");
+  k_iota<<<grid1(n), TPB, 0, st>>>(s.v0, n);
+  MMJ_CHECK_LAUNCH("k_iota");
+  MMJ_TRY(sort_pairs_i64(s.tmp, s.tmp_bytes, s.k0, s.k1, s.v0, s.v1, n, st));   // k1 sorted, v1 = positions
+  k_heads<<<grid1(n), TPB, 0, st>>>(s.k1, n, s.f0);
+  MMJ_CHECK_LAUNCH("k_heads");
+  MMJ_TRY(scan_u8_i32(s.f0, s.i0, n, s.scan0, st));   // i0 = E (exclusive head count), i0[n] = #runs
+  MMJ_TRY(cuda_status(cudaMemsetAsync(s.f1, 0, (size_t)n, st), "memset mark"));
+  k_run_first<<<grid1(n), TPB, 0, st>>>(s.f0, s.i0, s.v1, n, s.i1, s.f1);
+  MMJ_CHECK_LAUNCH("k_run_first");
+  MMJ_TRY(scan_u8_i32(s.f1, s.i2, n, s.scan1, st));   // i2 = P: rank of a first position
+  k_assign_ids<<<grid1(n), TPB, 0, st>>>(s.k1, s.f0, s.i0, s.v1, s.i1, s.i2, n, ids, dict);
+  MMJ_CHECK_LAUNCH("k_assign_ids");
+  // *ndict = number of runs (int32 -> int64)
+  MMJ_TRY(cuda_status(cudaMemsetAsync(ndict, 0, 8, st), "memset ndict"));
+  return cuda_status(cudaMemcpyAsync(ndict, s.i0 + n, 4, cudaMemcpyDeviceToDevice, st), "ndict");
+}
+
+}  // namespace mmj
+
+using namespace mmj;
+
+extern "C" {
+
+size_t mmj_ingest_workspace_bytes(int64_t n) { return ws_bytes(n < 0 ? 0 : n); }
+
+int mmj_ingest_dedup(const int64_t* pairs, int64_t n, int64_t* out, int64_t* n_out, void* ws, size_t ws_bytes,
+                     void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_dedup"));
+  if (n == 0) return cuda_status(cudaMemsetAsync(n_out, 0, 8, st), "memset");
+  Scratch s;
+  MMJ_TRY(carve(ws, ws_bytes, n, s));
+  // stable LSD: by right value, then by left value; ties keep input order
+  k_column<<<grid1(n), TPB, 0, st>>>(pairs + 1, 2, n, s.k0);
+  MMJ_CHECK_LAUNCH("k_column");
+  k_iota<<<grid1(n), TPB, 0, st>>>(s.v0, n);
+  MMJ_CHECK_LAUNCH("k_iota");
+  MMJ_TRY(sort_pairs_i64(s.tmp, s.tmp_bytes, s.k0, s.k1, s.v0, s.v1, n, st));
+  k_gather_column<<<grid1(n), TPB, 0, st>>>(pairs, 2, s.v1, n, s.k2);
+  MMJ_CHECK_LAUNCH("k_gather_column");
+  MMJ_TRY(sort_pairs_i64(s.tmp, s.tmp_bytes, s.k2, s.k3, s.v1, s.v0, n, st));   // v0 = perm by (a, b, pos)
+  k_pair_heads<<<grid1(n), TPB, 0, st>>>(pairs, s.v0, n, s.f0);
+  MMJ_CHECK_LAUNCH("k_pair_heads");
+  MMJ_TRY(scan_u8_i32(s.f0, s.i0, n, s.scan0, st));
+  k_compact_pairs<<<grid1(n), TPB, 0, st>>>(pairs, s.f0, s.i0, n, out);
+  MMJ_CHECK_LAUNCH("k_compact_pairs");
+  MMJ_TRY(cuda_status(cudaMemsetAsync(n_out, 0, 8, st), "memset n_out"));
+  return cuda_status(cudaMemcpyAsync(n_out, s.i0 + n, 4, cudaMemcpyDeviceToDevice, st), "n_out");
+}
+
+int mmj_ingest_first_seen(const int64_t* vals, int64_t stride, int64_t n, int32_t* ids, int64_t* dict,
+                          int64_t* ndict, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_first_seen"));
+  if (stride < 1) {
+    set_error("ingest_first_seen: stride must be >= 1");
+    return MMJ_ERR_ARG;
+  }
+  Scratch s;
+  MMJ_TRY(carve(ws, ws_bytes, n, s));
+  return first_seen(vals, stride, n, ids, dict, ndict, s, st);
+}
+
+int mmj_ingest_distinct(const int64_t* vals, int64_t stride, int64_t n, int64_t* out, int64_t* n_out, void* ws,
+                        size_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_distinct"));
+  if (n == 0) return cuda_status(cudaMemsetAsync(n_out, 0, 8, st), "memset");
+  Scratch s;
+  MMJ_TRY(carve(ws, ws_bytes, n, s));
+  k_column<<<grid1(n), TPB, 0, st>>>(vals, stride, n, s.k0);
+  MMJ_CHECK_LAUNCH("k_column");
+  k_iota<<<grid1(n), TPB, 0, st>>>(s.v0, n);
+  MMJ_CHECK_LAUNCH("k_iota");
+  MMJ_TRY(sort_pairs_i64(s.tmp, s.tmp_bytes, s.k0, s.k1, s.v0, s.v1, n, st));
+  k_heads<<<grid1(n), TPB, 0, st>>>(s.k1, n, s.f0);
+  MMJ_CHECK_LAUNCH("k_heads");
+  MMJ_TRY(scan_u8_i32(s.f0, s.i0, n, s.scan0, st));
+  k_compact_heads<<<grid1(n), TPB, 0, st>>>(s.k1, s.f0, s.i0, n, out);
+  MMJ_CHECK_LAUNCH("k_compact_heads");
+  MMJ_TRY(cuda_status(cudaMemsetAsync(n_out, 0, 8, st), "memset n_out"));
+  return cuda_status(cudaMemcpyAsync(n_out, s.i0 + n, 4, cudaMemcpyDeviceToDevice, st), "n_out");
+}
+
+int mmj_ingest_intersect(const int64_t* a, int64_t na, const int64_t* b, int64_t nb, int64_t* out, int64_t* n_out,
+                         void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(na, "ingest_intersect"));
+  MMJ_TRY(check_n(nb, "ingest_intersect"));
+  if (na == 0) return cuda_status(cudaMemsetAsync(n_out, 0, 8, st), "memset");
+  Scratch s;
+  MMJ_TRY(carve(ws, ws_bytes, na, s));
+  k_member<<<grid1(na), TPB, 0, st>>>(a, na, b, nb, s.f0);
+  MMJ_CHECK_LAUNCH("k_member");
+  MMJ_TRY(scan_u8_i32(s.f0, s.i0, na, s.scan0, st));
+  k_compact_flagged<<<grid1(na), TPB, 0, st>>>(a, s.f0, s.i0, na, out);
+  MMJ_CHECK_LAUNCH("k_compact_flagged");
+  MMJ_TRY(cuda_status(cudaMemsetAsync(n_out, 0, 8, st), "memset n_out"));
+  return cuda_status(cudaMemcpyAsync(n_out, s.i0 + na, 4, cudaMemcpyDeviceToDevice, st), "n_out");
+}
+
+int mmj_ingest_repr_order(const int64_t* vals, int64_t n, int64_t* out, int32_t* rank, void* ws, size_t ws_bytes,
+                          void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_repr_order"));
+  if (n == 0) return MMJ_OK;
+  Scratch s;
+  MMJ_TRY(carve(ws, ws_bytes, n, s));
+  uint64_t* hi = reinterpret_cast<uint64_t*>(s.k0);
+  uint64_t* lo = reinterpret_cast<uint64_t*>(s.k1);
+  k_repr_keys<<<grid1(n), TPB, 0, st>>>(vals, n, hi, lo);
+  MMJ_CHECK_LAUNCH("k_repr_keys");
+  k_iota<<<grid1(n), TPB, 0, st>>>(s.v0, n);
+  MMJ_CHECK_LAUNCH("k_iota");
+  // LSD: low 16 bits of the key first, then the high word, both stable
+  MMJ_TRY(sort_pairs_u64(s.tmp, s.tmp_bytes, lo, reinterpret_cast<uint64_t*>(s.k2), s.v0, s.v1, n, 0, 16, st));
+  k_gather_column<<<grid1(n), TPB, 0, st>>>(reinterpret_cast<const int64_t*>(hi), 1, s.v1, n, s.k3);
+  MMJ_CHECK_LAUNCH("k_gather_column");
+  MMJ_TRY(sort_pairs_u64(s.tmp, s.tmp_bytes, reinterpret_cast<const uint64_t*>(s.k3),
+                         reinterpret_cast<uint64_t*>(s.k2), s.v1, s.v0, n, 0, 64, st));
+  k_permute_i64<<<grid1(n), TPB, 0, st>>>(vals, s.v0, n, out, rank);
+  MMJ_CHECK_LAUNCH("k_permute_i64");
+  return MMJ_OK;
+}
+
+int mmj_ingest_lookup(const int64_t* sorted, const int32_t* id_of_sorted, int64_t nd, const int64_t* q,
+                      int64_t stride, int64_t nq, int32_t* ids, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(nd, "ingest_lookup"));
+  if (nq < 0 || stride < 1) {
+    set_error("ingest_lookup: bad query count / stride");
+    return MMJ_ERR_ARG;
+  }
+  if (nq == 0) return MMJ_OK;
+  k_lookup<<<grid1(nq), TPB, 0, st>>>(sorted, id_of_sorted, nd, q, stride, nq, ids);
+  MMJ_CHECK_LAUNCH("k_lookup");
+  return MMJ_OK;
+}
+
+int mmj_ingest_filter(const int64_t* pairs, const int32_t* rid, int64_t n, int64_t* left_out, int32_t* rid_out,
+                      int64_t* n_out, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_filter"));
+  if (n == 0) return cuda_status(cudaMemsetAsync(n_out, 0, 8, st), "memset");
+  Scratch s;
+  MMJ_TRY(carve(ws, ws_bytes, n, s));
+  k_filter_flags<<<grid1(n), TPB, 0, st>>>(rid, n, s.f0);
+  MMJ_CHECK_LAUNCH("k_filter_flags");
+  MMJ_TRY(scan_u8_i32(s.f0, s.i0, n, s.scan0, st));
+  k_compact_kept<<<grid1(n), TPB, 0, st>>>(pairs, rid, s.f0, s.i0, n, left_out, rid_out);
+  MMJ_CHECK_LAUNCH("k_compact_kept");
+  MMJ_TRY(cuda_status(cudaMemsetAsync(n_out, 0, 8, st), "memset n_out"));
+  return cuda_status(cudaMemcpyAsync(n_out, s.i0 + n, 4, cudaMemcpyDeviceToDevice, st), "n_out");
+}
+
+int mmj_ingest_csr(const int32_t* rows, const int32_t* cols, int64_t n, int64_t dom_rows, int64_t dom_cols,
+                   int32_t* ptr, int32_t* idx, int32_t* row_of, int32_t* deg, void* ws, size_t ws_bytes,
+                   void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_csr"));
+  MMJ_TRY(check_n(dom_rows, "ingest_csr"));
+  MMJ_TRY(check_n(dom_cols, "ingest_csr"));
+  Scratch s;
+  MMJ_TRY(carve(ws, ws_bytes, n > dom_rows ? n : dom_rows, s));
+  int32_t* cnt = s.i3;
+  MMJ_TRY(cuda_status(cudaMemsetAsync(cnt, 0, (size_t)(dom_rows + 1) * 4, st), "memset counts"));
+  if (n > 0) {
+    const int cb = bits_for(dom_cols);
+    const int rb = bits_for(dom_rows);
+    uint64_t* key = reinterpret_cast<uint64_t*>(s.k0);
+    uint64_t* key_sorted = reinterpret_cast<uint64_t*>(s.k1);
+    k_csr_keys<<<grid1(n), TPB, 0, st>>>(rows, cols, n, cb, key);
+    MMJ_CHECK_LAUNCH("k_csr_keys");
+    size_t tb = s.tmp_bytes;
+    MMJ_TRY(cuda_status(cub::DeviceRadixSort::SortKeys(s.tmp, tb, key, key_sorted, (int)n, 0, cb + rb, st),
+                        "cub SortKeys"));
+    count_launch();
+    k_csr_unpack<<<grid1(n), TPB, 0, st>>>(key_sorted, n, cb, idx, row_of, s.i2, cnt);
+    MMJ_CHECK_LAUNCH("k_csr_unpack");
+    k_csr_counts<<<grid1(n), TPB, 0, st>>>(key_sorted, n, cb, s.i2, cnt);
+    MMJ_CHECK_LAUNCH("k_csr_counts");
+  }
+  MMJ_TRY(scan_i32_i32(cnt, ptr, dom_rows, s.scan0, st));
+  if (deg && dom_rows > 0) {
+    k_degrees<<<grid1(dom_rows), TPB, 0, st>>>(ptr, dom_rows, deg);
+    MMJ_CHECK_LAUNCH("k_degrees");
+  }
+  return MMJ_OK;
+}
+
+}  // extern "C"

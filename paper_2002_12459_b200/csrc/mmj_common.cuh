@@ -55,6 +55,7 @@ size_t scan_ws_bytes(int64_t n);
 int scan_i32_i64(const int32_t* in, int64_t* out, int64_t n, void* ws, cudaStream_t st);
 int scan_u8_i32(const uint8_t* in, int32_t* out, int64_t n, void* ws, cudaStream_t st);
 int scan_i64_i64(const int64_t* in, int64_t* out, int64_t n, void* ws, cudaStream_t st);
+int scan_i32_i32(const int32_t* in, int32_t* out, int64_t n, void* ws, cudaStream_t st);
 
 }  // namespace mmj
 

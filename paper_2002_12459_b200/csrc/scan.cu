@@ -133,6 +133,9 @@ int scan_i32_i64(const int32_t* in, int64_t* out, int64_t n, void* ws, cudaStrea
 int scan_u8_i32(const uint8_t* in, int32_t* out, int64_t n, void* ws, cudaStream_t st) {
   return scan_impl<uint8_t, int32_t>(in, out, n, ws, st);
 }
+int scan_i32_i32(const int32_t* in, int32_t* out, int64_t n, void* ws, cudaStream_t st) {
+  return scan_impl<int32_t, int32_t>(in, out, n, ws, st);
+}
 int scan_i64_i64(const int64_t* in, int64_t* out, int64_t n, void* ws, cudaStream_t st) {
   return scan_impl<int64_t, int64_t>(in, out, n, ws, st);
 }
