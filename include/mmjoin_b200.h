@@ -231,6 +231,13 @@ int mmj_ingest_filter(const int64_t* pairs, const int32_t* rid, int64_t n, int64
                       int64_t* n_out, void* ws, size_t ws_bytes, void* stream);
 /* CSR of (rows, cols) with each row's cols ascending (relation.py:148-154): ptr[dom_rows+1],
  * idx[n], row_of[n] (may be NULL), deg[dom_rows] (may be NULL); all int32 */
+/* ascending vals with their positions: sorted[j] = vals[order[j]] (stable) */
+int mmj_ingest_sort_ids(const int64_t* vals, int64_t n, int64_t* sorted, int32_t* order, void* ws, size_t ws_bytes,
+                        void* stream);
+/* out[i] = map[idx[i]] */
+int mmj_ingest_remap(const int32_t* idx, int64_t n, const int32_t* map, int32_t* out, void* stream);
+/* cnt[v] = #{i : idx[i] == v}, v < dom (cnt zeroed first) */
+int mmj_ingest_histogram(const int32_t* idx, int64_t n, int64_t dom, int32_t* cnt, void* stream);
 int mmj_ingest_csr(const int32_t* rows, const int32_t* cols, int64_t n, int64_t dom_rows, int64_t dom_cols,
                    int32_t* ptr, int32_t* idx, int32_t* row_of, int32_t* deg, void* ws, size_t ws_bytes,
                    void* stream);

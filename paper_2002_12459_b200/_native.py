@@ -52,6 +52,9 @@ _SIGS = {
     "mmj_ingest_repr_order": (INT, [P, I64, P, P, P, SZ, P]),
     "mmj_ingest_lookup": (INT, [P, P, I64, P, I64, I64, P, P]),
     "mmj_ingest_filter": (INT, [P, P, I64, P, P, P, P, SZ, P]),
+    "mmj_ingest_sort_ids": (INT, [P, I64, P, P, P, SZ, P]),
+    "mmj_ingest_remap": (INT, [P, I64, P, P, P]),
+    "mmj_ingest_histogram": (INT, [P, I64, I64, P, P]),
     "mmj_ingest_csr": (INT, [P, P, I64, I64, I64, P, P, P, P, P, SZ, P]),
     "mmj_build_operand_pairs": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
     "mmj_light_z_csr": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P]),

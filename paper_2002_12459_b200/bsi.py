@@ -90,12 +90,49 @@ def _side(idx, y_map, dom_y, pinned=False) -> BsiSide:
     return BsiSide(len(fidx), idx.rel.dom_left, dev["fwd_ptr"], dev["fwd_idx"], dev["fwd_row"], ydeg, sv, od, nbytes)
 
 
+def _side_device(idx, y_map, dom_y, ws) -> BsiSide:
+    """BsiSide of a device-ingested relation without any host round trip:
+    y ids remapped into the shared space and each list re-sorted on the
+    device (ingest.cu)."""
+    from . import ingest
+    d = idx.device
+    if y_map is None:
+        fptr, fidx, frow = d.fwd_ptr, d.fwd_idx, d.fwd_row
+        ydeg = np.asarray(idx.right_deg, dtype=np.int32)
+    else:
+        mapped = ingest.remap(d.fwd_idx, y_map)
+        fptr, fidx, frow, _ = ingest.csr(d.fwd_row, mapped, d.dom_left, dom_y, ws)
+        ydeg = ingest.histogram(mapped, dom_y).cpu().numpy().astype(np.int32)
+    sv, od = ingest.sorted_ids(idx._left_values_dev, ws)
+    return BsiSide(d.n, d.dom_left, fptr, fidx, frow, ydeg, sv, od, 0)
+
+
+def _prepare_device(r, s):
+    from . import ingest
+    ws = ingest.IngestWorkspace()
+    if r.rel.right_values is s.rel.right_values:
+        dom_y = r.rel.dom_right
+        return _side_device(r, None, dom_y, ws), _side_device(s, None, dom_y, ws), dom_y
+    torch = _torch()
+    rv, sv = r._right_values_dev, s._right_values_dev
+    allv = ingest.distinct(torch.cat([rv, sv]), ws)
+    dom_y = int(allv.numel())
+    rmap, smap = ingest.lookup(allv, rv), ingest.lookup(allv, sv)
+    return _side_device(r, rmap, dom_y, ws), _side_device(s, smap, dom_y, ws), dom_y
+
+
 def prepare(r, s, pinned=False):
     """Device sides of R and S over one y id space (cached on the objects)."""
     key = (id(r), id(s))
     cache = getattr(r, "_mmj_bsi_cache", None)
     if cache is not None and cache[0] == key and not pinned:
         return cache[1]
+    from .ingest import DeviceIndexedRelation
+    if (isinstance(r, DeviceIndexedRelation) and isinstance(s, DeviceIndexedRelation) and not pinned
+            and r._right_values_dev is not None and s._right_values_dev is not None):
+        sides = _prepare_device(r, s)
+        r._mmj_bsi_cache = (key, sides)
+        return sides
     if r.rel.right_values is s.rel.right_values:
         dom_y = r.rel.dom_right
         sides = (_side(r, None, dom_y, pinned), _side(s, None, dom_y, pinned), dom_y)

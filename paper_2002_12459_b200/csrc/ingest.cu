@@ -257,6 +257,15 @@ __global__ void k_degrees(const int32_t* __restrict__ ptr, int64_t dom, int32_t*
   GRID_STRIDE(i, dom) deg[i] = ptr[i + 1] - ptr[i];
 }
 
+__global__ void k_remap(const int32_t* __restrict__ idx, int64_t n, const int32_t* __restrict__ map,
+                        int32_t* __restrict__ out) {
+  GRID_STRIDE(i, n) out[i] = map[idx[i]];
+}
+
+__global__ void k_histogram(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ cnt) {
+  GRID_STRIDE(i, n) atomicAdd(&cnt[idx[i]], 1);
+}
+
 int bits_for(int64_t v) {   // bits to represent values in [0, v)
   int b = 1;
   while (b < 62 && (1ll << b) < v) ++b;
@@ -516,6 +525,37 @@ int mmj_ingest_csr(const int32_t* rows, const int32_t* cols, int64_t n, int64_t 
     k_degrees<<<grid1(dom_rows), TPB, 0, st>>>(ptr, dom_rows, deg);
     MMJ_CHECK_LAUNCH("k_degrees");
   }
+  return MMJ_OK;
+}
+
+int mmj_ingest_sort_ids(const int64_t* vals, int64_t n, int64_t* sorted, int32_t* order, void* ws, size_t ws_bytes,
+                        void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_sort_ids"));
+  if (n == 0) return MMJ_OK;
+  Scratch s;
+  MMJ_TRY(carve(ws, ws_bytes, n, s));
+  k_iota<<<grid1(n), TPB, 0, st>>>(s.v0, n);
+  MMJ_CHECK_LAUNCH("k_iota");
+  return sort_pairs_i64(s.tmp, s.tmp_bytes, vals, sorted, s.v0, order, n, st);
+}
+
+int mmj_ingest_remap(const int32_t* idx, int64_t n, const int32_t* map, int32_t* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_remap"));
+  if (n == 0) return MMJ_OK;
+  k_remap<<<grid1(n), TPB, 0, st>>>(idx, n, map, out);
+  MMJ_CHECK_LAUNCH("k_remap");
+  return MMJ_OK;
+}
+
+int mmj_ingest_histogram(const int32_t* idx, int64_t n, int64_t dom, int32_t* cnt, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_histogram"));
+  MMJ_TRY(cuda_status(cudaMemsetAsync(cnt, 0, (size_t)(dom > 0 ? dom : 1) * 4, st), "memset histogram"));
+  if (n == 0) return MMJ_OK;
+  k_histogram<<<grid1(n), TPB, 0, st>>>(idx, n, cnt);
+  MMJ_CHECK_LAUNCH("k_histogram");
   return MMJ_OK;
 }
 

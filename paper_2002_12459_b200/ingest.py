@@ -31,7 +31,8 @@ from . import _native as nat
 from .device import DeviceRelation
 from .relation import ValueIndex
 
-__all__ = ["DeviceIndexedRelation", "from_raw_pairs_device", "semi_join_reduce_device", "IngestWorkspace"]
+__all__ = ["DeviceIndexedRelation", "from_raw_pairs_device", "semi_join_reduce_device", "IngestWorkspace",
+           "sorted_ids", "remap", "histogram", "distinct", "lookup", "csr"]
 
 
 def _torch():
@@ -132,7 +133,7 @@ class _DeviceRel:
         self.left_values = left_values          # numpy int64 (dom_left)
         self.right_values = right_values        # numpy int64 (dom_right), shared after a semi-join
         self._left_ids = None
-        self.right_ids = right_ids
+        self._right_ids = right_ids               # ValueIndex or a zero-arg factory (built on first use)
         self._pairs = None
 
     @property
@@ -146,6 +147,12 @@ class _DeviceRel:
     @property
     def dom_right(self) -> int:
         return len(self.right_values)
+
+    @property
+    def right_ids(self):
+        if callable(self._right_ids):
+            self._right_ids = self._right_ids()
+        return self._right_ids
 
     @property
     def left_ids(self):
@@ -184,8 +191,10 @@ class DeviceIndexedRelation:
     lazily, the degree vectors eagerly (they are small and the planners read
     them)."""
 
-    def __init__(self, name, lid, rid, left_values_dev, right_values_host, right_ids, ws: IngestWorkspace):
+    def __init__(self, name, lid, rid, left_values_dev, right_values_host, right_ids, ws: IngestWorkspace,
+                 right_values_dev=None):
         torch = _torch()
+        self._right_values_dev = right_values_dev
         n = int(lid.numel())
         dom_l = int(left_values_dev.numel())
         dom_r = len(right_values_host)
@@ -264,7 +273,7 @@ def from_raw_pairs_device(name: str, raw, ws: Optional[IngestWorkspace] = None) 
     lid, lvals = _first_seen(flat, 2, n, ws)
     rid, rvals = _first_seen(flat[1:] if n else flat, 2, n, ws)
     rv = rvals.cpu().numpy()
-    return DeviceIndexedRelation(name, lid, rid, lvals, rv, ValueIndex(rv), ws)
+    return DeviceIndexedRelation(name, lid, rid, lvals, rv, lambda: ValueIndex(rv), ws, right_values_dev=rvals)
 
 
 def semi_join_reduce_device(raws: Sequence, names: Optional[Sequence[str]] = None,
@@ -289,7 +298,12 @@ def semi_join_reduce_device(raws: Sequence, names: Optional[Sequence[str]] = Non
         nat.call("mmj_ingest_repr_order", nat.ptr(common), m, nat.ptr(right_sorted), nat.ptr(rank), nat.ptr(buf), nb,
                  nat.stream_handle())
     rv = right_sorted[:m].cpu().numpy()
-    rids = ValueIndex(rv)
+    shared_ids = []
+
+    def rids():   # one ValueIndex for the whole group, built on first use
+        if not shared_ids:
+            shared_ids.append(ValueIndex(rv))
+        return shared_ids[0]
     out = []
     for name, t in zip(names, deduped):
         n = t.shape[0]
@@ -305,5 +319,52 @@ def semi_join_reduce_device(raws: Sequence, names: Optional[Sequence[str]] = Non
                  nat.ptr(buf), nb, nat.stream_handle())
         k = _scalar(cnt)
         lid, lvals = _first_seen(left_kept, 1, k, ws)
-        out.append(DeviceIndexedRelation(name, lid, rid[:k], lvals, rv, rids, ws))
+        out.append(DeviceIndexedRelation(name, lid, rid[:k], lvals, rv, rids, ws, right_values_dev=right_sorted[:m]))
     return out
+
+
+# ---- small device helpers reused by the BSI preparation (bsi.py)
+def sorted_ids(vals, ws: Optional[IngestWorkspace] = None):
+    """(ascending values, int32 position of each) of a device int64 vector."""
+    torch = _torch()
+    ws = ws or IngestWorkspace()
+    n = int(vals.numel())
+    srt = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    order = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    buf, nb = ws.get(n)
+    nat.call("mmj_ingest_sort_ids", nat.ptr(vals), n, nat.ptr(srt), nat.ptr(order), nat.ptr(buf), nb,
+             nat.stream_handle())
+    return srt[:n], order[:n]
+
+
+def remap(idx, table):
+    torch = _torch()
+    out = torch.empty_like(idx)
+    nat.call("mmj_ingest_remap", nat.ptr(idx), int(idx.numel()), nat.ptr(table), nat.ptr(out), nat.stream_handle())
+    return out
+
+
+def histogram(idx, dom: int):
+    torch = _torch()
+    cnt = torch.empty(max(dom, 1), dtype=torch.int32, device="cuda")
+    nat.call("mmj_ingest_histogram", nat.ptr(idx), int(idx.numel()), dom, nat.ptr(cnt), nat.stream_handle())
+    return cnt[:dom]
+
+
+def distinct(vals, ws: Optional[IngestWorkspace] = None):
+    ws = ws or IngestWorkspace()
+    return _distinct(vals, 1, int(vals.numel()), ws)
+
+
+def lookup(sorted_vals, q, ids_of_sorted=None):
+    torch = _torch()
+    n = int(q.numel())
+    out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    nat.call("mmj_ingest_lookup", nat.ptr(sorted_vals), nat.ptr(ids_of_sorted) if ids_of_sorted is not None else 0,
+             int(sorted_vals.numel()), nat.ptr(q), 1, n, nat.ptr(out), nat.stream_handle())
+    return out[:n]
+
+
+def csr(rows, cols, dom_rows: int, dom_cols: int, ws: Optional[IngestWorkspace] = None, want_rows: bool = True):
+    ws = ws or IngestWorkspace()
+    return _csr(rows, cols, int(rows.numel()), dom_rows, dom_cols, ws, want_rows)

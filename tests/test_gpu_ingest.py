@@ -96,3 +96,25 @@ def test_device_ingested_join_matches_host(oracle):
     assert list(got.dims) == list(exp.dims)
     assert np.array_equal(got.codes, exp.codes)
     assert np.array_equal(got.counts, exp.counts)
+
+
+@pytest.mark.parametrize("shared", [False, True])
+def test_bsi_on_device_ingested(oracle, shared):
+    from conftest import zipf_pairs
+    from paper_2002_12459_b200.apps import bsi_answer_batch_arrays
+    from paper_2002_12459_b200.ingest import from_raw_pairs_device, semi_join_reduce_device
+    rng = np.random.default_rng(31 + shared)
+    rp = np.array(zipf_pairs(rng, 30000, 3000, 2000, 1.0)) * np.array([7, 3]) - np.array([500, 40])
+    sp = np.array(zipf_pairs(rng, 30000, 2500, 2600, 1.0)) * np.array([5, 3]) - np.array([9, 40])
+    q = np.stack([rng.integers(-600, 21500, 20000), rng.integers(-20, 12600, 20000)], axis=1)
+    if shared:
+        r, s = semi_join_reduce_device([rp, sp])
+        OR, OS = oracle.semi_join_many([oracle.encode(rp), oracle.encode(sp)])
+    else:
+        r, s = from_raw_pairs_device("R", rp), from_raw_pairs_device("S", sp)
+        OR, OS = oracle.encode(rp), oracle.encode(sp)
+    exp = oracle.bsi(OR, OS, q[:, 0], q[:, 1])
+    assert (exp == -1).any() and (exp == 1).any() and (exp == 0).any()
+    for hb in (128, 512):
+        got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], heavy_bits=hb)
+        assert np.array_equal(got, exp), hb

@@ -119,6 +119,48 @@ def cfg4():
     return rows
 
 
+def ingest():
+    """Device ingest (ingest.py) of every config's raw pairs: H2D of the raw
+    int64 pairs + dedup + dictionaries (+ semi-join) + both CSRs, vs the host
+    numpy path (relation.py) on the same arrays."""
+    import torch
+
+    from paper_2002_12459_b200 import datagen
+    from paper_2002_12459_b200.ingest import from_raw_pairs_device, semi_join_reduce_device
+    from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce_many
+    rows = []
+    for cfg in ("cfg2", "cfg5"):
+        wl = datagen.config(cfg)
+        raws = [np.ascontiguousarray(r, dtype=np.int64) for r in wl.relations]
+        pinned = [torch.from_numpy(r).pin_memory() for r in raws]
+        semi = cfg == "cfg2"
+
+        def dev():
+            if semi:
+                out = semi_join_reduce_device(pinned)
+            else:
+                out = [from_raw_pairs_device(f"R{j}", t) for j, t in enumerate(pinned)]
+            torch.cuda.synchronize()
+            return out
+        dev()
+        t0 = time.perf_counter()
+        out = dev()
+        t_dev = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rels = [Relation.from_raw_pairs(f"R{j}", r) for j, r in enumerate(raws)]
+        if semi:
+            rels = semi_join_reduce_many(rels)
+        host = [build_indexed(r) for r in rels]
+        t_host = time.perf_counter() - t0
+        same = all(np.array_equal(d.rel.left_values, h.rel.left_values) and np.array_equal(d.fwd_indices, h.fwd_indices)
+                   and np.array_equal(d.rev_indptr, h.rev_indptr) for d, h in zip(out, host))
+        n = sum(len(r) for r in raws)
+        rows.append({"config": cfg, "stage": "ingest (raw pairs -> dictionaries + CSR)", "raw_tuples": n,
+                     "semi_join": semi, "device_seconds_incl_h2d": t_dev, "device_tuples_per_s": n / t_dev,
+                     "host_numpy_seconds": t_host, "identical": bool(same)})
+    return rows
+
+
 def cfg5():
     import torch
 
@@ -156,7 +198,7 @@ def cfg5():
 if __name__ == "__main__":
     import torch
     torch.cuda.set_device(0)
-    names = sys.argv[1:] or ["cfg1", "cfg3", "cfg4", "cfg5"]
+    names = sys.argv[1:] or ["cfg1", "cfg3", "cfg4", "cfg5", "ingest"]
     for nm in names:
         for row in globals()[nm]():
             print(json.dumps(row), flush=True)
