@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const uint32_t* __restri
   }
 }
 
+
 void tile_geometry(int64_t wpr, int& G, int& cb, int& ncb) {
   if (wpr <= TILE_WORDS) {
     G = (int)(TILE_WORDS / wpr);
@@ -364,7 +365,7 @@ int emit_codes(const uint32_t* bm, const int64_t* segoff, int64_t rows, int64_t 
   if (nseg == 0) return MMJ_OK;
   static int segs = -1;
   if (segs < 0) {
-    const char* e = getenv("MMJ_EMIT_SEGS");
+    const char* e = getenv("MMJ_EMIT_SEGS");   // A/B knob: segments per emission CTA
     segs = e ? atoi(e) : EM_SEGS;
   }
   switch (segs) {

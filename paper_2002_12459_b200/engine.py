@@ -444,11 +444,18 @@ class TwoPathEngine:
         torch = self.torch
         self.prepare()
         dr, ds = self.dr, self.ds
-        main = torch.cuda.current_stream()
+        caller = torch.cuda.current_stream()
         if getattr(self, "_emit_stream", None) is None:
-            self._emit_stream = torch.cuda.Stream()
+            # emission (HBM-bound, floods the SMs with short CTAs) on a
+            # low-priority stream; the heavy product / merge / scan chain of
+            # the next chunk on a high-priority one, so its CTAs are placed
+            # first whenever emission CTAs retire
+            self._emit_stream = torch.cuda.Stream(priority=0)
+            self._work_stream = torch.cuda.Stream(priority=-1)
         es = self._emit_stream
-        es.wait_stream(main)
+        main = self._work_stream
+        main.wait_stream(caller)
+        es.wait_stream(caller)
         freed = [None, None]
         hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
         lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
@@ -500,7 +507,8 @@ class TwoPathEngine:
             ev.record(es)
             freed[b] = ev
             self.stats.chunks += 1
-        main.wait_stream(es)
+        caller.wait_stream(main)
+        caller.wait_stream(es)
         return codes
 
     def _async_slot(self):
