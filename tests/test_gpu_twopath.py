@@ -145,3 +145,36 @@ def test_fused_row_emit_wide_rows(pkg, oracle, dom_z):
     sp = zipf_pairs(rng, 8000, dom_z, 900, 1.1)
     plans = [("partitioned", 20, 1), ("partitioned", 5, 5), ("fulljoin", 1, 1)]
     _check(pkg, oracle, rp, sp, plans)
+
+
+def _pair_boundary_pairs(rng, deg_x0, n_y=300):
+    """x0 holds deg_x0 heavy y; z 0..15 reach all of them (count = deg_x0 on
+    both accumulator slots of several z pairs); filler tuples make every y heavy at
+    delta1 = 1 and keep the other degrees small."""
+    r = [(0, y) for y in range(deg_x0)]
+    # z 0..15 cover both slots of the first pair rows (z = k + 8j -> row 2k + j/2)
+    s = [(0, y) for y in range(n_y)] + [(z, y) for z in range(1, 16) for y in range(deg_x0)]
+    for y in range(n_y):
+        r += [(1 + int(rng.integers(0, 400)), y), (401 + y, y)]
+        s += [(2 + int(rng.integers(0, 400)), y), (403 + y, y)]
+    return sorted(set(r)), sorted(set(s))
+
+
+@pytest.mark.parametrize("deg_x0", [126, 127, 128])
+def test_pair_operand_count_boundary(pkg, oracle, deg_x0):
+    """BITMAP_PAIR packs two cells as c0 + 128*c1 (engine.py: on iff one
+    side's heavy degrees are <= 127): counts of exactly 127 on both slots must
+    not carry, and 128 must switch the pair form off."""
+    from paper_2002_12459_b200.joinproject import _collect, _engine
+    from paper_2002_12459_b200.optimizer import ThresholdPlan
+    rng = np.random.default_rng(deg_x0)
+    rp, sp = _pair_boundary_pairs(rng, deg_x0)
+    r, s = _mine(pkg, rp, sp)
+    plan = ThresholdPlan("partitioned", 1, 1)
+    eng = _engine(r, s, plan, False)
+    eng.prepare()
+    assert eng.pairs == (deg_x0 <= 127 or int(np.max(s.left_deg)) <= 127)
+    got = _collect(eng)
+    R, S = _oracle_rels(oracle, rp, sp)
+    exp = oracle.two_path(R, S, oracle.OPlan("partitioned", 1, 1))
+    assert np.array_equal(got[0], exp.codes)
