@@ -18,6 +18,7 @@ def __getattr__(name):
     # operator modules import torch lazily so the host data model stays usable
     # (and testable) on machines without a GPU
     import importlib
-    if name in ("joinproject", "matmul", "apps", "engine", "device", "datagen"):
+    if name in ("joinproject", "matmul", "apps", "engine", "device", "datagen", "ingest", "calibration", "bsi",
+                "star", "shard"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -24,6 +24,8 @@ from typing import Optional
 
 import numpy as np
 
+from .calibration import (DEFAULT_PROBE_DIMS, CalibrationError, CalibrationTable, calibrate,  # noqa: F401
+                          estimate_runtime)
 from .errors import MatrixOverflowError
 
 _FLOAT_EXACT_BOUND = 2 ** 53
@@ -36,7 +38,8 @@ _env = os.environ.get("MMJOIN_BACKEND")
 _KNOWN = ("auto", "cuda", "blas", "cython", "numpy")
 
 __all__ = ["CountMatrix", "MatrixOverflowError", "INT_BACKEND", "identity", "multiply_counts",
-           "theoretical_cost"]
+           "theoretical_cost", "CalibrationError", "CalibrationTable", "DEFAULT_PROBE_DIMS", "calibrate",
+           "estimate_runtime"]
 
 
 class CountMatrix:

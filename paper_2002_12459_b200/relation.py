@@ -14,6 +14,7 @@ reference also builds these structures before calling the operators.
 from __future__ import annotations
 
 from collections.abc import Mapping
+from dataclasses import dataclass, field
 from typing import Iterable, Iterator, Optional, TextIO
 
 import numpy as np
@@ -23,7 +24,7 @@ from .errors import ParseError
 __all__ = [
     "ParseError", "Relation", "IndexedRelation", "ValueIndex", "parse_edge_list",
     "parse_set_family_file", "semi_join_reduce", "semi_join_reduce_many",
-    "build_indexed", "gather_ranges",
+    "build_indexed", "gather_ranges", "DegreeStats", "degree_stats",
 ]
 
 
@@ -340,3 +341,75 @@ def gather_ranges(indptr: np.ndarray, indices: np.ndarray, keys: np.ndarray):
         return np.empty(0, dtype=indices.dtype), lens
     idx = np.arange(total, dtype=np.int64) - np.repeat(np.cumsum(lens) - lens - starts, lens)
     return indices[idx], lens
+
+
+# ------------------------------------------------------------ planner inputs
+@dataclass
+class DegreeStats:
+    """relation.py:205-252: degree vectors sorted ascending with prefix sums,
+    answering the cost model's threshold queries by binary search.
+
+    ``sum_x`` weighs each tuple (x, y) by the partner's |S.rev(y)|; lightness
+    is always judged by this relation's own degrees."""
+    n_tuples: int
+    dom_left: int
+    dom_right: int
+    left_sorted: np.ndarray
+    right_sorted: np.ndarray
+    _cdfx_prefix: np.ndarray = field(repr=False, default=None)
+    _sumy_prefix: np.ndarray = field(repr=False, default=None)
+    _sumx_prefix: np.ndarray = field(repr=False, default=None)
+
+    @staticmethod
+    def _upto(sorted_vec: np.ndarray, delta) -> int:
+        """number of entries <= delta"""
+        return int(np.searchsorted(sorted_vec, delta, side="right"))
+
+    def count_left(self, delta) -> int:
+        """#left values with degree <= delta"""
+        return self._upto(self.left_sorted, delta)
+
+    def count_right(self, delta) -> int:
+        return self._upto(self.right_sorted, delta)
+
+    def cdfx(self, delta) -> int:
+        """tuples whose right value has degree <= delta"""
+        return int(self._cdfx_prefix[self._upto(self.right_sorted, delta)])
+
+    def sum_y(self, delta) -> int:
+        """sum over right values of degree <= delta of partner degree^2"""
+        return int(self._sumy_prefix[self._upto(self.right_sorted, delta)])
+
+    def sum_x(self, delta) -> int:
+        """sum over left values of degree <= delta of their partner list lengths"""
+        return int(self._sumx_prefix[self._upto(self.left_sorted, delta)])
+
+    @property
+    def max_left_deg(self) -> int:
+        return int(self.left_sorted[-1]) if len(self.left_sorted) else 0
+
+    @property
+    def max_right_deg(self) -> int:
+        return int(self.right_sorted[-1]) if len(self.right_sorted) else 0
+
+
+def degree_stats(idx, partner=None) -> DegreeStats:
+    """relation.py:255-277."""
+    partner = idx if partner is None else partner
+    if not idx.shares_right_dict(partner):
+        raise ValueError("partner must share the right dictionary")
+    ldeg = np.asarray(idx.left_deg, dtype=np.int64)
+    rdeg = np.asarray(idx.right_deg, dtype=np.int64)
+    pdeg = np.asarray(partner.right_deg, dtype=np.int64)
+    zero = np.zeros(1, dtype=np.int64)
+    lo = np.argsort(ldeg, kind="stable")
+    # partner list length summed over each left value's forward list
+    w = np.concatenate([zero, np.cumsum(pdeg[np.asarray(idx.fwd_indices, dtype=np.int64)])])
+    fptr = np.asarray(idx.fwd_indptr, dtype=np.int64)
+    per_left = w[fptr[1:]] - w[fptr[:-1]]
+    ro = np.argsort(rdeg, kind="stable")
+    rs = rdeg[ro]
+    return DegreeStats(int(idx.n), int(idx.rel.dom_left), int(idx.rel.dom_right), ldeg[lo], rs,
+                       np.concatenate([zero, np.cumsum(rs)]),
+                       np.concatenate([zero, np.cumsum(pdeg[ro] * pdeg[ro])]),
+                       np.concatenate([zero, np.cumsum(per_left[lo])]))

@@ -257,6 +257,67 @@ def gen_plans(out):
     print("plans: ok")
 
 
+def gen_planner(out):
+    """Cost-based planner of the reference (relation.py:205-277 DegreeStats /
+    degree_stats, optimizer.py:57-197 CostConstants / modeled_costs /
+    optimize_thresholds, matmul/calibration.py:20-104 table + estimate_runtime)
+    on fixed inputs and the reference tests' synthetic calibration table
+    (test_optimizer.py:16-19), so no timing enters the fixture."""
+    from mmjoin.matmul import CalibrationTable, estimate_runtime
+    from mmjoin.relation import degree_stats, generate_community_graph
+    table = CalibrationTable({(100, 1): 1_000, (200, 1): 8_000, (400, 1): 64_000})
+    table2 = CalibrationTable({(16, 1): 10, (32, 1): 90, (64, 1): 700, (64, 2): 400, (128, 2): 3000})
+    est = []
+    for t, name in ((table, "t1"), (table2, "t2")):
+        for u, v, w, co in [(100, 100, 100, 1), (150, 230, 90, 1), (1000, 10, 10, 1), (64, 64, 64, 2),
+                            (300, 300, 300, 3), (5, 7, 11, 1)]:
+            est.append({"table": name, "uvw_co": [u, v, w, co], "nanos": estimate_runtime(t, u, v, w, co)})
+    insts = []
+    arrays = {}
+    rng = np.random.default_rng(4242)
+    sources = [("random", random_pairs(rng, 3000, 200, 150), random_pairs(rng, 3000, 180, 150)),
+               ("zipf", zipf_pairs(rng, 8000, 700, 900, 1.1), zipf_pairs(rng, 8000, 650, 900, 1.2))]
+    for nodes, k, p_, seed in [(210, 3, 0.85, 4), (300, 3, 0.5, 1), (420, 3, 0.35, 2)]:
+        rel = generate_community_graph(nodes, k, p_, seed=seed)
+        sources.append((f"community{nodes}", list(rel.raw_pairs()), None))
+    for i, (name, rp, sp) in enumerate(sources):
+        if sp is None:
+            r = s = build_indexed(Relation.from_raw_pairs("R", rp))
+        else:
+            r, s = reduced(rp, sp)
+        arrays[f"p{i}_R"] = np.asarray(rp, dtype=np.int64).reshape(-1, 2)
+        if sp is not None:
+            arrays[f"p{i}_S"] = np.asarray(sp, dtype=np.int64).reshape(-1, 2)
+        st_r = degree_stats(r, partner=s)
+        st_s = degree_stats(s)
+        deltas = sorted({1, 2, 3, 5, 8, 13, 40, 100, 1000, int(st_r.max_left_deg), int(st_s.max_right_deg)})
+        q = {"deltas": deltas,
+             "r": {f: [int(getattr(st_r, f)(d)) for d in deltas] for f in ("count_left", "count_right", "cdfx", "sum_y", "sum_x")},
+             "s": {f: [int(getattr(st_s, f)(d)) for d in deltas] for f in ("count_left", "count_right", "cdfx", "sum_y", "sum_x")},
+             "r_max": [int(st_r.max_left_deg), int(st_r.max_right_deg)], "s_max": [int(st_s.max_left_deg), int(st_s.max_right_deg)]}
+        n = max(r.n, s.n)
+        oj = r.out_join_with(s)
+        costs = []
+        for d1, d2 in [(1, 1), (2, 3), (5, 2), (10, 10), (n, n), (40, 1)]:
+            costs.append({"d": [d1, d2], "cost": list(opt.modeled_costs(st_r, st_s, r.rel.dom_left, d1, d2,
+                                                                       opt.DEFAULT_COSTS, table))})
+        plans = []
+        for step in (0.05, 0.2):
+            pl = opt.optimize_thresholds(st_r, st_s, r.rel.dom_left, oj, table=table, step=step)
+            plans.append({"step": step, "plan": [pl.strategy, pl.delta1, pl.delta2, pl.light_cost, pl.heavy_cost,
+                                                 pl.iterations]})
+        cc = opt.CostConstants(1.0, 5.0, 3.0, 1)
+        pl = opt.optimize_thresholds(st_r, st_s, r.rel.dom_left, oj, consts=cc, table=table)
+        plans.append({"consts": [1.0, 5.0, 3.0, 1], "plan": [pl.strategy, pl.delta1, pl.delta2, pl.light_cost,
+                                                             pl.heavy_cost, pl.iterations]})
+        insts.append({"name": name, "self_join": sp is None, "n": n, "out_join": int(oj), "stats": q,
+                      "costs": costs, "plans": plans})
+    np.savez_compressed(os.path.join(out, "planner.npz"), **arrays)
+    with open(os.path.join(out, "planner.json"), "w") as f:
+        json.dump({"estimate_runtime": est, "instances": insts}, f)
+    print("planner:", len(insts), "instances")
+
+
 def gen_cfg1(out):
     """Full BASELINE cfg1 through the reference (about 3 min, ~50 GB RAM):
     checksums of the 387M output codes + stats."""
@@ -285,6 +346,6 @@ if __name__ == "__main__":
         gen_cfg1(HERE)
     else:
         for name, fn in [("twopath", gen_twopath), ("example", gen_example), ("star", gen_star), ("ssj", gen_ssj),
-                         ("bsi", gen_bsi), ("matmul", gen_matmul), ("plans", gen_plans)]:
+                         ("bsi", gen_bsi), ("matmul", gen_matmul), ("plans", gen_plans), ("planner", gen_planner)]:
             if not a.only or name in a.only.split(","):
                 fn(HERE)
