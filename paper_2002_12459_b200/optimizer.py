@@ -229,6 +229,7 @@ class GpuCosts:
     witness_s_count: float = 7.3e-11
     cell_s: float = 1.03e-13
     cell_k_s: float = 2.27e-16
+    cell_k_s_count: float = 4.4e-16          # COUNT32 epilogue kernel (one cell per column)
     co: int = 1
 
     def heavy_seconds(self, u: int, k: int, w: int, pair: bool = True) -> float:
@@ -236,27 +237,33 @@ class GpuCosts:
         projection; the count path multiplies one cell per column."""
         if u <= 0 or k <= 0 or w <= 0:
             return 0.0
-        return float(u) * w * (self.cell_s + k * self.cell_k_s * (1 if pair else 2)) / self.co
+        return float(u) * w * (self.cell_s + k * (self.cell_k_s if pair else self.cell_k_s_count)) / self.co
 
 
 DEFAULT_GPU_COSTS = GpuCosts()
 
 
-def _time_heavy(rows: int, zcols: int, k: int, seed: int) -> float:
-    """seconds of one z-pair heavy product of rows x zcols cells at K = k"""
+def _time_heavy(rows: int, zcols: int, k: int, seed: int, counts: bool = False) -> float:
+    """seconds of one heavy product of rows x zcols cells at K = k (z-pair
+    bitmap, or int32 counts)"""
     import torch
     from . import _native as nat
     g = torch.Generator(device="cuda").manual_seed(seed)
     a = (torch.rand((rows, k), generator=g, device="cuda") < 0.05).to(torch.uint8)
     b = ((torch.rand((zcols // 2, k), generator=g, device="cuda") < 0.05).to(torch.uint8)
          + 128 * (torch.rand((zcols // 2, k), generator=g, device="cuda") < 0.05).to(torch.uint8))
-    out = torch.empty(rows * (zcols // 32), dtype=torch.int32, device="cuda")
     nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
     st = nat.stream_handle()
+    if counts:
+        b = (torch.rand((zcols, k), generator=g, device="cuda") < 0.05).to(torch.uint8)
+        out = torch.empty(rows * zcols, dtype=torch.int32, device="cuda")
+        args = (nat.ptr(b), zcols, k, 0, k, 0, rows, nat.MODE_COUNT32, 0, nat.ptr(out), zcols)
+    else:
+        out = torch.empty(rows * (zcols // 32), dtype=torch.int32, device="cuda")
+        args = (nat.ptr(b), zcols // 2, k, 0, k, 0, rows, nat.MODE_BITMAP_PAIR, 0, nat.ptr(out), zcols // 32)
 
     def run():
-        nat.call("mmj_heavy_mma", nat.ptr(a), rows, nat.ptr(b), zcols // 2, k, 0, k, 0, rows, nat.MODE_BITMAP_PAIR,
-                 0, nat.ptr(out), zcols // 32, nat.ptr(nnz), 0, st)
+        nat.call("mmj_heavy_mma", nat.ptr(a), rows, *args, nat.ptr(nnz), 0, st)
     run()
     ts = []
     for _ in range(3):
@@ -284,6 +291,8 @@ def measure_gpu_costs(seed: int = 0, co: int = 1) -> GpuCosts:
     cells = float(rows) * zc
     cell_k = max((t2 - t1) / (cells * (1024 - 128)), 1e-19)
     cell = max(t1 / cells - 128 * cell_k, 1e-16)
+    c1, c2 = _time_heavy(rows, 16384, 128, seed, True), _time_heavy(rows, 16384, 1024, seed, True)
+    cell_k_count = max((c2 - c1) / (float(rows) * 16384 * (1024 - 128)), 1e-19)
     rng = np.random.default_rng(seed)
 
     def zipf(n, dl, dr, a):
@@ -310,7 +319,8 @@ def measure_gpu_costs(seed: int = 0, co: int = 1) -> GpuCosts:
         e1.record()
         e1.synchronize()
         per[counts] = (e0.elapsed_time(e1) * 1e-3) / max(1, st.light_intermediate)
-    return GpuCosts(witness_s_bitmap=per[False], witness_s_count=per[True], cell_s=cell, cell_k_s=cell_k, co=co)
+    return GpuCosts(witness_s_bitmap=per[False], witness_s_count=per[True], cell_s=cell, cell_k_s=cell_k,
+                    cell_k_s_count=cell_k_count, co=co)
 
 
 def gpu_plan(r, s, candidates=None, *, counts: bool = False, min_count: int = 1,
@@ -356,6 +366,8 @@ def gpu_plan(r, s, candidates=None, *, counts: bool = False, min_count: int = 1,
         light = int(cum_light[n_light])
         kpad = -(-k // K_BLOCK) * K_BLOCK
         t_light, t_heavy = light * t_wit, costs.heavy_seconds(u, kpad, w, pair=not counts)
+        # upper_only: the product skips tiles below the diagonal and the
+        # expansion drops z <= x (empirically both about halve)
         t = share * (t_light + t_heavy)
         if best is None or t < best[0]:
             best = (t, d1, t_light, t_heavy)
