@@ -154,16 +154,18 @@ int mmj_bitmap_segments(const uint32_t* bm, int64_t nwords, int32_t* segcnt, int
 int mmj_bitmap_emit(const uint32_t* bm, int64_t nwords, int64_t wpr, const int64_t* seg_off, int64_t x0,
                     int64_t dom_z, int64_t* codes, void* stream);
 /* Count chunk (nrows x ld int32, ncols valid columns): cells with count >=
- * min_count (and col > x0+row if upper_only: the a < b filter of
- * apps.py:57-62) -> codes + int32 counts.  ld must be a multiple of 1024
- * (segments of 1024 cells never straddle rows); with upper_only, segments at
- * or below the diagonal are not read. */
+ * max(min_count, row_min[x0+row]) (row_min may be NULL) -> codes + int32
+ * counts.  cell_filter: 0 every cell, 1 col > x0+row (SSJ's a < b,
+ * apps.py:57-62), 2 col != x0+row (SCJ's a != b, apps.py:297-304).  ld must be a multiple of 1024
+ * (segments of 1024 cells never straddle rows); with cell_filter 1, segments
+ * at or below the diagonal are not read. */
 int64_t mmj_count_segment_count(int64_t ncell);
 int mmj_count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
-                       int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws, void* stream);
+                       const int32_t* row_min, int cell_filter, int32_t* segcnt, int64_t* seg_off, void* ws,
+                       void* stream);
 int mmj_count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
-                   int32_t min_count, int upper_only, const int64_t* seg_off, int64_t* codes, int32_t* counts,
-                   void* stream);
+                   int32_t min_count, const int32_t* row_min, int cell_filter, const int64_t* seg_off, int64_t* codes,
+                   int32_t* counts, void* stream);
 
 /* ---- star join-project, k = 2..4: joinproject.py:281-378 -------------------
  * Output as a two-path over composite rows (x1..x_{k-1}) x column x_k.
@@ -236,6 +238,8 @@ int mmj_ingest_sort_ids(const int64_t* vals, int64_t n, int64_t* sorted, int32_t
                         void* stream);
 /* out[i] = map[idx[i]] */
 int mmj_ingest_remap(const int32_t* idx, int64_t n, const int32_t* map, int32_t* out, void* stream);
+/* out[i] = src[idx[i]] for 4- or 8-byte elements */
+int mmj_ingest_gather(const void* src, int elem_bytes, const int32_t* idx, int64_t n, void* out, void* stream);
 /* cnt[v] = #{i : idx[i] == v}, v < dom (cnt zeroed first) */
 int mmj_ingest_histogram(const int32_t* idx, int64_t n, int64_t dom, int32_t* cnt, void* stream);
 int mmj_ingest_csr(const int32_t* rows, const int32_t* cols, int64_t n, int64_t dom_rows, int64_t dom_cols,

@@ -54,6 +54,7 @@ _SIGS = {
     "mmj_ingest_filter": (INT, [P, P, I64, P, P, P, P, SZ, P]),
     "mmj_ingest_sort_ids": (INT, [P, I64, P, P, P, SZ, P]),
     "mmj_ingest_remap": (INT, [P, I64, P, P, P]),
+    "mmj_ingest_gather": (INT, [P, INT, P, I64, P, P]),
     "mmj_ingest_histogram": (INT, [P, I64, I64, P, P]),
     "mmj_ingest_csr": (INT, [P, P, I64, I64, I64, P, P, P, P, P, SZ, P]),
     "mmj_build_operand_pairs": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
@@ -75,8 +76,8 @@ _SIGS = {
     "mmj_bitmap_segments": (INT, [P, I64, P, P, P, P]),
     "mmj_bitmap_emit": (INT, [P, I64, I64, P, I64, I64, P, P]),
     "mmj_count_segment_count": (I64, [I64]),
-    "mmj_count_segments": (INT, [P, I64, I64, I64, I64, I32, INT, P, P, P, P]),
-    "mmj_count_emit": (INT, [P, I64, I64, I64, I64, I64, I32, INT, P, P, P, P]),
+    "mmj_count_segments": (INT, [P, I64, I64, I64, I64, I32, P, INT, P, P, P, P]),
+    "mmj_count_emit": (INT, [P, I64, I64, I64, I64, I64, I32, P, INT, P, P, P, P]),
 }
 
 _lib = None

@@ -22,7 +22,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .optimizer import ThresholdPlan
+from .optimizer import PARTITIONED, ThresholdPlan
 from .relation import IndexedRelation, Relation, ValueIndex, build_indexed
 
 __all__ = ["SetFamily", "ssj_mmjoin", "ssj_mmjoin_arrays", "ssj_ordered", "scj_join_project",
@@ -64,10 +64,23 @@ def _ssj_plan(idx, plan: Optional[ThresholdPlan], c: int = 1, upper_only: bool =
     return plan if plan is not None else gpu_plan(idx, idx, counts=True, min_count=c, upper_only=upper_only)
 
 
-def ssj_mmjoin_arrays(family: SetFamily, c: int, plan: Optional[ThresholdPlan] = None,
-                      chunk_rows: Optional[int] = None):
-    """(a, b, overlap) int64 arrays of every unordered pair a < b (dense set
-    ids) with |a n b| >= c, in ascending (a, b) order."""
+def _device_pairs(eng):
+    """Run a count-path engine; (codes, counts) concatenated on the device
+    (each chunk is copied out of the engine's reused workspace)."""
+    import torch
+    codes, counts = [], []
+
+    def sink(ch):
+        codes.append(ch.codes.clone())
+        counts.append(ch.counts.clone())
+
+    eng.run(sink)
+    if not codes:
+        return (torch.empty(0, dtype=torch.int64, device="cuda"), torch.empty(0, dtype=torch.int32, device="cuda"))
+    return torch.cat(codes), torch.cat(counts)
+
+
+def _ssj_device(family: SetFamily, c: int, plan: Optional[ThresholdPlan], chunk_rows: Optional[int]):
     if c < 1:
         raise ValueError("c must be >= 1")
     from .joinproject import _engine
@@ -75,17 +88,20 @@ def ssj_mmjoin_arrays(family: SetFamily, c: int, plan: Optional[ThresholdPlan] =
     plan = _ssj_plan(idx, plan, int(c))
     plan.validate()
     eng = _engine(idx, idx, plan, True, min_count=int(c), upper_only=True, chunk_rows=chunk_rows)
-    dz = idx.rel.dom_left
-    codes, counts = [], []
+    return _device_pairs(eng)
 
-    def sink(ch):
-        codes.append(ch.codes.cpu().numpy())
-        counts.append(ch.counts.cpu().numpy())
 
-    eng.run(sink)
-    cd = np.concatenate(codes) if codes else np.empty(0, dtype=np.int64)
-    cn = (np.concatenate(counts) if counts else np.empty(0, dtype=np.int32)).astype(np.int64)
-    return cd // dz, cd % dz, cn
+def _split(codes: np.ndarray, dz: int):
+    return codes // dz, codes % dz
+
+
+def ssj_mmjoin_arrays(family: SetFamily, c: int, plan: Optional[ThresholdPlan] = None,
+                      chunk_rows: Optional[int] = None):
+    """(a, b, overlap) int64 arrays of every unordered pair a < b (dense set
+    ids) with |a n b| >= c, in ascending (a, b) order."""
+    cd, cn = _ssj_device(family, c, plan, chunk_rows)
+    a, b = _split(cd.cpu().numpy(), family.indexed.rel.dom_left)
+    return a, b, cn.cpu().numpy().astype(np.int64)
 
 
 def ssj_mmjoin(family: SetFamily, c: int, plan: Optional[ThresholdPlan] = None) -> dict:
@@ -95,23 +111,58 @@ def ssj_mmjoin(family: SetFamily, c: int, plan: Optional[ThresholdPlan] = None) 
     return dict(zip(zip(a.tolist(), b.tolist()), n.tolist()))
 
 
+def ssj_ordered_arrays(family: SetFamily, c: int, plan: Optional[ThresholdPlan] = None):
+    """(a, b, overlap) sorted by overlap descending, then (a, b) ascending
+    (apps.py:291-294), ordered on the device: the codes arrive ascending, so
+    one stable radix sort by (max overlap - overlap) gives the order."""
+    import torch
+
+    from . import _native as nat
+    from .ingest import IngestWorkspace, sorted_ids
+    cd, cn = _ssj_device(family, c, plan, None)
+    n = int(cd.numel())
+    if n:
+        top = int(cn.max().item())
+        key = (top - cn).to(torch.int64)
+        _, order = sorted_ids(key, IngestWorkspace())
+        cd2 = torch.empty_like(cd)
+        cn2 = torch.empty_like(cn)
+        st = nat.stream_handle()
+        nat.call("mmj_ingest_gather", nat.ptr(cd), 8, nat.ptr(order), n, nat.ptr(cd2), st)
+        nat.call("mmj_ingest_gather", nat.ptr(cn), 4, nat.ptr(order), n, nat.ptr(cn2), st)
+        cd, cn = cd2, cn2
+    a, b = _split(cd.cpu().numpy(), family.indexed.rel.dom_left)
+    return a, b, cn.cpu().numpy().astype(np.int64)
+
+
 def ssj_ordered(family: SetFamily, c: int) -> list:
     """apps.py:291-294: ssj_mmjoin sorted by overlap descending, pair ascending."""
-    a, b, n = ssj_mmjoin_arrays(family, c)
-    order = np.lexsort((b, a, -n))
-    return [((int(a[i]), int(b[i])), int(n[i])) for i in order]
+    a, b, n = ssj_ordered_arrays(family, c)
+    return [((x, y), k) for x, y, k in zip(a.tolist(), b.tolist(), n.tolist())]
+
+
+def scj_join_project_arrays(family: SetFamily, plan: Optional[ThresholdPlan] = None):
+    """(a, b) int64 arrays, ascending: every ordered pair a != b with a a
+    subset of b, i.e. overlap(a, b) == |a| (apps.py:297-304).  Fused into the
+    count path's emission: per-row threshold |a| (an overlap cannot exceed it)
+    and the diagonal excluded, so nothing else leaves the device."""
+    from .device import device_relation
+    from .engine import TwoPathEngine
+    idx = family.indexed
+    plan = _ssj_plan(idx, plan, 1, upper_only=False)
+    plan.validate()
+    dr = device_relation(idx)
+    d1, d2 = (plan.delta1, plan.delta2) if plan.strategy == PARTITIONED else (max(idx.n, 1),) * 2
+    eng = TwoPathEngine(dr, dr, plan.strategy, d1, d2, True, off_diagonal=True, row_min=dr.left_deg,
+                        host_left_deg_r=idx.left_deg, host_left_deg_s=idx.left_deg)
+    cd, _ = _device_pairs(eng)
+    return _split(cd.cpu().numpy(), idx.rel.dom_left)
 
 
 def scj_join_project(family: SetFamily) -> set:
-    """apps.py:297-304: ordered containment pairs (a, b), a != b, a subset of b,
-    i.e. overlap(a, b) == |a| on the exact count path."""
-    from .joinproject import two_path_join
-    idx = family.indexed
-    res = two_path_join(idx, idx, plan=_ssj_plan(idx, None, upper_only=False), want_counts=True)
-    t = res.tuples()
-    sizes = np.asarray(idx.left_deg)
-    keep = (t[:, 0] != t[:, 1]) & (res.counts == sizes[t[:, 0]])
-    return set(map(tuple, t[keep].tolist()))
+    """apps.py:297-304: ordered containment pairs (a, b), a != b, a subset of b."""
+    a, b = scj_join_project_arrays(family)
+    return set(zip(a.tolist(), b.tolist()))
 
 
 def bsi_batch_size(rate: float, n: int) -> int:

@@ -22,10 +22,10 @@ int64_t bitmap_nseg(int64_t);
 int64_t count_nseg(int64_t);
 int bitmap_segments(const uint32_t*, int64_t, int32_t*, int64_t*, void*, cudaStream_t);
 int bitmap_emit(const uint32_t*, int64_t, int64_t, const int64_t*, int64_t, int64_t, int64_t*, cudaStream_t);
-int count_segments(const int32_t*, int64_t, int64_t, int64_t, int64_t, int32_t, int, int32_t*, int64_t*, void*,
-                   cudaStream_t);
-int count_emit(const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t, int, const int64_t*, int64_t*,
-               int32_t*, cudaStream_t);
+int count_segments(const int32_t*, int64_t, int64_t, int64_t, int64_t, int32_t, const int32_t*, int, int32_t*,
+                   int64_t*, void*, cudaStream_t);
+int count_emit(const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t, const int32_t*, int,
+               const int64_t*, int64_t*, int32_t*, cudaStream_t);
 int64_t row_emit_tiles(int64_t, int64_t);
 int tile_merge(uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t*, const int32_t*, const int32_t*,
                int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int32_t*,
@@ -227,14 +227,24 @@ int mmj_bitmap_emit(const uint32_t* bm, int64_t nwords, int64_t wpr, const int64
 int64_t mmj_count_segment_count(int64_t ncell) { return mmj::count_nseg(ncell); }
 
 int mmj_count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
-                       int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws, void* stream) {
-  return mmj::count_segments(cnt, nrows, ld, ncols, x0, min_count, upper_only, segcnt, seg_off, ws, ST(stream));
+                       const int32_t* row_min, int cell_filter, int32_t* segcnt, int64_t* seg_off, void* ws,
+                       void* stream) {
+  if (cell_filter < 0 || cell_filter > 2) {
+    mmj::set_error("count_segments: cell_filter must be 0, 1 or 2");
+    return MMJ_ERR_ARG;
+  }
+  return mmj::count_segments(cnt, nrows, ld, ncols, x0, min_count, row_min, cell_filter, segcnt, seg_off, ws,
+                             ST(stream));
 }
 
 int mmj_count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
-                   int32_t min_count, int upper_only, const int64_t* seg_off, int64_t* codes, int32_t* counts,
-                   void* stream) {
-  return mmj::count_emit(cnt, nrows, ld, ncols, x0, dom_z, min_count, upper_only, seg_off, codes, counts,
+                   int32_t min_count, const int32_t* row_min, int cell_filter, const int64_t* seg_off, int64_t* codes,
+                   int32_t* counts, void* stream) {
+  if (cell_filter < 0 || cell_filter > 2) {
+    mmj::set_error("count_emit: cell_filter must be 0, 1 or 2");
+    return MMJ_ERR_ARG;
+  }
+  return mmj::count_emit(cnt, nrows, ld, ncols, x0, dom_z, min_count, row_min, cell_filter, seg_off, codes, counts,
                          ST(stream));
 }
 

@@ -262,6 +262,11 @@ __global__ void k_remap(const int32_t* __restrict__ idx, int64_t n, const int32_
   GRID_STRIDE(i, n) out[i] = map[idx[i]];
 }
 
+template <typename T>
+__global__ void k_gather(const T* __restrict__ src, const int32_t* __restrict__ idx, int64_t n, T* __restrict__ out) {
+  GRID_STRIDE(i, n) out[i] = src[idx[i]];
+}
+
 __global__ void k_histogram(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ cnt) {
   GRID_STRIDE(i, n) atomicAdd(&cnt[idx[i]], 1);
 }
@@ -546,6 +551,22 @@ int mmj_ingest_remap(const int32_t* idx, int64_t n, const int32_t* map, int32_t*
   if (n == 0) return MMJ_OK;
   k_remap<<<grid1(n), TPB, 0, st>>>(idx, n, map, out);
   MMJ_CHECK_LAUNCH("k_remap");
+  return MMJ_OK;
+}
+
+int mmj_ingest_gather(const void* src, int elem_bytes, const int32_t* idx, int64_t n, void* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "ingest_gather"));
+  if (n == 0) return MMJ_OK;
+  if (elem_bytes == 8)
+    k_gather<int64_t><<<grid1(n), TPB, 0, st>>>(static_cast<const int64_t*>(src), idx, n, static_cast<int64_t*>(out));
+  else if (elem_bytes == 4)
+    k_gather<int32_t><<<grid1(n), TPB, 0, st>>>(static_cast<const int32_t*>(src), idx, n, static_cast<int32_t*>(out));
+  else {
+    set_error("ingest_gather: elem_bytes must be 4 or 8");
+    return MMJ_ERR_ARG;
+  }
+  MMJ_CHECK_LAUNCH("k_gather");
   return MMJ_OK;
 }
 

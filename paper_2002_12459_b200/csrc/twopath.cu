@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(EXP_THREADS) k_light_expand(LightArgs a, const
       list_of(a, a.t0 + i, x, base, l, lz);
       const int32_t z = base[s - offs[i]];
       const int64_t row = (int64_t)x - x0;
-      if (a.upper_only && z <= x) continue;       // SSJ keeps a < b only (apps.py:60)
+      if (a.upper_only == 1 && z <= x) continue;  // SSJ keeps a < b only (apps.py:60)
       if (MODE == 0) {
         atomicOr(reinterpret_cast<uint32_t*>(out) + row * ld + (z >> 5), 1u << (z & 31));
       } else {
@@ -296,25 +296,28 @@ __device__ __forceinline__ CountSeg count_seg(int64_t sgi, int64_t spr, int64_t 
   CountSeg g;
   g.row = sgi / spr;
   g.col0 = (sgi - g.row * spr) * CSEG;
-  g.live = g.col0 < ncols && !(upper_only && g.col0 + CSEG - 1 <= x0 + g.row);
+  g.live = g.col0 < ncols && !(upper_only == 1 && g.col0 + CSEG - 1 <= x0 + g.row);
   return g;
 }
 
 // keep flags of one lane's 4 cells of iteration `it` as a nibble
+// cell filters: 0 every cell, 1 z > x (SSJ's a < b), 2 z != x (SCJ's a != b)
 __device__ __forceinline__ uint32_t keep_nibble(int4 v, int64_t col, int64_t x, int64_t ncols, int32_t min_count,
-                                                int upper_only) {
-  const int64_t lo = upper_only ? x + 1 : 0;   // first kept column
+                                                int filter) {
+  const int64_t lo = filter == 1 ? x + 1 : 0;   // first kept column
+  const int64_t skip = filter == 2 ? x : -1;    // the one excluded column
   uint32_t m = 0;
-  m |= (v.x >= min_count && col + 0 >= lo && col + 0 < ncols) ? 1u : 0u;
-  m |= (v.y >= min_count && col + 1 >= lo && col + 1 < ncols) ? 2u : 0u;
-  m |= (v.z >= min_count && col + 2 >= lo && col + 2 < ncols) ? 4u : 0u;
-  m |= (v.w >= min_count && col + 3 >= lo && col + 3 < ncols) ? 8u : 0u;
+  m |= (v.x >= min_count && col + 0 >= lo && col + 0 < ncols && col + 0 != skip) ? 1u : 0u;
+  m |= (v.y >= min_count && col + 1 >= lo && col + 1 < ncols && col + 1 != skip) ? 2u : 0u;
+  m |= (v.z >= min_count && col + 2 >= lo && col + 2 < ncols && col + 2 != skip) ? 4u : 0u;
+  m |= (v.w >= min_count && col + 3 >= lo && col + 3 < ncols && col + 3 != skip) ? 8u : 0u;
   return m;
 }
 
 __global__ void __launch_bounds__(256) k_count_seg_nnz(const int32_t* __restrict__ cnt, int64_t nseg, int64_t spr,
                                                        int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
-                                                       int upper_only, int32_t* __restrict__ segcnt) {
+                                                       const int32_t* __restrict__ row_min, int upper_only,
+                                                       int32_t* __restrict__ segcnt) {
   const int lane = threadIdx.x & 31;
   for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
        sgi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -322,12 +325,13 @@ __global__ void __launch_bounds__(256) k_count_seg_nnz(const int32_t* __restrict
     int n = 0;
     if (g.live) {
       const int4* src = reinterpret_cast<const int4*>(cnt + g.row * ld + g.col0) + lane;
+      const int32_t thr = row_min ? max(min_count, row_min[x0 + g.row]) : min_count;
       int4 v[CIT];
 #pragma unroll
       for (int it = 0; it < CIT; ++it) v[it] = __ldcs(src + it * 32);
 #pragma unroll
       for (int it = 0; it < CIT; ++it)
-        n += __popc(keep_nibble(v[it], g.col0 + it * 128 + lane * 4, x0 + g.row, ncols, min_count, upper_only));
+        n += __popc(keep_nibble(v[it], g.col0 + it * 128 + lane * 4, x0 + g.row, ncols, thr, upper_only));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
     }
@@ -337,8 +341,8 @@ __global__ void __launch_bounds__(256) k_count_seg_nnz(const int32_t* __restrict
 
 __global__ void __launch_bounds__(256) k_count_emit(const int32_t* __restrict__ cnt, int64_t nseg, int64_t spr,
                                                     int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
-                                                    int32_t min_count, int upper_only,
-                                                    const int64_t* __restrict__ seg_off,
+                                                    int32_t min_count, const int32_t* __restrict__ row_min,
+                                                    int upper_only, const int64_t* __restrict__ seg_off,
                                                     int64_t* __restrict__ codes, int32_t* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
@@ -348,6 +352,7 @@ __global__ void __launch_bounds__(256) k_count_emit(const int32_t* __restrict__ 
     const int64_t base = seg_off[sgi];
     if (seg_off[sgi + 1] == base) continue;
     const int4* src = reinterpret_cast<const int4*>(cnt + g.row * ld + g.col0) + lane;
+    const int32_t thr = row_min ? max(min_count, row_min[x0 + g.row]) : min_count;
     int4 v[CIT];
 #pragma unroll
     for (int it = 0; it < CIT; ++it) v[it] = __ldcs(src + it * 32);
@@ -356,7 +361,7 @@ __global__ void __launch_bounds__(256) k_count_emit(const int32_t* __restrict__ 
     uint64_t packed = 0;
 #pragma unroll
     for (int it = 0; it < CIT; ++it) {
-      nib[it] = keep_nibble(v[it], g.col0 + it * 128 + lane * 4, x0 + g.row, ncols, min_count, upper_only);
+      nib[it] = keep_nibble(v[it], g.col0 + it * 128 + lane * 4, x0 + g.row, ncols, thr, upper_only);
       packed |= (uint64_t)__popc(nib[it]) << (8 * it);
     }
     uint64_t incl = packed;
@@ -510,11 +515,13 @@ static int count_grid(int64_t nseg) {
 }
 
 int count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
-                   int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws, cudaStream_t st) {
+                   const int32_t* row_min, int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws,
+                   cudaStream_t st) {
   MMJ_TRY(check_count_pitch(ld, ncols));
   const int64_t nseg = count_nseg(nrows * ld);
   if (nseg > 0) {
-    k_count_seg_nnz<<<count_grid(nseg), 256, 0, st>>>(cnt, nseg, ld / CSEG, ld, ncols, x0, min_count, upper_only,
+    k_count_seg_nnz<<<count_grid(nseg), 256, 0, st>>>(cnt, nseg, ld / CSEG, ld, ncols, x0, min_count, row_min,
+                                                      upper_only,
                                                       segcnt);
     MMJ_CHECK_LAUNCH("k_count_seg_nnz");
   }
@@ -522,12 +529,13 @@ int count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols,
 }
 
 int count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
-               int32_t min_count, int upper_only, const int64_t* seg_off, int64_t* codes, int32_t* counts,
-               cudaStream_t st) {
+               int32_t min_count, const int32_t* row_min, int upper_only, const int64_t* seg_off, int64_t* codes,
+               int32_t* counts, cudaStream_t st) {
   MMJ_TRY(check_count_pitch(ld, ncols));
   const int64_t nseg = count_nseg(nrows * ld);
   if (nseg == 0) return MMJ_OK;
-  k_count_emit<<<count_grid(nseg), 256, 0, st>>>(cnt, nseg, ld / CSEG, ld, ncols, x0, dom_z, min_count, upper_only,
+  k_count_emit<<<count_grid(nseg), 256, 0, st>>>(cnt, nseg, ld / CSEG, ld, ncols, x0, dom_z, min_count, row_min,
+                                                 upper_only,
                                                  seg_off, codes, counts);
   MMJ_CHECK_LAUNCH("k_count_emit");
   return MMJ_OK;

@@ -66,8 +66,8 @@ class TwoPathEngine:
     """Device state for one (R, S, plan) two-path evaluation."""
 
     def __init__(self, dr: DeviceRelation, ds: DeviceRelation, strategy: str, delta1: int, delta2: int,
-                 want_counts: bool, *, min_count: int = 1, upper_only: bool = False,
-                 chunk_rows: Optional[int] = None, ws: Optional[Workspace] = None,
+                 want_counts: bool, *, min_count: int = 1, upper_only: bool = False, off_diagonal: bool = False,
+                 row_min=None, chunk_rows: Optional[int] = None, ws: Optional[Workspace] = None,
                  host_left_deg_r=None, host_left_deg_s=None, pair_operand: bool = True):
         import torch
         self.torch = torch
@@ -80,10 +80,14 @@ class TwoPathEngine:
         self.counts = bool(want_counts)
         self.min_count = int(min_count)
         self.upper_only = bool(upper_only)
-        if (self.upper_only or self.min_count > 1) and not self.counts:
-            raise ValueError("min_count / upper_only filter the count path; pass want_counts=True")
-        if self.upper_only and dr.dom_left != ds.dom_left:
-            raise ValueError("upper_only needs a self-join (x and z in one dictionary)")
+        # emission cell filter: 0 all, 1 z > x (SSJ), 2 z != x (SCJ); row_min: a
+        # per-x count threshold (int32 device vector over x, e.g. |a| for SCJ)
+        self.cell_filter = 1 if self.upper_only else (2 if off_diagonal else 0)
+        self.row_min = row_min
+        if (self.cell_filter or self.min_count > 1 or row_min is not None) and not self.counts:
+            raise ValueError("min_count / row_min / cell filters act on the count path; pass want_counts=True")
+        if self.cell_filter and dr.dom_left != ds.dom_left:
+            raise ValueError("upper_only / off_diagonal need a self-join (x and z in one dictionary)")
         # c-prefilter only when the caller discards counts < min_count (SSJ);
         # the light_intermediate statistic then counts the pruned witnesses only
         self.prefilter = self.min_count if (self.counts and self.min_count > 1) else 0
@@ -218,7 +222,7 @@ class TwoPathEngine:
         if self.counts:
             buf = self.ws.get("cnt", rows * self.ldc, torch.int32)
             ld = self.ldc
-            mode = nat.MODE_COUNT32 | (nat.MODE_UPPER if self.upper_only else 0)
+            mode = nat.MODE_COUNT32 | (nat.MODE_UPPER if self.cell_filter == 1 else 0)
         else:
             buf = self.ws.get("bm", rows * self.wpr, torch.int32)
             ld = self.wpr
@@ -257,8 +261,9 @@ class TwoPathEngine:
             nseg = int(self.lib.mmj_count_segment_count(ncell))
             segcnt = self.ws.get("segcnt", nseg, torch.int32)
             segoff = self.ws.get("segoff", nseg + 1, torch.int64)
-            nat.call("mmj_count_segments", nat.ptr(buf), rows, self.ldc, self.dom_z, x0, self.min_count,
-                     int(self.upper_only), nat.ptr(segcnt), nat.ptr(segoff), nat.ptr(self.ws.scan_ws(nseg)), st)
+            rm = nat.ptr(self.row_min) if self.row_min is not None else 0
+            nat.call("mmj_count_segments", nat.ptr(buf), rows, self.ldc, self.dom_z, x0, self.min_count, rm,
+                     self.cell_filter, nat.ptr(segcnt), nat.ptr(segoff), nat.ptr(self.ws.scan_ws(nseg)), st)
         else:
             nwords = rows * self.wpr
             nseg = int(self.lib.mmj_bitmap_segment_count(nwords))
@@ -284,7 +289,7 @@ class TwoPathEngine:
             counts = self.ws.get("counts", cap, torch.int32)
             if cap:
                 nat.call("mmj_count_emit", nat.ptr(buf), rows, self.ldc, self.dom_z, x0, self.dom_z, self.min_count,
-                         int(self.upper_only), nat.ptr(segoff), nat.ptr(codes), nat.ptr(counts), st)
+                         rm, self.cell_filter, nat.ptr(segoff), nat.ptr(codes), nat.ptr(counts), st)
         elif cap:
             nat.call("mmj_bitmap_emit", nat.ptr(buf), rows * self.wpr, self.wpr, nat.ptr(segoff), x0, self.dom_z,
                      nat.ptr(codes), st)

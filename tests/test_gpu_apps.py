@@ -158,3 +158,30 @@ def test_star_zipf_k3_vs_oracle(oracle):
     got = star_join(idxs, 100, 1, want_counts=True, heavy_rows_cap=1 << 30)
     assert np.array_equal(got.codes, exp.codes) and np.array_equal(got.counts, exp.counts)
     assert list(got.stats["heavy_dims"]) == list(exp.stats["heavy_dims"])
+
+
+def test_ssj_ordered_and_scj_on_device(oracle):
+    """Device consumers: ssj_ordered's (-overlap, a, b) order
+    from one stable device sort, and scj's containment filter fused into the
+    count emission (per-row threshold |a|, diagonal excluded)."""
+    from paper_2002_12459_b200 import datagen
+    from paper_2002_12459_b200.apps import (SetFamily, scj_join_project_arrays, ssj_ordered,
+                                            ssj_ordered_arrays)
+    from paper_2002_12459_b200.relation import Relation
+    pairs = datagen.set_family_pairs(11, 20000, 1500, 200, 1.4, 600, 1.1)
+    fam = SetFamily(Relation.from_raw_pairs("sets", pairs))
+    ofam = oracle.encode(pairs)
+    ea, eb, en = oracle.ssj_arrays(ofam, 2)
+    order = np.lexsort((eb, ea, -en))
+    a, b, n = ssj_ordered_arrays(fam, 2)
+    assert np.array_equal(a, ea[order]) and np.array_equal(b, eb[order]) and np.array_equal(n, en[order])
+    assert ssj_ordered(fam, 2)[:50] == [((int(x), int(y)), int(k)) for x, y, k in
+                                        zip(ea[order][:50], eb[order][:50], en[order][:50])]
+    full = oracle.two_path(ofam, ofam, None, want_counts=True)
+    dz = full.dims[1]
+    x, z = full.codes // dz, full.codes % dz
+    sizes = ofam.left_deg
+    keep = (x != z) & (full.counts == sizes[x])
+    sa, sb = scj_join_project_arrays(fam)
+    assert np.array_equal(sa, x[keep]) and np.array_equal(sb, z[keep])
+    assert keep.sum() > 0
