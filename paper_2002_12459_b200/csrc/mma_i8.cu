@@ -46,15 +46,25 @@ constexpr int B_BYTES = BN * BK;        // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int ACC_STAGES = 2;
 constexpr int TMEM_COLS = 512;          // 2 x 256 s32 accumulator columns
-constexpr int EPI_WARPS = 8;            // two warps per TMEM lane quadrant (one per 128-column half)
+// 8 epilogue warps (128 columns each); 16 (64 columns, 640 threads) measured
+// no faster: the epilogue is bound by the TMEM read-out (128 rows x 256
+// columns x 4 B per tile at ~64 B/clk), not by its instruction latency
+#ifndef MMJ_EPI_WARPS
+#define MMJ_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = MMJ_EPI_WARPS;  // 4 x EPI_GROUPS: one warp per (TMEM lane quadrant, column group)
+constexpr int EPI_GROUPS = EPI_WARPS / 4;
+constexpr int CW = 256 / EPI_GROUPS;      // accumulator columns per epilogue warp
 constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
+static_assert(CW == 64 || CW == 128, "epilogue column split");
 constexpr int EPI_PITCH = 36;           // COUNT32 staging: words per row (16-B aligned, conflict-free v4)
 constexpr int EPI_STAGE_BYTES = EPI_WARPS * 32 * EPI_PITCH * 4;
 constexpr int smem_bytes_for(int stages, bool staged) {
   return stages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + (staged ? EPI_STAGE_BYTES : 0);
 }
-static_assert(smem_bytes_for(3, true) <= smem_bytes_for(STAGES, false), "staged COUNT32 launch must fit");
-static_assert(smem_bytes_for(STAGES, false) <= 227 * 1024, "shared memory budget");
+constexpr int SMEM_MAX = smem_bytes_for(3, true) > smem_bytes_for(STAGES, false) ? smem_bytes_for(3, true)
+                                                                                  : smem_bytes_for(STAGES, false);
+static_assert(SMEM_MAX <= 227 * 1024, "shared memory budget");
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
 enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, BITMAP_PAIR = 4, MODE_UPPER = 16 };
@@ -386,7 +396,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------- epilogue
     const int q = warp & 3;              // TMEM lane quadrant
-    const int half = (warp - 4) >> 2;    // 128-column half of the 256-column tile
+    const int grp = (warp - 4) >> 2;     // CW-column group of the 256-column tile
     int acc = 0;
     uint32_t acc_ph = 0;
     unsigned long long my_nnz = 0;
@@ -397,53 +407,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int64_t row = (int64_t)c.m_blk * BM + q * 32 + lane;   // local output row
       const bool row_ok = row < p.m_rows;
-      const int64_t col0 = (int64_t)c.n_blk * BN + half * 128;
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * 128;
+      const int64_t col0 = (int64_t)c.n_blk * BN + grp * CW;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + grp * CW;
       if (p.mode == BITMAP || p.mode == BITMAP_PAIR) {
-        uint32_t r0[32], r1[32];
-        TMEM_LD_32x32b_X32_PACK16(taddr, r0);        // columns [0, 64) of the half
-        TMEM_LD_32x32b_X32_PACK16(taddr + 64, r1);   // columns [64, 128)
+        constexpr int NR = CW / 2;                   // pack::16b registers (2 columns each)
+        uint32_t r[NR];
+#pragma unroll
+        for (int h = 0; h < NR / 32; ++h) {
+          uint32_t* rh = r + 32 * h;
+          TMEM_LD_32x32b_X32_PACK16(taddr + 64 * h, rh);
+        }
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
-        // BITMAP: 128 columns -> 4 words; BITMAP_PAIR: 128 accumulators = 256 z -> 8 words
+        // BITMAP: CW columns -> CW/32 words; BITMAP_PAIR: CW accumulators = 2*CW z -> CW/16 words
         const bool pair = (p.mode == BITMAP_PAIR);
-        const int ow = pair ? 16 : 8;                // words per tile row
-        uint32_t w[8];
+        constexpr int NW = CW / 16;
+        uint32_t w[NW];
         if (pair) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            w[k] = pack_bits_pair(r0 + 8 * k);
-            w[k + 4] = pack_bits_pair(r1 + 8 * k);
-          }
+          for (int k = 0; k < NW; ++k) w[k] = pack_bits_pair(r + 8 * k);
         } else {
-          if (p.debug) {
-            w[0] = r0[0] | r0[7]; w[1] = r0[16]; w[2] = r1[3]; w[3] = r1[31];
-          } else if (p.small_counts) {
-            // every count < 256 (K <= 255) -> 4 counts per register (PRMT), SWAR
-            // nonzero test, 4-flag movemask by one multiply
-            w[0] = pack_bits_u8(r0);
-            w[1] = pack_bits_u8(r0 + 16);
-            w[2] = pack_bits_u8(r1);
-            w[3] = pack_bits_u8(r1 + 16);
-          } else {
-            w[0] = pack_bits_u16(r0);
-            w[1] = pack_bits_u16(r0 + 16);
-            w[2] = pack_bits_u16(r1);
-            w[3] = pack_bits_u16(r1 + 16);
-          }
-          w[4] = w[5] = w[6] = w[7] = 0;
-        }
-        if (row_ok) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) my_nnz += __popc(w[k]);
+          for (int k = 0; k < NW / 2; ++k) {
+            if (p.debug) w[k] = r[16 * k] | r[16 * k + 7];
+            else if (p.small_counts) w[k] = pack_bits_u8(r + 16 * k);    // counts < 256: PRMT + SWAR
+            else w[k] = pack_bits_u16(r + 16 * k);
+          }
+#pragma unroll
+          for (int k = NW / 2; k < NW; ++k) w[k] = 0;
         }
         if (row_ok) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out +
-                                                (int64_t)c.n_blk * ow + half * (ow / 2));
-          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          if (pair) dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out +
+                          (pair ? (int64_t)c.n_blk * 16 + grp * NW : (int64_t)c.n_blk * 8 + grp * (NW / 2));
+          if (pair) {
+#pragma unroll
+            for (int k = 0; k < NW; k += 4)
+              *reinterpret_cast<uint4*>(dst + k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+          } else if (NW / 2 >= 4) {
+#pragma unroll
+            for (int k = 0; k < NW / 2; k += 4)
+              *reinterpret_cast<uint4*>(dst + k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+          } else {
+            *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+          }
+#pragma unroll
+          for (int k = 0; k < NW; ++k) my_nnz += __popc(w[k]);
         }
       } else if (p.mode == COUNT32) {
         // 32x32 blocks: lane (= row) stages its 32 counts in shared memory,
@@ -452,7 +462,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int64_t row_base = (int64_t)c.m_blk * BM + q * 32;
         const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
 #pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < CW / 32; ++j) {
           uint32_t r[32];
           TMEM_LD_32x32b_X32(taddr + j * 32, r);
           tmem_wait_ld();
@@ -481,7 +491,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {  // ACC64
         int64_t* dst = reinterpret_cast<int64_t*>(p.out) + row * p.ld_out + col0;
 #pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < CW / 32; ++j) {
           uint32_t r[32];
           TMEM_LD_32x32b_X32(taddr + j * 32, r);
           tmem_wait_ld();
@@ -630,7 +640,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   static bool attr_set = false;
   if (!attr_set) {
     MMJ_TRY(cuda_status(cudaFuncSetAttribute(heavy_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem_bytes_for(STAGES, false)),   // >= smem_bytes_for(3, true)
+                                             SMEM_MAX),
                         "cudaFuncSetAttribute(heavy_mma)"));
     attr_set = true;
   }
