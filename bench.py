@@ -57,7 +57,7 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-slice-x", type=int, default=32, help="x values per reference-arm sample")
     ap.add_argument("--x-limit", type=int, default=0, help="debug: only the first X output rows")
-    ap.add_argument("--schedule", default="mma_ahead", choices=["serial", "mma_ahead", "pipelined"],
+    ap.add_argument("--schedule", default="serial", choices=["serial", "mma_ahead", "pipelined"],
                     help="chunk schedule: one stream, heavy product one chunk ahead on a side stream, "
                          "or emission on a side stream")
     return ap.parse_args()

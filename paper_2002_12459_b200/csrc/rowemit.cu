@@ -36,6 +36,7 @@ constexpr int TM_THREADS = 256;
 constexpr int TUP_BATCH = TM_THREADS;   // light tuples staged per round
 constexpr int TILE_WORDS = 16384;       // up to 64 KB of bitmap per tile (whole rows up to 524288 cells)
 constexpr int SHORT_LIST = 96;          // lists up to this length are filtered, longer ones bisected
+constexpr int MERGE_ILP = 8;            // witness slots per thread per step of the merge
 constexpr int EM_WARPS = 8;
 constexpr int EM_SEGS = 64;             // segments per emission CTA (8 per warp: balances uneven row densities)
 
@@ -199,12 +200,32 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
     const int nt = (int)min((int64_t)TUP_BATCH, t_end - tb);
     int kept = 0;
     int ti = 0;   // tuple of the current slot; slots grow, so the cursor only moves forward
-    for (int s = tid; s < tot; s += TM_THREADS) {
-      while (ti + 1 < nt && s_tb_len[ti + 1] <= s) ++ti;
-      const int32_t z = s_tb_base[ti][s - s_tb_len[ti]];
-      if (s_tb_filt[ti] && (z < zlo || z >= zhi)) continue;
-      atomicOr(&sbm[s_tb_row[ti] * cw + ((z - zlo) >> 5)], 1u << (z & 31));
-      ++kept;
+    // MERGE_ILP slots per thread per step: their list loads are issued
+    // together before the shared-memory atomics (the loads are the latency)
+    for (int s0 = tid; s0 < tot; s0 += MERGE_ILP * TM_THREADS) {
+      int32_t zv[MERGE_ILP];
+      int rowv[MERGE_ILP];
+      bool ok[MERGE_ILP];
+#pragma unroll
+      for (int u = 0; u < MERGE_ILP; ++u) {
+        const int s = s0 + u * TM_THREADS;
+        ok[u] = s < tot;
+        rowv[u] = 0;
+        zv[u] = 0;
+        if (ok[u]) {
+          while (ti + 1 < nt && s_tb_len[ti + 1] <= s) ++ti;
+          zv[u] = __ldg(s_tb_base[ti] + (s - s_tb_len[ti]));
+          rowv[u] = s_tb_row[ti] | (s_tb_filt[ti] << 30);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < MERGE_ILP; ++u) {
+        if (!ok[u]) continue;
+        const int32_t z = zv[u];
+        if ((rowv[u] >> 30) && (z < zlo || z >= zhi)) continue;
+        atomicOr(&sbm[(rowv[u] & 0x3FFFFFFF) * cw + ((z - zlo) >> 5)], 1u << (z & 31));
+        ++kept;
+      }
     }
     my_w += kept;
     if (tot > 0 && tid == 0) s_touched = 1;
