@@ -175,15 +175,17 @@ int mmj_count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols,
  * hold dom_y (+1) entries.  mmj_star_operand: A[r] = AND_{j<k-1} H_j[x_j] for
  * the composite rows r of x1 in [x1_begin, ..) (kpad % 16 == 0).
  * mmj_star_light: every light witness with x1 in [x1_begin, x1_end) is OR-ed
- * (mode 0, ld words) or counted (mode 1, ld int32) into the chunk matrix. */
+ * (mode 0, ld words) or counted (mode 1, ld int32) into the chunk matrix,
+ * balanced by witness index (needs mmj_star_light_workspace_bytes(n_light)). */
 int mmj_star_split(int k, const int32_t* const* rev_ptr, int64_t dom_y, double threshold, uint8_t* heavy_flag,
                    uint8_t* light_flag, int32_t* heavy_scan, int32_t* light_scan, int32_t* hpos, int32_t* light_y,
                    void* ws, void* stream);
 int mmj_star_operand(int k, const int64_t* dims, const uint8_t* const* heavy, int64_t kpad, int64_t x1_begin,
                      int64_t rows, uint8_t* A, void* stream);
+size_t mmj_star_light_workspace_bytes(int64_t n_light);
 int mmj_star_light(int k, const int64_t* dims, const int32_t* const* rev_ptr, const int32_t* const* rev_idx,
                    const int32_t* light_y, int64_t n_light, int64_t x1_begin, int64_t x1_end, int mode, void* out,
-                   int64_t ld, unsigned long long* witnesses, void* stream);
+                   int64_t ld, unsigned long long* witnesses, void* ws, void* stream);
 
 /* ---- batched boolean set intersection: apps.py:314-351 ----------------------
  * Heavy y (hpos >= 0, from mmj_heavy_y_positions) -> per-left-id bitsets of

@@ -71,7 +71,8 @@ _SIGS = {
     "mmj_bsi_answer": (INT, [P, P, I64, P, P, I64, P, P, I64, P, P, INT, P, P, P, P, P, P]),
     "mmj_star_split": (INT, [INT, P, I64, C.c_double, P, P, P, P, P, P, P, P]),
     "mmj_star_operand": (INT, [INT, P, P, I64, I64, I64, P, P]),
-    "mmj_star_light": (INT, [INT, P, P, P, P, I64, I64, I64, INT, P, I64, P, P]),
+    "mmj_star_light_workspace_bytes": (SZ, [I64]),
+    "mmj_star_light": (INT, [INT, P, P, P, P, I64, I64, I64, INT, P, I64, P, P, P]),
     "mmj_bitmap_segment_count": (I64, [I64]),
     "mmj_bitmap_segments": (INT, [P, I64, P, P, P, P]),
     "mmj_bitmap_emit": (INT, [P, I64, I64, P, I64, I64, P, P]),

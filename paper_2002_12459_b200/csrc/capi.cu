@@ -40,8 +40,9 @@ int bsi_answer(const int64_t*, const int64_t*, int64_t, const int64_t*, const in
 int star_split(int, const int32_t* const*, int64_t, double, uint8_t*, uint8_t*, int32_t*, int32_t*, int32_t*, int32_t*,
                void*, cudaStream_t);
 int star_operand(int, const int64_t*, const uint8_t* const*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
+size_t star_light_ws_bytes(int64_t);
 int star_light(int, const int64_t*, const int32_t* const*, const int32_t* const*, const int32_t*, int64_t, int64_t,
-               int64_t, int, void*, int64_t, unsigned long long*, cudaStream_t);
+               int64_t, int, void*, int64_t, unsigned long long*, void*, cudaStream_t);
 namespace mma {
 int launch_heavy_mma(const uint8_t*, int64_t, const uint8_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                      int, int, void*, int64_t, unsigned long long*, int, cudaStream_t);
@@ -205,11 +206,13 @@ int mmj_star_operand(int k, const int64_t* dims, const uint8_t* const* heavy, in
   return mmj::star_operand(k, dims, heavy, kpad, x1_begin, rows, A, ST(stream));
 }
 
+size_t mmj_star_light_workspace_bytes(int64_t n_light) { return mmj::star_light_ws_bytes(n_light); }
+
 int mmj_star_light(int k, const int64_t* dims, const int32_t* const* rev_ptr, const int32_t* const* rev_idx,
                    const int32_t* light_y, int64_t n_light, int64_t x1_begin, int64_t x1_end, int mode, void* out,
-                   int64_t ld, unsigned long long* witnesses, void* stream) {
+                   int64_t ld, unsigned long long* witnesses, void* ws, void* stream) {
   return mmj::star_light(k, dims, rev_ptr, rev_idx, light_y, n_light, x1_begin, x1_end, mode, out, ld, witnesses,
-                         ST(stream));
+                         ws, ST(stream));
 }
 
 int64_t mmj_bitmap_segment_count(int64_t nwords) { return mmj::bitmap_nseg(nwords); }

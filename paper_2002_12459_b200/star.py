@@ -97,6 +97,8 @@ class StarEngine:
         self.ldc = _rup(max(self.dk, 1), 1024)
         self.row_per_x1 = math.prod(self.dims[1:-1]) if self.k > 2 else 1
         row_bytes = self.ldc * 4 if want_counts else self.wpr * 4
+        import os
+        chunk_bytes = int(os.environ.get("MMJ_STAR_CHUNK_BYTES", chunk_bytes))
         self.x1_per_chunk = max(1, chunk_bytes // max(row_bytes * self.row_per_x1, 1))
         self.nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.wit = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -118,15 +120,28 @@ class StarEngine:
         kk, nl = (int(v) for v in torch.stack([hscan[dom_y], lscan[dom_y]]).cpu())
         self.kh, self.n_light = kk, nl
         self.H = None
+        self.pairs = False
         if kk > 0:
             self.kpad = _rup(kk, BK)
             self.H = []
+            # z-pair B operand (two x_k per accumulator, c0 + 128*c1) when every
+            # count is < 128: a composite row's heavy degree is at most the
+            # smallest left degree among R_1..R_{k-1} rows, and x_k's its own
+            import os
+            maxdeg = [int(np.asarray(r.left_deg).max(initial=0)) for r in self.rels]
+            self.pairs = (not self.counts and os.environ.get("MMJ_PAIR", "1") != "0"
+                          and (kk <= 127 or min(maxdeg[:-1]) <= 127 or maxdeg[-1] <= 127))
             for j, d in enumerate(self.dev):
                 pad = 1024 if j == self.k - 1 else 256
                 rows = _rup(max(d.dom_left, 1), pad)
-                h = torch.empty((rows, self.kpad), dtype=torch.uint8, device="cuda")
-                nat.call("mmj_build_operand", nat.ptr(d.fwd_row), nat.ptr(d.fwd_idx), d.n, nat.ptr(d.left_deg), 0,
-                         nat.ptr(self.hpos), nat.ptr(h), 0, rows, self.kpad, st)
+                if j == self.k - 1 and self.pairs:
+                    h = torch.empty((rows // 2, self.kpad), dtype=torch.uint8, device="cuda")
+                    nat.call("mmj_build_operand_pairs", nat.ptr(d.fwd_row), nat.ptr(d.fwd_idx), d.n,
+                             nat.ptr(d.left_deg), 0, nat.ptr(self.hpos), nat.ptr(h), 0, rows, self.kpad, st)
+                else:
+                    h = torch.empty((rows, self.kpad), dtype=torch.uint8, device="cuda")
+                    nat.call("mmj_build_operand", nat.ptr(d.fwd_row), nat.ptr(d.fwd_idx), d.n, nat.ptr(d.left_deg),
+                             0, nat.ptr(self.hpos), nat.ptr(h), 0, rows, self.kpad, st)
                 self.H.append(h)
 
     def run(self, sink=None):
@@ -152,14 +167,19 @@ class StarEngine:
                 A = self.ws.get("star_A", arows * self.kpad, torch.uint8)
                 nat.call("mmj_star_operand", self.k, dims_arr, heavy_ptrs, self.kpad, xa, rows, nat.ptr(A), st)
                 B = self.H[-1]
+                if self.counts:
+                    mode = nat.MODE_COUNT32
+                elif self.pairs:
+                    mode = nat.MODE_BITMAP_PAIR
+                else:
+                    mode = nat.MODE_BITMAP_U8 if self.kh <= 255 else nat.MODE_BITMAP
                 nat.call("mmj_heavy_mma", nat.ptr(A), arows, nat.ptr(B), B.shape[0], self.kpad, 0, self.kpad, 0, rows,
-                         nat.MODE_COUNT32 if self.counts else (nat.MODE_BITMAP_U8 if self.kh <= 255 else nat.MODE_BITMAP),
-                         0, nat.ptr(buf), ld, nat.ptr(self.nnz),
-                         0, st)
+                         mode, 0, nat.ptr(buf), ld, nat.ptr(self.nnz), 0, st)
             else:
                 buf.zero_()
+            lws = self.ws.get("star_lws", int(self.lib.mmj_star_light_workspace_bytes(self.n_light)), torch.uint8)
             nat.call("mmj_star_light", self.k, dims_arr, rev_ptrs, rev_idxs, nat.ptr(self.light_y), self.n_light, xa,
-                     xb, 1 if self.counts else 0, nat.ptr(buf), ld, nat.ptr(self.wit), st)
+                     xb, 1 if self.counts else 0, nat.ptr(buf), ld, nat.ptr(self.wit), nat.ptr(lws), st)
             x0 = xa * self.row_per_x1
             if self.counts:
                 ncell = rows * self.ldc

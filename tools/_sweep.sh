@@ -1,3 +1,2 @@
-python -m pytest tests/test_gpu_twopath.py tests/test_gpu_golden.py -x -q 2>&1 | tail -1
-for i in 1 2; do python bench.py --no-e2e --no-cpu-baseline --schedule serial 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('serial', d['ms_per_step'], {k:round(v['ms'],1) for k,v in d['phases'].items()})"; done
-python bench.py --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('mma_ahead', d['ms_per_step'], {k:round(v['ms'],1) for k,v in d['phases'].items()})"
+python -m pytest tests/test_gpu_apps.py tests/test_gpu_fullsize.py -x -q -k "star or cfg3" 2>&1 | tail -1
+for v in "MMJ_PAIR=1" "MMJ_STAR_CHUNK_BYTES=1073741824"; do env $v python tools/bench_configs.py cfg3 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', d['seconds'], d['light_witnesses'])"; done
