@@ -194,6 +194,10 @@ int mmj_star_light(int k, const int64_t* dims, const int32_t* const* rev_ptr, co
  * query ids through each relation's sorted raw left values (r_sorted/r_order;
  * NULL = queries are dense ids already) and writes ans[q] = 1 (intersect),
  * 0 (disjoint) or -1 (id unknown to the unreduced relation = None). */
+/* histogram of max(rdeg[y], sdeg[y]) > 0: 64 log2 bins (log2mode) or nbins
+ * (<= 1024) linear bins over [lo, hi); picks the heavy-y threshold on the device */
+int mmj_bsi_degree_histogram(const int32_t* rdeg, const int32_t* sdeg, int64_t dom_y, int64_t lo, int64_t hi,
+                             int nbins, int log2mode, int32_t* hist, void* stream);
 int mmj_bsi_bits(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* hpos, int words, uint32_t* bits,
                  int64_t dom_left, void* stream);
 int mmj_bsi_light_lists(const int32_t* fwd_ptr, const int32_t* fwd_idx, int64_t n, int64_t dom_left,

@@ -66,6 +66,7 @@ _SIGS = {
     "mmj_tile_count": (I64, [I64, I64]),
     "mmj_tile_merge": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P]),
     "mmj_emit_codes": (INT, [P, P, I64, I64, I64, I64, P, P]),
+    "mmj_bsi_degree_histogram": (INT, [P, P, I64, I64, I64, INT, INT, P, P]),
     "mmj_bsi_bits": (INT, [P, P, I64, P, INT, P, I64, P]),
     "mmj_bsi_light_lists": (INT, [P, P, I64, I64, P, P, P, P, P, P, P]),
     "mmj_bsi_answer": (INT, [P, P, I64, P, P, I64, P, P, I64, P, P, INT, P, P, P, P, P, P]),

@@ -39,7 +39,7 @@ class BsiSide:
     fwd_ptr: object
     fwd_idx: object
     fwd_row: object
-    ydeg: np.ndarray          # host degrees over the shared y space
+    ydeg: object              # device int32 degrees over the shared y space
     sorted_vals: object       # device int64 sorted raw left values (or None)
     order: object             # device int32 dense id of each sorted value
     h2d_bytes: int = 0
@@ -71,7 +71,7 @@ def _side(idx, y_map, dom_y, pinned=False) -> BsiSide:
         fidx = y_map[fidx]
         order = np.lexsort((fidx, rows))          # keep each list sorted by shared y id
         fidx = fidx[order]
-    ydeg = np.bincount(fidx, minlength=dom_y).astype(np.int32)
+    ydeg = torch.from_numpy(np.bincount(fidx, minlength=dom_y).astype(np.int32)).to("cuda")
     lk = _left_lookup_arrays(idx.rel)
     dev = {}
     nbytes = 0
@@ -98,11 +98,11 @@ def _side_device(idx, y_map, dom_y, ws) -> BsiSide:
     d = idx.device
     if y_map is None:
         fptr, fidx, frow = d.fwd_ptr, d.fwd_idx, d.fwd_row
-        ydeg = np.asarray(idx.right_deg, dtype=np.int32)
+        ydeg = d.right_deg
     else:
         mapped = ingest.remap(d.fwd_idx, y_map)
         fptr, fidx, frow, _ = ingest.csr(d.fwd_row, mapped, d.dom_left, dom_y, ws)
-        ydeg = ingest.histogram(mapped, dom_y).cpu().numpy().astype(np.int32)
+        ydeg = ingest.histogram(mapped, dom_y)
     sv, od = ingest.sorted_ids(idx._left_values_dev, ws)
     return BsiSide(d.n, d.dom_left, fptr, fidx, frow, ydeg, sv, od, 0)
 
@@ -172,16 +172,36 @@ class BsiEngine:
         self.sR, self.sS, self.dom_y = sR, sS, dom_y
         self.heavy_bits = max(BITS_BLOCK, -(-heavy_bits // BITS_BLOCK) * BITS_BLOCK)
         self.ws = ws or Workspace()
-        m = np.maximum(sR.ydeg, sS.ydeg)
-        # delta1 = the heavy_bits-th largest max-degree: y heavy iff max deg > delta1
-        if len(m) > self.heavy_bits:
-            self.delta1 = max(1, int(np.partition(m, len(m) - self.heavy_bits)[len(m) - self.heavy_bits]))
-        else:
-            self.delta1 = 1
-        torch = _torch()
-        self.rdeg = torch.from_numpy(sR.ydeg).to("cuda")
-        self.sdeg = torch.from_numpy(sS.ydeg).to("cuda")
+        self.rdeg, self.sdeg = sR.ydeg, sS.ydeg
+        self.delta1 = self._threshold()
         self.k = 0
+
+    def _threshold(self) -> int:
+        """Smallest delta1 >= 1 with #{y : max(degR, degS) > delta1} <=
+        heavy_bits, from two device histograms (log2 buckets, then linear
+        bins inside the crossing bucket).  Which y are heavy never changes the
+        answers (bitsets and light lists are both exact), only the split."""
+        torch = _torch()
+        st = nat.stream_handle()
+        hist = self.ws.get("bsi_hist", 1024, torch.int32)
+        nat.call("mmj_bsi_degree_histogram", nat.ptr(self.rdeg), nat.ptr(self.sdeg), self.dom_y, 0, 1, 64, 1,
+                 nat.ptr(hist), st)
+        h = hist[:64].cpu().numpy().astype(np.int64)
+        above = np.concatenate([np.cumsum(h[::-1])[::-1], [0]])     # above[b] = #{m >= 2^b}
+        if above[0] <= self.heavy_bits:
+            return 1
+        b = int(np.nonzero(above > self.heavy_bits)[0].max())        # bucket holding the crossing
+        lo, hi = 1 << b, 1 << (b + 1)
+        nb = int(min(1024, hi - lo))
+        nat.call("mmj_bsi_degree_histogram", nat.ptr(self.rdeg), nat.ptr(self.sdeg), self.dom_y, lo, hi, nb, 0,
+                 nat.ptr(hist), st)
+        g = hist[:nb].cpu().numpy().astype(np.int64)
+        # count(m > t) for t = the last value of linear bin i: above[b+1] + sum of bins after i
+        tail = above[b + 1] + np.concatenate([np.cumsum(g[::-1])[::-1][1:], [0]])
+        ok = np.nonzero(tail <= self.heavy_bits)[0]
+        i = int(ok.min())
+        t = lo + ((i + 1) * (hi - lo) + nb - 1) // nb - 1              # largest m in bin i
+        return max(1, t)
 
     def build(self):
         torch = _torch()

@@ -121,6 +121,27 @@ __global__ void k_bsi_answer(const BsiArgs a) {
 
 }  // namespace
 
+// histogram of m(y) = max(rdeg[y], sdeg[y]) over y with m > 0: log2 bins
+// (bin b holds m in [2^b, 2^(b+1))) or nbins linear bins over [lo, hi)
+__global__ void k_bsi_deg_hist(const int32_t* __restrict__ rdeg, const int32_t* __restrict__ sdeg, int64_t dom_y,
+                               int64_t lo, int64_t hi, int nbins, int log2mode, int32_t* __restrict__ hist) {
+  __shared__ int32_t sh[1024];
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < dom_y; y += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = max(rdeg[y], sdeg[y]);
+    if (m <= 0) continue;
+    if (log2mode) {
+      atomicAdd(&sh[63 - __clzll((unsigned long long)m)], 1);
+    } else if (m >= lo && m < hi) {
+      atomicAdd(&sh[(int)((m - lo) * nbins / (hi - lo))], 1);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
 int bsi_bits(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* hpos, int words, uint32_t* bits,
              int64_t dom, cudaStream_t st) {
   MMJ_TRY(cuda_status(cudaMemsetAsync(bits, 0, (size_t)dom * words * 4, st), "memset bits"));
@@ -159,6 +180,21 @@ int bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* 
             r_lptr, r_lidx, s_lptr, s_lidx, ans};
   k_bsi_answer<<<grid_for(nq, TPB, 16), TPB, 0, st>>>(a);
   MMJ_CHECK_LAUNCH("k_bsi_answer");
+  return MMJ_OK;
+}
+
+int bsi_degree_histogram(const int32_t* rdeg, const int32_t* sdeg, int64_t dom_y, int64_t lo, int64_t hi, int nbins,
+                         int log2mode, int32_t* hist, cudaStream_t st) {
+  if (nbins < 1 || nbins > 1024 || (!log2mode && hi <= lo) || (log2mode && nbins < 64)) {
+    set_error("bsi_degree_histogram: 1 <= nbins <= 1024 (64 for log2 bins), lo < hi");
+    return MMJ_ERR_ARG;
+  }
+  MMJ_TRY(cuda_status(cudaMemsetAsync(hist, 0, (size_t)nbins * 4, st), "memset hist"));
+  if (dom_y == 0) return MMJ_OK;
+  int64_t g = ceil_div(dom_y, TPB);
+  if (g > (int64_t)sm_count() * 4) g = (int64_t)sm_count() * 4;
+  k_bsi_deg_hist<<<(unsigned)g, TPB, 0, st>>>(rdeg, sdeg, dom_y, lo, hi, nbins, log2mode, hist);
+  MMJ_CHECK_LAUNCH("k_bsi_deg_hist");
   return MMJ_OK;
 }
 

@@ -43,6 +43,7 @@ int star_operand(int, const int64_t*, const uint8_t* const*, int64_t, int64_t, i
 size_t star_light_ws_bytes(int64_t);
 int star_light(int, const int64_t*, const int32_t* const*, const int32_t* const*, const int32_t*, int64_t, int64_t,
                int64_t, int, void*, int64_t, unsigned long long*, void*, cudaStream_t);
+int bsi_degree_histogram(const int32_t*, const int32_t*, int64_t, int64_t, int64_t, int, int, int32_t*, cudaStream_t);
 namespace mma {
 int launch_heavy_mma(const uint8_t*, int64_t, const uint8_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                      int, int, void*, int64_t, unsigned long long*, int, cudaStream_t);
@@ -173,6 +174,11 @@ int mmj_tile_merge(uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, in
 int mmj_emit_codes(const uint32_t* bitmap, const int64_t* seg_off, int64_t rows, int64_t wpr, int64_t x0,
                    int64_t dom_z, int64_t* codes, void* stream) {
   return mmj::emit_codes(bitmap, seg_off, rows, wpr, x0, dom_z, codes, ST(stream));
+}
+
+int mmj_bsi_degree_histogram(const int32_t* rdeg, const int32_t* sdeg, int64_t dom_y, int64_t lo, int64_t hi,
+                             int nbins, int log2mode, int32_t* hist, void* stream) {
+  return mmj::bsi_degree_histogram(rdeg, sdeg, dom_y, lo, hi, nbins, log2mode, hist, ST(stream));
 }
 
 int mmj_bsi_bits(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* hpos, int words, uint32_t* bits,

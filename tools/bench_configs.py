@@ -166,17 +166,21 @@ def cfg5():
 
     from paper_2002_12459_b200 import datagen
     from paper_2002_12459_b200.bsi import BsiEngine, prepare
-    from paper_2002_12459_b200.relation import Relation, build_indexed
-    t0 = time.time()
+    from paper_2002_12459_b200.ingest import from_raw_pairs_device
     wl = datagen.config("cfg5")
-    r = build_indexed(Relation.from_raw_pairs("R", wl.relations[0]))
-    s = build_indexed(Relation.from_raw_pairs("S", wl.relations[1]))
-    prep = time.time() - t0
-    sR, sS, dom_y = prepare(r, s)
+    raws = [torch.from_numpy(np.ascontiguousarray(r, dtype=np.int64)).pin_memory() for r in wl.relations]
     qa = torch.from_numpy(wl.batch[:, 0].copy()).cuda()
     qb = torch.from_numpy(wl.batch[:, 1].copy()).cuda()
     nq = len(wl.batch)
     holder = {}
+
+    def ingest_prepare():
+        r = from_raw_pairs_device("R", raws[0])
+        s = from_raw_pairs_device("S", raws[1])
+        holder["sides"] = prepare(r, s)
+        return r, s
+    t_ing, _ = _timed(ingest_prepare, reps=2)
+    sR, sS, dom_y = holder["sides"]
 
     def full():
         eng = BsiEngine(sR, sS, dom_y, 256)
@@ -187,12 +191,14 @@ def cfg5():
     eng = holder["eng"]
     t_ans, _ = _timed(lambda: eng.answer(qa, qb, nq))
     a = ans.cpu().numpy()
-    in_bytes = 8 * (r.n + s.n) + 9 * nq
+    in_bytes = 8 * (raws[0].shape[0] + raws[1].shape[0]) + 9 * nq
     return [{"config": "cfg5", "workload": wl.description, "queries": nq, "true": int((a == 1).sum()),
              "none": int((a == -1).sum()), "seconds_build_plus_answer": t_full, "answers_per_s": nq / t_full,
              "seconds_answer_only": t_ans, "answers_per_s_answer_only": nq / t_ans,
-             "lower_bound_bytes": in_bytes, "achieved_GBps_vs_lower_bound": in_bytes / t_full / 1e9,
-             "host_prep_seconds": prep}]
+             "seconds_raw_pairs_to_device_index": t_ing,
+             "note": "device ingest (H2D of 2 x 64M pinned raw pairs, dedup, dictionaries, CSR) + BSI y-space "
+                     "union/remap, then heavy-y bitsets + light lists (build) and the batch answer",
+             "lower_bound_bytes": in_bytes, "achieved_GBps_vs_lower_bound": in_bytes / t_full / 1e9}]
 
 
 if __name__ == "__main__":
