@@ -45,6 +45,8 @@ extern "C" {
 #define MMJ_MODE_BITMAP_PAIR 4 /* BITMAP over a z-pair B operand (mmj_build_operand_pairs): b_rows = pair
                                   rows, 2 bits per accumulator; needs every count < 128 (a side whose
                                   heavy degrees are <= 127); ld_out*16 >= b_rows rounded up to 256 */
+#define MMJ_MODE_COUNT16 5     /* exact counts as uint16 (caller guarantees every count < 65536); ld_out in
+                                  uint16 elements, multiple of 8 */
 #define MMJ_MODE_UPPER 16      /* OR-flag: self-join, skip tiles whose columns are all <= their rows
                                   (cells there are left unwritten; consumers keep z > x only) */
 
@@ -93,7 +95,7 @@ int mmj_light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, i
  * mmj_light_lengths writes len[ntup] and offs[ntup+1] (exclusive scan; offs[ntup]
  * is the light intermediate size).  mmj_light_expand sets bit (x-x0, z) of a
  * bitmap (mode 0, ld in words) or adds 1 to count cell (x-x0, z) (mode 1, ld in
- * int32).  min_deg > 1 (SSJ threshold c) skips rows of sets smaller than c
+ * int32; mode 2, ld in uint16 elements, every count < 65536).  min_deg > 1 (SSJ threshold c) skips rows of sets smaller than c
  * and light-z lists when delta2 < c; upper_only skips witnesses with z <= x. */
 int mmj_light_lengths(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int64_t ntup,
                       const int32_t* rdeg_x, int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr,
@@ -153,19 +155,20 @@ int mmj_bitmap_segments(const uint32_t* bm, int64_t nwords, int32_t* segcnt, int
                         void* stream);
 int mmj_bitmap_emit(const uint32_t* bm, int64_t nwords, int64_t wpr, const int64_t* seg_off, int64_t x0,
                     int64_t dom_z, int64_t* codes, void* stream);
-/* Count chunk (nrows x ld int32, ncols valid columns): cells with count >=
+/* Count chunk (nrows x ld cells, int32 or uint16 by cell_bytes = 4 / 2, ncols
+ * valid columns; uint16 when every count is < 65536): cells with count >=
  * max(min_count, row_min[x0+row]) (row_min may be NULL) -> codes + int32
  * counts.  cell_filter: 0 every cell, 1 col > x0+row (SSJ's a < b,
  * apps.py:57-62), 2 col != x0+row (SCJ's a != b, apps.py:297-304).  ld must be a multiple of 1024
  * (segments of 1024 cells never straddle rows); with cell_filter 1, segments
  * at or below the diagonal are not read. */
 int64_t mmj_count_segment_count(int64_t ncell);
-int mmj_count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
-                       const int32_t* row_min, int cell_filter, int32_t* segcnt, int64_t* seg_off, void* ws,
-                       void* stream);
-int mmj_count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
-                   int32_t min_count, const int32_t* row_min, int cell_filter, const int64_t* seg_off, int64_t* codes,
-                   int32_t* counts, void* stream);
+int mmj_count_segments(const void* cnt, int cell_bytes, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0,
+                       int32_t min_count, const int32_t* row_min, int cell_filter, int32_t* segcnt, int64_t* seg_off,
+                       void* ws, void* stream);
+int mmj_count_emit(const void* cnt, int cell_bytes, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0,
+                   int64_t dom_z, int32_t min_count, const int32_t* row_min, int cell_filter, const int64_t* seg_off,
+                   int64_t* codes, int32_t* counts, void* stream);
 
 /* ---- star join-project, k = 2..4: joinproject.py:281-378 -------------------
  * Output as a two-path over composite rows (x1..x_{k-1}) x column x_k.

@@ -26,6 +26,7 @@ MODE_COUNT32 = 1
 MODE_ACC64 = 2
 MODE_BITMAP_U8 = 3
 MODE_BITMAP_PAIR = 4
+MODE_COUNT16 = 5
 MODE_UPPER = 16
 
 P = C.c_void_p
@@ -78,8 +79,8 @@ _SIGS = {
     "mmj_bitmap_segments": (INT, [P, I64, P, P, P, P]),
     "mmj_bitmap_emit": (INT, [P, I64, I64, P, I64, I64, P, P]),
     "mmj_count_segment_count": (I64, [I64]),
-    "mmj_count_segments": (INT, [P, I64, I64, I64, I64, I32, P, INT, P, P, P, P]),
-    "mmj_count_emit": (INT, [P, I64, I64, I64, I64, I64, I32, P, INT, P, P, P, P]),
+    "mmj_count_segments": (INT, [P, INT, I64, I64, I64, I64, I32, P, INT, P, P, P, P]),
+    "mmj_count_emit": (INT, [P, INT, I64, I64, I64, I64, I64, I32, P, INT, P, P, P, P]),
 }
 
 _lib = None

@@ -22,9 +22,9 @@ int64_t bitmap_nseg(int64_t);
 int64_t count_nseg(int64_t);
 int bitmap_segments(const uint32_t*, int64_t, int32_t*, int64_t*, void*, cudaStream_t);
 int bitmap_emit(const uint32_t*, int64_t, int64_t, const int64_t*, int64_t, int64_t, int64_t*, cudaStream_t);
-int count_segments(const int32_t*, int64_t, int64_t, int64_t, int64_t, int32_t, const int32_t*, int, int32_t*,
+int count_segments(const void*, int, int64_t, int64_t, int64_t, int64_t, int32_t, const int32_t*, int, int32_t*,
                    int64_t*, void*, cudaStream_t);
-int count_emit(const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t, const int32_t*, int,
+int count_emit(const void*, int, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t, const int32_t*, int,
                const int64_t*, int64_t*, int32_t*, cudaStream_t);
 int64_t row_emit_tiles(int64_t, int64_t);
 int tile_merge(uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t*, const int32_t*, const int32_t*,
@@ -126,8 +126,8 @@ int mmj_light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0,
                      const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx, int64_t min_deg,
                      int upper_only, const int64_t* offs, int64_t total_hint, int mode, int64_t x0, void* out,
                      int64_t ld, void* stream) {
-  if (mode != 0 && mode != 1) {
-    mmj::set_error("light_expand: mode must be 0 (bitmap) or 1 (counts)");
+  if (mode < 0 || mode > 2) {
+    mmj::set_error("light_expand: mode must be 0 (bitmap), 1 (int32 counts) or 2 (uint16 counts)");
     return MMJ_ERR_ARG;
   }
   return mmj::light_expand(fwd_row, fwd_idx, t0, ntup, rdeg_x, delta2, hpos, s_rev_ptr, s_rev_idx, lz_ptr, lz_idx,
@@ -138,8 +138,9 @@ int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_
                   int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out, int64_t ld_out,
                   unsigned long long* nnz, int max_ctas, void* stream) {
   const int base_mode = mode & ~MMJ_MODE_UPPER;
-  if (base_mode < 0 || base_mode > 4 || (mode != base_mode && base_mode != MMJ_MODE_COUNT32)) {
-    mmj::set_error("heavy_mma: unknown mode %d (MMJ_MODE_UPPER combines with COUNT32 only)", mode);
+  if (base_mode < 0 || base_mode > 5 ||
+      (mode != base_mode && base_mode != MMJ_MODE_COUNT32 && base_mode != MMJ_MODE_COUNT16)) {
+    mmj::set_error("heavy_mma: unknown mode %d (MMJ_MODE_UPPER combines with the count modes only)", mode);
     return MMJ_ERR_ARG;
   }
   return mmj::mma::launch_heavy_mma(a, a_rows, b, b_rows, kpad, k_off, k_len, m_begin, m_rows, mode, shift, out,
@@ -235,25 +236,34 @@ int mmj_bitmap_emit(const uint32_t* bm, int64_t nwords, int64_t wpr, const int64
 
 int64_t mmj_count_segment_count(int64_t ncell) { return mmj::count_nseg(ncell); }
 
-int mmj_count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
-                       const int32_t* row_min, int cell_filter, int32_t* segcnt, int64_t* seg_off, void* ws,
-                       void* stream) {
+int mmj_count_segments(const void* cnt, int cell_bytes, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0,
+                       int32_t min_count, const int32_t* row_min, int cell_filter, int32_t* segcnt, int64_t* seg_off,
+                       void* ws, void* stream) {
+  if (cell_bytes != 2 && cell_bytes != 4) {
+    mmj::set_error("count_segments: cell_bytes must be 2 (uint16) or 4 (int32)");
+    return MMJ_ERR_ARG;
+  }
   if (cell_filter < 0 || cell_filter > 2) {
     mmj::set_error("count_segments: cell_filter must be 0, 1 or 2");
     return MMJ_ERR_ARG;
   }
-  return mmj::count_segments(cnt, nrows, ld, ncols, x0, min_count, row_min, cell_filter, segcnt, seg_off, ws,
+  return mmj::count_segments(cnt, cell_bytes, nrows, ld, ncols, x0, min_count, row_min, cell_filter, segcnt, seg_off, ws,
                              ST(stream));
 }
 
-int mmj_count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
-                   int32_t min_count, const int32_t* row_min, int cell_filter, const int64_t* seg_off, int64_t* codes,
-                   int32_t* counts, void* stream) {
+int mmj_count_emit(const void* cnt, int cell_bytes, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0,
+                   int64_t dom_z, int32_t min_count, const int32_t* row_min, int cell_filter, const int64_t* seg_off,
+                   int64_t* codes, int32_t* counts, void* stream) {
+  if (cell_bytes != 2 && cell_bytes != 4) {
+    mmj::set_error("count_emit: cell_bytes must be 2 (uint16) or 4 (int32)");
+    return MMJ_ERR_ARG;
+  }
   if (cell_filter < 0 || cell_filter > 2) {
     mmj::set_error("count_emit: cell_filter must be 0, 1 or 2");
     return MMJ_ERR_ARG;
   }
-  return mmj::count_emit(cnt, nrows, ld, ncols, x0, dom_z, min_count, row_min, cell_filter, seg_off, codes, counts,
+  return mmj::count_emit(cnt, cell_bytes, nrows, ld, ncols, x0, dom_z, min_count, row_min, cell_filter, seg_off, codes,
+                         counts,
                          ST(stream));
 }
 

@@ -15,6 +15,7 @@
 //       BITMAP : nonzero test, 32 cells -> one 32-bit word, 32 B per row/tile
 //                (the projection / intersection output);
 //       COUNT32: exact int32 counts (witness counts / set overlaps);
+//       COUNT16: the same as uint16 when every count is < 2^16 (half the bytes);
 //       ACC64  : out[i][j] += count << shift  (int64 digit recombination for
 //                the generic multiply_counts backend);
 //       BITMAP_PAIR: B rows are z pairs weighted (1, 128) (mmj_build_operand_pairs),
@@ -67,7 +68,7 @@ constexpr int SMEM_MAX = smem_bytes_for(3, true) > smem_bytes_for(STAGES, false)
 static_assert(SMEM_MAX <= 227 * 1024, "shared memory budget");
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
-enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, BITMAP_PAIR = 4, MODE_UPPER = 16 };
+enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, BITMAP_PAIR = 4, COUNT16 = 5, MODE_UPPER = 16 };
 
 struct Params {
   int64_t m_begin;      // first A row of this launch (multiple of BM not required)
@@ -455,6 +456,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < NW; ++k) my_nnz += __popc(w[k]);
         }
+      } else if (p.mode == COUNT16) {
+        // counts < 2^16 (caller's guarantee): pack::16b registers hold two
+        // cells each; 32 rows x 32 words (64 cells) per block, staged and
+        // stored 4 rows (128 B each) per instruction as in COUNT32
+        uint32_t* stg = epi_stage + (warp - 4) * 32 * EPI_PITCH;
+        const int64_t row_base = (int64_t)c.m_blk * BM + q * 32;
+        const int sub_r = lane >> 3, sub_c = (lane & 7) * 4;
+        const int64_t ldw = p.ld_out >> 1;                 // words per row
+#pragma unroll 1
+        for (int j = 0; j < CW / 64; ++j) {
+          uint32_t r[32];
+          TMEM_LD_32x32b_X32_PACK16(taddr + j * 64, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<uint4*>(stg + lane * EPI_PITCH + i) = make_uint4(r[i], r[i + 1], r[i + 2], r[i + 3]);
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int64_t cc = col0 + j * 64 + 2 * i;
+              my_nnz += ((r[i] & 0xFFFFu) != 0u && cc < p.n_cols) + ((r[i] >> 16) != 0u && cc + 1 < p.n_cols);
+            }
+          }
+          __syncwarp();
+          const int64_t wcol = ((col0 + j * 64) >> 1) + sub_c;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = sub_r + 4 * i;
+            const int64_t orow = row_base + rr;
+            const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * EPI_PITCH + sub_c);
+            if (orow < p.m_rows && wcol + 4 <= ldw)
+              *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(p.out) + orow * ldw + wcol) = v;
+          }
+          __syncwarp();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
       } else if (p.mode == COUNT32) {
         // 32x32 blocks: lane (= row) stages its 32 counts in shared memory,
         // then the warp stores 4 full rows (128 B each) per instruction.
@@ -591,6 +630,10 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
     set_error("heavy_mma: count pitch must be a multiple of 4");
     return MMJ_ERR_ARG;
   }
+  if (mode == COUNT16 && ld_out % 8 != 0) {
+    set_error("heavy_mma: uint16 count pitch must be a multiple of 8");
+    return MMJ_ERR_ARG;
+  }
   if ((mode == BITMAP || mode == BITMAP_U8 || mode == BITMAP_PAIR) && k_len > 65535) {
     set_error("heavy_mma: BITMAP mode packs 16-bit counts; K window must be < 65536");
     return MMJ_ERR_ARG;
@@ -615,7 +658,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
     }
     if (st_env >= 2 && st_env <= STAGES) p.stages = st_env;
   }
-  const bool staged = (mode == COUNT32);
+  const bool staged = (mode == COUNT32 || mode == COUNT16);
   if (staged && p.stages > 3) p.stages = 3;   // room for the epilogue staging buffers
   p.small_counts = (mode == BITMAP_U8 || k_len <= 255) ? 1 : 0;
   {

@@ -180,7 +180,7 @@ __device__ __forceinline__ int64_t upper_bound_i64(const int64_t* __restrict__ v
   return lo;
 }
 
-// mode 0: bitmap atomicOr; mode 1: int32 counts atomicAdd
+// mode 0: bitmap atomicOr; mode 1: int32 counts atomicAdd; mode 2: uint16 counts
 template <int MODE>
 __global__ void __launch_bounds__(EXP_THREADS) k_light_expand(LightArgs a, const int64_t* __restrict__ offs,
                                                               int64_t ntup, int64_t x0, void* __restrict__ out,
@@ -209,8 +209,10 @@ __global__ void __launch_bounds__(EXP_THREADS) k_light_expand(LightArgs a, const
       if (a.upper_only == 1 && z <= x) continue;  // SSJ keeps a < b only (apps.py:60)
       if (MODE == 0) {
         atomicOr(reinterpret_cast<uint32_t*>(out) + row * ld + (z >> 5), 1u << (z & 31));
-      } else {
+      } else if (MODE == 1) {
         atomicAdd(reinterpret_cast<int32_t*>(out) + row * ld + z, 1);
+      } else {   // uint16 counts, two per word (no carry: every count < 2^16)
+        atomicAdd(reinterpret_cast<unsigned int*>(out) + row * (ld >> 1) + (z >> 1), (z & 1) ? 0x10000u : 1u);
       }
     }
     __syncthreads();
@@ -278,14 +280,21 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32) k_bitmap_emit(const uint32_t*
   }
 }
 
-// count matrix (rows x ld int32, ld a multiple of CSEG, ncols valid): keep
-// cells with value >= min_count and (if upper_only) z > x.  One warp per
-// 1024-cell segment, which always lies inside one row; lane l loads cells
-// it*128 + 4l .. +3 (it = 0..7) as coalesced int4s.  Segments entirely at or
-// below the diagonal (upper_only) or right of ncols are never read - the
-// MMA leaves the former unwritten.
+// count matrix (rows x ld cells of int32 or uint16, ld a multiple of CSEG,
+// ncols valid): keep cells with value >= min_count (per-row max(min_count,
+// row_min[x])) that pass the cell filter.  One warp per 1024-cell segment,
+// which always lies inside one row; lane l loads VEC cells per int4 (4 int32
+// or 8 uint16), ITS coalesced int4s per lane.  Segments entirely at or below
+// the diagonal (filter 1) or right of ncols are never read - the MMA leaves
+// the former unwritten.
 constexpr int CSEG = 1024;   // cells per count segment
-constexpr int CIT = CSEG / 128;
+
+template <typename CellT>
+struct CellGeo {
+  static constexpr int VEC = 16 / (int)sizeof(CellT);    // cells per int4
+  static constexpr int ITS = CSEG / (32 * VEC);            // int4 loads per lane
+  static constexpr int FIELD = 32 * VEC >= 256 ? 16 : 8;   // bits of a per-iteration count field
+};
 
 struct CountSeg {
   int64_t row, col0;
@@ -300,24 +309,39 @@ __device__ __forceinline__ CountSeg count_seg(int64_t sgi, int64_t spr, int64_t 
   return g;
 }
 
-// keep flags of one lane's 4 cells of iteration `it` as a nibble
+template <typename CellT>
+__device__ __forceinline__ int32_t cell_of(int4 v, int j) {
+  const int32_t words[4] = {v.x, v.y, v.z, v.w};
+  if constexpr (sizeof(CellT) == 4) {
+    return words[j];
+  } else {
+    const uint32_t w = (uint32_t)words[j >> 1];
+    return (int32_t)((j & 1) ? (w >> 16) : (w & 0xFFFFu));   // low half = even column
+  }
+}
+
+// keep flags of one int4 of cells (VEC bits, cell j -> bit j)
 // cell filters: 0 every cell, 1 z > x (SSJ's a < b), 2 z != x (SCJ's a != b)
-__device__ __forceinline__ uint32_t keep_nibble(int4 v, int64_t col, int64_t x, int64_t ncols, int32_t min_count,
-                                                int filter) {
+template <typename CellT>
+__device__ __forceinline__ uint32_t keep_mask(int4 v, int64_t col, int64_t x, int64_t ncols, int32_t min_count,
+                                              int filter) {
   const int64_t lo = filter == 1 ? x + 1 : 0;   // first kept column
   const int64_t skip = filter == 2 ? x : -1;    // the one excluded column
   uint32_t m = 0;
-  m |= (v.x >= min_count && col + 0 >= lo && col + 0 < ncols && col + 0 != skip) ? 1u : 0u;
-  m |= (v.y >= min_count && col + 1 >= lo && col + 1 < ncols && col + 1 != skip) ? 2u : 0u;
-  m |= (v.z >= min_count && col + 2 >= lo && col + 2 < ncols && col + 2 != skip) ? 4u : 0u;
-  m |= (v.w >= min_count && col + 3 >= lo && col + 3 < ncols && col + 3 != skip) ? 8u : 0u;
+#pragma unroll
+  for (int j = 0; j < CellGeo<CellT>::VEC; ++j) {
+    const int64_t c = col + j;
+    m |= (cell_of<CellT>(v, j) >= min_count && c >= lo && c < ncols && c != skip) ? (1u << j) : 0u;
+  }
   return m;
 }
 
-__global__ void __launch_bounds__(256) k_count_seg_nnz(const int32_t* __restrict__ cnt, int64_t nseg, int64_t spr,
+template <typename CellT>
+__global__ void __launch_bounds__(256) k_count_seg_nnz(const CellT* __restrict__ cnt, int64_t nseg, int64_t spr,
                                                        int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
                                                        const int32_t* __restrict__ row_min, int upper_only,
                                                        int32_t* __restrict__ segcnt) {
+  using G = CellGeo<CellT>;
   const int lane = threadIdx.x & 31;
   for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
        sgi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -326,12 +350,13 @@ __global__ void __launch_bounds__(256) k_count_seg_nnz(const int32_t* __restrict
     if (g.live) {
       const int4* src = reinterpret_cast<const int4*>(cnt + g.row * ld + g.col0) + lane;
       const int32_t thr = row_min ? max(min_count, row_min[x0 + g.row]) : min_count;
-      int4 v[CIT];
+      int4 v[G::ITS];
 #pragma unroll
-      for (int it = 0; it < CIT; ++it) v[it] = __ldcs(src + it * 32);
+      for (int it = 0; it < G::ITS; ++it) v[it] = __ldcs(src + it * 32);
 #pragma unroll
-      for (int it = 0; it < CIT; ++it)
-        n += __popc(keep_nibble(v[it], g.col0 + it * 128 + lane * 4, x0 + g.row, ncols, thr, upper_only));
+      for (int it = 0; it < G::ITS; ++it)
+        n += __popc(keep_mask<CellT>(v[it], g.col0 + (it * 32 + lane) * G::VEC, x0 + g.row, ncols, thr,
+                                     upper_only));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
     }
@@ -339,11 +364,14 @@ __global__ void __launch_bounds__(256) k_count_seg_nnz(const int32_t* __restrict
   }
 }
 
-__global__ void __launch_bounds__(256) k_count_emit(const int32_t* __restrict__ cnt, int64_t nseg, int64_t spr,
+template <typename CellT>
+__global__ void __launch_bounds__(256) k_count_emit(const CellT* __restrict__ cnt, int64_t nseg, int64_t spr,
                                                     int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
                                                     int32_t min_count, const int32_t* __restrict__ row_min,
                                                     int upper_only, const int64_t* __restrict__ seg_off,
                                                     int64_t* __restrict__ codes, int32_t* __restrict__ counts) {
+  using G = CellGeo<CellT>;
+  constexpr uint64_t FMASK = (1ull << G::FIELD) - 1;
   const int lane = threadIdx.x & 31;
   for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
        sgi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -353,16 +381,16 @@ __global__ void __launch_bounds__(256) k_count_emit(const int32_t* __restrict__ 
     if (seg_off[sgi + 1] == base) continue;
     const int4* src = reinterpret_cast<const int4*>(cnt + g.row * ld + g.col0) + lane;
     const int32_t thr = row_min ? max(min_count, row_min[x0 + g.row]) : min_count;
-    int4 v[CIT];
+    int4 v[G::ITS];
 #pragma unroll
-    for (int it = 0; it < CIT; ++it) v[it] = __ldcs(src + it * 32);
-    // 8-bit count field per iteration, packed, warp-scanned in one pass
-    uint32_t nib[CIT];
+    for (int it = 0; it < G::ITS; ++it) v[it] = __ldcs(src + it * 32);
+    // a count field per iteration, packed, warp-scanned in one pass
+    uint32_t msk[G::ITS];
     uint64_t packed = 0;
 #pragma unroll
-    for (int it = 0; it < CIT; ++it) {
-      nib[it] = keep_nibble(v[it], g.col0 + it * 128 + lane * 4, x0 + g.row, ncols, thr, upper_only);
-      packed |= (uint64_t)__popc(nib[it]) << (8 * it);
+    for (int it = 0; it < G::ITS; ++it) {
+      msk[it] = keep_mask<CellT>(v[it], g.col0 + (it * 32 + lane) * G::VEC, x0 + g.row, ncols, thr, upper_only);
+      packed |= (uint64_t)__popc(msk[it]) << (G::FIELD * it);
     }
     uint64_t incl = packed;
 #pragma unroll
@@ -375,19 +403,18 @@ __global__ void __launch_bounds__(256) k_count_emit(const int32_t* __restrict__ 
     const int64_t code_row = (x0 + g.row) * dom_z + g.col0;
     int64_t it_base = base;
 #pragma unroll
-    for (int it = 0; it < CIT; ++it) {
-      uint32_t m = nib[it];
-      int64_t k = it_base + (int64_t)((excl >> (8 * it)) & 0xff);
-      const int32_t vals[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+    for (int it = 0; it < G::ITS; ++it) {
+      const uint32_t m = msk[it];
+      int64_t k = it_base + (int64_t)((excl >> (G::FIELD * it)) & FMASK);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < G::VEC; ++j) {
         if (m & (1u << j)) {
-          __stcs(codes + k, code_row + it * 128 + lane * 4 + j);
-          __stcs(counts + k, vals[j]);
+          __stcs(codes + k, code_row + (it * 32 + lane) * G::VEC + j);
+          __stcs(counts + k, cell_of<CellT>(v[it], j));
           ++k;
         }
       }
-      it_base += (int64_t)((tot >> (8 * it)) & 0xff);
+      it_base += (int64_t)((tot >> (G::FIELD * it)) & FMASK);
     }
   }
 }
@@ -469,8 +496,10 @@ int light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0, int
   const int grid = grid_for(work, EXP_SPAN, 8);
   if (mode == 0)
     k_light_expand<0><<<grid, EXP_THREADS, 0, st>>>(a, offs, ntup, x0, out, ld);
-  else
+  else if (mode == 1)
     k_light_expand<1><<<grid, EXP_THREADS, 0, st>>>(a, offs, ntup, x0, out, ld);
+  else
+    k_light_expand<2><<<grid, EXP_THREADS, 0, st>>>(a, offs, ntup, x0, out, ld);
   MMJ_CHECK_LAUNCH("k_light_expand");
   return MMJ_OK;
 }
@@ -514,29 +543,38 @@ static int count_grid(int64_t nseg) {
   return (int)(ctas < cap ? ctas : cap);
 }
 
-int count_segments(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
-                   const int32_t* row_min, int upper_only, int32_t* segcnt, int64_t* seg_off, void* ws,
-                   cudaStream_t st) {
+int count_segments(const void* cnt, int cell_bytes, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0,
+                   int32_t min_count, const int32_t* row_min, int upper_only, int32_t* segcnt, int64_t* seg_off,
+                   void* ws, cudaStream_t st) {
   MMJ_TRY(check_count_pitch(ld, ncols));
   const int64_t nseg = count_nseg(nrows * ld);
   if (nseg > 0) {
-    k_count_seg_nnz<<<count_grid(nseg), 256, 0, st>>>(cnt, nseg, ld / CSEG, ld, ncols, x0, min_count, row_min,
-                                                      upper_only,
-                                                      segcnt);
+    if (cell_bytes == 2)
+      k_count_seg_nnz<uint16_t><<<count_grid(nseg), 256, 0, st>>>(static_cast<const uint16_t*>(cnt), nseg, ld / CSEG,
+                                                                   ld, ncols, x0, min_count, row_min, upper_only,
+                                                                   segcnt);
+    else
+      k_count_seg_nnz<int32_t><<<count_grid(nseg), 256, 0, st>>>(static_cast<const int32_t*>(cnt), nseg, ld / CSEG, ld,
+                                                                  ncols, x0, min_count, row_min, upper_only, segcnt);
     MMJ_CHECK_LAUNCH("k_count_seg_nnz");
   }
   return scan_i32_i64(segcnt, seg_off, nseg, ws, st);
 }
 
-int count_emit(const int32_t* cnt, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
+int count_emit(const void* cnt, int cell_bytes, int64_t nrows, int64_t ld, int64_t ncols, int64_t x0, int64_t dom_z,
                int32_t min_count, const int32_t* row_min, int upper_only, const int64_t* seg_off, int64_t* codes,
                int32_t* counts, cudaStream_t st) {
   MMJ_TRY(check_count_pitch(ld, ncols));
   const int64_t nseg = count_nseg(nrows * ld);
   if (nseg == 0) return MMJ_OK;
-  k_count_emit<<<count_grid(nseg), 256, 0, st>>>(cnt, nseg, ld / CSEG, ld, ncols, x0, dom_z, min_count, row_min,
-                                                 upper_only,
-                                                 seg_off, codes, counts);
+  if (cell_bytes == 2)
+    k_count_emit<uint16_t><<<count_grid(nseg), 256, 0, st>>>(static_cast<const uint16_t*>(cnt), nseg, ld / CSEG, ld,
+                                                              ncols, x0, dom_z, min_count, row_min, upper_only,
+                                                              seg_off, codes, counts);
+  else
+    k_count_emit<int32_t><<<count_grid(nseg), 256, 0, st>>>(static_cast<const int32_t*>(cnt), nseg, ld / CSEG, ld,
+                                                             ncols, x0, dom_z, min_count, row_min, upper_only,
+                                                             seg_off, codes, counts);
   MMJ_CHECK_LAUNCH("k_count_emit");
   return MMJ_OK;
 }

@@ -106,7 +106,12 @@ class TwoPathEngine:
         self.lz_idx = None
         self._host_ldeg_r = host_left_deg_r
         self._host_ldeg_s = host_left_deg_s
-        row_bytes = (self.ldc * 4) if self.counts else (self.wpr * 4)
+        # uint16 count cells when no count can reach 2^16: a count is at most
+        # the smaller of the two left degrees (env MMJ_COUNT16=0 forces int32)
+        self.count16 = (self.counts and __import__("os").environ.get("MMJ_COUNT16", "1") != "0"
+                        and min(self._max_deg(host_left_deg_r, dr), self._max_deg(host_left_deg_s, ds)) < 65536)
+        self.cell_bytes = 2 if self.count16 else 4
+        row_bytes = (self.ldc * self.cell_bytes) if self.counts else (self.wpr * 4)
         if chunk_rows is None:
             budget = DEFAULT_COUNT_CHUNK_BYTES if self.counts else DEFAULT_BITMAP_CHUNK_BYTES
             chunk_rows = max(BM, (budget // max(row_bytes, 1)) // BM * BM)
@@ -220,9 +225,10 @@ class TwoPathEngine:
         dr, ds = self.dr, self.ds
         rows = x1 - x0
         if self.counts:
-            buf = self.ws.get("cnt", rows * self.ldc, torch.int32)
+            buf = self.ws.get("cnt", rows * self.ldc, torch.int16 if self.count16 else torch.int32)
             ld = self.ldc
-            mode = nat.MODE_COUNT32 | (nat.MODE_UPPER if self.cell_filter == 1 else 0)
+            mode = ((nat.MODE_COUNT16 if self.count16 else nat.MODE_COUNT32)
+                    | (nat.MODE_UPPER if self.cell_filter == 1 else 0))
         else:
             buf = self.ws.get("bm", rows * self.wpr, torch.int32)
             ld = self.wpr
@@ -252,7 +258,7 @@ class TwoPathEngine:
                  nat.ptr(lens), nat.ptr(offs), nat.ptr(self.ws.scan_ws(ntup)), st)
         nat.call("mmj_light_expand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), t0, ntup, nat.ptr(dr.left_deg),
                  self.d2, hp, nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, self.prefilter, int(self.upper_only),
-                 nat.ptr(offs), -1, 1 if self.counts else 0, x0, nat.ptr(buf), ld, st)
+                 nat.ptr(offs), -1, (2 if self.count16 else 1) if self.counts else 0, x0, nat.ptr(buf), ld, st)
         self._ph("light", False)
         # merge: segment sizes -> offsets -> codes
         self._ph("segments", True)
@@ -262,7 +268,8 @@ class TwoPathEngine:
             segcnt = self.ws.get("segcnt", nseg, torch.int32)
             segoff = self.ws.get("segoff", nseg + 1, torch.int64)
             rm = nat.ptr(self.row_min) if self.row_min is not None else 0
-            nat.call("mmj_count_segments", nat.ptr(buf), rows, self.ldc, self.dom_z, x0, self.min_count, rm,
+            nat.call("mmj_count_segments", nat.ptr(buf), self.cell_bytes, rows, self.ldc, self.dom_z, x0,
+                     self.min_count, rm,
                      self.cell_filter, nat.ptr(segcnt), nat.ptr(segoff), nat.ptr(self.ws.scan_ws(nseg)), st)
         else:
             nwords = rows * self.wpr
@@ -288,8 +295,8 @@ class TwoPathEngine:
         if self.counts:
             counts = self.ws.get("counts", cap, torch.int32)
             if cap:
-                nat.call("mmj_count_emit", nat.ptr(buf), rows, self.ldc, self.dom_z, x0, self.dom_z, self.min_count,
-                         rm, self.cell_filter, nat.ptr(segoff), nat.ptr(codes), nat.ptr(counts), st)
+                nat.call("mmj_count_emit", nat.ptr(buf), self.cell_bytes, rows, self.ldc, self.dom_z, x0, self.dom_z,
+                         self.min_count, rm, self.cell_filter, nat.ptr(segoff), nat.ptr(codes), nat.ptr(counts), st)
         elif cap:
             nat.call("mmj_bitmap_emit", nat.ptr(buf), rows * self.wpr, self.wpr, nat.ptr(segoff), x0, self.dom_z,
                      nat.ptr(codes), st)

@@ -186,13 +186,13 @@ class StarEngine:
                 nseg = int(self.lib.mmj_count_segment_count(ncell))
                 segcnt = self.ws.get("segcnt", nseg, torch.int32)
                 segoff = self.ws.get("segoff", nseg + 1, torch.int64)
-                nat.call("mmj_count_segments", nat.ptr(buf), rows, self.ldc, self.dk, x0, 1, 0, 0, nat.ptr(segcnt),
+                nat.call("mmj_count_segments", nat.ptr(buf), 4, rows, self.ldc, self.dk, x0, 1, 0, 0, nat.ptr(segcnt),
                          nat.ptr(segoff), nat.ptr(self.ws.scan_ws(nseg)), st)
                 total = int(segoff[nseg].item())
                 codes = self.ws.get("codes", total, torch.int64)
                 cnts = self.ws.get("counts", total, torch.int32)
                 if total:
-                    nat.call("mmj_count_emit", nat.ptr(buf), rows, self.ldc, self.dk, x0, self.dk, 1, 0, 0,
+                    nat.call("mmj_count_emit", nat.ptr(buf), 4, rows, self.ldc, self.dk, x0, self.dk, 1, 0, 0,
                              nat.ptr(segoff), nat.ptr(codes), nat.ptr(cnts), st)
                 if sink is not None:
                     sink(xa, xb, codes[:total], cnts[:total])
