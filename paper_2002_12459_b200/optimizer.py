@@ -229,7 +229,7 @@ class GpuCosts:
     witness_s_count: float = 7.3e-11
     cell_s: float = 1.03e-13
     cell_k_s: float = 2.27e-16
-    cell_k_s_count: float = 4.4e-16          # COUNT32 epilogue kernel (one cell per column)
+    cell_k_s_count: float = 7.0e-16          # count epilogue kernel, one cell per column (cfg4 slope)
     co: int = 1
 
     def heavy_seconds(self, u: int, k: int, w: int, pair: bool = True) -> float:
