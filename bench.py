@@ -419,7 +419,7 @@ def _e2e(args, r, s, plan, x_lo, x_hi, world):
 
     from paper_2002_12459_b200.joinproject import two_path_join_chunks
 
-    e2e_rows = min(args.chunk_rows, 2048)
+    e2e_rows = min(args.chunk_rows, int(os.environ.get("MMJ_E2E_ROWS", "4096")))
     host_out = torch.empty(e2e_rows * s.rel.dom_left, dtype=torch.int64, pin_memory=True)
     best = None
     h2d = d2h = 0
