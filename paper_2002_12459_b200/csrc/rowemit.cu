@@ -17,7 +17,8 @@
 //                 materialised keys), the merged tile is written back and the
 //                 popcount of every 32-word segment is recorded;
 //   (exclusive scan of the segment counts, scan.cu)
-//   k_emit        one warp per segment: prefix of the 32 word popcounts, the
+//   k_emit(_pf)   one warp per segment (the CTA's 32 segments of bitmap words and
+//                 offsets prefetched into shared memory first): prefix of the 32 word popcounts, the
 //                 lane's set bits staged as 32-bit cell offsets in a swizzled
 //                 shared buffer, then coalesced 16-byte streaming stores of
 //                 the int64 codes x*dom_z + z.
@@ -310,6 +311,67 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const uint32_t* __restri
 }
 
 
+// Prefetching variant: the CTA's SEGS x 32 bitmap words and SEGS + 1 segment
+// offsets are loaded up front by all threads (8 independent loads each) into
+// shared memory, so no warp waits on a DRAM round trip per segment.
+template <int SEGS>
+__global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf(const uint32_t* __restrict__ bm,
+                                                           const int64_t* __restrict__ segoff, int64_t nseg,
+                                                           int64_t segs_per_row, int64_t x0, int64_t dom_z,
+                                                           int64_t* __restrict__ codes) {
+  __shared__ __align__(16) uint32_t stage_all[EM_WARPS][1024];
+  __shared__ __align__(16) uint32_t sbits[SEGS * 32];
+  __shared__ int64_t soff[SEGS + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* stage = stage_all[warp];
+  auto sl = [](int k) { return k ^ ((k >> 5) & 31); };
+  const int64_t s0 = (int64_t)blockIdx.x * SEGS;
+  const int64_t nhere = min((int64_t)SEGS, nseg - s0);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(bm + s0 * 32);
+    uint4* dst = reinterpret_cast<uint4*>(sbits);
+    const int nq = (int)(nhere * 8);
+#pragma unroll 2
+    for (int i = threadIdx.x; i < nq; i += EM_WARPS * 32) dst[i] = __ldcs(src + i);
+    for (int i = threadIdx.x; i <= nhere; i += EM_WARPS * 32) soff[i] = segoff[s0 + i];
+  }
+  __syncthreads();
+  for (int si = warp; si < nhere; si += EM_WARPS) {
+    const int64_t s = s0 + si;
+    uint32_t word = sbits[si * 32 + lane];
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const int64_t row = s / segs_per_row;
+    const int64_t base = (x0 + row) * dom_z + (s - row * segs_per_row) * 1024;
+    const uint32_t off0 = lane * 32;
+    int k = incl - c;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      stage[sl(k)] = off0 + b;
+      ++k;
+      word &= word - 1;
+    }
+    __syncwarp();
+    int64_t* out = codes + soff[si];
+    const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
+    if (lane < h) st_cs(out + lane, base + stage[sl(lane)]);
+    const int np = (tot - h) >> 1;
+    for (int p = lane; p < np; p += 32) {
+      const int i = h + 2 * p;
+      st_cs2(out + i, base + stage[sl(i)], base + stage[sl(i + 1)]);
+    }
+    const int done = h + 2 * np;
+    if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(done + lane)]);
+    __syncwarp();
+  }
+}
+
 void tile_geometry(int64_t wpr, int& G, int& cb, int& ncb) {
   if (wpr <= TILE_WORDS) {
     G = (int)(TILE_WORDS / wpr);
@@ -388,6 +450,21 @@ int emit_codes(const uint32_t* bm, const int64_t* segoff, int64_t rows, int64_t 
   if (segs < 0) {
     const char* e = getenv("MMJ_EMIT_SEGS");   // A/B knob: segments per emission CTA
     segs = e ? atoi(e) : EM_SEGS;
+  }
+  static int ver = -1;
+  if (ver < 0) {
+    const char* e = getenv("MMJ_EMIT_V");   // 1: the round-1 kernel without prefetch (A/B reference)
+    ver = e ? atoi(e) : 2;
+  }
+  if (ver == 2) {
+    if (!getenv("MMJ_EMIT_SEGS") || segs == 32)
+      k_emit_pf<32><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes);
+    else if (segs == 16)
+      k_emit_pf<16><<<(unsigned)ceil_div(nseg, 16), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes);
+    else
+      k_emit_pf<64><<<(unsigned)ceil_div(nseg, 64), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes);
+    MMJ_CHECK_LAUNCH("k_emit_pf");
+    return MMJ_OK;
   }
   switch (segs) {
     case 8: k_emit<8><<<(unsigned)ceil_div(nseg, 8), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes); break;
