@@ -372,6 +372,66 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf(const uint32_t* __res
   }
 }
 
+// Same as k_emit_pf with 16-bit staging (cell offsets < 1024): half the
+// shared memory per CTA, so 8 CTAs (64 warps) fit per SM instead of 6.  Element
+// i is staged at slot i + h (h = the output's 16-B misalignment) so every
+// stored pair is one aligned 32-bit shared load.
+template <int SEGS>
+__global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf16(const uint32_t* __restrict__ bm,
+                                                             const int64_t* __restrict__ segoff, int64_t nseg,
+                                                             int64_t segs_per_row, int64_t x0, int64_t dom_z,
+                                                             int64_t* __restrict__ codes) {
+  __shared__ __align__(16) uint16_t stage_all[EM_WARPS][1024 + 8];
+  __shared__ __align__(16) uint32_t sbits[SEGS * 32];
+  __shared__ int64_t soff[SEGS + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint16_t* stage = stage_all[warp];
+  const int64_t s0 = (int64_t)blockIdx.x * SEGS;
+  const int64_t nhere = min((int64_t)SEGS, nseg - s0);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(bm + s0 * 32);
+    uint4* dst = reinterpret_cast<uint4*>(sbits);
+    const int nq = (int)(nhere * 8);
+#pragma unroll 2
+    for (int i = threadIdx.x; i < nq; i += EM_WARPS * 32) dst[i] = __ldcs(src + i);
+    for (int i = threadIdx.x; i <= nhere; i += EM_WARPS * 32) soff[i] = segoff[s0 + i];
+  }
+  __syncthreads();
+  for (int si = warp; si < nhere; si += EM_WARPS) {
+    const int64_t s = s0 + si;
+    uint32_t word = sbits[si * 32 + lane];
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const int64_t row = s / segs_per_row;
+    const int64_t base = (x0 + row) * dom_z + (s - row * segs_per_row) * 1024;
+    int64_t* out = codes + soff[si];
+    const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
+    const uint32_t off0 = lane * 32;
+    uint16_t* st = stage + h + (incl - c);
+    while (word) {
+      const int b = __ffs(word) - 1;
+      *st++ = (uint16_t)(off0 + b);
+      word &= word - 1;
+    }
+    __syncwarp();
+    if (lane < h) st_cs(out, base + stage[h]);
+    const int np = (tot - h) >> 1;
+    for (int p = lane; p < np; p += 32) {
+      const uint32_t two = *reinterpret_cast<const uint32_t*>(stage + 2 * h + 2 * p);
+      st_cs2(out + h + 2 * p, base + (two & 0xFFFFu), base + (two >> 16));
+    }
+    const int done = h + 2 * np;
+    if (lane < tot - done) st_cs(out + done + lane, base + stage[h + done + lane]);
+    __syncwarp();
+  }
+}
+
 void tile_geometry(int64_t wpr, int& G, int& cb, int& ncb) {
   if (wpr <= TILE_WORDS) {
     G = (int)(TILE_WORDS / wpr);
@@ -453,8 +513,20 @@ int emit_codes(const uint32_t* bm, const int64_t* segoff, int64_t rows, int64_t 
   }
   static int ver = -1;
   if (ver < 0) {
-    const char* e = getenv("MMJ_EMIT_V");   // 1: the round-1 kernel without prefetch (A/B reference)
-    ver = e ? atoi(e) : 2;
+    // 3 (default): prefetch + 16-bit staging; 2: prefetch + 32-bit staging;
+    // 1: the round-1 kernel without prefetch (A/B references)
+    const char* e = getenv("MMJ_EMIT_V");
+    ver = e ? atoi(e) : 3;
+  }
+  if (ver == 3) {
+    if (getenv("MMJ_EMIT_SEGS") && segs == 64)
+      k_emit_pf16<64><<<(unsigned)ceil_div(nseg, 64), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z,
+                                                                              codes);
+    else
+      k_emit_pf16<32><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z,
+                                                                              codes);
+    MMJ_CHECK_LAUNCH("k_emit_pf16");
+    return MMJ_OK;
   }
   if (ver == 2) {
     if (!getenv("MMJ_EMIT_SEGS") || segs == 32)
