@@ -372,11 +372,12 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf(const uint32_t* __res
   }
 }
 
-// Same as k_emit_pf with 16-bit staging (cell offsets < 1024): half the
+// Same as k_emit_pf with 16-bit staging (cell offsets < 1024) and a
+// branch-free bit-slice expansion for dense words: half the
 // shared memory per CTA, so 8 CTAs (64 warps) fit per SM instead of 6.  Element
 // i is staged at slot i + h (h = the output's 16-B misalignment) so every
 // stored pair is one aligned 32-bit shared load.
-template <int SEGS>
+template <int SEGS, bool BITSLICE>
 __global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf16(const uint32_t* __restrict__ bm,
                                                              const int64_t* __restrict__ segoff, int64_t nseg,
                                                              int64_t segs_per_row, int64_t x0, int64_t dom_z,
@@ -386,6 +387,10 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf16(const uint32_t* __r
   __shared__ int64_t soff[SEGS + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint16_t* stage = stage_all[warp];
+  // slot of element k: XOR bits 1-5 with bits 5-9 so the 32 lanes' runs (one
+  // per 32-cell word, up to 32 long) fall in 32 different banks even when the
+  // words are full; bit 0 is kept, so an even/odd pair shares one 32-bit word
+  auto sl = [](int k) { return k ^ (((k >> 5) & 31) << 1); };
   const int64_t s0 = (int64_t)blockIdx.x * SEGS;
   const int64_t nhere = min((int64_t)SEGS, nseg - s0);
   {
@@ -413,21 +418,35 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf16(const uint32_t* __r
     int64_t* out = codes + soff[si];
     const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
     const uint32_t off0 = lane * 32;
-    uint16_t* st = stage + h + (incl - c);
-    while (word) {
-      const int b = __ffs(word) - 1;
-      *st++ = (uint16_t)(off0 + b);
-      word &= word - 1;
+    int k = h + (incl - c);
+    // dense words (the warp's fullest lane >= 10 bits): the branch-free bit
+    // slice; sparse ones: the ffs loop (warp-uniform choice)
+    if (BITSLICE && __reduce_max_sync(0xffffffffu, (unsigned)c) >= 10u) {
+      // branch-free: 32 predicated 16-bit stores, independent of the density
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        if (word & (1u << b)) {
+          stage[sl(k)] = (uint16_t)(off0 + b);
+          ++k;
+        }
+      }
+    } else {
+      while (word) {
+        const int b = __ffs(word) - 1;
+        stage[sl(k)] = (uint16_t)(off0 + b);
+        ++k;
+        word &= word - 1;
+      }
     }
     __syncwarp();
-    if (lane < h) st_cs(out, base + stage[h]);
+    if (lane < h) st_cs(out, base + stage[sl(h)]);
     const int np = (tot - h) >> 1;
     for (int p = lane; p < np; p += 32) {
-      const uint32_t two = *reinterpret_cast<const uint32_t*>(stage + 2 * h + 2 * p);
+      const uint32_t two = *reinterpret_cast<const uint32_t*>(stage + sl(2 * h + 2 * p));
       st_cs2(out + h + 2 * p, base + (two & 0xFFFFu), base + (two >> 16));
     }
     const int done = h + 2 * np;
-    if (lane < tot - done) st_cs(out + done + lane, base + stage[h + done + lane]);
+    if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(h + done + lane)]);
     __syncwarp();
   }
 }
@@ -519,12 +538,20 @@ int emit_codes(const uint32_t* bm, const int64_t* segoff, int64_t rows, int64_t 
     ver = e ? atoi(e) : 3;
   }
   if (ver == 3) {
-    if (getenv("MMJ_EMIT_SEGS") && segs == 64)
-      k_emit_pf16<64><<<(unsigned)ceil_div(nseg, 64), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z,
+    static int bs = -1;
+    if (bs < 0) {
+      const char* e = getenv("MMJ_EMIT_BITSLICE");
+      bs = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (bs)
+      k_emit_pf16<32, true><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0,
+                                                                                    dom_z, codes);
+    else if (getenv("MMJ_EMIT_SEGS") && segs == 64)
+      k_emit_pf16<64, false><<<(unsigned)ceil_div(nseg, 64), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z,
                                                                               codes);
     else
-      k_emit_pf16<32><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z,
-                                                                              codes);
+      k_emit_pf16<32, false><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0,
+                                                                                     dom_z, codes);
     MMJ_CHECK_LAUNCH("k_emit_pf16");
     return MMJ_OK;
   }
