@@ -62,6 +62,19 @@ class EngineStats:
     extra: dict = field(default_factory=dict)
 
 
+_STREAMS: dict = {}
+
+
+def _stream_pair(tag: str):
+    """(low-priority, high-priority) CUDA streams of the current device, created
+    once per process (stream creation costs more than a small join)."""
+    import torch
+    key = (tag, torch.cuda.current_device())
+    if key not in _STREAMS:
+        _STREAMS[key] = (torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1))
+    return _STREAMS[key]
+
+
 class TwoPathEngine:
     """Device state for one (R, S, plan) two-path evaluation."""
 
@@ -366,8 +379,7 @@ class TwoPathEngine:
             # the in-order merge -> scan -> emit chain is the critical path: give
             # it the high-priority stream so its CTAs are scheduled ahead of the
             # side-stream heavy product's
-            self._mma_stream = torch.cuda.Stream(priority=0)
-            self._main_stream = torch.cuda.Stream(priority=-1)
+            self._mma_stream, self._main_stream = _stream_pair("mma_ahead")
         ms = self._mma_stream
         main = self._main_stream
         main.wait_stream(caller)
@@ -462,8 +474,7 @@ class TwoPathEngine:
             # low-priority stream; the heavy product / merge / scan chain of
             # the next chunk on a high-priority one, so its CTAs are placed
             # first whenever emission CTAs retire
-            self._emit_stream = torch.cuda.Stream(priority=0)
-            self._work_stream = torch.cuda.Stream(priority=-1)
+            self._emit_stream, self._work_stream = _stream_pair("pipelined")
         es = self._emit_stream
         main = self._work_stream
         main.wait_stream(caller)
