@@ -37,11 +37,8 @@ constexpr int TM_THREADS = 256;
 constexpr int TUP_BATCH = TM_THREADS;   // light tuples staged per round
 constexpr int TILE_WORDS = 16384;       // up to 64 KB of bitmap per tile (whole rows up to 524288 cells)
 constexpr int SHORT_LIST = 96;          // lists up to this length are filtered, longer ones bisected
-// no minimum-CTA bound for the emission: forcing 6 or 8 resident CTAs per SM
-// (40 / 32 registers) measured 1-4% slower than the unconstrained 48 registers
-#ifndef EMIT_MIN_CTAS
-#define EMIT_MIN_CTAS 1
-#endif
+// (the emission kernel has no minimum-CTA bound: forcing 6 or 8 resident CTAs
+// per SM (40 / 32 registers) measured 1-4% slower than ptxas's 48 registers)
 constexpr int MERGE_ILP = 8;            // witness slots per thread per step of the merge
 constexpr int EM_WARPS = 8;
 constexpr int EM_SEGS = 64;             // segments per emission CTA (8 per warp: balances uneven row densities)
@@ -383,7 +380,7 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf(const uint32_t* __res
 // i is staged at slot i + h (h = the output's 16-B misalignment) so every
 // stored pair is one aligned 32-bit shared load.
 template <int SEGS, bool BITSLICE>
-__global__ void __launch_bounds__(EM_WARPS * 32, EMIT_MIN_CTAS) k_emit_pf16(const uint32_t* __restrict__ bm,
+__global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf16(const uint32_t* __restrict__ bm,
                                                              const int64_t* __restrict__ segoff, int64_t nseg,
                                                              int64_t segs_per_row, int64_t x0, int64_t dom_z,
                                                              int64_t* __restrict__ codes) {
