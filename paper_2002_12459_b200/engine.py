@@ -48,6 +48,7 @@ class ChunkResult:
     codes: object            # torch int64 view (device)
     counts: Optional[object]  # torch int32 view (device) or None
     light: int
+    total_dev: Optional[object] = None   # async chunks: device int64[1] holding n
 
 
 @dataclass
@@ -229,7 +230,7 @@ class TwoPathEngine:
         if self.timer is not None:
             (self.timer.start if start else self.timer.stop)(name)
 
-    def run_chunk(self, x0: int, x1: int, sync: bool = True) -> ChunkResult:
+    def run_chunk(self, x0: int, x1: int, sync: bool = True, codes_key: str = "codes") -> ChunkResult:
         """Evaluate output rows [x0, x1).  With ``sync=False`` no host sync
         happens: the code buffer is sized for the worst case (rows*dom_z) and
         the chunk's sizes are fetched later by :meth:`finish`."""
@@ -255,7 +256,7 @@ class TwoPathEngine:
             buf.zero_()
         self._ph("heavy_mma", False)
         if self.fused:
-            return self._fused_tail(x0, x1, rows, buf, sync)
+            return self._fused_tail(x0, x1, rows, buf, sync, codes_key)
         # light passes (x-driven; FULL_JOIN when hpos is None)
         t0 = int(dr.fwd_ptr_host[x0])
         t1 = int(dr.fwd_ptr_host[x1])
@@ -321,7 +322,7 @@ class TwoPathEngine:
         self.stats.out_size += total
         return ChunkResult(x0, x1, total, codes[:total], None if counts is None else counts[:total], light)
 
-    def _fused_tail(self, x0, x1, rows, buf, sync):
+    def _fused_tail(self, x0, x1, rows, buf, sync, codes_key="codes"):
         """Light witnesses merged into the bitmap tile by tile, segment scan,
         emission (mmj_tile_merge -> mmj_exclusive_scan_i32 -> mmj_emit_codes)."""
         torch = self.torch
@@ -347,7 +348,7 @@ class TwoPathEngine:
             cap = total
         else:
             cap = rows * self.dom_z
-        codes = self.ws.get("codes", cap, torch.int64)
+        codes = self.ws.get(codes_key, cap, torch.int64)
         self._ph("emit", True)
         if cap:
             nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dom_z,
@@ -357,7 +358,7 @@ class TwoPathEngine:
         if not sync:
             slot = self._async_slot()
             slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
-            return ChunkResult(x0, x1, -1, codes, None, -1)
+            return ChunkResult(x0, x1, -1, codes, None, -1, slot[0:1])
         light = int(self.wit.item()) - wit0
         self.stats.out_size += total
         return ChunkResult(x0, x1, total, codes[:total], None, light)

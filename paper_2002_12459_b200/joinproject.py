@@ -181,6 +181,10 @@ def two_path_join_chunks(r, s, plan: Optional[ThresholdPlan] = None, want_counts
         eng.h2d_bytes = 0
     eng.prepare()
     lo, hi = (0, r.rel.dom_left) if x_range is None else x_range
+    if isinstance(host_buffer, (tuple, list)) and not want_counts and eng.fused:
+        yield from _pipelined_to_host(eng, list(eng.chunk_bounds(lo, hi)), host_buffer, dims, plan)
+        eng.finish()
+        return
     for x0, x1 in eng.chunk_bounds(lo, hi):
         ch = eng.run_chunk(x0, x1)
         if device_output:
@@ -203,6 +207,64 @@ def two_path_join_chunks(r, s, plan: Optional[ThresholdPlan] = None, want_counts
 
 
 _D2H_STREAMS = []
+
+
+def _pipelined_to_host(eng, bounds, host_bufs, dims, plan):
+    """Projection chunks into two pinned host buffers: chunk i+1 is computed
+    (into the other device code buffer) while chunk i's codes cross PCIe on
+    the copy streams, so the link never waits for the GPU."""
+    import torch
+    if len(host_bufs) != 2:
+        raise ValueError("host_buffer must be one pinned tensor or a pair of them")
+    cur = torch.cuda.current_stream()
+    tot = torch.empty(2, dtype=torch.int64, pin_memory=True)
+
+    def launch(i):
+        x0, x1 = bounds[i]
+        ch = eng.run_chunk(x0, x1, sync=False, codes_key=f"codes{i & 1}")
+        tot[i & 1:(i & 1) + 1].copy_(ch.total_dev, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        return x0, x1, ch.codes, ev
+
+    nxt = launch(0) if bounds else None
+    for i in range(len(bounds)):
+        x0, x1, codes, ev = nxt
+        ev.synchronize()
+        n = int(tot[i & 1])
+        hb = host_bufs[i & 1]
+        if n > hb.numel():
+            raise ValueError("host_buffer smaller than a chunk's output")
+        done = _d2h_split_async(hb[:n], codes[:n], ev) if n else []
+        if i + 1 < len(bounds):
+            nxt = launch(i + 1)
+        for e in done:
+            e.synchronize()
+        eng.stats.out_size += n
+        yield OutputSet(hb[:n].numpy(), dims, None, {"x_range": (x0, x1), "plan": plan,
+                                                       "h2d_bytes": eng.h2d_bytes})
+
+
+def _d2h_split_async(host, dev, after, parts: int = 4):
+    """Start `parts` concurrent device -> pinned host copies once event `after`
+    has fired; returns their completion events."""
+    import torch
+    while len(_D2H_STREAMS) < parts:
+        _D2H_STREAMS.append(torch.cuda.Stream())
+    n = dev.numel()
+    step = -(-n // parts)
+    evs = []
+    for i in range(parts):
+        if i * step >= n:
+            break
+        s = _D2H_STREAMS[i]
+        s.wait_event(after)
+        with torch.cuda.stream(s):
+            host[i * step:(i + 1) * step].copy_(dev[i * step:(i + 1) * step], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(s)
+        evs.append(e)
+    return evs
 
 
 def _d2h_split(host, dev, parts: int = 4):
