@@ -188,22 +188,43 @@ def _int8_peak_measure():
 
 
 # ----------------------------------------------------------------- CPU legs
-def _oracle_slice(wl, r, x_lo: int, nx: int):
+def _oracle_slice(wl, r, x_lo: int, nx: int, barrier=None):
     """Oracle two_path on sigma_{x in X'} R (X' = nx consecutive dense x) and S,
-    pre-reduced (untimed); returns (elapsed_s, |OUT|)."""
+    pre-reduced (untimed); returns (elapsed_s, |OUT|).  Single-threaded: BLAS
+    pools are limited to one thread so `cores` is exact.  With `barrier`,
+    all workers of a parallel step start the timed operator together."""
+    from threadpoolctl import threadpool_limits
+
     from oracle import mmjoin_oracle as o
     lv = np.asarray(r.rel.left_values)
     xs = lv[x_lo:x_lo + nx]
     Rraw = wl.relations[0]
     sel = Rraw[np.isin(Rraw[:, 0], xs)]
     Sraw = wl.relations[0] if wl.self_join else wl.relations[1]
-    a, b = o.semi_join_many([o.encode(sel), o.encode(Sraw)])
-    t0 = time.perf_counter()
-    res = o.two_path(a, b, None)
-    return time.perf_counter() - t0, len(res.codes)
+    with threadpool_limits(limits=1):
+        a, b = o.semi_join_many([o.encode(sel), o.encode(Sraw)])
+        if barrier is not None:
+            barrier.wait()
+        t0 = time.perf_counter()
+        res = o.two_path(a, b, None)
+        dt = time.perf_counter() - t0
+    return dt, len(res.codes)
+
+
+_REF = {}
+
+
+def _ref_worker(args):
+    x_lo, nx = args
+    return _oracle_slice(_REF["wl"], _REF["r"], x_lo, nx, _REF["barrier"])
 
 
 def run_reference(args):
+    """The reference's CPU implementation of the path (the pinned oracle port)
+    on every host core: each step runs one x-slice per core in parallel
+    single-threaded worker processes (their timed operators start together);
+    step time = the slowest worker, throughput = all slices' tuples / that."""
+    import multiprocessing as mp
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -216,26 +237,29 @@ def run_reference(args):
     class _I:   # minimal stand-in exposing rel.left_values for slicing
         rel = R
     nx = args.ref_slice_x
-    offsets = np.linspace(0, max(dom - nx, 0), args.warmup + args.steps + 1).astype(np.int64)
-    for i in range(args.warmup):
-        _oracle_slice(wl, _I, int(offsets[i]), nx)
+    cores = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
+    ctx = mp.get_context("fork")
+    _REF.update(wl=wl, r=_I, barrier=ctx.Barrier(cores))
+    nsl = (args.warmup + args.steps) * cores
+    offsets = np.linspace(0, max(dom - nx, 0), nsl + 1).astype(np.int64)
     tt, nout = 0.0, 0
-    for i in range(args.steps):
-        dt, n = _oracle_slice(wl, _I, int(offsets[args.warmup + i]), nx)
-        tt += dt
-        nout += n
+    with ctx.Pool(cores) as pool:
+        for it in range(args.warmup + args.steps):
+            batch = [(int(offsets[it * cores + k]), nx) for k in range(cores)]
+            res = pool.map(_ref_worker, batch, chunksize=1)
+            if it >= args.warmup:
+                tt += max(dt for dt, _ in res)
+                nout += sum(n for _, n in res)
     v = nout / tt if tt > 0 else 0.0
-    cores = os.cpu_count()
     line = {
         "metric": METRIC, "impl": "reference", "value": v, "unit": "tuples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(args.steps, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{args.config} x-slices of {nx} dense x (two_path_join, default plan)",
-                   "config_name": args.config},
+        "config": {"workload": f"{args.config} x-slices of {nx} dense x (two_path_join, default plan), "
+                               f"{cores} in parallel per step", "config_name": args.config},
         "cpu_baseline": {"value": v, "unit": "tuples/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} x-slices of {nx} consecutive dense x values, "
-                                   f"{nout} distinct output tuples; 1 Python thread + numpy/OpenBLAS "
-                                   f"({cores} host threads available)"},
+                         "sample": f"{args.steps} steps x {cores} x-slices of {nx} consecutive dense x values, "
+                                   f"{nout} distinct output tuples; {cores} single-threaded worker processes"},
         "e2e": {"value": v, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -380,9 +404,9 @@ def run_b200(args):
         nx = 64
         mid = (x_lo + x_hi) // 2
         dt, n = _oracle_slice(wl, r, mid, nx)
-        cpu = {"value": n / dt, "unit": "tuples/s", "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": n / dt, "unit": "tuples/s", "cores": 1, "kind": "port",
                "sample": f"oracle two_path_join (default plan) on the {nx} dense x values starting at {mid}: "
-                         f"{n} distinct tuples in {dt:.2f} s; 1 Python thread + numpy/OpenBLAS"}
+                         f"{n} distinct tuples in {dt:.2f} s; one thread (BLAS limited to 1)"}
 
     # ---- end to end through the public API with host buffers
     e2e = None
