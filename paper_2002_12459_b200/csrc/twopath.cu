@@ -336,6 +336,32 @@ __device__ __forceinline__ uint32_t keep_mask(int4 v, int64_t col, int64_t x, in
   return m;
 }
 
+// interior segments (no cell filter or pitch edge inside): value test only,
+// two uint16 cells per SIMD compare
+template <typename CellT>
+__device__ __forceinline__ uint32_t keep_mask_fast(int4 v, int32_t thr) {
+  if constexpr (sizeof(CellT) == 4) {
+    return (uint32_t)(v.x >= thr) | ((uint32_t)(v.y >= thr) << 1) | ((uint32_t)(v.z >= thr) << 2) |
+           ((uint32_t)(v.w >= thr) << 3);
+  } else {
+    if (thr > 65535) return 0u;
+    const uint32_t t2 = (uint32_t)thr * 0x00010001u;
+    const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = __vcmpgeu2(w[k], t2);
+      m |= ((c & 1u) | ((c >> 15) & 2u)) << (2 * k);
+    }
+    return m;
+  }
+}
+
+__device__ __forceinline__ bool interior_seg(const CountSeg& g, int64_t x, int64_t ncols, int filter) {
+  const int64_t lo = filter == 1 ? x + 1 : 0;
+  return g.col0 >= lo && g.col0 + CSEG <= ncols && !(filter == 2 && x >= g.col0 && x < g.col0 + CSEG);
+}
+
 template <typename CellT>
 __global__ void __launch_bounds__(256) k_count_seg_nnz(const CellT* __restrict__ cnt, int64_t nseg, int64_t spr,
                                                        int64_t ld, int64_t ncols, int64_t x0, int32_t min_count,
@@ -353,10 +379,15 @@ __global__ void __launch_bounds__(256) k_count_seg_nnz(const CellT* __restrict__
       int4 v[G::ITS];
 #pragma unroll
       for (int it = 0; it < G::ITS; ++it) v[it] = __ldcs(src + it * 32);
+      if (interior_seg(g, x0 + g.row, ncols, upper_only)) {
 #pragma unroll
-      for (int it = 0; it < G::ITS; ++it)
-        n += __popc(keep_mask<CellT>(v[it], g.col0 + (it * 32 + lane) * G::VEC, x0 + g.row, ncols, thr,
-                                     upper_only));
+        for (int it = 0; it < G::ITS; ++it) n += __popc(keep_mask_fast<CellT>(v[it], thr));
+      } else {
+#pragma unroll
+        for (int it = 0; it < G::ITS; ++it)
+          n += __popc(keep_mask<CellT>(v[it], g.col0 + (it * 32 + lane) * G::VEC, x0 + g.row, ncols, thr,
+                                       upper_only));
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
     }
@@ -387,9 +418,12 @@ __global__ void __launch_bounds__(256) k_count_emit(const CellT* __restrict__ cn
     // a count field per iteration, packed, warp-scanned in one pass
     uint32_t msk[G::ITS];
     uint64_t packed = 0;
+    const bool inner = interior_seg(g, x0 + g.row, ncols, upper_only);
 #pragma unroll
     for (int it = 0; it < G::ITS; ++it) {
-      msk[it] = keep_mask<CellT>(v[it], g.col0 + (it * 32 + lane) * G::VEC, x0 + g.row, ncols, thr, upper_only);
+      msk[it] = inner ? keep_mask_fast<CellT>(v[it], thr)
+                      : keep_mask<CellT>(v[it], g.col0 + (it * 32 + lane) * G::VEC, x0 + g.row, ncols, thr,
+                                         upper_only);
       packed |= (uint64_t)__popc(msk[it]) << (G::FIELD * it);
     }
     uint64_t incl = packed;
