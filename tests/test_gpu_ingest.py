@@ -118,3 +118,28 @@ def test_bsi_on_device_ingested(oracle, shared):
     for hb in (128, 512):
         got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], heavy_bits=hb)
         assert np.array_equal(got, exp), hb
+
+
+def test_ingest_from_cuda_tensor_and_errors(oracle):
+    import torch
+    from paper_2002_12459_b200 import _native as nat
+    from paper_2002_12459_b200.ingest import from_raw_pairs_device
+    raw = _raw(np.random.default_rng(99), 5000, -1000, 1000)
+    _check(from_raw_pairs_device("R", torch.from_numpy(raw).cuda()), oracle.encode(raw))
+    # a workspace smaller than mmj_ingest_workspace_bytes(n) is an argument error
+    t = torch.from_numpy(raw).cuda()
+    out = torch.empty_like(t)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        nat.call("mmj_ingest_dedup", nat.ptr(t), t.shape[0], nat.ptr(out), nat.ptr(cnt), nat.ptr(ws), 16,
+                 nat.stream_handle())
+    buf = torch.zeros(1024, dtype=torch.int32, device="cuda")
+    seg = torch.zeros(2, dtype=torch.int32, device="cuda")
+    off = torch.zeros(3, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):   # cell_bytes must be 2 or 4
+        nat.call("mmj_count_segments", nat.ptr(buf), 3, 1, 1024, 1000, 0, 1, 0, 0, nat.ptr(seg), nat.ptr(off),
+                 nat.ptr(ws), nat.stream_handle())
+    with pytest.raises(ValueError):   # pitch not a multiple of 1024
+        nat.call("mmj_count_segments", nat.ptr(buf), 4, 1, 1000, 1000, 0, 1, 0, 0, nat.ptr(seg), nat.ptr(off),
+                 nat.ptr(ws), nat.stream_handle())
