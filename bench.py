@@ -470,9 +470,31 @@ def _e2e(args, r, s, plan, x_lo, x_hi, world):
         d2h = 8 * nout
         v = nout / dt
         best = v if best is None else max(best, v)
-    return {"value": best, "unit": "tuples/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "steps": args.e2e_steps,
-            "api": "joinproject.two_path_join_chunks(upload='fresh', host_buffer=(pinned, pinned))"}
+    out = {"value": best, "unit": "tuples/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+           "steps": args.e2e_steps,
+           "api": "joinproject.two_path_join_chunks(upload='fresh', host_buffer=(pinned, pinned))"}
+    # informational: the same public call with the output consumed on the
+    # device (device_output=True, only each chunk's size read back): what a
+    # GPU-side consumer of the join sees, inputs still uploaded every step
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    nout = 0
+    for part in two_path_join_chunks(r, s, plan, chunk_rows=args.chunk_rows, device_output=True, upload="fresh",
+                                     x_range=(x_lo, x_hi)):
+        nout += int(part.codes.numel())
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt, float(nout)], dtype=torch.float64, device="cuda")
+        tm = t[:1].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ts = t[1:].clone()
+        dist.all_reduce(ts, op=dist.ReduceOp.SUM)
+        dt, nout = float(tm.item()), int(ts.item())
+    out["device_output"] = {"value": nout / dt, "unit": "tuples/s", "h2d_bytes_per_step": int(h2d),
+                            "d2h_bytes_per_step": 8 * ((x_hi - x_lo) // max(args.chunk_rows, 1) + 1),
+                            "api": "joinproject.two_path_join_chunks(upload='fresh', device_output=True)"}
+    return out
 
 
 def main():
