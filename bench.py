@@ -55,6 +55,7 @@ def _args():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-light-work", action="store_true", help="skip the light-pass byte count (diagnostic)")
     ap.add_argument("--ref-slice-x", type=int, default=32, help="x values per reference-arm sample")
     ap.add_argument("--x-limit", type=int, default=0, help="debug: only the first X output rows")
     ap.add_argument("--schedule", default="serial", choices=["serial", "mma_ahead", "pipelined"],
@@ -87,6 +88,58 @@ def _plan(args, r, s):
         return default_plan(r, s)
     d1, d2 = (int(v) for v in args.plan.split(","))
     return ThresholdPlan(PARTITIONED, d1, d2)
+
+
+def _light_work(eng, r, s, x_lo: int, x_hi: int):
+    """SURVEY.md 8(d) algorithmic bytes of the light passes over rows
+    [x_lo, x_hi): B_light = 8 N_Rl + 4 A_l + 8 D_l.
+
+    N_Rl: R tuples that drive a light list (joinproject.py:183-203 restated
+    x-side: the full S.rev(y) when y is light or x is light, the light-z part
+    of S.rev(y) otherwise); A_l: total length of the distinct lists touched,
+    each once; D_l: distinct light (x, z) keys, counted on the device by
+    merging the light witnesses alone (k_tile_merge with no heavy bits, outside
+    the timed region)."""
+    import torch
+    from paper_2002_12459_b200 import _native as nat
+    from paper_2002_12459_b200.optimizer import PARTITIONED
+    t0, t1 = int(r.fwd_indptr[x_lo]), int(r.fwd_indptr[x_hi])
+    ys = np.asarray(r.fwd_indices[t0:t1], dtype=np.int64)
+    xs = np.repeat(np.arange(x_lo, x_hi, dtype=np.int64), np.diff(r.fwd_indptr[x_lo:x_hi + 1]))
+    sdeg_y = np.asarray(s.right_deg, dtype=np.int64)
+    if eng.strategy == PARTITIONED and eng.hpos is not None:
+        heavy_y = eng.hpos.cpu().numpy()[: len(sdeg_y)] >= 0
+        full = (~heavy_y[ys]) | (np.asarray(r.left_deg)[xs] <= eng.d2)
+        light_z = np.asarray(s.left_deg) <= eng.d2
+        lz_deg = np.add.reduceat(light_z[np.asarray(s.rev_indices)].astype(np.int64),
+                                 np.asarray(s.rev_indptr[:-1])) if len(s.rev_indices) else np.zeros(0, np.int64)
+        lz_deg = np.where(sdeg_y > 0, lz_deg, 0)
+    else:
+        full = np.ones(len(ys), bool)
+        lz_deg = np.zeros_like(sdeg_y)
+    lens = np.where(full, sdeg_y[ys], lz_deg[ys])
+    n_rl = int((lens > 0).sum())
+    yf = np.unique(ys[full])
+    yl = np.unique(ys[~full])
+    a_l = int(sdeg_y[yf].sum() + lz_deg[yl].sum())
+    # D_l: light-only bitmap per chunk
+    d_l = 0
+    dr, ds = eng.dr, eng.ds
+    hp = nat.ptr(eng.hpos) if eng.strategy == PARTITIONED else 0
+    lzp = nat.ptr(eng.lz_ptr) if eng.lz_ptr is not None else 0
+    lzi = nat.ptr(eng.lz_idx) if eng.lz_idx is not None else 0
+    wit = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for a, b in eng.chunk_bounds(x_lo, x_hi):
+        rows = b - a
+        bm = eng.ws.get("bm", rows * eng.wpr, torch.int32)
+        nseg = rows * eng.wpr // 32
+        segcnt = eng.ws.get("segcnt", nseg, torch.int32)
+        nat.call("mmj_tile_merge", nat.ptr(bm), 0, a, rows, eng.wpr, eng.dom_z,
+                 nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), eng.d2, hp, nat.ptr(ds.rev_ptr),
+                 nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(wit), nat.stream_handle())
+        d_l += int(segcnt[:nseg].sum(dtype=torch.int64).item())
+    return {"n_rl": n_rl, "a_l": a_l, "d_l": d_l, "witnesses_check": int(wit.item()),
+            "b_light": 8 * n_rl + 4 * a_l + 8 * d_l}
 
 
 def _shard(r, s, rank: int, world: int):
@@ -298,8 +351,11 @@ def run_b200(args):
         return TwoPathEngine(dr, ds, plan.strategy, d1, d2, False, chunk_rows=args.chunk_rows, ws=ws,
                              host_left_deg_r=r.left_deg, host_left_deg_s=s.left_deg)
 
+    holder = {}
+
     def step(timer=None):
         eng = make_engine()
+        holder["eng"] = eng
         if args.schedule == "serial":
             eng.timer = timer
             eng.prepare()
@@ -353,6 +409,10 @@ def run_b200(args):
 
     # ---- roofline of the dominant kernel + the heavy-MMA tensor figure
     hbm, hbm_kind = _peaks()
+    eng_last = holder["eng"]
+    light_work = None
+    if not args.no_light_work and "light_merge" in phases:
+        light_work = _light_work(eng_last, r, s, x_lo, x_hi)
     u = int((np.asarray(r.left_deg)[x_lo:x_hi] > d2).sum())
     w = int((np.asarray(s.left_deg) > d2).sum())
     v_k = stats.k_heavy
@@ -372,6 +432,12 @@ def run_b200(args):
                 info.update(peak_measured_cublaslt=int8_peak / 1e12, frac_measured=ops / int8_peak)
         if name in ("light", "light_merge") and t > 0:
             info.update(witnesses=stats.light_intermediate, witness_rate=stats.light_intermediate / t)
+            if light_work is not None:
+                ach = light_work["b_light"] / t / 1e9
+                info.update(achieved=ach, unit="GB/s", peak=hbm, frac=ach / hbm, algorithmic=light_work,
+                            bitmap_bytes_per_step=2 * 4 * (x_hi - x_lo) * eng_last.wpr,
+                            note="B_light = 8 N_Rl + 4 A_l + 8 D_l (SURVEY 8(d)); the merge also reads and "
+                                 "writes the chunk bitmap (bitmap_bytes_per_step), which B_light does not credit")
         phase_info[name] = info
     dominant = max(phases, key=lambda k: phases[k]) if phases else "emit"
     # DRAM bytes per launch from the committed ncu --set full capture, scaled
