@@ -411,7 +411,7 @@ def run_b200(args):
     hbm, hbm_kind = _peaks()
     eng_last = holder["eng"]
     light_work = None
-    if not args.no_light_work and "light_merge" in phases:
+    if not args.no_light_work and ("light_merge" in phases or "merge_emit" in phases):
         light_work = _light_work(eng_last, r, s, x_lo, x_hi)
     u = int((np.asarray(r.left_deg)[x_lo:x_hi] > d2).sum())
     w = int((np.asarray(s.left_deg) > d2).sum())
@@ -420,9 +420,17 @@ def run_b200(args):
     phase_info = {}
     for name, t in phases.items():
         info = {"ms": 1e3 * t, "share_of_step": t / t_step}
-        if name == "emit" and t > 0:
+        if name in ("emit", "merge_emit") and t > 0:
             ach = 8.0 * out_local / t / 1e9
             info.update(achieved=ach, unit="GB/s", peak=hbm, frac=ach / hbm, bytes_per_step=8 * out_local)
+        if name == "merge_emit" and t > 0:
+            info.update(witnesses=stats.light_intermediate, witness_rate=stats.light_intermediate / t)
+            if light_work is not None:
+                b = 8.0 * out_local + light_work["b_light"]
+                info.update(algorithmic_with_light=light_work, achieved_with_light=b / t / 1e9,
+                            frac_with_light=b / t / 1e9 / hbm,
+                            note="one kernel: light merge + segment scan + look-back + emission; achieved counts "
+                                 "the 8 B code writes only, *_with_light adds B_light = 8 N_Rl + 4 A_l + 8 D_l")
         if name == "heavy_mma" and t > 0 and w_mma > 0:
             ops = w_mma / t
             info.update(achieved=ops / 1e12, unit="TOPS(int8)", peak_datasheet=INT8_DATASHEET_OPS / 1e12,
@@ -447,7 +455,7 @@ def run_b200(args):
     if os.path.exists(tpath):
         with open(tpath) as f:
             t = json.load(f).get(dominant)
-        if isinstance(t, dict) and dominant == "emit" and stats.chunks:
+        if isinstance(t, dict) and dominant in ("emit", "merge_emit") and stats.chunks:
             traffic = t["traffic_over_algorithmic"] * 8.0 * out_local / stats.chunks
         elif isinstance(t, dict):
             traffic = t.get("dram_bytes_per_launch")
@@ -457,7 +465,7 @@ def run_b200(args):
                     "unit": "TOPS", "frac": dom.get("frac_datasheet"), "traffic": traffic,
                     "kernel": "heavy_mma_kernel", "peak_kind": "datasheet int8 dense"}
     else:
-        kern = {"emit": "k_emit", "light": "k_light_expand", "light_merge": "k_tile_merge",
+        kern = {"emit": "k_emit", "merge_emit": "k_merge_emit", "light": "k_light_expand", "light_merge": "k_tile_merge",
                 "segments": "tile_scan"}.get(dominant)
         ach = dom.get("achieved")
         roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",

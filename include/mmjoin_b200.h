@@ -145,6 +145,27 @@ int mmj_tile_merge(uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, in
                    const int32_t* lz_idx, int32_t* segcnt, unsigned long long* witnesses, void* stream);
 int mmj_emit_codes(const uint32_t* bitmap, const int64_t* seg_off, int64_t rows, int64_t wpr, int64_t x0,
                    int64_t dom_z, int64_t* codes, void* stream);
+/* The same three steps fused into one kernel (no merged-bitmap write-back,
+ * no segment-count array): tiles taken in ticket order merge their light
+ * witnesses, scan their segments and find their output offset by a
+ * decoupled look-back over per-tile status words, then emit.  codes must hold
+ * the chunk's output (rows*dom_z is always enough); *total receives its size.
+ * ws: caller-owned workspace of mmj_merge_emit_workspace_size(rows, wpr)
+ * bytes (reset by the call, on `stream`). */
+size_t mmj_merge_emit_workspace_size(int64_t rows, int64_t wpr);
+int mmj_merge_emit(const uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
+                   const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
+                   const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
+                   const int32_t* lz_idx, const int32_t* split_full, const int32_t* split_lz,
+                   unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws, size_t ws_bytes,
+                   void* stream);
+/* Column blocks per row of the fused kernel's tiles, and the optional list
+ * split table it reads instead of bisecting every long list per tile:
+ * split[y*(ncb+1)+j] = position in idx of list y's first entry >= the j-th
+ * block's first column (dom_y*(ncb+1) int32; NULL split pointers = bisect). */
+int mmj_merge_emit_col_blocks(int64_t wpr);
+int mmj_list_splits(const int32_t* ptr, const int32_t* idx, int64_t dom_y, int64_t wpr, int32_t* split,
+                    void* stream);
 
 /* ---- merge / emission: joinproject.py:220-225 -------------------------------
  * Bitmap chunk of nwords words (wpr words per row, row r <-> x = x0 + r):

@@ -31,6 +31,12 @@ int tile_merge(uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t
                int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int32_t*,
                unsigned long long*, cudaStream_t);
 int emit_codes(const uint32_t*, const int64_t*, int64_t, int64_t, int64_t, int64_t, int64_t*, cudaStream_t);
+size_t merge_emit_ws_bytes(int64_t, int64_t);
+int merge_emit(const uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t*, const int32_t*, const int32_t*,
+               int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*,
+               const int32_t*, const int32_t*, unsigned long long*, int64_t*, int64_t*, void*, size_t, cudaStream_t);
+int merge_emit_col_blocks(int64_t);
+int list_splits(const int32_t*, const int32_t*, int64_t, int64_t, int32_t*, cudaStream_t);
 int bsi_bits(const int32_t*, const int32_t*, int64_t, const int32_t*, int, uint32_t*, int64_t, cudaStream_t);
 int bsi_light_lists(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, uint8_t*, int32_t*, int32_t*,
                     int32_t*, void*, cudaStream_t);
@@ -170,6 +176,26 @@ int mmj_tile_merge(uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, in
                    const int32_t* lz_idx, int32_t* segcnt, unsigned long long* witnesses, void* stream) {
   return mmj::tile_merge(bitmap, has_heavy, x0, rows, wpr, dom_z, fwd_ptr, fwd_idx, rdeg_x, delta2, hpos, s_rev_ptr,
                          s_rev_idx, lz_ptr, lz_idx, segcnt, witnesses, ST(stream));
+}
+
+size_t mmj_merge_emit_workspace_size(int64_t rows, int64_t wpr) { return mmj::merge_emit_ws_bytes(rows, wpr); }
+
+int mmj_merge_emit(const uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
+                   const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
+                   const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
+                   const int32_t* lz_idx, const int32_t* split_full, const int32_t* split_lz,
+                   unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws, size_t ws_bytes,
+                   void* stream) {
+  return mmj::merge_emit(bitmap, has_heavy, x0, rows, wpr, dom_z, fwd_ptr, fwd_idx, rdeg_x, delta2, hpos, s_rev_ptr,
+                         s_rev_idx, lz_ptr, lz_idx, split_full, split_lz, witnesses, codes, total, ws, ws_bytes,
+                         ST(stream));
+}
+
+int mmj_merge_emit_col_blocks(int64_t wpr) { return mmj::merge_emit_col_blocks(wpr); }
+
+int mmj_list_splits(const int32_t* ptr, const int32_t* idx, int64_t dom_y, int64_t wpr, int32_t* split,
+                    void* stream) {
+  return mmj::list_splits(ptr, idx, dom_y, wpr, split, ST(stream));
 }
 
 int mmj_emit_codes(const uint32_t* bitmap, const int64_t* seg_off, int64_t rows, int64_t wpr, int64_t x0,

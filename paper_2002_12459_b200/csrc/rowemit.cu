@@ -28,6 +28,8 @@
 #include <cub/block/block_scan.cuh>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "mmj_common.cuh"
 
 namespace mmj {
@@ -107,7 +109,113 @@ struct TileArgs {
   const int32_t* lz_idx;
   int32_t* segcnt;            // popcount per 32-word segment of the chunk
   unsigned long long* witnesses;
+  // optional (dom_y x (ncb+1)) absolute list positions of the column-block
+  // boundaries (full S.rev lists / light-z lists): replaces per-tile bisection
+  const int32_t* split_full = nullptr;
+  const int32_t* split_lz = nullptr;
 };
+
+// Light witnesses of one tile OR-ed into its shared-memory bitmap (rows
+// [xa, xb), columns [zlo, zhi), cw words per row): R tuples are staged NT at a
+// time, each expanding its z-sorted S-side list -- the full S.rev(y) when y
+// is light or x is light, the light-z part otherwise (joinproject.py:183-203
+// restated from the x side) -- with MERGE_ILP list loads in flight per thread
+// before the shared-memory atomics.  Returns this thread's witness count.
+template <int NT>
+__device__ __forceinline__ unsigned long long merge_light(
+    const TileArgs& a, uint32_t* sbm, int64_t xa, int64_t xb, int64_t t_begin, int64_t t_end, int32_t zlo,
+    int32_t zhi, int cw, int cbi, typename cub::BlockScan<int, NT>::TempStorage& scan_tmp, int* s_tb_len,
+    const int32_t** s_tb_base, int* s_tb_row, int* s_tb_filt, int* s_touched) {
+  const int tid = threadIdx.x;
+  unsigned long long my_w = 0;
+  for (int64_t tb = t_begin; tb < t_end; tb += NT) {
+    const int64_t t = tb + tid;
+    int len = 0, row = 0, filt = 0;
+    const int32_t* base = nullptr;
+    if (t < t_end) {
+      int64_t lo = xa, hi = xb;   // row of tuple t: last x with fwd_ptr[x] <= t
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a.fwd_ptr[mid] <= t) lo = mid;
+        else hi = mid;
+      }
+      row = (int)(lo - xa);
+      const int32_t y = a.fwd_idx[t];
+      // joinproject.py:183-203: y light or x light -> S.rev(y); else light z only
+      const bool full = (a.hpos == nullptr) || (a.hpos[y] < 0) || (a.rdeg_x[lo] <= a.d2);
+      int32_t b, e;
+      if (full) {
+        b = a.s_rev_ptr[y];
+        e = a.s_rev_ptr[y + 1];
+        base = a.s_rev_idx + b;
+      } else {
+        b = a.lz_ptr[y];
+        e = a.lz_ptr[y + 1];
+        base = a.lz_idx + b;
+      }
+      len = e - b;
+      if (a.ncb > 1) {
+        const int32_t* sp = full ? a.split_full : a.split_lz;
+        if (sp != nullptr) {
+          // precomputed column-block boundaries of the list (mmj_list_splits)
+          const int32_t* q = sp + (int64_t)y * (a.ncb + 1) + cbi;
+          const int32_t lb = q[0], ub = q[1];
+          base += lb - b;
+          len = ub - lb;
+        } else if (len > SHORT_LIST) {
+          const int lb = lower_bound_i32(base, len, zlo);
+          const int ub = lb + lower_bound_i32(base + lb, len - lb, zhi);
+          base += lb;
+          len = ub - lb;
+        } else {
+          filt = 1;
+        }
+      }
+    }
+    int excl, tot;
+    cub::BlockScan<int, NT>(scan_tmp).ExclusiveSum(len, excl, tot);
+    s_tb_len[tid] = excl;
+    s_tb_base[tid] = base;
+    s_tb_row[tid] = row;
+    s_tb_filt[tid] = filt;
+    if (tid == 0) s_tb_len[NT] = tot;
+    __syncthreads();
+    const int nt = (int)min((int64_t)NT, t_end - tb);
+    int kept = 0;
+    int ti = 0;   // tuple of the current slot; slots grow, so the cursor only moves forward
+    // MERGE_ILP slots per thread per step: their list loads are issued
+    // together before the shared-memory atomics (the loads are the latency)
+    for (int s0 = tid; s0 < tot; s0 += MERGE_ILP * TM_THREADS) {
+      int32_t zv[MERGE_ILP];
+      int rowv[MERGE_ILP];
+      bool ok[MERGE_ILP];
+#pragma unroll
+      for (int u = 0; u < MERGE_ILP; ++u) {
+        const int s = s0 + u * TM_THREADS;
+        ok[u] = s < tot;
+        rowv[u] = 0;
+        zv[u] = 0;
+        if (ok[u]) {
+          while (ti + 1 < nt && s_tb_len[ti + 1] <= s) ++ti;
+          zv[u] = __ldg(s_tb_base[ti] + (s - s_tb_len[ti]));
+          rowv[u] = s_tb_row[ti] | (s_tb_filt[ti] << 30);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < MERGE_ILP; ++u) {
+        if (!ok[u]) continue;
+        const int32_t z = zv[u];
+        if ((rowv[u] >> 30) && (z < zlo || z >= zhi)) continue;
+        atomicOr(&sbm[(rowv[u] & 0x3FFFFFFF) * cw + ((z - zlo) >> 5)], 1u << (z & 31));
+        ++kept;
+      }
+    }
+    my_w += kept;
+    if (tot > 0 && tid == 0) *s_touched = 1;
+    __syncthreads();
+  }
+  return my_w;
+}
 
 __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   using BScan = cub::BlockScan<int, TM_THREADS>;
@@ -155,85 +263,8 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   unsigned long long my_w = 0;
   __syncthreads();
   if (a.has_heavy) bar_wait0(&s_bar);   // tile bytes landed (all threads observe the phase)
-  for (int64_t tb = t_begin; tb < t_end; tb += TUP_BATCH) {
-    const int64_t t = tb + tid;
-    int len = 0, row = 0, filt = 0;
-    const int32_t* base = nullptr;
-    if (t < t_end) {
-      int64_t lo = xa, hi = xb;   // row of tuple t: last x with fwd_ptr[x] <= t
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (a.fwd_ptr[mid] <= t) lo = mid;
-        else hi = mid;
-      }
-      row = (int)(lo - xa);
-      const int32_t y = a.fwd_idx[t];
-      // joinproject.py:183-203: y light or x light -> S.rev(y); else light z only
-      const bool full = (a.hpos == nullptr) || (a.hpos[y] < 0) || (a.rdeg_x[lo] <= a.d2);
-      int32_t b, e;
-      if (full) {
-        b = a.s_rev_ptr[y];
-        e = a.s_rev_ptr[y + 1];
-        base = a.s_rev_idx + b;
-      } else {
-        b = a.lz_ptr[y];
-        e = a.lz_ptr[y + 1];
-        base = a.lz_idx + b;
-      }
-      len = e - b;
-      if (a.ncb > 1) {
-        if (len > SHORT_LIST) {
-          const int lb = lower_bound_i32(base, len, zlo);
-          const int ub = lb + lower_bound_i32(base + lb, len - lb, zhi);
-          base += lb;
-          len = ub - lb;
-        } else {
-          filt = 1;
-        }
-      }
-    }
-    int excl, tot;
-    BScan(scan_tmp).ExclusiveSum(len, excl, tot);
-    s_tb_len[tid] = excl;
-    s_tb_base[tid] = base;
-    s_tb_row[tid] = row;
-    s_tb_filt[tid] = filt;
-    if (tid == 0) s_tb_len[TUP_BATCH] = tot;
-    __syncthreads();
-    const int nt = (int)min((int64_t)TUP_BATCH, t_end - tb);
-    int kept = 0;
-    int ti = 0;   // tuple of the current slot; slots grow, so the cursor only moves forward
-    // MERGE_ILP slots per thread per step: their list loads are issued
-    // together before the shared-memory atomics (the loads are the latency)
-    for (int s0 = tid; s0 < tot; s0 += MERGE_ILP * TM_THREADS) {
-      int32_t zv[MERGE_ILP];
-      int rowv[MERGE_ILP];
-      bool ok[MERGE_ILP];
-#pragma unroll
-      for (int u = 0; u < MERGE_ILP; ++u) {
-        const int s = s0 + u * TM_THREADS;
-        ok[u] = s < tot;
-        rowv[u] = 0;
-        zv[u] = 0;
-        if (ok[u]) {
-          while (ti + 1 < nt && s_tb_len[ti + 1] <= s) ++ti;
-          zv[u] = __ldg(s_tb_base[ti] + (s - s_tb_len[ti]));
-          rowv[u] = s_tb_row[ti] | (s_tb_filt[ti] << 30);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < MERGE_ILP; ++u) {
-        if (!ok[u]) continue;
-        const int32_t z = zv[u];
-        if ((rowv[u] >> 30) && (z < zlo || z >= zhi)) continue;
-        atomicOr(&sbm[(rowv[u] & 0x3FFFFFFF) * cw + ((z - zlo) >> 5)], 1u << (z & 31));
-        ++kept;
-      }
-    }
-    my_w += kept;
-    if (tot > 0 && tid == 0) s_touched = 1;
-    __syncthreads();
-  }
+  my_w = merge_light<TM_THREADS>(a, sbm, xa, xb, t_begin, t_end, zlo, zhi, cw, cbi, scan_tmp, s_tb_len, s_tb_base,
+                                 s_tb_row, s_tb_filt, &s_touched);
   {
     unsigned long long w = my_w;
 #pragma unroll
@@ -453,19 +484,382 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf16(const uint32_t* __r
   }
 }
 
-void tile_geometry(int64_t wpr, int& G, int& cb, int& ncb) {
-  if (wpr <= TILE_WORDS) {
-    G = (int)(TILE_WORDS / wpr);
+
+// ---------------------------------------------------------------------------
+// Fused light merge + emission (one kernel per chunk, no bitmap write-back,
+// no separate segment scan).  Tiles are taken in ticket order; each tile
+//   1. stages its heavy bitmap words (TMA bulk copy) or zeros in shared memory,
+//   2. ORs in its light witnesses (merge_light, as k_tile_merge),
+//   3. popcounts and scans its 32-word segments in shared memory,
+//   4. publishes its code count and obtains the codes of all earlier tiles by
+//      a decoupled look-back over the per-tile status words (flag in bits
+//      62-63: 1 = tile aggregate, 2 = inclusive prefix),
+//   5. emits its sorted codes x*dom_z + z exactly as k_emit_pf16.
+// Tickets make the look-back deadlock-free: a tile only waits on tiles whose
+// CTAs were scheduled before it.
+struct FuseArgs {
+  TileArgs t;
+  int64_t ntiles;
+  unsigned int* ticket;
+  unsigned long long* status;
+  int64_t* total;           // chunk code count (written by the last tile)
+  int64_t* codes;
+};
+
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int NT>
+struct FuseSmem {
+  typename cub::BlockScan<int, NT>::TempStorage scan_tmp;
+  union {
+    struct {
+      int tb_len[NT + 1];
+      const int32_t* tb_base[NT];
+      int tb_row[NT];
+      int tb_filt[NT];
+    } m;
+    uint16_t stage[NT / 32][1024 + 8];
+  } u;
+  int touched;
+  int next_seg;
+  unsigned int tile;
+  long long prefix;
+  __align__(8) uint64_t bar;
+};
+
+template <int TW, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
+  constexpr int NWARP = NT / 32;
+  constexpr int MAXSEG = TW / 32;
+  __shared__ FuseSmem<NT> sm;
+  __shared__ int s_segoff[MAXSEG];
+  extern __shared__ __align__(16) uint32_t sbm[];
+  const TileArgs& a = f.t;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    sm.tile = atomicAdd(f.ticket, 1u);
+    sm.touched = 0;
+  }
+  __syncthreads();
+  const int64_t tile = sm.tile;
+  const int64_t rg = tile / a.ncb;
+  const int cbi = (int)(tile - rg * a.ncb);
+  const int64_t r0 = rg * a.G;
+  const int64_t r1 = min(r0 + (int64_t)a.G, a.rows);
+  const int64_t c0w = (int64_t)cbi * a.cb_words;
+  const int cw = (int)min((int64_t)a.cb_words, a.wpr - c0w);
+  const int nrow = (int)(r1 - r0);
+  const int words = nrow * cw;
+  const int32_t zlo = (int32_t)(c0w * 32);
+  const int32_t zhi = (int32_t)min((c0w + cw) * 32, a.dom_z);
+  const uint32_t* gtile = a.bm + r0 * a.wpr + c0w;
+  if (a.has_heavy) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      bulk_g2s(sbm, gtile, (uint32_t)words * 4u, &sm.bar);
+    }
+  } else {
+    for (int i = tid; i < words; i += NT) sbm[i] = 0;
+  }
+  const int64_t xa = a.x0 + r0, xb = a.x0 + r1;
+  const int64_t t_begin = a.fwd_ptr[xa], t_end = a.fwd_ptr[xb];
+  __syncthreads();
+  if (a.has_heavy) bar_wait0(&sm.bar);
+  unsigned long long my_w = merge_light<NT>(a, sbm, xa, xb, t_begin, t_end, zlo, zhi, cw, cbi, sm.scan_tmp, sm.u.m.tb_len,
+                                            sm.u.m.tb_base, sm.u.m.tb_row, sm.u.m.tb_filt, &sm.touched);
+  {
+    unsigned long long w = my_w;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (lane == 0 && w) atomicAdd(a.witnesses, w);
+  }
+  __syncthreads();   // merged tile complete
+  // segment popcounts (REDUX over the 32 words of a segment, one warp per 32 segments)
+  const int nseg = words >> 5;
+  for (int sb = warp * 32; sb < nseg; sb += NT) {
+    int mine = 0;
+    const int ns = min(32, nseg - sb);
+    for (int j = 0; j < ns; ++j) {
+      const int c = __reduce_add_sync(0xffffffffu, __popc(sbm[(sb + j) * 32 + lane]));
+      if (lane == j) mine = c;
+    }
+    if (lane < ns) s_segoff[sb + lane] = mine;
+  }
+  __syncthreads();
+  // exclusive scan of the segment counts (MAXSEG / NT items per thread)
+  constexpr int IPT = (MAXSEG + NT - 1) / NT;
+  int v[IPT];
+  int loc = 0;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int sg = tid * IPT + i;
+    v[i] = sg < nseg ? s_segoff[sg] : 0;
+    loc += v[i];
+  }
+  int excl, agg;
+  cub::BlockScan<int, NT>(sm.scan_tmp).ExclusiveSum(loc, excl, agg);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int sg = tid * IPT + i;
+    if (sg < nseg) s_segoff[sg] = excl;
+    excl += v[i];
+  }
+  // decoupled look-back (warp 0)
+  if (warp == 0) {
+    long long prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st_status(f.status, ST_INC | (unsigned long long)agg);
+    } else {
+      if (lane == 0) st_status(f.status + tile, ST_AGG | (unsigned long long)agg);
+      int64_t pos = tile - 1;
+      while (true) {
+        const int64_t idx = pos - lane;
+        unsigned long long st = idx >= 0 ? ld_status(f.status + idx) : ST_INC;
+        while (__any_sync(0xffffffffu, (st >> 62) == 0)) {
+          if ((st >> 62) == 0) st = ld_status(f.status + idx);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        long long val = lane <= stop ? (long long)(st & ST_VAL) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (inc) break;
+        pos -= 32;
+      }
+      if (lane == 0) st_status(f.status + tile, ST_INC | (unsigned long long)(prefix + agg));
+    }
+    if (lane == 0) {
+      sm.prefix = prefix;
+      sm.next_seg = NWARP;
+      if (tile == f.ntiles - 1) *f.total = prefix + agg;
+    }
+  }
+  __syncthreads();
+  // emission: one warp per segment (k_emit_pf16's staging and stores)
+  uint16_t* stage = sm.u.stage[warp];
+  auto sl = [](int k) { return k ^ (((k >> 5) & 31) << 1); };
+  const int segs_per_piece = cw >> 5;
+  int64_t* const codes = f.codes + sm.prefix;
+  // segments are handed out dynamically (segment densities vary: a static
+  // round robin left warps idle at the CTA's exit waiting for the slowest)
+  for (int si = warp; si < nseg;) {
+    uint32_t word = sbm[si * 32 + lane];
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int vv = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += vv;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const int cur = si;
+    {
+      int nx = 0;
+      if (lane == 0) nx = atomicAdd(&sm.next_seg, 1);
+      si = __shfl_sync(0xffffffffu, nx, 0);
+    }
+    if (tot == 0) continue;
+    const int rr = cur / segs_per_piece;
+    const int64_t base = (a.x0 + r0 + rr) * a.dom_z + (c0w + (int64_t)(cur - rr * segs_per_piece) * 32) * 32;
+    int64_t* out = codes + s_segoff[cur];
+    const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
+    const uint32_t off0 = lane * 32;
+    int k = h + (incl - c);
+    if (__reduce_max_sync(0xffffffffu, (unsigned)c) >= 10u) {
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        if (word & (1u << b)) {
+          stage[sl(k)] = (uint16_t)(off0 + b);
+          ++k;
+        }
+      }
+    } else {
+      while (word) {
+        const int b = __ffs(word) - 1;
+        stage[sl(k)] = (uint16_t)(off0 + b);
+        ++k;
+        word &= word - 1;
+      }
+    }
+    __syncwarp();
+    if (lane < h) st_cs(out, base + stage[sl(h)]);
+    const int np = (tot - h) >> 1;
+    for (int p = lane; p < np; p += 32) {
+      const uint32_t two = *reinterpret_cast<const uint32_t*>(stage + sl(2 * h + 2 * p));
+      st_cs2(out + h + 2 * p, base + (two & 0xFFFFu), base + (two >> 16));
+    }
+    const int done = h + 2 * np;
+    if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(h + done + lane)]);
+    __syncwarp();
+  }
+}
+
+// split[y*(ncb+1) + j] = absolute position in idx of the first entry of list
+// y (ptr[y] .. ptr[y+1], sorted) that is >= j * cb_cells
+__global__ void k_list_splits(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx, int64_t dom_y,
+                              int ncb, int64_t cb_cells, int32_t* __restrict__ split) {
+  const int64_t n = dom_y * (ncb + 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = i / (ncb + 1);
+    const int j = (int)(i - y * (ncb + 1));
+    const int32_t b = ptr[y], e = ptr[y + 1];
+    int32_t pos;
+    if (j == 0) pos = b;
+    else if (j == ncb) pos = e;
+    else {
+      const int64_t key = (int64_t)j * cb_cells;
+      int lo = b, hi = e;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((int64_t)idx[mid] < key) lo = mid + 1;
+        else hi = mid;
+      }
+      pos = lo;
+    }
+    split[i] = pos;
+  }
+}
+
+void tile_geometry(int64_t wpr, int& G, int& cb, int& ncb, int64_t tile_words = TILE_WORDS) {
+  if (wpr <= tile_words) {
+    G = (int)(tile_words / wpr);
     cb = (int)wpr;
     ncb = 1;
   } else {
     G = 1;
-    cb = TILE_WORDS;
-    ncb = (int)ceil_div(wpr, TILE_WORDS);
+    cb = (int)tile_words;
+    ncb = (int)ceil_div(wpr, tile_words);
   }
 }
 
+// tile words of the fused kernel (env MMJ_FUSE_TW: 4096 / 8192 / 16384)
+int fuse_tile_words() {
+  static int tw = -1;
+  if (tw < 0) {
+    const char* e = getenv("MMJ_FUSE_TW");
+    tw = e ? atoi(e) : 8192;
+    if (tw != 4096 && tw != 8192 && tw != 16384) tw = 8192;
+  }
+  return tw;
+}
+
+template <int TW, int NT, int MINB>
+int launch_merge_emit(const FuseArgs& f, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    MMJ_TRY(cuda_status(cudaFuncSetAttribute(k_merge_emit<TW, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             TW * 4),
+                        "cudaFuncSetAttribute(k_merge_emit)"));
+    attr = true;
+  }
+  const size_t smem = (size_t)f.t.G * f.t.cb_words * 4;
+  k_merge_emit<TW, NT, MINB><<<(unsigned)f.ntiles, NT, smem, st>>>(f);
+  MMJ_CHECK_LAUNCH("k_merge_emit");
+  return MMJ_OK;
+}
+
 }  // namespace
+
+int merge_emit_col_blocks(int64_t wpr) {
+  int G, cb, ncb;
+  tile_geometry(wpr, G, cb, ncb, fuse_tile_words());
+  return ncb;
+}
+
+int list_splits(const int32_t* ptr, const int32_t* idx, int64_t dom_y, int64_t wpr, int32_t* split, cudaStream_t st) {
+  int G, cb, ncb;
+  tile_geometry(wpr, G, cb, ncb, fuse_tile_words());
+  const int64_t n = dom_y * (ncb + 1);
+  if (n == 0) return MMJ_OK;
+  const int64_t g = std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 16);
+  k_list_splits<<<(unsigned)g, 256, 0, st>>>(ptr, idx, dom_y, ncb, (int64_t)cb * 32, split);
+  MMJ_CHECK_LAUNCH("k_list_splits");
+  return MMJ_OK;
+}
+
+int64_t merge_emit_tiles(int64_t rows, int64_t wpr) {
+  int G, cb, ncb;
+  tile_geometry(wpr, G, cb, ncb, fuse_tile_words());
+  return ceil_div(rows, G) * ncb;
+}
+
+size_t merge_emit_ws_bytes(int64_t rows, int64_t wpr) {
+  return 16 + (size_t)merge_emit_tiles(rows, wpr) * 8;
+}
+
+int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
+               const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t d2, const int32_t* hpos,
+               const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx,
+               const int32_t* split_full, const int32_t* split_lz, unsigned long long* witnesses, int64_t* codes,
+               int64_t* total, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (wpr <= 0 || wpr % 32 != 0) {
+    set_error("merge_emit: bitmap pitch must be a positive multiple of 32 words");
+    return MMJ_ERR_ARG;
+  }
+  if (rows <= 0) return cuda_status(cudaMemsetAsync(total, 0, sizeof(int64_t), st), "merge_emit: total");
+  const int tw = fuse_tile_words();
+  FuseArgs f;
+  TileArgs& a = f.t;
+  a.bm = const_cast<uint32_t*>(bm);
+  a.has_heavy = has_heavy;
+  a.x0 = x0;
+  a.rows = rows;
+  a.wpr = wpr;
+  a.dom_z = dom_z;
+  tile_geometry(wpr, a.G, a.cb_words, a.ncb, tw);
+  f.ntiles = ceil_div(rows, a.G) * a.ncb;
+  if (f.ntiles >= (1ll << 31)) {
+    set_error("merge_emit: too many tiles in one chunk");
+    return MMJ_ERR_ARG;
+  }
+  const size_t need = 16 + (size_t)f.ntiles * 8;
+  if (ws == nullptr || ws_bytes < need) {
+    set_error("merge_emit: workspace of %zu bytes needed (got %zu)", need, ws_bytes);
+    return MMJ_ERR_CAPACITY;
+  }
+  a.fwd_ptr = fwd_ptr;
+  a.fwd_idx = fwd_idx;
+  a.rdeg_x = rdeg_x;
+  a.d2 = d2;
+  a.hpos = hpos;
+  a.s_rev_ptr = s_rev_ptr;
+  a.s_rev_idx = s_rev_idx;
+  a.lz_ptr = lz_ptr;
+  a.lz_idx = lz_idx;
+  a.segcnt = nullptr;
+  a.witnesses = witnesses;
+  a.split_full = split_full;
+  a.split_lz = split_lz;
+  f.ticket = static_cast<unsigned int*>(ws);
+  f.status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 16);
+  f.total = total;
+  f.codes = codes;
+  MMJ_TRY(cuda_status(cudaMemsetAsync(ws, 0, need, st), "merge_emit: workspace reset"));
+  static int variant = -1;
+  if (variant < 0) {
+    const char* e = getenv("MMJ_FUSE_VARIANT");   // A/B: 1 = (4096, 256 thr, 6 CTAs/SM), 2 = (16384, 512 thr)
+    variant = e ? atoi(e) : 0;
+  }
+  if (variant == 1 && tw == 4096) return launch_merge_emit<4096, 256, 6>(f, st);
+  if (variant == 2 && tw == 16384) return launch_merge_emit<16384, 512, 2>(f, st);
+  switch (tw) {
+    case 4096: return launch_merge_emit<4096, 256, 4>(f, st);
+    case 16384: return launch_merge_emit<16384, 256, 2>(f, st);
+    default: return launch_merge_emit<8192, 256, 4>(f, st);
+  }
+}
 
 int64_t row_emit_tiles(int64_t rows, int64_t wpr) {
   int G, cb, ncb;

@@ -34,6 +34,7 @@ BK = 128          # K block (bytes)
 DEFAULT_BITMAP_CHUNK_BYTES = 1 << 30
 DEFAULT_COUNT_CHUNK_BYTES = 4 << 30
 FUSED_SMEM_LIMIT = 200 * 1024
+SYNC_FUSED_CAP_BYTES = 4 << 30
 
 
 def _rup(a: int, b: int) -> int:
@@ -136,6 +137,10 @@ class TwoPathEngine:
         # bitmap fits in shared memory (dom_z up to ~1.2M)
         self.group_rows = max(1, min(32, (48 * 1024) // (self.wpr * 4)))
         self.fused = (not self.counts) and self.dom_z < (1 << 31)
+        # merge + scan + emission as one kernel (decoupled look-back); env
+        # MMJ_FUSED_EMIT=0 selects the three-kernel path for A/B runs
+        self._splits = None
+        self.one_kernel_tail = self.fused and __import__("os").environ.get("MMJ_FUSED_EMIT", "1") != "0"
         self._prepared = False
         self._sizes_dev = None
         self._n_async = 0
@@ -323,8 +328,15 @@ class TwoPathEngine:
         return ChunkResult(x0, x1, total, codes[:total], None if counts is None else counts[:total], light)
 
     def _fused_tail(self, x0, x1, rows, buf, sync, codes_key="codes"):
-        """Light witnesses merged into the bitmap tile by tile, segment scan,
-        emission (mmj_tile_merge -> mmj_exclusive_scan_i32 -> mmj_emit_codes)."""
+        """Light witnesses merged into the bitmap and the sorted codes emitted:
+        one kernel (mmj_merge_emit: merge, segment scan, decoupled look-back,
+        emission) or, with MMJ_FUSED_EMIT=0, the three-kernel path
+        (mmj_tile_merge -> mmj_exclusive_scan_i32 -> mmj_emit_codes)."""
+        # the fused kernel learns the chunk's output size only as it runs, so
+        # its code buffer is sized for every cell of the chunk; synchronous
+        # callers with larger chunks take the exact-size three-kernel path
+        if self.one_kernel_tail and (not sync or rows * self.dom_z * 8 <= SYNC_FUSED_CAP_BYTES):
+            return self._merge_emit_tail(x0, x1, rows, buf, sync, codes_key)
         torch = self.torch
         st = self._st()
         dr, ds = self.dr, self.ds
@@ -359,6 +371,62 @@ class TwoPathEngine:
             slot = self._async_slot()
             slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
             return ChunkResult(x0, x1, -1, codes, None, -1, slot[0:1])
+        light = int(self.wit.item()) - wit0
+        self.stats.out_size += total
+        return ChunkResult(x0, x1, total, codes[:total], None, light)
+
+    def _list_splits(self):
+        """(full, light-z) column-block split tables of the S-side lists for
+        the fused kernel, built once per engine; (0, 0) when a row is a single
+        tile or the table would be large (the kernel then bisects)."""
+        if self._splits is None:
+            torch = self.torch
+            ncb = int(self.lib.mmj_merge_emit_col_blocks(self.wpr))
+            n = self.dom_y * (ncb + 1)
+            if ncb <= 1 or n > (64 << 20):
+                self._splits = (0, 0, None)
+            else:
+                st = self._st()
+                full = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+                nat.call("mmj_list_splits", nat.ptr(self.ds.rev_ptr), nat.ptr(self.ds.rev_idx), self.dom_y, self.wpr,
+                         nat.ptr(full), st)
+                keep = [full]
+                lz = 0
+                if self.lz_ptr is not None:
+                    lzt = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+                    nat.call("mmj_list_splits", nat.ptr(self.lz_ptr), nat.ptr(self.lz_idx), self.dom_y, self.wpr,
+                             nat.ptr(lzt), st)
+                    keep.append(lzt)
+                    lz = nat.ptr(lzt)
+                self._splits = (nat.ptr(full), lz, keep)
+        return self._splits[0], self._splits[1]
+
+    def _merge_emit_tail(self, x0, x1, rows, buf, sync, codes_key):
+        torch = self.torch
+        st = self._st()
+        dr, ds = self.dr, self.ds
+        hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
+        lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
+        lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
+        wit0 = int(self.wit.item()) if sync else 0
+        wsb = int(self.lib.mmj_merge_emit_workspace_size(rows, self.wpr))
+        ws = self.ws.get("fuse_ws", wsb, torch.uint8)
+        # capacity: the chunk's cells (the output size is known only after the kernel)
+        cap = rows * self.dom_z
+        codes = self.ws.get(codes_key, cap, torch.int64)
+        slot = self._async_slot()
+        spf, spl = self._list_splits()
+        self._ph("merge_emit", True)
+        nat.call("mmj_merge_emit", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
+                 nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp, nat.ptr(ds.rev_ptr),
+                 nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(slot),
+                 nat.ptr(ws), wsb, st)
+        self._ph("merge_emit", False)
+        self.stats.chunks += 1
+        if not sync:
+            return ChunkResult(x0, x1, -1, codes, None, -1, slot[0:1])
+        self._n_async -= 1          # consumed here, not by finish()
+        total = int(slot[0].item())
         light = int(self.wit.item()) - wit0
         self.stats.out_size += total
         return ChunkResult(x0, x1, total, codes[:total], None, light)
