@@ -45,6 +45,9 @@ extern "C" {
 #define MMJ_MODE_BITMAP_PAIR 4 /* BITMAP over a z-pair B operand (mmj_build_operand_pairs): b_rows = pair
                                   rows, 2 bits per accumulator; needs every count < 128 (a side whose
                                   heavy degrees are <= 127); ld_out*16 >= b_rows rounded up to 256 */
+#define MMJ_MODE_BITMAP_TRIPLE 6 /* BITMAP over z-triple operands (mmj_build_operand_triple): K window = 2*kpad
+                                  of the builders' kpad, 3 bits per accumulator, 24 words per 256 B rows;
+                                  needs every count < 128; words at or past ld_out are not written */
 #define MMJ_MODE_COUNT16 5     /* exact counts as uint16 (caller guarantees every count < 65536); ld_out in
                                   uint16 elements, multiple of 8 */
 #define MMJ_MODE_UPPER 16      /* OR-flag: self-join, skip tiles whose columns are all <= their rows
@@ -80,6 +83,16 @@ int mmj_build_operand(const int32_t* rows, const int32_t* cols, int64_t n, const
 int mmj_build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
                             int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
                             int64_t kpad, void* stream);
+
+/* z-triple form for MMJ_MODE_BITMAP_TRIPLE (both operands have pitch 2*kpad,
+ * zeroed first).  side 0 (A): row r = [R_h row | 128 x R_h row].  side 1 (B):
+ * z = row0 + 96G + 32w + 8b + k (w < 3, b < 4, k < 8) goes to mat row
+ * 32G + 8((4w+b)/3) + k, field (4w+b)%3: weight 1 / 128 in the first K half
+ * for fields 0 / 1, weight 128 in the second half for field 2; mat_rows >=
+ * ceil(nrows/96)*32. */
+int mmj_build_operand_triple(int side, const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
+                             int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
+                             int64_t mat_rows, int64_t kpad, void* stream);
 
 /* ---- light-z CSR of S for pass 3: joinproject.py:195-203 --------------------
  * lz_ptr[dom_y+1]/lz_idx: S.rev(y) restricted to z with deg_S(z) <= delta2.

@@ -27,6 +27,7 @@ MODE_ACC64 = 2
 MODE_BITMAP_U8 = 3
 MODE_BITMAP_PAIR = 4
 MODE_COUNT16 = 5
+MODE_BITMAP_TRIPLE = 6
 MODE_UPPER = 16
 
 P = C.c_void_p
@@ -59,6 +60,7 @@ _SIGS = {
     "mmj_ingest_histogram": (INT, [P, I64, I64, P, P]),
     "mmj_ingest_csr": (INT, [P, P, I64, I64, I64, P, P, P, P, P, SZ, P]),
     "mmj_build_operand_pairs": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
+    "mmj_build_operand_triple": (INT, [INT, P, P, I64, P, I64, P, P, I64, I64, I64, I64, P]),
     "mmj_light_z_csr": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P]),
     "mmj_light_lengths": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, I64, INT, P, P, P, P]),
     "mmj_light_expand": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, I64, INT, P, I64, INT, I64, P, I64, P]),

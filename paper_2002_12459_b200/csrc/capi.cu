@@ -8,6 +8,8 @@ int heavy_y_positions(const int32_t*, const int32_t*, int64_t, int64_t, uint8_t*
                       cudaStream_t);
 int build_operand(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint8_t*, int64_t,
                   int64_t, int64_t, cudaStream_t);
+int build_operand_triple(int, const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*,
+                         uint8_t*, int64_t, int64_t, int64_t, int64_t, cudaStream_t);
 int build_operand_pairs(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint8_t*,
                         int64_t, int64_t, int64_t, cudaStream_t);
 int light_z_csr(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, uint8_t*, int32_t*,
@@ -112,6 +114,13 @@ int mmj_build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n,
   return mmj::build_operand_pairs(rows, cols, n, left_deg, delta2, hpos, mat, row0, nrows, kpad, ST(stream));
 }
 
+int mmj_build_operand_triple(int side, const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
+                             int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
+                             int64_t mat_rows, int64_t kpad, void* stream) {
+  return mmj::build_operand_triple(side, rows, cols, n, left_deg, delta2, hpos, mat, row0, nrows, mat_rows, kpad,
+                                   ST(stream));
+}
+
 int mmj_light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, int64_t dom_y,
                     const int32_t* left_deg, int64_t delta2, uint8_t* flag_ws, int32_t* pos_ws, int32_t* lz_ptr,
                     int32_t* lz_idx, void* ws, void* stream) {
@@ -144,7 +153,7 @@ int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_
                   int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out, int64_t ld_out,
                   unsigned long long* nnz, int max_ctas, void* stream) {
   const int base_mode = mode & ~MMJ_MODE_UPPER;
-  if (base_mode < 0 || base_mode > 5 ||
+  if (base_mode < 0 || base_mode > MMJ_MODE_BITMAP_TRIPLE ||
       (mode != base_mode && base_mode != MMJ_MODE_COUNT32 && base_mode != MMJ_MODE_COUNT16)) {
     mmj::set_error("heavy_mma: unknown mode %d (MMJ_MODE_UPPER combines with the count modes only)", mode);
     return MMJ_ERR_ARG;

@@ -20,7 +20,11 @@
 //                the generic multiply_counts backend);
 //       BITMAP_PAIR: B rows are z pairs weighted (1, 128) (mmj_build_operand_pairs),
 //                one accumulator = two cells: half the MMAs and half the TMEM
-//                read-out per output bit, 64 B per row/tile.
+//                read-out per output bit, 64 B per row/tile;
+//       BITMAP_TRIPLE: A = [R_h | 128 R_h] (K doubled), B rows hold three z
+//                weighted (1, 128 | 128): one accumulator = c0 + 128 c1 +
+//                16384 c2, three cells per TMEM word (the read-out bound),
+//                96 B per row/tile.
 //
 // Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
 // w3 idle, w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4) .. +31 and the
@@ -68,7 +72,8 @@ constexpr int SMEM_MAX = smem_bytes_for(3, true) > smem_bytes_for(STAGES, false)
 static_assert(SMEM_MAX <= 227 * 1024, "shared memory budget");
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
-enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, BITMAP_PAIR = 4, COUNT16 = 5, MODE_UPPER = 16 };
+enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, BITMAP_PAIR = 4, COUNT16 = 5, BITMAP_TRIPLE = 6,
+                  MODE_UPPER = 16 };
 
 struct Params {
   int64_t m_begin;      // first A row of this launch (multiple of BM not required)
@@ -79,6 +84,7 @@ struct Params {
   int num_kb;           // Kp / BK
   int stages;           // smem ring depth (2..STAGES)
   int debug;            // 1: epilogue skips the bit packing (profiling experiment)
+  int alt;              // BITMAP_PAIR / BITMAP_TRIPLE: alternating epilogue warp groups (env MMJ_EPI_ALT)
   int small_counts;     // BITMAP: every product entry < 256 (K window <= 255 nonzero columns)
   int mode;
   int shift;            // ACC64 only
@@ -254,6 +260,32 @@ __device__ __forceinline__ uint32_t pack_bits_pair(const uint32_t* r) {
   return w;   // register k's flags now sit at bits k, 8+k, 16+k, 24+k
 }
 
+// BITMAP_TRIPLE: a = c0 + 128 c1 + 16384 c2 with every c < 128.  a + (c1 << 7)
+// + 3 (c2 << 14) moves the fields to bytes 0, 1, 2; + 0x7F per byte sets each
+// byte's MSB iff its field is nonzero (no carry leaves a byte).
+__device__ __forceinline__ uint32_t triple_flags(uint32_t a) {
+  const uint32_t t1 = a & 0x3F80u, t2 = a & 0x1FC000u;
+  return (a + t1 + 0x7F7F7Fu + 3u * t2) & 0x808080u;
+}
+
+// 32 accumulators -> 3 bitmap words.  Accumulator 8q + k (q < 4, k < 8)
+// lands at bit k of bytes 0..2 of chain c[q] (fields 0..2); the 12 chain
+// bytes c0.b0 c0.b1 c0.b2 c1.b0 ... c3.b2 are the 3 words' 12 bytes in order.
+// The operand builder (mmj_build_operand_triples) places z accordingly.
+__device__ __forceinline__ void pack_bits_triple(const uint32_t* r, uint32_t* w) {
+  uint32_t c[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t v = triple_flags(r[8 * q]);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) v = (v >> 1) | triple_flags(r[8 * q + k]);
+    c[q] = v;
+  }
+  w[0] = __byte_perm(c[0], c[1], 0x4210);
+  w[1] = __byte_perm(c[1], c[2], 0x5421);
+  w[2] = __byte_perm(c[2], c[3], 0x6542);
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -330,7 +362,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < ACC_STAGES; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], EPI_WARPS);
+      mbar_init(&tempty[s], p.alt ? 4 : EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -394,6 +426,94 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (++acc == ACC_STAGES) { acc = 0; acc_ph ^= 1; }
       }
     }
+  } else if (warp >= 4 && p.alt) {
+    // ------------------------------------------------------- epilogue, alternating groups
+    // Warps 4-7 (group 0) take the CTA's even tiles (accumulator stage 0),
+    // warps 8-11 (group 1) the odd ones (stage 1), each warp all 256 columns
+    // of its TMEM lane quadrant.  The groups run half a tile apart, so one
+    // group's packing overlaps the other's TMEM read-out (with both groups on
+    // every tile, all warps load, then all pack, and the SM's TMEM read
+    // port idles during the packing).
+    const int q = warp & 3;
+    const int grp = (warp - 4) >> 2;
+    uint32_t acc_ph = 0;
+    unsigned long long my_nnz = 0;
+    int64_t li = 0;
+    for (int64_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      TileCoord c = tile_of(t, mt, nt);
+      if (below_diagonal(p, c)) continue;
+      if ((int)(li++ & 1) != grp) continue;
+      const int acc = grp;
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      const int64_t row = (int64_t)c.m_blk * BM + q * 32 + lane;
+      const bool row_ok = row < p.m_rows;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (p.mode == BITMAP_TRIPLE) {
+        constexpr int NWT = 3 * BN / 32;   // 24 words
+        uint32_t w[NWT];
+        // two 32-column loads in flight per wait (the TMEM load latency,
+        // not its bandwidth, bounds a warp that waits on every 32 columns)
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j) {
+          uint32_t r[64];
+          uint32_t* r1 = r + 32;
+          TMEM_LD_32x32b_X32(taddr + 64 * j, r);
+          TMEM_LD_32x32b_X32(taddr + 64 * j + 32, r1);
+          tmem_wait_ld();
+          if (j == BN / 64 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          pack_bits_triple(r, w + 6 * j);
+          pack_bits_triple(r1, w + 6 * j + 3);
+        }
+        if (row_ok) {
+          const int64_t wbase = (int64_t)c.n_blk * NWT;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + wbase;
+#pragma unroll
+          for (int k = 0; k < NWT; k += 4) {
+            if (wbase + k + 4 <= p.ld_out) {
+              *reinterpret_cast<uint4*>(dst + k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+              my_nnz += __popc(w[k]) + __popc(w[k + 1]) + __popc(w[k + 2]) + __popc(w[k + 3]);
+            }
+          }
+        }
+      } else {   // BITMAP_PAIR
+        constexpr int NW = BN / 16;        // 16 words
+        uint32_t w[NW];
+#pragma unroll
+        for (int j = 0; j < BN / 128; ++j) {
+          uint32_t r[64];
+          uint32_t* r1 = r + 32;
+          TMEM_LD_32x32b_X32_PACK16(taddr + 128 * j, r);
+          TMEM_LD_32x32b_X32_PACK16(taddr + 128 * j + 64, r1);
+          tmem_wait_ld();
+          if (j == BN / 128 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) w[8 * j + k] = pack_bits_pair(r + 8 * k);
+        }
+        if (row_ok) {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + (int64_t)c.n_blk * NW;
+#pragma unroll
+          for (int k = 0; k < NW; k += 4) {
+            *reinterpret_cast<uint4*>(dst + k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+            my_nnz += __popc(w[k]) + __popc(w[k + 1]) + __popc(w[k + 2]) + __popc(w[k + 3]);
+          }
+        }
+      }
+      acc_ph ^= 1;
+    }
+    if (p.nnz != nullptr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) my_nnz += __shfl_xor_sync(0xffffffffu, my_nnz, o);
+      if (lane == 0 && my_nnz) atomicAdd(p.nnz, my_nnz);
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------- epilogue
     const int q = warp & 3;              // TMEM lane quadrant
@@ -455,6 +575,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
 #pragma unroll
           for (int k = 0; k < NW; ++k) my_nnz += __popc(w[k]);
+        }
+      } else if (p.mode == BITMAP_TRIPLE) {
+        // CW accumulators = 3*CW z -> 3*CW/32 words, 32-column chunks
+        constexpr int NWT = 3 * CW / 32;
+        constexpr int NC = CW / 32;
+        uint32_t w[NWT];
+        uint32_t ra[32], rb[32];
+        TMEM_LD_32x32b_X32(taddr, ra);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          uint32_t* cur = (j & 1) ? rb : ra;
+          uint32_t* nxt = (j & 1) ? ra : rb;
+          if (j + 1 < NC) {
+            TMEM_LD_32x32b_X32(taddr + 32 * (j + 1), nxt);
+          } else {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          pack_bits_triple(cur, w + 3 * j);
+          if (j + 1 < NC) tmem_wait_ld();
+        }
+        if (row_ok) {
+          const int64_t wbase = (int64_t)c.n_blk * (3 * BN / 32) + grp * NWT;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + wbase;
+#pragma unroll
+          for (int k = 0; k < NWT; k += 4) {
+            if (wbase + k + 4 <= p.ld_out) {   // the last tile of a row may pass its end
+              *reinterpret_cast<uint4*>(dst + k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+              my_nnz += __popc(w[k]) + __popc(w[k + 1]) + __popc(w[k + 2]) + __popc(w[k + 3]);
+            }
+          }
         }
       } else if (p.mode == COUNT16) {
         // counts < 2^16 (caller's guarantee): pack::16b registers hold two
@@ -626,12 +779,21 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
     set_error("heavy_mma: pair-bitmap pitch %lld words too small / unaligned", (long long)ld_out);
     return MMJ_ERR_ARG;
   }
+  if (mode == BITMAP_TRIPLE && (ld_out % 4 != 0 || ceil_div(b_rows, BN) * (3 * BN / 32) < ld_out)) {
+    set_error("heavy_mma: triple-bitmap pitch %lld words unaligned or not covered by %lld B rows", (long long)ld_out,
+              (long long)b_rows);
+    return MMJ_ERR_ARG;
+  }
   if (mode == COUNT32 && ld_out % 4 != 0) {
     set_error("heavy_mma: count pitch must be a multiple of 4");
     return MMJ_ERR_ARG;
   }
   if (mode == COUNT16 && ld_out % 8 != 0) {
     set_error("heavy_mma: uint16 count pitch must be a multiple of 8");
+    return MMJ_ERR_ARG;
+  }
+  if (mode < 0 || mode > BITMAP_TRIPLE) {
+    set_error("heavy_mma: unknown mode %d", mode);
     return MMJ_ERR_ARG;
   }
   if ((mode == BITMAP || mode == BITMAP_U8 || mode == BITMAP_PAIR) && k_len > 65535) {
@@ -668,6 +830,12 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
       dbg = (e && e[0] == '1') ? 1 : 0;
     }
     p.debug = dbg;
+    static int alt = -1;
+    if (alt < 0) {
+      const char* e = getenv("MMJ_EPI_ALT");
+      alt = (e && e[0] == '0') ? 0 : 1;
+    }
+    p.alt = (alt && (mode == BITMAP_PAIR || mode == BITMAP_TRIPLE)) ? 1 : 0;
     static int bo = -1;
     if (bo < 0) {
       const char* e = getenv("MMJ_BACKOFF");

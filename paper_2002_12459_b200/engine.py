@@ -117,6 +117,8 @@ class TwoPathEngine:
         self.pairs = False
         self.allow_pairs = bool(pair_operand)   # False: B stays one z per row (heavy_matrices reads it)
         self.kpad = 0
+        self.mma_kpad = 0       # K window of the heavy product (2 * kpad for the z-triple operands)
+        self.triple = False
         self.lz_ptr = None
         self.lz_idx = None
         self._host_ldeg_r = host_left_deg_r
@@ -175,14 +177,33 @@ class TwoPathEngine:
                 self.kpad = kpad
                 arows = _rup(max(self.dom_x, 1), BN)
                 brows = _rup(max(self.dom_z, 1), 1024)   # product covers every word of the padded rows
-                self.A = torch.empty((arows, kpad), dtype=torch.uint8, device="cuda")
-                nat.call("mmj_build_operand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n, nat.ptr(dr.left_deg),
-                         self.d2, nat.ptr(self.hpos), nat.ptr(self.A), 0, arows, kpad, st)
                 self.pairs = (self.allow_pairs and not self.counts
                               and __import__("os").environ.get("MMJ_PAIR", "1") != "0"
                               and (k <= 127 or self._max_deg(self._host_ldeg_r, dr) <= 127
                                    or self._max_deg(self._host_ldeg_s, ds) <= 127))
-                if self.pairs:
+                # z triples (3 cells per TMEM word) are opt-in: measured slower than
+                # pairs on cfg2 (35.1 vs 26.5 ms: the extra packing ALU outweighs the
+                # saved TMEM read-out), kept as an A/B option (MMJ_TRIPLE=1)
+                self.triple = self.pairs and __import__("os").environ.get("MMJ_TRIPLE", "0") == "1"
+                self.mma_kpad = kpad
+                if not self.triple:
+                    self.A = torch.empty((arows, kpad), dtype=torch.uint8, device="cuda")
+                    nat.call("mmj_build_operand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n,
+                             nat.ptr(dr.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.A), 0, arows, kpad, st)
+                if self.triple:
+                    # three z per accumulator (weights 1, 128 | 128 with A =
+                    # [R_h | 128 R_h]): one TMEM word carries three cells
+                    self.mma_kpad = 2 * kpad
+                    brows_t = -(-(brows // 32) // 24) * BN
+                    self.A = torch.empty((arows, 2 * kpad), dtype=torch.uint8, device="cuda")
+                    nat.call("mmj_build_operand_triple", 0, nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n,
+                             nat.ptr(dr.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.A), 0, arows, arows,
+                             kpad, st)
+                    self.B = torch.empty((brows_t, 2 * kpad), dtype=torch.uint8, device="cuda")
+                    nat.call("mmj_build_operand_triple", 1, nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n,
+                             nat.ptr(ds.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.B), 0, brows, brows_t,
+                             kpad, st)
+                elif self.pairs:
                     # z pairs share one accumulator (weights 1, 128): every
                     # count is < 128 because one side's heavy degrees are
                     self.B = torch.empty((brows // 2, kpad), dtype=torch.uint8, device="cuda")
@@ -207,6 +228,8 @@ class TwoPathEngine:
     def _bitmap_mode(self) -> int:
         # every product entry counts <= K shared heavy y: with K <= 255 the
         # epilogue may pack counts as bytes
+        if self.triple:
+            return nat.MODE_BITMAP_TRIPLE
         if self.pairs:
             return nat.MODE_BITMAP_PAIR
         return nat.MODE_BITMAP_U8 if 0 < self.stats.k_heavy <= 255 else nat.MODE_BITMAP
@@ -256,7 +279,7 @@ class TwoPathEngine:
         self._ph("heavy_mma", True)
         if self.A is not None:
             nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
-                     self.kpad, 0, self.kpad, x0, rows, mode, 0, nat.ptr(buf), ld, nat.ptr(self.nnz), 0, st)
+                     self.mma_kpad, 0, self.mma_kpad, x0, rows, mode, 0, nat.ptr(buf), ld, nat.ptr(self.nnz), 0, st)
         else:
             buf.zero_()
         self._ph("heavy_mma", False)
@@ -473,7 +496,7 @@ class TwoPathEngine:
                 timer.start("heavy_mma", ms)
             if self.A is not None:
                 nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
-                         self.kpad, 0, self.kpad, x0, x1 - x0, self._bitmap_mode(), 0, nat.ptr(bufs[b]), self.wpr,
+                         self.mma_kpad, 0, self.mma_kpad, x0, x1 - x0, self._bitmap_mode(), 0, nat.ptr(bufs[b]), self.wpr,
                          nat.ptr(self.nnz), self.mma_ctas, sst)
             if timer is not None:
                 timer.stop("heavy_mma", ms)
@@ -568,7 +591,7 @@ class TwoPathEngine:
                 timer.start("heavy_mma", main)
             if self.A is not None:
                 nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
-                         self.kpad, 0, self.kpad, x0, rows, self._bitmap_mode(), 0, nat.ptr(buf), self.wpr,
+                         self.mma_kpad, 0, self.mma_kpad, x0, rows, self._bitmap_mode(), 0, nat.ptr(buf), self.wpr,
                          nat.ptr(self.nnz), 0, mst)
             if timer is not None:
                 timer.stop("heavy_mma", main)
