@@ -343,7 +343,14 @@ def run_b200(args):
     if args.x_limit:
         x_hi = min(x_hi, x_lo + args.x_limit)
     dr = device_relation(r)
-    ds = dr if s is r else device_relation(s)
+    if s is r:
+        ds = dr
+    elif world > 1:
+        # S replicated from rank 0 over NVLink (NCCL broadcast of its CSR)
+        from paper_2002_12459_b200.shard import replicate_relation
+        ds = replicate_relation(device_relation(s) if rank == 0 else None, 0)
+    else:
+        ds = device_relation(s)
     d1, d2 = (plan.delta1, plan.delta2) if plan.strategy != FULL_JOIN else (max(r.n, s.n),) * 2
     ws = Workspace()
 

@@ -64,3 +64,59 @@ def two_path_join_shard(r, s, plan=None, rank: int = 0, world: int = 1, want_cou
     counts = (_np.concatenate([p.counts for p in parts]) if parts else _np.empty(0, _np.int64)) if want_counts else None
     dims = (r.rel.dom_left, s.rel.dom_left)
     return OutputSet(codes, dims, counts, {"x_range": (lo, hi), "rank": rank, "world": world})
+
+
+REL_FIELDS = ("fwd_ptr", "fwd_idx", "fwd_row", "rev_ptr", "rev_idx", "left_deg", "right_deg")
+
+
+def replicate_relation(dr, src: int = 0, group=None):
+    """Replicate a device relation (the S side, or S_h's source) from rank
+    `src` to every rank of the process group: one broadcast per CSR array
+    (NCCL over NVLink on GPUs; any backend whose tensors live where `dr`'s
+    do).  Non-source ranks pass an object with the same fields, or None and
+    receive a fresh one; sizes travel first so they need no host copy of S.
+    SURVEY.md 8(e): S is replicated, R sharded by x range."""
+    import torch
+    import torch.distributed as dist
+    from .device import DeviceRelation
+    rank = dist.get_rank(group)
+    if rank == src:
+        dev = dr.fwd_ptr.device
+        meta = torch.tensor([dr.n, dr.dom_left, dr.dom_right], dtype=torch.int64, device=dev)
+    else:
+        dev = _group_device(group)
+        meta = torch.zeros(3, dtype=torch.int64, device=dev)
+    dist.broadcast(meta, src, group=group)
+    n, dom_l, dom_r = (int(v) for v in meta.tolist())
+    if rank != src:
+        dr = DeviceRelation()
+        dr.fwd_ptr_host = None
+        dr.n, dr.dom_left, dr.dom_right = n, dom_l, dom_r
+        dr.device = dev
+        sizes = {"fwd_ptr": dom_l + 1, "fwd_idx": n, "fwd_row": n, "rev_ptr": dom_r + 1, "rev_idx": n,
+                 "left_deg": dom_l, "right_deg": dom_r}
+        for k in REL_FIELDS:
+            setattr(dr, k, torch.empty(sizes[k], dtype=torch.int32, device=dev))
+        dr.h2d_bytes = 0
+    for k in REL_FIELDS:
+        dist.broadcast(getattr(dr, k), src, group=group)
+    if getattr(dr, "fwd_ptr_host", None) is None:
+        dr.fwd_ptr_host = dr.fwd_ptr.cpu().numpy().astype(np.int64)
+    return dr
+
+
+def global_right_degrees(local_deg, group=None):
+    """deg_R(y) of an x-sharded R: the sum of the shards' y-degree vectors
+    (all-reduce; the heavy/light split of joinproject.py:178-180 needs the
+    global degree).  In place on `local_deg`, returned for chaining."""
+    import torch.distributed as dist
+    dist.all_reduce(local_deg, op=dist.ReduceOp.SUM, group=group)
+    return local_deg
+
+
+def _group_device(group):
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")

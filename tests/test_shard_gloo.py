@@ -14,7 +14,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from conftest import ROOT, zipf_pairs
+from conftest import ROOT, random_pairs, zipf_pairs
 
 
 def _free_port():
@@ -86,3 +86,56 @@ def test_gloo_two_ranks_concatenate_to_full():
     assert ok
     assert sum(sizes) > 0 and all(x > 0 for x in sizes)
     assert tmax == pytest.approx(0.02)
+
+
+def _replicate_worker(rank, world, port, out):
+    try:
+        _replicate_body(rank, world, port, out)
+    except Exception as e:  # noqa: BLE001 - report to the parent
+        out.put((rank, repr(e)))
+
+
+def _replicate_body(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_12459_b200.device import DeviceRelation
+    from paper_2002_12459_b200.relation import Relation, build_indexed
+    from paper_2002_12459_b200.shard import global_right_degrees, replicate_relation
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    rng = np.random.default_rng(5)
+    sp = np.array(random_pairs(rng, 3000, 200, 90), dtype=np.int64)
+    S = build_indexed(Relation.from_raw_pairs("S", sp))
+    src = None
+    if rank == 0:          # a CPU stand-in for the device copy (gloo broadcasts CPU tensors)
+        src = DeviceRelation()
+        src.n, src.dom_left, src.dom_right = S.rel.n, S.rel.dom_left, S.rel.dom_right
+        host = {"fwd_ptr": S.fwd_indptr, "fwd_idx": S.fwd_indices, "rev_ptr": S.rev_indptr,
+                "rev_idx": S.rev_indices, "left_deg": S.left_deg, "right_deg": S.right_deg,
+                "fwd_row": np.repeat(np.arange(S.rel.dom_left), S.left_deg)}
+        for k, v in host.items():
+            setattr(src, k, torch.from_numpy(np.ascontiguousarray(v, dtype=np.int32)))
+    got = replicate_relation(src, 0)
+    ok = (got.n == S.rel.n and np.array_equal(got.rev_idx.numpy(), S.rev_indices)
+          and np.array_equal(got.fwd_ptr.numpy(), S.fwd_indptr) and np.array_equal(got.fwd_ptr_host, S.fwd_indptr))
+    # x-sharded R: per-shard y degrees all-reduce to the global ones
+    rp = np.array(random_pairs(rng, 4000, 300, 90), dtype=np.int64)
+    mine = rp[(rp[:, 0] % world) == rank]
+    local = torch.from_numpy(np.bincount(mine[:, 1], minlength=90).astype(np.int64))
+    glob = global_right_degrees(local)
+    ok = ok and np.array_equal(glob.numpy(), np.bincount(rp[:, 1], minlength=90))
+    out.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+def test_gloo_replicate_relation_and_global_degrees():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replicate_worker, args=(k, 2, port, q)) for k in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=120) for _ in procs), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [(0, True), (1, True)]

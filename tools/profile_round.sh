@@ -15,6 +15,6 @@ $LL > $OUT/ll_plain.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $LL > $OUT/ll_ncu.log 2>&1
 FC="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --chunk-rows 4096 --x-limit 16384"
 $FC > $OUT/full_plain.json 2>&1 && \
-  ncu --set full --import-source on --clock-control none -k regex:"k_emit|heavy_mma_kernel|k_tile_merge" -s 6 -c 3 \
+  ncu --set full --import-source on --clock-control none -k regex:"k_merge_emit|heavy_mma_kernel" -s 4 -c 2 \
       -o $OUT/full_mma_merge_emit $FC > $OUT/full_ncu.log 2>&1
 ls -la $OUT
