@@ -10,7 +10,7 @@ mkdir -p $OUT
 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err || exit 1
 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 python tools/bench_configs.py > $OUT/configs.jsonl 2> $OUT/configs.err
-LL="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+LL="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-light-work"
 $LL > $OUT/ll_plain.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $LL > $OUT/ll_ncu.log 2>&1
 FC="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --chunk-rows 4096 --x-limit 16384"
