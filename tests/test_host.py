@@ -165,6 +165,32 @@ def test_capi_host_only_queries():
     assert lib.mmj_scan_workspace_bytes(10 ** 6) > 0
     assert lib.mmj_tile_count(2048, 15648 // 32 * 32) > 0
     assert lib.mmj_bitmap_segment_count(64) == 2
+    # fused tail: 16-byte ticket + one status word per 8192-word tile; cfg2 rows of
+    # 15648 words split in two column blocks
+    assert lib.mmj_merge_emit_col_blocks(15648) == 2
+    assert lib.mmj_merge_emit_col_blocks(1024) == 1
+    assert lib.mmj_merge_emit_workspace_size(16384, 15648) == 16 + 8 * 16384 * 2
+    assert lib.mmj_merge_emit_workspace_size(100, 32) == 16 + 8 * 1   # 256 rows per tile
+
+
+def test_capi_argument_errors_without_gpu():
+    """Argument checks run before any CUDA call (no GPU needed)."""
+    import ctypes
+    from paper_2002_12459_b200 import _native
+    if not _native.lib_path().exists():
+        pytest.skip("libmmjoin_b200.so not built")
+    lib = _native.load()
+    # a pitch that is not a multiple of 32 words
+    rc = lib.mmj_merge_emit(None, 0, 0, 4, 33, 1000, None, None, None, 1, None, None, None, None, None, None, None,
+                            None, None, None, None, 0, None)
+    assert rc == 1 and b"multiple of 32" in lib.mmj_last_error()
+    # a workspace smaller than mmj_merge_emit_workspace_size
+    rc = lib.mmj_merge_emit(None, 0, 0, 4, 32, 1000, None, None, None, 1, None, None, None, None, None, None, None,
+                            None, None, None, ctypes.c_void_p(16), 8, None)
+    assert rc == 5 and b"workspace" in lib.mmj_last_error()
+    # heavy product modes outside the enum
+    rc = lib.mmj_heavy_mma(None, 256, None, 256, 128, 0, 128, 0, 128, 7, 0, None, 8, None, 0, None)
+    assert rc == 1 and b"unknown mode" in lib.mmj_last_error()
 
 
 def test_product_fails_loudly_without_gpu():
