@@ -52,6 +52,9 @@ extern "C" {
                                   uint16 elements, multiple of 8 */
 #define MMJ_MODE_UPPER 16      /* OR-flag: self-join, skip tiles whose columns are all <= their rows
                                   (cells there are left unwritten; consumers keep z > x only) */
+#define MMJ_MODE_COLOC 32      /* OR-flag for MMJ_MODE_BITMAP_PAIR: the co-resident build (<= 85
+                                  registers, 2-stage ring, ~97 KB shared memory) that fits on an SM
+                                  beside two CTAs of mmj_merge_emit */
 
 int mmj_abi_version(void);
 const char* mmj_last_error(void);

@@ -29,6 +29,7 @@ MODE_BITMAP_PAIR = 4
 MODE_COUNT16 = 5
 MODE_BITMAP_TRIPLE = 6
 MODE_UPPER = 16
+MODE_COLOC = 32
 
 P = C.c_void_p
 I64 = C.c_int64

@@ -152,9 +152,11 @@ int mmj_light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0,
 int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_rows, int64_t kpad, int64_t k_off,
                   int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out, int64_t ld_out,
                   unsigned long long* nnz, int max_ctas, void* stream) {
-  const int base_mode = mode & ~MMJ_MODE_UPPER;
+  const int base_mode = mode & ~(MMJ_MODE_UPPER | MMJ_MODE_COLOC);
+  const int upper = mode & MMJ_MODE_UPPER, coloc = mode & MMJ_MODE_COLOC;
   if (base_mode < 0 || base_mode > MMJ_MODE_BITMAP_TRIPLE ||
-      (mode != base_mode && base_mode != MMJ_MODE_COUNT32 && base_mode != MMJ_MODE_COUNT16)) {
+      (upper && base_mode != MMJ_MODE_COUNT32 && base_mode != MMJ_MODE_COUNT16) ||
+      (coloc && base_mode != MMJ_MODE_BITMAP_PAIR)) {
     mmj::set_error("heavy_mma: unknown mode %d (MMJ_MODE_UPPER combines with the count modes only)", mode);
     return MMJ_ERR_ARG;
   }

@@ -73,7 +73,7 @@ static_assert(SMEM_MAX <= 227 * 1024, "shared memory budget");
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
 enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, BITMAP_PAIR = 4, COUNT16 = 5, BITMAP_TRIPLE = 6,
-                  MODE_UPPER = 16 };
+                  MODE_UPPER = 16, MODE_COLOC = 32 };
 
 struct Params {
   int64_t m_begin;      // first A row of this launch (multiple of BM not required)
@@ -328,7 +328,12 @@ __device__ __forceinline__ bool below_diagonal(const Params& p, TileCoord c) {
 }
 
 // ----------------------------------------------------------------- the kernel
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// MINB = 2: the co-resident build (<= 85 registers, used with a 2-stage ring,
+// ~97 KB of shared memory) that leaves room on every SM for two CTAs of the
+// fused projection tail, so a chunk's heavy product (TMEM-read-bound) runs
+// beside the previous chunk's emission (HBM-write-bound).
+template <int MINB>
+__global__ void __launch_bounds__(NUM_THREADS, MINB)
     heavy_mma_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -426,7 +431,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (++acc == ACC_STAGES) { acc = 0; acc_ph ^= 1; }
       }
     }
-  } else if (warp >= 4 && p.alt) {
+  } else if (warp >= 4 && (MINB == 2 || p.alt)) {
     // ------------------------------------------------------- epilogue, alternating groups
     // Warps 4-7 (group 0) take the CTA's even tiles (accumulator stage 0),
     // warps 8-11 (group 1) the odd ones (stage 1), each warp all 256 columns
@@ -449,7 +454,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int64_t row = (int64_t)c.m_blk * BM + q * 32 + lane;
       const bool row_ok = row < p.m_rows;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (p.mode == BITMAP_TRIPLE) {
+      if (MINB == 1 && p.mode == BITMAP_TRIPLE) {
         constexpr int NWT = 3 * BN / 32;   // 24 words
         uint32_t w[NWT];
         // two 32-column loads in flight per wait (the TMEM load latency,
@@ -483,20 +488,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {   // BITMAP_PAIR
         constexpr int NW = BN / 16;        // 16 words
         uint32_t w[NW];
+        if (MINB == 1) {
 #pragma unroll
-        for (int j = 0; j < BN / 128; ++j) {
-          uint32_t r[64];
-          uint32_t* r1 = r + 32;
-          TMEM_LD_32x32b_X32_PACK16(taddr + 128 * j, r);
-          TMEM_LD_32x32b_X32_PACK16(taddr + 128 * j + 64, r1);
-          tmem_wait_ld();
-          if (j == BN / 128 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+          for (int j = 0; j < BN / 128; ++j) {
+            uint32_t r[64];
+            uint32_t* r1 = r + 32;
+            TMEM_LD_32x32b_X32_PACK16(taddr + 128 * j, r);
+            TMEM_LD_32x32b_X32_PACK16(taddr + 128 * j + 64, r1);
+            tmem_wait_ld();
+            if (j == BN / 128 - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[acc]);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w[8 * j + k] = pack_bits_pair(r + 8 * k);
           }
+        } else {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) w[8 * j + k] = pack_bits_pair(r + 8 * k);
+          for (int j = 0; j < BN / 64; ++j) {
+            uint32_t r[32];
+            TMEM_LD_32x32b_X32_PACK16(taddr + 64 * j, r);
+            tmem_wait_ld();
+            if (j == BN / 64 - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[acc]);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[4 * j + k] = pack_bits_pair(r + 8 * k);
+          }
         }
         if (row_ok) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + (int64_t)c.n_blk * NW;
@@ -514,7 +535,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int o = 16; o > 0; o >>= 1) my_nnz += __shfl_xor_sync(0xffffffffu, my_nnz, o);
       if (lane == 0 && my_nnz) atomicAdd(p.nnz, my_nnz);
     }
-  } else if (warp >= 4) {
+  } else if (MINB == 1 && warp >= 4) {
     // ------------------------------------------------------- epilogue
     const int q = warp & 3;              // TMEM lane quadrant
     const int grp = (warp - 4) >> 2;     // CW-column group of the 256-column tile
@@ -755,7 +776,12 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
                      int64_t k_off, int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out,
                      int64_t ld_out, unsigned long long* nnz, int max_ctas, cudaStream_t st) {
   const int upper = (mode & MODE_UPPER) ? 1 : 0;
-  mode &= ~MODE_UPPER;
+  const bool coloc = (mode & MODE_COLOC) != 0;
+  mode &= ~(MODE_UPPER | MODE_COLOC);
+  if (coloc && mode != BITMAP_PAIR) {
+    set_error("heavy_mma: MMJ_MODE_COLOC is built for MMJ_MODE_BITMAP_PAIR only");
+    return MMJ_ERR_ARG;
+  }
   if (kpad <= 0 || kpad % BK != 0 || k_off < 0 || k_len <= 0 || k_off % BK != 0 || k_len % BK != 0 ||
       k_off + k_len > kpad) {
     set_error("heavy_mma: K window [%lld,+%lld) of pitch %lld must be multiples of %d", (long long)k_off,
@@ -850,16 +876,26 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   p.nnz = nnz;
   static bool attr_set = false;
   if (!attr_set) {
-    MMJ_TRY(cuda_status(cudaFuncSetAttribute(heavy_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MMJ_TRY(cuda_status(cudaFuncSetAttribute(heavy_mma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              SMEM_MAX),
                         "cudaFuncSetAttribute(heavy_mma)"));
+    MMJ_TRY(cuda_status(cudaFuncSetAttribute(heavy_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem_bytes_for(2, false)),
+                        "cudaFuncSetAttribute(heavy_mma coloc)"));
     attr_set = true;
+  }
+  if (coloc) {
+    p.stages = 2;
+    p.alt = 1;
   }
   const int64_t tiles = ceil_div(m_rows, BM) * ceil_div(b_rows, BN);
   int grid = sm_count();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (tiles < grid) grid = (int)tiles;
-  heavy_mma_kernel<<<grid, NUM_THREADS, smem_bytes_for(p.stages, staged), st>>>(ma, mb, p);
+  if (coloc)
+    heavy_mma_kernel<2><<<grid, NUM_THREADS, smem_bytes_for(p.stages, staged), st>>>(ma, mb, p);
+  else
+    heavy_mma_kernel<1><<<grid, NUM_THREADS, smem_bytes_for(p.stages, staged), st>>>(ma, mb, p);
   MMJ_CHECK_LAUNCH("heavy_mma_kernel");
   return MMJ_OK;
 }

@@ -455,23 +455,24 @@ class TwoPathEngine:
         return ChunkResult(x0, x1, total, codes[:total], None, light)
 
     def run_mma_ahead(self, x_begin: int = 0, x_end: Optional[int] = None, timer=None):
-        """Projection with the heavy product of chunk i+1 running on a side
-        stream while chunk i's light merge, scan and emission run in order on
-        the current stream (the tensor-core kernel overlaps the HBM-bound
-        emission; the latency-bound merge keeps its SMs).  Chunk bitmaps are
-        double-buffered."""
+        """Projection with the heavy product of chunk i+1 running on a
+        high-priority side stream while chunk i's fused tail (mmj_merge_emit)
+        runs on a low-priority one.  The product uses the co-resident build
+        (MMJ_MODE_COLOC: <= 85 registers, 2-stage ring) when the operand is in
+        z-pair form, so each SM hosts one product CTA beside two tail CTAs:
+        the TMEM-read-bound product overlaps the HBM-write-bound emission.
+        Chunk bitmaps are double-buffered; codes go to one reused buffer
+        (streaming consumer).  Without the fused tail (MMJ_FUSED_EMIT=0) the
+        three-kernel tail is used."""
         if not self.fused:
             raise ValueError("run_mma_ahead needs the bitmap (no counts) path")
         torch = self.torch
         self.prepare()
         dr, ds = self.dr, self.ds
         caller = torch.cuda.current_stream()
-        lo_pri, hi_pri = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
         if getattr(self, "_mma_stream", None) is None:
-            # the in-order merge -> scan -> emit chain is the critical path: give
-            # it the high-priority stream so its CTAs are scheduled ahead of the
-            # side-stream heavy product's
-            self._mma_stream, self._main_stream = _stream_pair("mma_ahead")
+            lo, hi = _stream_pair("mma_ahead")
+            self._mma_stream, self._main_stream = hi, lo
         ms = self._mma_stream
         main = self._main_stream
         main.wait_stream(caller)
@@ -486,6 +487,11 @@ class TwoPathEngine:
         bufs = [self.ws.get(f"bm{b}", rows_max * self.wpr, torch.int32) for b in (0, 1)]
         freed = [None, None]
         mma_done = {}
+        coloc = self.pairs and not self.triple and __import__("os").environ.get("MMJ_COLOC", "1") != "0"
+        mode = self._bitmap_mode() | (nat.MODE_COLOC if coloc else 0)
+        spf, spl = self._list_splits() if self.one_kernel_tail else (0, 0)
+        wsb = int(self.lib.mmj_merge_emit_workspace_size(rows_max, self.wpr))
+        fws = self.ws.get("fuse_ws", wsb, torch.uint8)
 
         def issue_mma(i):
             x0, x1 = bounds[i]
@@ -496,7 +502,7 @@ class TwoPathEngine:
                 timer.start("heavy_mma", ms)
             if self.A is not None:
                 nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
-                         self.mma_kpad, 0, self.mma_kpad, x0, x1 - x0, self._bitmap_mode(), 0, nat.ptr(bufs[b]), self.wpr,
+                         self.mma_kpad, 0, self.mma_kpad, x0, x1 - x0, mode, 0, nat.ptr(bufs[b]), self.wpr,
                          nat.ptr(self.nnz), self.mma_ctas, sst)
             if timer is not None:
                 timer.stop("heavy_mma", ms)
@@ -504,42 +510,49 @@ class TwoPathEngine:
             ev.record(ms)
             mma_done[i] = ev
 
-        merge_first = __import__("os").environ.get("MMJ_MERGE_FIRST", "0") == "1"
         if bounds:
             issue_mma(0)
         for i, (x0, x1) in enumerate(bounds):
-            if i + 1 < len(bounds) and not merge_first:
+            if i + 1 < len(bounds):
                 issue_mma(i + 1)
             b = i & 1
             rows = x1 - x0
-            nseg = rows * self.wpr // 32
             buf = bufs[b]
-            segcnt = self.ws.get("segcnt", rows_max * self.wpr // 32, torch.int32)
-            segoff = self.ws.get("segoff", rows_max * self.wpr // 32 + 1, torch.int64)
             main.wait_event(mma_done.pop(i))
-            if timer is not None:
-                timer.start("light_merge", main)
-            nat.call("mmj_tile_merge", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
-                     nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp,
-                     nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(self.wit), mst)
-            if timer is not None:
-                timer.stop("light_merge", main)
-            if i + 1 < len(bounds) and merge_first:
-                issue_mma(i + 1)
-            if timer is not None:
-                timer.start("segments", main)
-            nat.call("mmj_exclusive_scan_i32", nat.ptr(segcnt), nat.ptr(segoff), nseg,
-                     nat.ptr(self.ws.scan_ws(rows_max * self.wpr // 32)), mst)
-            if timer is not None:
-                timer.stop("segments", main)
-                timer.start("emit", main)
-            nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dom_z,
-                     nat.ptr(codes), mst)
-            if timer is not None:
-                timer.stop("emit", main)
             with torch.cuda.stream(main):
                 slot = self._async_slot()
-                slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
+            if self.one_kernel_tail:
+                if timer is not None:
+                    timer.start("merge_emit", main)
+                nat.call("mmj_merge_emit", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
+                         nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp,
+                         nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, nat.ptr(self.wit),
+                         nat.ptr(codes), nat.ptr(slot), nat.ptr(fws), wsb, mst)
+                if timer is not None:
+                    timer.stop("merge_emit", main)
+            else:
+                nseg = rows * self.wpr // 32
+                segcnt = self.ws.get("segcnt", rows_max * self.wpr // 32, torch.int32)
+                segoff = self.ws.get("segoff", rows_max * self.wpr // 32 + 1, torch.int64)
+                if timer is not None:
+                    timer.start("light_merge", main)
+                nat.call("mmj_tile_merge", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
+                         nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp,
+                         nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(self.wit), mst)
+                if timer is not None:
+                    timer.stop("light_merge", main)
+                    timer.start("segments", main)
+                nat.call("mmj_exclusive_scan_i32", nat.ptr(segcnt), nat.ptr(segoff), nseg,
+                         nat.ptr(self.ws.scan_ws(rows_max * self.wpr // 32)), mst)
+                if timer is not None:
+                    timer.stop("segments", main)
+                    timer.start("emit", main)
+                nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dom_z,
+                         nat.ptr(codes), mst)
+                if timer is not None:
+                    timer.stop("emit", main)
+                with torch.cuda.stream(main):
+                    slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(main)
             freed[b] = ev
