@@ -167,7 +167,9 @@ int mmj_emit_codes(const uint32_t* bitmap, const int64_t* seg_off, int64_t rows,
  * decoupled look-back over per-tile status words, then emit.  codes must hold
  * the chunk's output (rows*dom_z is always enough); *total receives its size.
  * ws: caller-owned workspace of mmj_merge_emit_workspace_size(rows, wpr)
- * bytes (reset by the call, on `stream`). */
+ * bytes (reset by the call, on `stream`).  fwd_ptr == NULL: no light merge
+ * (the bitmap is complete; e.g. the star path, whose light part is OR-ed in
+ * by mmj_star_light): segment scan + look-back + emission only. */
 size_t mmj_merge_emit_workspace_size(int64_t rows, int64_t wpr);
 int mmj_merge_emit(const uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,

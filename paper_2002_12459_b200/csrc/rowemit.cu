@@ -573,7 +573,8 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     for (int i = tid; i < words; i += NT) sbm[i] = 0;
   }
   const int64_t xa = a.x0 + r0, xb = a.x0 + r1;
-  const int64_t t_begin = a.fwd_ptr[xa], t_end = a.fwd_ptr[xb];
+  // fwd_ptr == nullptr: the bitmap is already complete (no light witnesses to merge)
+  const int64_t t_begin = a.fwd_ptr ? a.fwd_ptr[xa] : 0, t_end = a.fwd_ptr ? a.fwd_ptr[xb] : 0;
   __syncthreads();
   if (a.has_heavy) bar_wait0(&sm.bar);
   unsigned long long my_w = merge_light<NT>(a, sbm, xa, xb, t_begin, t_end, zlo, zhi, cw, cbi, sm.scan_tmp, sm.u.m.tb_len,

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from typing import Optional, Sequence
 
 import numpy as np
@@ -102,6 +103,8 @@ class StarEngine:
         self.x1_per_chunk = max(1, chunk_bytes // max(row_bytes * self.row_per_x1, 1))
         self.nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.wit = torch.zeros(1, dtype=torch.int64, device="cuda")
+        # projection tail: scan + look-back + emission in one kernel (MMJ_FUSED_EMIT=0: scan, then emission)
+        self.one_kernel_tail = os.environ.get("MMJ_FUSED_EMIT", "1") != "0"
 
     def prepare(self):
         torch = self.torch
@@ -199,6 +202,20 @@ class StarEngine:
                 else:
                     codes_out.append(codes[:total].cpu().numpy())
                     counts_out.append(cnts[:total].cpu().numpy().astype(np.int64))
+            elif self.one_kernel_tail:
+                # scan + look-back + emission in one kernel (mmj_merge_emit with
+                # no light lists: mmj_star_light already OR-ed them in)
+                wsb = int(self.lib.mmj_merge_emit_workspace_size(rows, self.wpr))
+                fws = self.ws.get("fuse_ws", wsb, torch.uint8)
+                codes = self.ws.get("codes", rows * self.dk, torch.int64)
+                tot = self.ws.get("star_total", 1, torch.int64)
+                nat.call("mmj_merge_emit", nat.ptr(buf), 1, x0, rows, self.wpr, self.dk, 0, 0, 0, 0, 0, 0, 0, 0, 0,
+                         0, 0, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(tot), nat.ptr(fws), wsb, st)
+                total = int(tot.item())
+                if sink is not None:
+                    sink(xa, xb, codes[:total], None)
+                else:
+                    codes_out.append(codes[:total].cpu().numpy())
             else:
                 nwords = rows * self.wpr
                 nseg = int(self.lib.mmj_bitmap_segment_count(nwords))
