@@ -26,7 +26,7 @@ INCLUDE = PKG.parent / "include"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v"]
+         "-Xptxas", "-v"] + os.environ.get("MMJ_NVCC_EXTRA", "").split()
 
 
 def _nvcc() -> str:

@@ -26,6 +26,7 @@
 // every code is written once: emission is bound by the HBM write of the
 // sorted output (8 B per distinct (x, z)).
 #include <cub/block/block_scan.cuh>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -504,6 +505,7 @@ struct FuseArgs {
   unsigned long long* status;
   int64_t* total;           // chunk code count (written by the last tile)
   int64_t* codes;
+  int dbg;                  // debug bisection flags (MMJ_DEBUG_BOUNDS builds)
 };
 
 constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
@@ -707,6 +709,356 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent, warp-specialised form of k_merge_emit: one producer warp per CTA
+// prepares tile i+1 (ticket, bulk copy of the heavy bits, light merge,
+// segment scan, decoupled look-back) in one shared-memory buffer while NEW
+// emitter warps write tile i's codes from the other, so the tile's
+// pre-emission latency (dependent list loads, the look-back) no longer idles
+// the emitters.  Buffers hand over through mbarriers (full: producer ->
+// emitters, empty: emitters -> producer).  Deadlock-free: a producer takes a
+// ticket only when it holds a free buffer, and a tile's look-back only waits
+// on tiles whose tickets were taken earlier by producers that are not blocked.
+__device__ __forceinline__ void mbar_wait_par(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// light witnesses of one tile OR-ed in by a single warp (32 R tuples per batch)
+__device__ __forceinline__ unsigned long long merge_light_warp(const TileArgs& a, uint32_t* sbm, int64_t xa,
+                                                               int64_t xb, int64_t t_begin, int64_t t_end,
+                                                               int32_t zlo, int32_t zhi, int cw, int cbi) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long my_w = 0;
+  for (int64_t tb = t_begin; tb < t_end; tb += 32) {
+    const int64_t t = tb + lane;
+    int len = 0, row = 0, filt = 0;
+    const int32_t* base = nullptr;
+    if (t < t_end) {
+      int64_t lo = xa, hi = xb;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a.fwd_ptr[mid] <= t) lo = mid;
+        else hi = mid;
+      }
+      row = (int)(lo - xa);
+      const int32_t y = a.fwd_idx[t];
+      const bool full = (a.hpos == nullptr) || (a.hpos[y] < 0) || (a.rdeg_x[lo] <= a.d2);
+      int32_t b, e;
+      if (full) {
+        b = a.s_rev_ptr[y];
+        e = a.s_rev_ptr[y + 1];
+        base = a.s_rev_idx + b;
+      } else {
+        b = a.lz_ptr[y];
+        e = a.lz_ptr[y + 1];
+        base = a.lz_idx + b;
+      }
+      len = e - b;
+      if (a.ncb > 1) {
+        const int32_t* sp = full ? a.split_full : a.split_lz;
+        if (sp != nullptr) {
+          const int32_t* q = sp + (int64_t)y * (a.ncb + 1) + cbi;
+          const int32_t lb = q[0], ub = q[1];
+          base += lb - b;
+          len = ub - lb;
+        } else if (len > SHORT_LIST) {
+          const int lb = lower_bound_i32(base, len, zlo);
+          const int ub = lb + lower_bound_i32(base + lb, len - lb, zhi);
+          base += lb;
+          len = ub - lb;
+        } else {
+          filt = 1;
+        }
+      }
+    }
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const int excl = incl - len;
+    const int nt = (int)min((int64_t)32, t_end - tb);
+    int ti = 0;
+    // warp-uniform trip count: the cursor below uses full-warp shuffles
+    for (int s00 = 0; s00 < tot; s00 += MERGE_ILP * 32) {
+      const int s0 = s00 + lane;
+      int32_t zv[MERGE_ILP];
+      int rowv[MERGE_ILP];
+      bool ok[MERGE_ILP];
+#pragma unroll
+      for (int u = 0; u < MERGE_ILP; ++u) {
+        const int sidx = s0 + u * 32;
+        ok[u] = sidx < tot;
+        rowv[u] = 0;
+        zv[u] = 0;
+        // tuple of slot sidx: the last tuple whose exclusive offset is <= sidx
+        // (tuples are scanned from the cursor; slots only grow)
+        while (true) {
+          const int nx = __shfl_sync(0xffffffffu, excl, min(ti + 1, 31));
+          const bool adv = ok[u] && ti + 1 < nt && nx <= sidx;
+          if (!__any_sync(0xffffffffu, adv)) break;
+          if (adv) ++ti;
+        }
+        const int e0 = __shfl_sync(0xffffffffu, excl, ti);
+        const int32_t* bs = reinterpret_cast<const int32_t*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(base), ti));
+        const int rw = __shfl_sync(0xffffffffu, row | (filt << 30), ti);
+        if (ok[u]) {
+#ifdef MMJ_DEBUG_BOUNDS
+          if (bs == nullptr || sidx - e0 < 0) {
+            printf("merge_light_warp: bad slot %d e0 %d ti %d nt %d tot %d\n", sidx, e0, ti, nt, tot);
+            __trap();
+          }
+#endif
+          zv[u] = __ldg(bs + (sidx - e0));
+          rowv[u] = rw;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < MERGE_ILP; ++u) {
+        if (!ok[u]) continue;
+        const int32_t z = zv[u];
+        if ((rowv[u] >> 30) && (z < zlo || z >= zhi)) continue;
+        atomicOr(&sbm[(rowv[u] & 0x3FFFFFFF) * cw + ((z - zlo) >> 5)], 1u << (z & 31));
+        ++my_w;
+      }
+    }
+  }
+  return my_w;
+}
+
+template <int TW, int NEW>
+struct PSmem {
+  uint32_t bm[2][TW];
+  int segoff[2][TW / 32];
+  uint16_t stage[NEW][1024 + 8];
+  long long prefix[2];
+  int tile[2];
+  int nseg[2];
+  int next_seg[2];
+  __align__(8) uint64_t full[2];
+  __align__(8) uint64_t empty[2];
+  __align__(8) uint64_t tbar[2];
+};
+
+template <int TW, int NEW>
+__global__ void __launch_bounds__((NEW + 1) * 32, 4) k_merge_emit_p(const FuseArgs f) {
+  extern __shared__ __align__(16) uint8_t p_raw[];
+  PSmem<TW, NEW>& sm = *reinterpret_cast<PSmem<TW, NEW>*>(p_raw);
+  const TileArgs& a = f.t;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.full[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&sm.empty[b])), "r"(NEW));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.tbar[b])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NEW) {
+    // ------------------------------------------------------------ producer
+    unsigned long long wit = 0;
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      const uint32_t use = (uint32_t)(k >> 1);
+      mbar_wait_par(&sm.empty[b], (use & 1) ^ 1);
+      unsigned int tk = 0;
+      if (lane == 0) tk = atomicAdd(f.ticket, 1u);
+      tk = __shfl_sync(0xffffffffu, tk, 0);
+      if ((int64_t)tk >= f.ntiles) {
+        if (lane == 0) {
+          sm.tile[b] = -1;
+          mbar_arrive_cta(&sm.full[b]);
+        }
+        break;
+      }
+      const int64_t tile = tk;
+      const int64_t rg = tile / a.ncb;
+      const int cbi = (int)(tile - rg * a.ncb);
+      const int64_t r0 = rg * a.G;
+      const int64_t r1 = min(r0 + (int64_t)a.G, a.rows);
+      const int64_t c0w = (int64_t)cbi * a.cb_words;
+      const int cw = (int)min((int64_t)a.cb_words, a.wpr - c0w);
+      const int words = (int)(r1 - r0) * cw;
+      const int32_t zlo = (int32_t)(c0w * 32);
+      const int32_t zhi = (int32_t)min((c0w + cw) * 32, a.dom_z);
+      uint32_t* sbm = sm.bm[b];
+#ifdef MMJ_DEBUG_BOUNDS
+      if (words > TW || words <= 0 || cw <= 0 || r1 <= r0) {
+        printf("producer tile %lld words %d cw %d r0 %lld r1 %lld G %d ncb %d\n", (long long)tile, words, cw,
+               (long long)r0, (long long)r1, a.G, a.ncb);
+        __trap();
+      }
+#endif
+      if (a.has_heavy) {
+        if (lane == 0) bulk_g2s(sbm, a.bm + r0 * a.wpr + c0w, (uint32_t)words * 4u, &sm.tbar[b]);
+      } else {
+        for (int i = lane; i < words; i += 32) sbm[i] = 0;
+      }
+      const int64_t xa = a.x0 + r0, xb = a.x0 + r1;
+      const int64_t t_begin = a.fwd_ptr ? a.fwd_ptr[xa] : 0, t_end = a.fwd_ptr ? a.fwd_ptr[xb] : 0;
+      if (a.has_heavy) mbar_wait_par(&sm.tbar[b], use & 1);
+      __syncwarp();
+#ifdef MMJ_DEBUG_BOUNDS
+      if (!(f.dbg & 1))
+#endif
+      wit += merge_light_warp(a, sbm, xa, xb, t_begin, t_end, zlo, zhi, cw, cbi);
+      __syncwarp();
+      // segment counts and their exclusive scan (nseg <= TW/32, one warp)
+      const int nseg = words >> 5;
+      int run = 0;
+      for (int s0 = 0; s0 < nseg; s0 += 32) {
+        int mine = 0;
+        const int ns = min(32, nseg - s0);
+        for (int j = 0; j < ns; ++j) {
+          const int c = __reduce_add_sync(0xffffffffu, __popc(sbm[(s0 + j) * 32 + lane]));
+          if (lane == j) mine = c;
+        }
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        if (lane < ns) sm.segoff[b][s0 + lane] = run + incl - mine;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      const long long agg = run;
+      // decoupled look-back
+      long long prefix = 0;
+      if (tile == 0) {
+        if (lane == 0) st_status(f.status, ST_INC | (unsigned long long)agg);
+      } else {
+        if (lane == 0) st_status(f.status + tile, ST_AGG | (unsigned long long)agg);
+        int64_t pos = tile - 1;
+        while (true) {
+          const int64_t idx = pos - lane;
+          unsigned long long st = idx >= 0 ? ld_status(f.status + idx) : ST_INC;
+          while (__any_sync(0xffffffffu, (st >> 62) == 0)) {
+            if ((st >> 62) == 0) st = ld_status(f.status + idx);
+          }
+          const unsigned inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+          const int stop = inc ? __ffs(inc) - 1 : 31;
+          long long val = lane <= stop ? (long long)(st & ST_VAL) : 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+          prefix += val;
+          if (inc) break;
+          pos -= 32;
+        }
+        if (lane == 0) st_status(f.status + tile, ST_INC | (unsigned long long)(prefix + agg));
+      }
+      if (lane == 0) {
+        if (tile == f.ntiles - 1) *f.total = prefix + agg;
+        sm.prefix[b] = prefix;
+        sm.tile[b] = (int)tile;
+        sm.nseg[b] = nseg;
+        sm.next_seg[b] = NEW;
+        mbar_arrive_cta(&sm.full[b]);   // release: the tile's words, offsets and info
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wit += __shfl_xor_sync(0xffffffffu, wit, o);
+    if (lane == 0 && wit) atomicAdd(a.witnesses, wit);
+  } else {
+    // ------------------------------------------------------------ emitters
+    uint16_t* stage = sm.stage[warp];
+    auto sl = [](int k) { return k ^ (((k >> 5) & 31) << 1); };
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      mbar_wait_par(&sm.full[b], (uint32_t)(k >> 1) & 1);
+      const int tile = sm.tile[b];
+      if (tile < 0) break;
+      const int64_t rg = tile / a.ncb;
+      const int cbi = (int)(tile - rg * a.ncb);
+      const int64_t r0 = rg * a.G;
+      const int64_t c0w = (int64_t)cbi * a.cb_words;
+      const int cw = (int)min((int64_t)a.cb_words, a.wpr - c0w);
+      const int segs_per_piece = cw >> 5;
+      const int nseg = sm.nseg[b];
+      const uint32_t* sbm = sm.bm[b];
+      int64_t* const codes = f.codes + sm.prefix[b];
+      for (int si = warp; si < nseg;) {
+        uint32_t word = sbm[si * 32 + lane];
+        const int c = __popc(word);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int vv = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += vv;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        const int cur = si;
+        {
+          int nx = 0;
+          if (lane == 0) nx = atomicAdd(&sm.next_seg[b], 1);
+          si = __shfl_sync(0xffffffffu, nx, 0);
+        }
+        if (tot == 0) continue;
+#ifdef MMJ_DEBUG_BOUNDS
+        if (f.dbg & 2) continue;
+#endif
+        const int rr = cur / segs_per_piece;
+        const int64_t base = (a.x0 + r0 + rr) * a.dom_z + (c0w + (int64_t)(cur - rr * segs_per_piece) * 32) * 32;
+        int64_t* out = codes + sm.segoff[b][cur];
+#ifdef MMJ_DEBUG_BOUNDS
+        if (sm.prefix[b] + sm.segoff[b][cur] + tot > a.rows * a.dom_z || cur >= nseg) {
+          printf("emitter: tile %d cur %d nseg %d prefix %lld segoff %d tot %d cap %lld\n", tile, cur, nseg,
+                 sm.prefix[b], sm.segoff[b][cur], tot, (long long)(a.rows * a.dom_z));
+          __trap();
+        }
+#endif
+        const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
+        const uint32_t off0 = lane * 32;
+        int kk = h + (incl - c);
+        if (__reduce_max_sync(0xffffffffu, (unsigned)c) >= 10u) {
+#pragma unroll
+          for (int bb = 0; bb < 32; ++bb) {
+            if (word & (1u << bb)) {
+              stage[sl(kk)] = (uint16_t)(off0 + bb);
+              ++kk;
+            }
+          }
+        } else {
+          while (word) {
+            const int bb = __ffs(word) - 1;
+            stage[sl(kk)] = (uint16_t)(off0 + bb);
+            ++kk;
+            word &= word - 1;
+          }
+        }
+        __syncwarp();
+        if (lane < h) st_cs(out, base + stage[sl(h)]);
+        const int np = (tot - h) >> 1;
+        for (int p = lane; p < np; p += 32) {
+          const uint32_t two = *reinterpret_cast<const uint32_t*>(stage + sl(2 * h + 2 * p));
+          st_cs2(out + h + 2 * p, base + (two & 0xFFFFu), base + (two >> 16));
+        }
+        const int done = h + 2 * np;
+        if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(h + done + lane)]);
+        __syncwarp();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&sm.empty[b]);   // this warp is done reading buffer b
+    }
+  }
+}
+
 // split[y*(ncb+1) + j] = absolute position in idx of the first entry of list
 // y (ptr[y] .. ptr[y+1], sorted) that is >= j * cb_cells
 __global__ void k_list_splits(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx, int64_t dom_y,
@@ -745,15 +1097,47 @@ void tile_geometry(int64_t wpr, int& G, int& cb, int& ncb, int64_t tile_words = 
   }
 }
 
+// MMJ_FUSE_PERSIST=1: the persistent warp-specialised tail (k_merge_emit_p,
+// 4096-word tiles); measured slower on cfg2 (191 vs 170 ms: one producer warp
+// per CTA does not keep 8 emitter warps fed), so one CTA per tile is the default
+bool fuse_persistent() {
+  static int persist = -1;
+  if (persist < 0) {
+    const char* e = getenv("MMJ_FUSE_PERSIST");
+    persist = (e && e[0] == '1') ? 1 : 0;
+  }
+  return persist != 0;
+}
+
 // tile words of the fused kernel (env MMJ_FUSE_TW: 4096 / 8192 / 16384)
 int fuse_tile_words() {
   static int tw = -1;
   if (tw < 0) {
     const char* e = getenv("MMJ_FUSE_TW");
-    tw = e ? atoi(e) : 8192;
+    tw = e ? atoi(e) : (fuse_persistent() ? 4096 : 8192);
     if (tw != 4096 && tw != 8192 && tw != 16384) tw = 8192;
   }
   return tw;
+}
+
+template <int TW, int NEW>
+int launch_merge_emit_p(const FuseArgs& f, cudaStream_t st) {
+  constexpr size_t smem = sizeof(PSmem<TW, NEW>);
+  static bool attr = false;
+  if (!attr) {
+    MMJ_TRY(cuda_status(cudaFuncSetAttribute(k_merge_emit_p<TW, NEW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem),
+                        "cudaFuncSetAttribute(k_merge_emit_p)"));
+    attr = true;
+  }
+  int per_sm = 0;
+  MMJ_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_emit_p<TW, NEW>, (NEW + 1) * 32,
+                                                                    smem),
+                      "occupancy(k_merge_emit_p)"));
+  const int64_t grid = std::min<int64_t>(f.ntiles, (int64_t)std::max(per_sm, 1) * sm_count());
+  k_merge_emit_p<TW, NEW><<<(unsigned)grid, (NEW + 1) * 32, smem, st>>>(f);
+  MMJ_CHECK_LAUNCH("k_merge_emit_p");
+  return MMJ_OK;
 }
 
 template <int TW, int NT, int MINB>
@@ -847,7 +1231,12 @@ int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int6
   f.status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 16);
   f.total = total;
   f.codes = codes;
+  {
+    const char* e = getenv("MMJ_DBG_FUSE");
+    f.dbg = e ? atoi(e) : 0;
+  }
   MMJ_TRY(cuda_status(cudaMemsetAsync(ws, 0, need, st), "merge_emit: workspace reset"));
+  if (fuse_persistent() && tw == 4096) return launch_merge_emit_p<4096, 8>(f, st);
   static int variant = -1;
   if (variant < 0) {
     const char* e = getenv("MMJ_FUSE_VARIANT");   // A/B: 1 = (4096, 256 thr, 6 CTAs/SM), 2 = (16384, 512 thr)

@@ -165,12 +165,13 @@ def test_capi_host_only_queries():
     assert lib.mmj_scan_workspace_bytes(10 ** 6) > 0
     assert lib.mmj_tile_count(2048, 15648 // 32 * 32) > 0
     assert lib.mmj_bitmap_segment_count(64) == 2
-    # fused tail: 16-byte ticket + one status word per 8192-word tile; cfg2 rows of
-    # 15648 words split in two column blocks
-    assert lib.mmj_merge_emit_col_blocks(15648) == 2
+    # fused tail: 16-byte ticket + one status word per tile (4096 or 8192 words);
+    # cfg2 rows of 15648 words split in column blocks
+    ncb = lib.mmj_merge_emit_col_blocks(15648)
+    assert ncb in (2, 4)
     assert lib.mmj_merge_emit_col_blocks(1024) == 1
-    assert lib.mmj_merge_emit_workspace_size(16384, 15648) == 16 + 8 * 16384 * 2
-    assert lib.mmj_merge_emit_workspace_size(100, 32) == 16 + 8 * 1   # 256 rows per tile
+    assert lib.mmj_merge_emit_workspace_size(16384, 15648) == 16 + 8 * 16384 * ncb
+    assert lib.mmj_merge_emit_workspace_size(100, 32) == 16 + 8 * 1   # >= 128 rows per tile
 
 
 def test_capi_argument_errors_without_gpu():
