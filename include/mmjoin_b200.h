@@ -175,13 +175,25 @@ int mmj_merge_emit(const uint32_t* bitmap, int has_heavy, int64_t x0, int64_t ro
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
                    const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
                    const int32_t* lz_idx, const int32_t* split_full, const int32_t* split_lz,
-                   unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws, size_t ws_bytes,
-                   void* stream);
+                   const void* entries, unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws,
+                   size_t ws_bytes, void* stream);
+/* Optional per-(R tuple, column block) list ranges for mmj_merge_emit
+ * (entries: n x ncb pairs of int32 (begin | 1<<31 for a light-z list, end),
+ * ncb = mmj_merge_emit_col_blocks(wpr)); with them a tile reads one pair per
+ * R tuple instead of the tuple -> y -> degrees -> list -> split chain.  The
+ * split tables are required when ncb > 1, the light-z lists for a
+ * partitioned plan. */
+int mmj_tuple_entries(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t n, const int32_t* rdeg_x,
+                      int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* lz_ptr,
+                      const int32_t* split_full, const int32_t* split_lz, int64_t wpr, void* entries, void* stream);
 /* Column blocks per row of the fused kernel's tiles, and the optional list
  * split table it reads instead of bisecting every long list per tile:
  * split[y*(ncb+1)+j] = position in idx of list y's first entry >= the j-th
  * block's first column (dom_y*(ncb+1) int32; NULL split pointers = bisect). */
 int mmj_merge_emit_col_blocks(int64_t wpr);
+/* profiling aid: per-tile phase timestamps of mmj_merge_emit (8 x uint64 per
+ * tile, %globaltimer ns; recorded only by -DMMJ_DEBUG_TIMING builds) */
+void mmj_debug_timing_buffer(unsigned long long* buf);
 int mmj_list_splits(const int32_t* ptr, const int32_t* idx, int64_t dom_y, int64_t wpr, int32_t* split,
                     void* stream);
 

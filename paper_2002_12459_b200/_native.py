@@ -71,8 +71,10 @@ _SIGS = {
     "mmj_tile_merge": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P]),
     "mmj_emit_codes": (INT, [P, P, I64, I64, I64, I64, P, P]),
     "mmj_merge_emit_workspace_size": (SZ, [I64, I64]),
-    "mmj_merge_emit": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "mmj_merge_emit": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "mmj_tuple_entries": (INT, [P, P, I64, P, I64, P, P, P, P, P, I64, P, P]),
     "mmj_merge_emit_col_blocks": (INT, [I64]),
+    "mmj_debug_timing_buffer": (None, [P]),
     "mmj_list_splits": (INT, [P, P, I64, I64, P, P]),
     "mmj_bsi_degree_histogram": (INT, [P, P, I64, I64, I64, INT, INT, P, P]),
     "mmj_bsi_bits": (INT, [P, P, I64, P, INT, P, I64, P]),

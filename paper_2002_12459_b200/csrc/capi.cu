@@ -36,8 +36,12 @@ int emit_codes(const uint32_t*, const int64_t*, int64_t, int64_t, int64_t, int64
 size_t merge_emit_ws_bytes(int64_t, int64_t);
 int merge_emit(const uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t*, const int32_t*, const int32_t*,
                int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*,
-               const int32_t*, const int32_t*, unsigned long long*, int64_t*, int64_t*, void*, size_t, cudaStream_t);
+               const int32_t*, const int32_t*, const void*, unsigned long long*, int64_t*, int64_t*, void*, size_t,
+               cudaStream_t);
+int tuple_entries(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, const int32_t*,
+                  const int32_t*, const int32_t*, const int32_t*, int64_t, void*, cudaStream_t);
 int merge_emit_col_blocks(int64_t);
+extern unsigned long long* tdbg_buffer;
 int list_splits(const int32_t*, const int32_t*, int64_t, int64_t, int32_t*, cudaStream_t);
 int bsi_bits(const int32_t*, const int32_t*, int64_t, const int32_t*, int, uint32_t*, int64_t, cudaStream_t);
 int bsi_light_lists(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, uint8_t*, int32_t*, int32_t*,
@@ -195,14 +199,25 @@ int mmj_merge_emit(const uint32_t* bitmap, int has_heavy, int64_t x0, int64_t ro
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
                    const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
                    const int32_t* lz_idx, const int32_t* split_full, const int32_t* split_lz,
-                   unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws, size_t ws_bytes,
-                   void* stream) {
+                   const void* entries, unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws,
+                   size_t ws_bytes, void* stream) {
   return mmj::merge_emit(bitmap, has_heavy, x0, rows, wpr, dom_z, fwd_ptr, fwd_idx, rdeg_x, delta2, hpos, s_rev_ptr,
-                         s_rev_idx, lz_ptr, lz_idx, split_full, split_lz, witnesses, codes, total, ws, ws_bytes,
-                         ST(stream));
+                         s_rev_idx, lz_ptr, lz_idx, split_full, split_lz, entries, witnesses, codes, total, ws,
+                         ws_bytes, ST(stream));
+}
+
+int mmj_tuple_entries(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t n, const int32_t* rdeg_x,
+                      int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* lz_ptr,
+                      const int32_t* split_full, const int32_t* split_lz, int64_t wpr, void* entries, void* stream) {
+  return mmj::tuple_entries(fwd_row, fwd_idx, n, rdeg_x, delta2, hpos, s_rev_ptr, lz_ptr, split_full, split_lz, wpr,
+                            entries, ST(stream));
 }
 
 int mmj_merge_emit_col_blocks(int64_t wpr) { return mmj::merge_emit_col_blocks(wpr); }
+
+/* profiling aid: per-tile phase timestamps of mmj_merge_emit (8 x uint64 per
+ * tile; recorded only by -DMMJ_DEBUG_TIMING builds); NULL switches it off */
+void mmj_debug_timing_buffer(unsigned long long* buf) { mmj::tdbg_buffer = buf; }
 
 int mmj_list_splits(const int32_t* ptr, const int32_t* idx, int64_t dom_y, int64_t wpr, int32_t* split,
                     void* stream) {

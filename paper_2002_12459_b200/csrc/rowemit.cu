@@ -114,6 +114,8 @@ struct TileArgs {
   // boundaries (full S.rev lists / light-z lists): replaces per-tile bisection
   const int32_t* split_full = nullptr;
   const int32_t* split_lz = nullptr;
+  // optional per-(R tuple, column block) list ranges (mmj_tuple_entries)
+  const int2* ent = nullptr;
 };
 
 // Light witnesses of one tile OR-ed into its shared-memory bitmap (rows
@@ -133,7 +135,24 @@ __device__ __forceinline__ unsigned long long merge_light(
     const int64_t t = tb + tid;
     int len = 0, row = 0, filt = 0;
     const int32_t* base = nullptr;
-    if (t < t_end) {
+    if (t < t_end && a.ent != nullptr) {
+      // precomputed (list begin | lz flag, list end) of tuple t in this column
+      // block (mmj_tuple_entries): one load instead of the dependent chain
+      // tuple -> y -> degrees / list pointers -> split table
+      const int2 en = a.ent[t * a.ncb + cbi];
+      if (a.G > 1) {
+        int64_t lo = xa, hi = xb;
+        while (hi - lo > 1) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (a.fwd_ptr[mid] <= t) lo = mid;
+          else hi = mid;
+        }
+        row = (int)(lo - xa);
+      }
+      const int32_t b = en.x & 0x7FFFFFFF;
+      base = ((en.x < 0) ? a.lz_idx : a.s_rev_idx) + b;
+      len = en.y - b;
+    } else if (t < t_end) {
       int64_t lo = xa, hi = xb;   // row of tuple t: last x with fwd_ptr[x] <= t
       while (hi - lo > 1) {
         const int64_t mid = (lo + hi) >> 1;
@@ -505,10 +524,17 @@ struct FuseArgs {
   unsigned long long* status;
   int64_t* total;           // chunk code count (written by the last tile)
   int64_t* codes;
+  unsigned long long* tdbg;  // MMJ_DEBUG_TIMING: per-tile phase timestamps (8 per tile)
   int dbg;                  // debug bisection flags (MMJ_DEBUG_BOUNDS builds)
 };
 
 constexpr unsigned long long ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
   unsigned long long v;
@@ -553,6 +579,10 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     sm.touched = 0;
   }
   __syncthreads();
+
+#ifdef MMJ_DEBUG_TIMING
+  if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 0] = gtimer();
+#endif
   const int64_t tile = sm.tile;
   const int64_t rg = tile / a.ncb;
   const int cbi = (int)(tile - rg * a.ncb);
@@ -579,6 +609,10 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
   const int64_t t_begin = a.fwd_ptr ? a.fwd_ptr[xa] : 0, t_end = a.fwd_ptr ? a.fwd_ptr[xb] : 0;
   __syncthreads();
   if (a.has_heavy) bar_wait0(&sm.bar);
+
+#ifdef MMJ_DEBUG_TIMING
+  if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 1] = gtimer();
+#endif
   unsigned long long my_w = merge_light<NT>(a, sbm, xa, xb, t_begin, t_end, zlo, zhi, cw, cbi, sm.scan_tmp, sm.u.m.tb_len,
                                             sm.u.m.tb_base, sm.u.m.tb_row, sm.u.m.tb_filt, &sm.touched);
   {
@@ -588,6 +622,10 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     if (lane == 0 && w) atomicAdd(a.witnesses, w);
   }
   __syncthreads();   // merged tile complete
+
+#ifdef MMJ_DEBUG_TIMING
+  if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 2] = gtimer();
+#endif
   // segment popcounts (REDUX over the 32 words of a segment, one warp per 32 segments)
   const int nseg = words >> 5;
   for (int sb = warp * 32; sb < nseg; sb += NT) {
@@ -618,6 +656,10 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     if (sg < nseg) s_segoff[sg] = excl;
     excl += v[i];
   }
+
+#ifdef MMJ_DEBUG_TIMING
+  if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 3] = gtimer();
+#endif
   // decoupled look-back (warp 0)
   if (warp == 0) {
     long long prefix = 0;
@@ -650,6 +692,9 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     }
   }
   __syncthreads();
+#ifdef MMJ_DEBUG_TIMING
+  if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 4] = gtimer();
+#endif
   // emission: one warp per segment (k_emit_pf16's staging and stores)
   uint16_t* stage = sm.u.stage[warp];
   auto sl = [](int k) { return k ^ (((k >> 5) & 31) << 1); };
@@ -707,6 +752,10 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(h + done + lane)]);
     __syncwarp();
   }
+#ifdef MMJ_DEBUG_TIMING
+  __syncthreads();
+  if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 5] = gtimer();
+#endif
 }
 
 
@@ -1059,6 +1108,35 @@ __global__ void __launch_bounds__((NEW + 1) * 32, 4) k_merge_emit_p(const FuseAr
   }
 }
 
+// ent[t*ncb + j] = (first position | (1 << 31) if the light-z list, end position)
+// of R tuple t's S-side list restricted to column block j: the x-side
+// restatement of joinproject.py:183-203 (full S.rev(y) when y or x is light,
+// the light-z list otherwise), evaluated once per engine.
+__global__ void k_tuple_entries(const int32_t* __restrict__ fwd_row, const int32_t* __restrict__ fwd_idx, int64_t n,
+                                const int32_t* __restrict__ rdeg_x, int64_t d2, const int32_t* __restrict__ hpos,
+                                const int32_t* __restrict__ s_rev_ptr, const int32_t* __restrict__ lz_ptr,
+                                const int32_t* __restrict__ split_full, const int32_t* __restrict__ split_lz, int ncb,
+                                int2* __restrict__ ent) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t y = fwd_idx[t];
+    const bool full = (hpos == nullptr) || (hpos[y] < 0) || (rdeg_x[fwd_row[t]] <= d2);
+    const int32_t* ptr = full ? s_rev_ptr : lz_ptr;
+    const int32_t* sp = full ? split_full : split_lz;
+    const int32_t flag = full ? 0 : (int32_t)0x80000000u;
+    for (int j = 0; j < ncb; ++j) {
+      int32_t b, e;
+      if (ncb == 1) {
+        b = ptr[y];
+        e = ptr[y + 1];
+      } else {
+        b = sp[(int64_t)y * (ncb + 1) + j];
+        e = sp[(int64_t)y * (ncb + 1) + j + 1];
+      }
+      ent[t * ncb + j] = make_int2(b | flag, e);
+    }
+  }
+}
+
 // split[y*(ncb+1) + j] = absolute position in idx of the first entry of list
 // y (ptr[y] .. ptr[y+1], sorted) that is >= j * cb_cells
 __global__ void k_list_splits(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx, int64_t dom_y,
@@ -1174,6 +1252,27 @@ int list_splits(const int32_t* ptr, const int32_t* idx, int64_t dom_y, int64_t w
   return MMJ_OK;
 }
 
+int tuple_entries(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t n, const int32_t* rdeg_x, int64_t d2,
+                  const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* lz_ptr, const int32_t* split_full,
+                  const int32_t* split_lz, int64_t wpr, void* ent, cudaStream_t st) {
+  int G, cb, ncb;
+  tile_geometry(wpr, G, cb, ncb, fuse_tile_words());
+  if (ncb > 1 && (split_full == nullptr || (hpos != nullptr && lz_ptr != nullptr && split_lz == nullptr))) {
+    set_error("tuple_entries: rows span %d column blocks: the split tables are required", ncb);
+    return MMJ_ERR_ARG;
+  }
+  if (hpos != nullptr && lz_ptr == nullptr) {
+    set_error("tuple_entries: a partitioned plan needs the light-z lists");
+    return MMJ_ERR_ARG;
+  }
+  if (n == 0) return MMJ_OK;
+  const int64_t g = std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 16);
+  k_tuple_entries<<<(unsigned)g, 256, 0, st>>>(fwd_row, fwd_idx, n, rdeg_x, d2, hpos, s_rev_ptr, lz_ptr, split_full,
+                                              split_lz, ncb, static_cast<int2*>(ent));
+  MMJ_CHECK_LAUNCH("k_tuple_entries");
+  return MMJ_OK;
+}
+
 int64_t merge_emit_tiles(int64_t rows, int64_t wpr) {
   int G, cb, ncb;
   tile_geometry(wpr, G, cb, ncb, fuse_tile_words());
@@ -1184,11 +1283,13 @@ size_t merge_emit_ws_bytes(int64_t rows, int64_t wpr) {
   return 16 + (size_t)merge_emit_tiles(rows, wpr) * 8;
 }
 
+unsigned long long* tdbg_buffer = nullptr;   // MMJ_DEBUG_TIMING builds: set by mmj_debug_timing_buffer
+
 int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t d2, const int32_t* hpos,
                const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx,
-               const int32_t* split_full, const int32_t* split_lz, unsigned long long* witnesses, int64_t* codes,
-               int64_t* total, void* ws, size_t ws_bytes, cudaStream_t st) {
+               const int32_t* split_full, const int32_t* split_lz, const void* ent, unsigned long long* witnesses,
+               int64_t* codes, int64_t* total, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (wpr <= 0 || wpr % 32 != 0) {
     set_error("merge_emit: bitmap pitch must be a positive multiple of 32 words");
     return MMJ_ERR_ARG;
@@ -1227,6 +1328,7 @@ int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int6
   a.witnesses = witnesses;
   a.split_full = split_full;
   a.split_lz = split_lz;
+  a.ent = static_cast<const int2*>(ent);
   f.ticket = static_cast<unsigned int*>(ws);
   f.status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 16);
   f.total = total;
@@ -1235,6 +1337,7 @@ int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int6
     const char* e = getenv("MMJ_DBG_FUSE");
     f.dbg = e ? atoi(e) : 0;
   }
+  f.tdbg = tdbg_buffer;
   MMJ_TRY(cuda_status(cudaMemsetAsync(ws, 0, need, st), "merge_emit: workspace reset"));
   if (fuse_persistent() && tw == 4096) return launch_merge_emit_p<4096, 8>(f, st);
   static int variant = -1;

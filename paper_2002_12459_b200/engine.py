@@ -402,27 +402,46 @@ class TwoPathEngine:
         """(full, light-z) column-block split tables of the S-side lists for
         the fused kernel, built once per engine; (0, 0) when a row is a single
         tile or the table would be large (the kernel then bisects)."""
+        return self._tail_tables()[:2]
+
+    def _tail_tables(self):
+        """Per-engine tables of the fused tail: the (full, light-z) split tables
+        (first list position of every column block; only when a row spans
+        several tiles) and the per-(R tuple, column block) list ranges
+        (mmj_tuple_entries), each 0 when absent."""
         if self._splits is None:
             torch = self.torch
+            st = self._st()
             ncb = int(self.lib.mmj_merge_emit_col_blocks(self.wpr))
             n = self.dom_y * (ncb + 1)
-            if ncb <= 1 or n > (64 << 20):
-                self._splits = (0, 0, None)
-            else:
-                st = self._st()
+            keep = []
+            spf = spl = 0
+            if ncb > 1 and n <= (64 << 20):
                 full = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
                 nat.call("mmj_list_splits", nat.ptr(self.ds.rev_ptr), nat.ptr(self.ds.rev_idx), self.dom_y, self.wpr,
                          nat.ptr(full), st)
-                keep = [full]
-                lz = 0
+                keep.append(full)
+                spf = nat.ptr(full)
                 if self.lz_ptr is not None:
                     lzt = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
                     nat.call("mmj_list_splits", nat.ptr(self.lz_ptr), nat.ptr(self.lz_idx), self.dom_y, self.wpr,
                              nat.ptr(lzt), st)
                     keep.append(lzt)
-                    lz = nat.ptr(lzt)
-                self._splits = (nat.ptr(full), lz, keep)
-        return self._splits[0], self._splits[1]
+                    spl = nat.ptr(lzt)
+            ent = 0
+            hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
+            ok = (ncb == 1 or spf) and (hp == 0 or self.lz_ptr is not None) and (ncb == 1 or hp == 0 or spl)
+            # opt-in (MMJ_TUPLE_ENTRIES=1): measured neutral on cfg2 (170.7 vs 170.5 ms): the
+            # tile's merge latency is hidden by the other CTAs on the SM
+            if ok and self.dr.n * ncb <= (256 << 20) and __import__("os").environ.get("MMJ_TUPLE_ENTRIES", "0") == "1":
+                e = torch.empty((max(self.dr.n * ncb, 1), 2), dtype=torch.int32, device="cuda")
+                nat.call("mmj_tuple_entries", nat.ptr(self.dr.fwd_row), nat.ptr(self.dr.fwd_idx), self.dr.n,
+                         nat.ptr(self.dr.left_deg), self.d2, hp, nat.ptr(self.ds.rev_ptr),
+                         nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0, spf, spl, self.wpr, nat.ptr(e), st)
+                keep.append(e)
+                ent = nat.ptr(e)
+            self._splits = (spf, spl, ent, keep)
+        return self._splits[:3]
 
     def _merge_emit_tail(self, x0, x1, rows, buf, sync, codes_key):
         torch = self.torch
@@ -438,11 +457,11 @@ class TwoPathEngine:
         cap = rows * self.dom_z
         codes = self.ws.get(codes_key, cap, torch.int64)
         slot = self._async_slot()
-        spf, spl = self._list_splits()
+        spf, spl, ent = self._tail_tables()
         self._ph("merge_emit", True)
         nat.call("mmj_merge_emit", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
                  nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp, nat.ptr(ds.rev_ptr),
-                 nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(slot),
+                 nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, ent, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(slot),
                  nat.ptr(ws), wsb, st)
         self._ph("merge_emit", False)
         self.stats.chunks += 1
@@ -489,7 +508,7 @@ class TwoPathEngine:
         mma_done = {}
         coloc = self.pairs and not self.triple and __import__("os").environ.get("MMJ_COLOC", "1") != "0"
         mode = self._bitmap_mode() | (nat.MODE_COLOC if coloc else 0)
-        spf, spl = self._list_splits() if self.one_kernel_tail else (0, 0)
+        spf, spl, ent = self._tail_tables() if self.one_kernel_tail else (0, 0, 0)
         wsb = int(self.lib.mmj_merge_emit_workspace_size(rows_max, self.wpr))
         fws = self.ws.get("fuse_ws", wsb, torch.uint8)
 
@@ -526,7 +545,7 @@ class TwoPathEngine:
                     timer.start("merge_emit", main)
                 nat.call("mmj_merge_emit", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
                          nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp,
-                         nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, nat.ptr(self.wit),
+                         nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, ent, nat.ptr(self.wit),
                          nat.ptr(codes), nat.ptr(slot), nat.ptr(fws), wsb, mst)
                 if timer is not None:
                     timer.stop("merge_emit", main)

@@ -210,7 +210,7 @@ class StarEngine:
                 codes = self.ws.get("codes", rows * self.dk, torch.int64)
                 tot = self.ws.get("star_total", 1, torch.int64)
                 nat.call("mmj_merge_emit", nat.ptr(buf), 1, x0, rows, self.wpr, self.dk, 0, 0, 0, 0, 0, 0, 0, 0, 0,
-                         0, 0, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(tot), nat.ptr(fws), wsb, st)
+                         0, 0, 0, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(tot), nat.ptr(fws), wsb, st)
                 total = int(tot.item())
                 if sink is not None:
                     sink(xa, xb, codes[:total], None)
