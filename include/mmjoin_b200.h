@@ -302,6 +302,27 @@ int mmj_ingest_remap(const int32_t* idx, int64_t n, const int32_t* map, int32_t*
 int mmj_ingest_gather(const void* src, int elem_bytes, const int32_t* idx, int64_t n, void* out, void* stream);
 /* cnt[v] = #{i : idx[i] == v}, v < dom (cnt zeroed first) */
 int mmj_ingest_histogram(const int32_t* idx, int64_t n, int64_t dom, int32_t* cnt, void* stream);
+/* Row compaction before an SSJ / thresholded count join (apps.py:57-62: a set
+ * with fewer than c elements reaches no overlap >= c, so its row and column of
+ * the count matrix can be dropped).  Keeps the rows x with left_deg[x] >=
+ * min_deg, renumbered 0..dom'-1 in id order (new_id[dom], -1 = dropped;
+ * orig[dom'] its inverse), and writes the compacted relation's CSR in both
+ * directions without a sort (kept entries keep their order; offsets are the
+ * keep-flag scans at the old offsets): fwd_ptr_out[dom'+1], fwd_idx_out /
+ * fwd_row_out [n'], left_deg_out[dom'], rev_ptr_out[dom_y+1], rev_idx_out[n'],
+ * right_deg_out[dom_y].  Caller sizes the outputs for dom / n.  sizes[0] = dom',
+ * sizes[1] = n' (device int64).  Workspace: mmj_ingest_workspace_bytes(max(n,
+ * dom, dom_y)). */
+int mmj_compact_rows(const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* fwd_row,
+                     const int32_t* rev_ptr, const int32_t* rev_idx, const int32_t* left_deg, int64_t n, int64_t dom,
+                     int64_t dom_y, int64_t min_deg, int32_t* new_id, int32_t* orig, int32_t* fwd_ptr_out,
+                     int32_t* fwd_idx_out, int32_t* fwd_row_out, int32_t* left_deg_out, int32_t* rev_ptr_out,
+                     int32_t* rev_idx_out, int32_t* right_deg_out, int64_t* sizes, void* ws, size_t ws_bytes,
+                     void* stream);
+/* out[i] = orig_l[in[i] / dom_c] * dom_out + orig_r[in[i] % dom_c] (in == out allowed):
+ * compact codes back to the caller's dense-id codes; ascending stays ascending */
+int mmj_decode_compact_codes(const int64_t* in, int64_t n, int64_t dom_c, const int32_t* orig_l,
+                             const int32_t* orig_r, int64_t dom_out, int64_t* out, void* stream);
 int mmj_ingest_csr(const int32_t* rows, const int32_t* cols, int64_t n, int64_t dom_rows, int64_t dom_cols,
                    int32_t* ptr, int32_t* idx, int32_t* row_of, int32_t* deg, void* ws, size_t ws_bytes,
                    void* stream);

@@ -299,6 +299,81 @@ int sort_pairs_u64(void* tmp, size_t tmp_bytes, const uint64_t* k_in, uint64_t* 
   return MMJ_OK;
 }
 
+
+// ---- row compaction (SSJ: sets smaller than c reach no overlap >= c) ----
+__global__ void k_row_keep(const int32_t* __restrict__ deg, int64_t dom, int32_t min_deg, uint8_t* __restrict__ keep) {
+  GRID_STRIDE(i, dom) keep[i] = deg[i] >= min_deg ? 1 : 0;
+}
+
+__global__ void k_row_ids(const uint8_t* __restrict__ keep, const int32_t* __restrict__ pos, int64_t dom,
+                          int32_t* __restrict__ new_id, int32_t* __restrict__ orig) {
+  GRID_STRIDE(i, dom) {
+    const bool k = keep[i] != 0;
+    new_id[i] = k ? pos[i] : -1;
+    if (k) orig[pos[i]] = (int32_t)i;
+  }
+}
+
+// tuples (or reverse-list entries) whose left id is kept
+__global__ void k_entry_keep(const int32_t* __restrict__ left, int64_t n, const int32_t* __restrict__ new_id,
+                             uint8_t* __restrict__ keep) {
+  GRID_STRIDE(i, n) keep[i] = new_id[left[i]] >= 0 ? 1 : 0;
+}
+
+// kept entries to their scanned positions: out_left = the renumbered left id,
+// out_other = the other column unchanged (either may be null)
+__global__ void k_entry_compact(const int32_t* __restrict__ left, const int32_t* __restrict__ other, int64_t n,
+                                const int32_t* __restrict__ new_id, const uint8_t* __restrict__ keep,
+                                const int32_t* __restrict__ pos, int32_t* __restrict__ out_left,
+                                int32_t* __restrict__ out_other) {
+  GRID_STRIDE(i, n) {
+    if (keep[i]) {
+      if (out_left) out_left[pos[i]] = new_id[left[i]];
+      if (out_other) out_other[pos[i]] = other[i];
+    }
+  }
+}
+
+// forward offsets / degrees of the kept rows: ptr'[new_id[x]] = tpos[ptr[x]]
+__global__ void k_fwd_ptr(const int32_t* __restrict__ ptr, const int32_t* __restrict__ deg, int64_t dom,
+                          const int32_t* __restrict__ new_id, const int32_t* __restrict__ rowpos,
+                          const int32_t* __restrict__ tpos, int64_t n, int32_t* __restrict__ ptr_out,
+                          int32_t* __restrict__ deg_out) {
+  GRID_STRIDE(i, dom + 1) {
+    if (i == dom) {
+      ptr_out[rowpos[dom]] = tpos[n];
+    } else if (new_id[i] >= 0) {
+      ptr_out[new_id[i]] = tpos[ptr[i]];
+      deg_out[new_id[i]] = deg[i];
+    }
+  }
+}
+
+// reverse offsets: the scanned keep positions at the old list starts
+__global__ void k_rev_ptr(const int32_t* __restrict__ ptr, int64_t dom_y, const int32_t* __restrict__ rpos,
+                          int32_t* __restrict__ ptr_out, int32_t* __restrict__ deg_out) {
+  GRID_STRIDE(y, dom_y + 1) {
+    const int32_t p = rpos[ptr[y]];
+    ptr_out[y] = p;
+    if (y < dom_y) deg_out[y] = rpos[ptr[y + 1]] - p;
+  }
+}
+
+// compact code a' * dom_c + b' -> orig_l[a'] * dom_out + orig_r[b'] (both maps
+// strictly increasing, so ascending codes stay ascending)
+__global__ void k_decode_codes(const int64_t* in, int64_t n, int64_t dom_c, double inv,
+                               const int32_t* __restrict__ orig_l, const int32_t* __restrict__ orig_r,
+                               int64_t dom_out, int64_t* out) {
+  GRID_STRIDE(i, n) {
+    const int64_t c = in[i];
+    int64_t a = (int64_t)((double)c * inv);
+    int64_t b = c - a * dom_c;
+    while (b < 0) { --a; b += dom_c; }
+    while (b >= dom_c) { ++a; b -= dom_c; }
+    out[i] = (int64_t)orig_l[a] * dom_out + orig_r[b];
+  }
+}
+
 struct Scratch {
   Bump w;
   int64_t *k0, *k1, *k2, *k3;
@@ -496,6 +571,78 @@ int mmj_ingest_filter(const int64_t* pairs, const int32_t* rid, int64_t n, int64
   MMJ_CHECK_LAUNCH("k_compact_kept");
   MMJ_TRY(cuda_status(cudaMemsetAsync(n_out, 0, 8, st), "memset n_out"));
   return cuda_status(cudaMemcpyAsync(n_out, s.i0 + n, 4, cudaMemcpyDeviceToDevice, st), "n_out");
+}
+
+int mmj_compact_rows(const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* fwd_row,
+                     const int32_t* rev_ptr, const int32_t* rev_idx, const int32_t* left_deg, int64_t n, int64_t dom,
+                     int64_t dom_y, int64_t min_deg, int32_t* new_id, int32_t* orig, int32_t* fwd_ptr_out,
+                     int32_t* fwd_idx_out, int32_t* fwd_row_out, int32_t* left_deg_out, int32_t* rev_ptr_out,
+                     int32_t* rev_idx_out, int32_t* right_deg_out, int64_t* sizes, void* ws, size_t ws_bytes,
+                     void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "compact_rows"));
+  MMJ_TRY(check_n(dom, "compact_rows"));
+  MMJ_TRY(check_n(dom_y, "compact_rows"));
+  if (min_deg < 0 || min_deg > INT32_MAX) {
+    set_error("compact_rows: min_deg %lld out of range", (long long)min_deg);
+    return MMJ_ERR_ARG;
+  }
+  Scratch s;
+  int64_t m = n > dom ? n : dom;
+  m = m > dom_y ? m : dom_y;
+  MMJ_TRY(carve(ws, ws_bytes, m, s));
+  MMJ_TRY(cuda_status(cudaMemsetAsync(sizes, 0, 16, st), "memset sizes"));
+  // kept rows, their new ids (monotone) and the inverse map
+  if (dom > 0) {
+    k_row_keep<<<grid1(dom), TPB, 0, st>>>(left_deg, dom, (int32_t)min_deg, s.f0);
+    MMJ_CHECK_LAUNCH("k_row_keep");
+    MMJ_TRY(scan_u8_i32(s.f0, s.i0, dom, s.scan0, st));
+    k_row_ids<<<grid1(dom), TPB, 0, st>>>(s.f0, s.i0, dom, new_id, orig);
+    MMJ_CHECK_LAUNCH("k_row_ids");
+  } else {
+    MMJ_TRY(cuda_status(cudaMemsetAsync(s.i0, 0, 4, st), "memset rowpos"));
+  }
+  MMJ_TRY(cuda_status(cudaMemcpyAsync(sizes, s.i0 + dom, 4, cudaMemcpyDeviceToDevice, st), "sizes[0]"));
+  // forward direction: kept tuples stay in (row, col) order, offsets from the scan
+  if (n > 0) {
+    k_entry_keep<<<grid1(n), TPB, 0, st>>>(fwd_row, n, new_id, s.f1);
+    MMJ_CHECK_LAUNCH("k_entry_keep");
+  }
+  MMJ_TRY(scan_u8_i32(s.f1, s.i1, n, s.scan1, st));
+  if (n > 0) {
+    k_entry_compact<<<grid1(n), TPB, 0, st>>>(fwd_row, fwd_idx, n, new_id, s.f1, s.i1, fwd_row_out, fwd_idx_out);
+    MMJ_CHECK_LAUNCH("k_entry_compact");
+  }
+  k_fwd_ptr<<<grid1(dom + 1), TPB, 0, st>>>(fwd_ptr, left_deg, dom, new_id, s.i0, s.i1, n, fwd_ptr_out, left_deg_out);
+  MMJ_CHECK_LAUNCH("k_fwd_ptr");
+  MMJ_TRY(cuda_status(cudaMemcpyAsync(sizes + 1, s.i1 + n, 4, cudaMemcpyDeviceToDevice, st), "sizes[1]"));
+  // reverse direction: each y list filtered in place order (ascending new ids)
+  if (n > 0) {
+    k_entry_keep<<<grid1(n), TPB, 0, st>>>(rev_idx, n, new_id, s.f1);
+    MMJ_CHECK_LAUNCH("k_entry_keep");
+  }
+  MMJ_TRY(scan_u8_i32(s.f1, s.i2, n, s.scan1, st));
+  if (n > 0) {
+    k_entry_compact<<<grid1(n), TPB, 0, st>>>(rev_idx, nullptr, n, new_id, s.f1, s.i2, rev_idx_out, nullptr);
+    MMJ_CHECK_LAUNCH("k_entry_compact");
+  }
+  k_rev_ptr<<<grid1(dom_y + 1), TPB, 0, st>>>(rev_ptr, dom_y, s.i2, rev_ptr_out, right_deg_out);
+  MMJ_CHECK_LAUNCH("k_rev_ptr");
+  return MMJ_OK;
+}
+
+int mmj_decode_compact_codes(const int64_t* in, int64_t n, int64_t dom_c, const int32_t* orig_l,
+                             const int32_t* orig_r, int64_t dom_out, int64_t* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MMJ_TRY(check_n(n, "decode_compact_codes"));
+  if (dom_c <= 0 || dom_out <= 0) {
+    set_error("decode_compact_codes: domains must be positive (got %lld, %lld)", (long long)dom_c, (long long)dom_out);
+    return MMJ_ERR_ARG;
+  }
+  if (n == 0) return MMJ_OK;
+  k_decode_codes<<<grid1(n), TPB, 0, st>>>(in, n, dom_c, 1.0 / (double)dom_c, orig_l, orig_r, dom_out, out);
+  MMJ_CHECK_LAUNCH("k_decode_codes");
+  return MMJ_OK;
 }
 
 int mmj_ingest_csr(const int32_t* rows, const int32_t* cols, int64_t n, int64_t dom_rows, int64_t dom_cols,

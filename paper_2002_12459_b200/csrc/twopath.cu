@@ -446,7 +446,13 @@ __global__ void __launch_bounds__(256) k_count_emit(const CellT* __restrict__ cn
                                                     int64_t* __restrict__ codes, int32_t* __restrict__ counts) {
   using G = CellGeo<CellT>;
   constexpr uint64_t FMASK = (1ull << G::FIELD) - 1;
+  // per-warp staging of the segment's kept cells (column offset, count), so
+  // the codes and counts leave as coalesced runs instead of one scattered
+  // 8-B / 4-B store per kept cell per lane
+  __shared__ uint16_t s_col[8][CSEG];
+  __shared__ int32_t s_cnt[8][CSEG];
   const int lane = threadIdx.x & 31;
+  const int wib = (threadIdx.x >> 5) & 7;
   for (int64_t sgi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; sgi < nseg;
        sgi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const CountSeg g = count_seg(sgi, spr, ncols, x0, upper_only);
@@ -478,21 +484,27 @@ __global__ void __launch_bounds__(256) k_count_emit(const CellT* __restrict__ cn
     const uint64_t tot = __shfl_sync(0xffffffffu, incl, 31);   // per-iteration totals
     const uint64_t excl = incl - packed;
     const int64_t code_row = (x0 + g.row) * dom_z + g.col0;
-    int64_t it_base = base;
+    int it_base = 0;
 #pragma unroll
     for (int it = 0; it < G::ITS; ++it) {
       const uint32_t m = msk[it];
-      int64_t k = it_base + (int64_t)((excl >> (G::FIELD * it)) & FMASK);
+      int k = it_base + (int)((excl >> (G::FIELD * it)) & FMASK);
 #pragma unroll
       for (int j = 0; j < G::VEC; ++j) {
         if (m & (1u << j)) {
-          __stcs(codes + k, code_row + (it * 32 + lane) * G::VEC + j);
-          __stcs(counts + k, cell_of<CellT>(v[it], j));
+          s_col[wib][k] = (uint16_t)((it * 32 + lane) * G::VEC + j);
+          s_cnt[wib][k] = cell_of<CellT>(v[it], j);
           ++k;
         }
       }
-      it_base += (int64_t)((tot >> (G::FIELD * it)) & FMASK);
+      it_base += (int)((tot >> (G::FIELD * it)) & FMASK);
     }
+    __syncwarp();
+    for (int p = lane; p < it_base; p += 32) {
+      __stcs(codes + base + p, code_row + s_col[wib][p]);
+      __stcs(counts + base + p, s_cnt[wib][p]);
+    }
+    __syncwarp();
   }
 }
 

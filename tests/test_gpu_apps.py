@@ -6,6 +6,7 @@ import json
 import os
 
 import numpy as np
+import torch
 import pytest
 
 from conftest import GOLDEN, random_pairs, zipf_pairs
@@ -51,6 +52,52 @@ def test_ssj_zipf_family_vs_oracle(oracle, c):
     for plan in (None, ThresholdPlan(PARTITIONED, 26, 26), ThresholdPlan(PARTITIONED, 200, 1)):
         a, b, n = ssj_mmjoin_arrays(fam, c, plan=plan, chunk_rows=256)
         assert np.array_equal(a, ea) and np.array_equal(b, eb) and np.array_equal(n, en)
+
+
+@pytest.mark.parametrize("c", [2, 4])
+def test_ssj_compaction_matches_full_matrix(oracle, c):
+    """Sets smaller than c dropped and the rest renumbered before the count
+    join (mmj_compact_rows), codes mapped back (mmj_decode_compact_codes):
+    identical arrays to the uncompacted count matrix and to the oracle."""
+    from paper_2002_12459_b200 import datagen
+    from paper_2002_12459_b200.apps import SetFamily, _compact_family, _ssj_device, _split
+    from paper_2002_12459_b200.relation import Relation
+    pairs = datagen.set_family_pairs(5, 40000, 4000, 400, 1.5, 1500, 1.1)
+    fam = SetFamily(Relation.from_raw_pairs("sets", pairs))
+    comp = _compact_family(fam.indexed, c)
+    assert comp is not None, "the Zipf(1.5) family has a large share of sets below c"
+    dc, orig, hdeg = comp
+    ldeg = np.asarray(fam.indexed.left_deg)
+    assert dc.dom_left == int((ldeg >= c).sum()) and dc.n == int(ldeg[ldeg >= c].sum())
+    assert np.array_equal(orig.cpu().numpy(), np.flatnonzero(ldeg >= c))
+    assert np.array_equal(dc.left_deg.cpu().numpy(), hdeg)
+    # both CSR directions of the compacted family vs a host rebuild
+    idx = fam.indexed
+    rows = np.repeat(np.arange(len(ldeg)), ldeg)
+    kept = ldeg[rows] >= c
+    new_id = np.cumsum(ldeg >= c) - 1
+    r2, y2 = new_id[rows[kept]], np.asarray(idx.fwd_indices)[kept]
+    assert np.array_equal(dc.fwd_row.cpu().numpy(), r2) and np.array_equal(dc.fwd_idx.cpu().numpy(), y2)
+    assert np.array_equal(dc.fwd_ptr.cpu().numpy(), dc.fwd_ptr_host)
+    order = np.lexsort((r2, y2))
+    rdeg = np.bincount(y2, minlength=dc.dom_right)
+    assert np.array_equal(dc.rev_idx.cpu().numpy(), r2[order])
+    assert np.array_equal(dc.right_deg.cpu().numpy(), rdeg)
+    assert np.array_equal(dc.rev_ptr.cpu().numpy(), np.concatenate([[0], np.cumsum(rdeg)]))
+    got = _ssj_device(fam, c, None, 512, compact=True)
+    ref = _ssj_device(fam, c, None, 512, compact=False)
+    assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1])
+    a, b = _split(got[0].cpu().numpy(), fam.relation.dom_left)
+    ea, eb, en = oracle.ssj_arrays(oracle.encode(pairs), c)
+    assert np.array_equal(a, ea) and np.array_equal(b, eb) and np.array_equal(got[1].cpu().numpy(), en)
+
+
+def test_compact_abi_errors():
+    from paper_2002_12459_b200 import _native as nat
+    nat.require_cuda()
+    lib = nat.load()
+    assert lib.mmj_compact_rows(*([0] * 6), 0, 0, 0, -1, *([0] * 11), 0, 0) == nat.MMJ_ERR_ARG
+    assert lib.mmj_decode_compact_codes(0, 1, 0, 0, 0, 10, 0, 0) == nat.MMJ_ERR_ARG
 
 
 def test_bsi_golden():

@@ -88,7 +88,6 @@ def cfg3():
 def cfg4():
     from paper_2002_12459_b200 import datagen
     from paper_2002_12459_b200.apps import SetFamily
-    from paper_2002_12459_b200.joinproject import _engine
     from paper_2002_12459_b200.optimizer import gpu_plan
     from paper_2002_12459_b200.relation import Relation
     fam = SetFamily(Relation.from_raw_pairs("sets", datagen.config("cfg4").relations[0]))
@@ -98,24 +97,33 @@ def cfg4():
     for spec in filter(None, os.environ.get("MMJ_CFG4_PLANS", "").split(";")):
         d1, d2 = (int(v) for v in spec.split(","))
         plans.append(ThresholdPlan("partitioned", d1, d2))
+    from paper_2002_12459_b200.apps import _ssj_engine
     rows = []
     for plan in plans:
-        def run():
-            eng = _engine(idx, idx, plan, True, min_count=4, upper_only=True)
-            n = [0]
-            eng.run(lambda ch: n.__setitem__(0, n[0] + ch.n))
-            eng.finish()
-            return n[0]
-        t, n = _timed(run)
-        # one more pass with CUDA-event phase brackets (separate from the timed runs)
-        from bench import PhaseTimer
-        eng = _engine(idx, idx, plan, True, min_count=4, upper_only=True)
-        eng.timer = PhaseTimer()
-        eng.run(lambda ch: None)
-        phases = {k: round(v, 3) for k, v in eng.timer.totals().items()}
-        rows.append({"config": "cfg4", "workload": "SSJ c=4, 2M (set, element) pairs, 100k sets", "plan":
-                     [plan.strategy, plan.delta1, plan.delta2], "out_pairs": n, "seconds": t, "pairs_per_s": n / t,
-                     "k_heavy": int(eng.kpad), "chunks": eng.stats.chunks, "phase_ms": phases})
+        for compact in (True, False):
+            def run():
+                # compaction (sets below c dropped), engine, count join and
+                # the decode of every chunk's codes are all inside the timing
+                eng, decode = _ssj_engine(idx, 4, plan, compact=compact)
+                n = [0]
+
+                def sink(ch):
+                    decode(ch.codes)
+                    n[0] += ch.n
+                eng.run(sink)
+                eng.finish()
+                return n[0]
+            t, n = _timed(run)
+            # one more pass with CUDA-event phase brackets (separate from the timed runs)
+            from bench import PhaseTimer
+            eng, _ = _ssj_engine(idx, 4, plan, compact=compact)
+            eng.timer = PhaseTimer()
+            eng.run(lambda ch: None)
+            phases = {k: round(v, 3) for k, v in eng.timer.totals().items()}
+            rows.append({"config": "cfg4", "workload": "SSJ c=4, 2M (set, element) pairs, 100k sets", "plan":
+                         [plan.strategy, plan.delta1, plan.delta2], "compact_sets": compact,
+                         "matrix_rows": eng.dom_x, "out_pairs": n, "seconds": t, "pairs_per_s": n / t,
+                         "k_heavy": int(eng.kpad), "chunks": eng.stats.chunks, "phase_ms": phases})
     return rows
 
 
