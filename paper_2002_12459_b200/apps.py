@@ -101,8 +101,9 @@ def _compact_family(idx, c: int):
     from .ingest import IngestWorkspace
     ldeg = np.asarray(idx.left_deg)
     keep = ldeg >= c
-    if keep.sum() > COMPACT_MAX_KEPT * len(ldeg):
-        return None
+    nk = int(keep.sum())
+    if nk == 0 or nk > COMPACT_MAX_KEPT * len(ldeg):
+        return None   # nothing to save (or nothing left: the plain engine handles empty outputs)
     dr = device_relation(idx)
     n, dom, dom_y = dr.n, dr.dom_left, dr.dom_right
 

@@ -55,7 +55,7 @@ __device__ __forceinline__ void st_cs(int64_t* p, int64_t a) {
 
 // 32-byte store (sm_100: st.global.v4.b64)
 __device__ __forceinline__ void st_v4(int64_t* p, int64_t a, int64_t b, int64_t c, int64_t d) {
-  asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+  asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {

@@ -92,6 +92,24 @@ def test_ssj_compaction_matches_full_matrix(oracle, c):
     assert np.array_equal(a, ea) and np.array_equal(b, eb) and np.array_equal(got[1].cpu().numpy(), en)
 
 
+def test_ssj_compaction_edges(oracle):
+    """c above every set size (nothing kept), c = 1 (no compaction), a family
+    where every set survives: same arrays as the oracle."""
+    from paper_2002_12459_b200 import datagen
+    from paper_2002_12459_b200.apps import SetFamily, _compact_family, ssj_mmjoin_arrays
+    from paper_2002_12459_b200.relation import Relation
+    pairs = datagen.set_family_pairs(7, 6000, 800, 60, 1.5, 300, 1.1)
+    fam = SetFamily(Relation.from_raw_pairs("sets", pairs))
+    big = int(np.asarray(fam.indexed.left_deg).max()) + 1
+    assert _compact_family(fam.indexed, big) is None
+    a, b, n = ssj_mmjoin_arrays(fam, big)
+    assert len(a) == len(b) == len(n) == 0
+    for c in (1, 2, 5):
+        ea, eb, en = oracle.ssj_arrays(oracle.encode(pairs), c)
+        a, b, n = ssj_mmjoin_arrays(fam, c)
+        assert np.array_equal(a, ea) and np.array_equal(b, eb) and np.array_equal(n, en)
+
+
 def test_compact_abi_errors():
     from paper_2002_12459_b200 import _native as nat
     nat.require_cuda()

@@ -1,5 +1,3 @@
 set -u
-O=gpurun_out/cta; mkdir -p $O
-MMJ_CTA_EMIT=1 timeout 600 python -m pytest tests/test_gpu_fused.py tests/test_gpu_twopath.py tests/test_gpu_golden.py -x -q > $O/tests.log 2>&1; echo EXIT $? >> $O/tests.log
-for v in 0 1 0 1; do MMJ_CTA_EMIT=$v timeout 600 python bench.py --no-e2e --no-cpu-baseline --no-light-work > $O/bench_$v.json 2>>$O/bench.err; cp $O/bench_$v.json $O/bench_${v}_$RANDOM.json; done
-MMJ_CTA_EMIT=1 timeout 600 python tools/bench_configs.py cfg1 cfg3 > $O/configs1.jsonl 2>&1
+O=gpurun_out/cta2; mkdir -p $O
+for v in 1 0 1; do MMJ_CTA_EMIT=$v timeout 600 python bench.py --no-e2e --no-cpu-baseline --no-light-work > $O/bench_${v}_$RANDOM.json 2>>$O/bench.err; done
