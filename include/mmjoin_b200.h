@@ -261,6 +261,17 @@ int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64
                    int64_t r_n, const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const uint32_t* r_bits,
                    const uint32_t* s_bits, int words, const int32_t* r_lptr, const int32_t* r_lidx,
                    const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, void* stream);
+/* direct-address id map for dense raw id ranges: table[range] = dense id of
+ * raw value vmin + i, -1 where absent (replaces the per-query binary search of
+ * mmj_bsi_answer by one load; range = max - min + 1 < 2^31) */
+int mmj_bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
+                         int32_t* table, void* stream);
+/* mmj_bsi_answer with both query sides resolved through direct tables */
+int mmj_bsi_answer_tables(const int64_t* qa, const int64_t* qb, int64_t nq, const int32_t* r_table, int64_t r_min,
+                          int64_t r_range, const int32_t* s_table, int64_t s_min, int64_t s_range,
+                          const uint32_t* r_bits, const uint32_t* s_bits, int words, const int32_t* r_lptr,
+                          const int32_t* r_lidx, const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans,
+                          void* stream);
 
 
 /* ---- device ingest: relation.py:37-69, 119-140, 148-186 ----

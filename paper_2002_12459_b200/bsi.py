@@ -24,6 +24,7 @@ from . import _native as nat
 from .device import Workspace
 
 BITS_BLOCK = 128     # bitset width granularity (4 words)
+DIRECT_SPREAD = 4    # direct id table when max - min + 1 <= 4 x the number of ids
 
 
 def _torch():
@@ -226,6 +227,24 @@ class BsiEngine:
                      nat.ptr(self.hpos), nat.ptr(lflag), nat.ptr(lpos), nat.ptr(lptr), nat.ptr(lidx),
                      nat.ptr(self.ws.scan_ws(sd.n)), st)
             self.sides.append((bits, lptr, lidx))
+        self.tables = [self._direct_table(tag, sd) for tag, sd in (("r", self.sR), ("s", self.sS))]
+
+    def _direct_table(self, tag, sd: BsiSide):
+        """(table, vmin, range) when the side's raw ids fill at most
+        DIRECT_SPREAD x their count of a value range: each query id then
+        resolves with one load instead of a binary search (cfg5: 4M ids in
+        [0, 4M), a 16 MB table that stays in L2)."""
+        if sd.sorted_vals is None or sd.dom_left == 0:
+            return None
+        torch = _torch()
+        ends = torch.stack([sd.sorted_vals[0], sd.sorted_vals[sd.dom_left - 1]]).cpu().tolist()
+        vmin, rng = int(ends[0]), int(ends[1]) - int(ends[0]) + 1
+        if rng > DIRECT_SPREAD * sd.dom_left or rng >= (1 << 31) - 1:
+            return None
+        table = self.ws.get(f"direct_{tag}", rng, torch.int32)
+        nat.call("mmj_bsi_direct_table", nat.ptr(sd.sorted_vals), nat.ptr(sd.order), sd.dom_left, vmin, rng,
+                 nat.ptr(table), nat.stream_handle())
+        return table, vmin, rng
 
     def answer(self, qa_dev, qb_dev, nq, dense_a=False, dense_b=False, out=None):
         torch = _torch()
@@ -233,6 +252,12 @@ class BsiEngine:
         ans = out if out is not None else torch.empty(max(nq, 1), dtype=torch.int8, device="cuda")
         (rb, rlp, rli), (sb, slp, sli) = self.sides
         sR, sS = self.sR, self.sS
+        ta, tb = getattr(self, "tables", (None, None))
+        if not dense_a and not dense_b and ta is not None and tb is not None:
+            nat.call("mmj_bsi_answer_tables", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, nat.ptr(ta[0]), ta[1], ta[2],
+                     nat.ptr(tb[0]), tb[1], tb[2], nat.ptr(rb), nat.ptr(sb), self.words, nat.ptr(rlp), nat.ptr(rli),
+                     nat.ptr(slp), nat.ptr(sli), nat.ptr(ans), st)
+            return ans[:nq]
         rs = 0 if dense_a else nat.ptr(sR.sorted_vals)
         ro = 0 if dense_a else nat.ptr(sR.order)
         ss = 0 if dense_b else nat.ptr(sS.sorted_vals)

@@ -86,10 +86,28 @@ struct BsiArgs {
   int8_t* ans;
 };
 
-__global__ void k_bsi_answer(const BsiArgs a) {
+// raw id -> dense id: binary search over the sorted raw values, or one load
+// from a direct-address table (dense_of[raw - vmin], -1 = unknown id)
+struct IdMap {
+  const int64_t* sorted;
+  const int32_t* order;
+  int64_t n;
+  const int32_t* table;
+  int64_t vmin, range;
+};
+
+__device__ __forceinline__ int32_t map_id(const IdMap& m, int64_t v) {
+  if (m.table) {
+    const int64_t o = v - m.vmin;
+    return (o >= 0 && o < m.range) ? __ldg(m.table + o) : -1;
+  }
+  return m.sorted ? lookup(m.sorted, m.order, m.n, v) : (int32_t)v;
+}
+
+__global__ void k_bsi_answer(const BsiArgs a, const IdMap ma, const IdMap mb) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.nq; q += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t ia = a.r_sorted ? lookup(a.r_sorted, a.r_order, a.r_n, a.qa[q]) : (int32_t)a.qa[q];
-    const int32_t ib = a.s_sorted ? lookup(a.s_sorted, a.s_order, a.s_n, a.qb[q]) : (int32_t)a.qb[q];
+    const int32_t ia = map_id(ma, a.qa[q]);
+    const int32_t ib = map_id(mb, a.qb[q]);
     if (ia < 0 || ib < 0) {
       a.ans[q] = -1;
       continue;
@@ -116,6 +134,14 @@ __global__ void k_bsi_answer(const BsiArgs a) {
       }
     }
     a.ans[q] = hit ? 1 : 0;
+  }
+}
+
+__global__ void k_direct_table(const int64_t* __restrict__ sorted, const int32_t* __restrict__ order, int64_t n,
+                               int64_t vmin, int64_t range, int32_t* __restrict__ table) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = sorted[i] - vmin;
+    if (o >= 0 && o < range) table[o] = order[i];
   }
 }
 
@@ -170,7 +196,8 @@ int bsi_light_lists(const int32_t* ptr, const int32_t* cols, int64_t n, int64_t 
 int bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted, const int32_t* r_order,
                int64_t r_n, const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const uint32_t* r_bits,
                const uint32_t* s_bits, int words, const int32_t* r_lptr, const int32_t* r_lidx,
-               const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, cudaStream_t st) {
+               const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, const int32_t* r_table, int64_t r_min,
+               int64_t r_range, const int32_t* s_table, int64_t s_min, int64_t s_range, cudaStream_t st) {
   if (words % 4 != 0 || words <= 0) {
     set_error("bsi_answer: bitset words must be a positive multiple of 4");
     return MMJ_ERR_ARG;
@@ -178,8 +205,23 @@ int bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* 
   if (nq == 0) return MMJ_OK;
   BsiArgs a{qa, qb, nq, r_sorted, r_order, r_n, s_sorted, s_order, s_n, r_bits, s_bits, words,
             r_lptr, r_lidx, s_lptr, s_lidx, ans};
-  k_bsi_answer<<<grid_for(nq, TPB, 16), TPB, 0, st>>>(a);
+  const IdMap ma{r_sorted, r_order, r_n, r_table, r_min, r_range};
+  const IdMap mb{s_sorted, s_order, s_n, s_table, s_min, s_range};
+  k_bsi_answer<<<grid_for(nq, TPB, 16), TPB, 0, st>>>(a, ma, mb);
   MMJ_CHECK_LAUNCH("k_bsi_answer");
+  return MMJ_OK;
+}
+
+int bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
+                     int32_t* table, cudaStream_t st) {
+  if (range <= 0 || range >= (1ll << 31)) {
+    set_error("bsi_direct_table: range %lld out of (0, 2^31)", (long long)range);
+    return MMJ_ERR_ARG;
+  }
+  MMJ_TRY(cuda_status(cudaMemsetAsync(table, 0xFF, (size_t)range * 4, st), "memset direct table"));
+  if (n == 0) return MMJ_OK;
+  k_direct_table<<<grid_for(n), TPB, 0, st>>>(sorted, order, n, vmin, range, table);
+  MMJ_CHECK_LAUNCH("k_direct_table");
   return MMJ_OK;
 }
 

@@ -48,7 +48,9 @@ int bsi_light_lists(const int32_t*, const int32_t*, int64_t, int64_t, const int3
                     int32_t*, void*, cudaStream_t);
 int bsi_answer(const int64_t*, const int64_t*, int64_t, const int64_t*, const int32_t*, int64_t, const int64_t*,
                const int32_t*, int64_t, const uint32_t*, const uint32_t*, int, const int32_t*, const int32_t*,
-               const int32_t*, const int32_t*, int8_t*, cudaStream_t);
+               const int32_t*, const int32_t*, int8_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t,
+               int64_t, cudaStream_t);
+int bsi_direct_table(const int64_t*, const int32_t*, int64_t, int64_t, int64_t, int32_t*, cudaStream_t);
 int star_split(int, const int32_t* const*, int64_t, double, uint8_t*, uint8_t*, int32_t*, int32_t*, int32_t*, int32_t*,
                void*, cudaStream_t);
 int star_operand(int, const int64_t*, const uint8_t* const*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
@@ -250,7 +252,25 @@ int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64
                    const uint32_t* s_bits, int words, const int32_t* r_lptr, const int32_t* r_lidx,
                    const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, void* stream) {
   return mmj::bsi_answer(qa, qb, nq, r_sorted, r_order, r_n, s_sorted, s_order, s_n, r_bits, s_bits, words, r_lptr,
-                         r_lidx, s_lptr, s_lidx, ans, ST(stream));
+                         r_lidx, s_lptr, s_lidx, ans, nullptr, 0, 0, nullptr, 0, 0, ST(stream));
+}
+
+int mmj_bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
+                         int32_t* table, void* stream) {
+  return mmj::bsi_direct_table(sorted, order, n, vmin, range, table, ST(stream));
+}
+
+int mmj_bsi_answer_tables(const int64_t* qa, const int64_t* qb, int64_t nq, const int32_t* r_table, int64_t r_min,
+                          int64_t r_range, const int32_t* s_table, int64_t s_min, int64_t s_range,
+                          const uint32_t* r_bits, const uint32_t* s_bits, int words, const int32_t* r_lptr,
+                          const int32_t* r_lidx, const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans,
+                          void* stream) {
+  if (r_table == nullptr || s_table == nullptr) {
+    mmj::set_error("bsi_answer_tables: both direct tables are required (mmj_bsi_answer resolves by search)");
+    return MMJ_ERR_ARG;
+  }
+  return mmj::bsi_answer(qa, qb, nq, nullptr, nullptr, 0, nullptr, nullptr, 0, r_bits, s_bits, words, r_lptr, r_lidx,
+                         s_lptr, s_lidx, ans, r_table, r_min, r_range, s_table, s_min, s_range, ST(stream));
 }
 
 int mmj_star_split(int k, const int32_t* const* rev_ptr, int64_t dom_y, double threshold, uint8_t* heavy_flag,

@@ -174,6 +174,40 @@ def test_bsi_zipf_vs_oracle(oracle, heavy_bits):
     assert (exp == -1).any() and (exp == 1).any() and (exp == 0).any()
 
 
+@pytest.mark.parametrize("spread", [1, 1000])
+def test_bsi_direct_table_vs_search(oracle, spread, monkeypatch):
+    """Query ids resolved through the direct-address tables (dense raw id
+    ranges) and through the binary search (DIRECT_SPREAD = 0, and ids spread
+    x1000 so no table is built): identical answers, equal to the oracle."""
+    from paper_2002_12459_b200 import bsi
+    from paper_2002_12459_b200.apps import bsi_answer_batch_arrays
+    from paper_2002_12459_b200.relation import Relation, build_indexed
+    rng = np.random.default_rng(77 + spread)
+    rp = np.array(zipf_pairs(rng, 40000, 3000, 6000, 1.0))
+    sp = np.array(zipf_pairs(rng, 40000, 3000, 6000, 1.0))
+    rp[:, 0] *= spread
+    sp[:, 0] *= spread
+    q = rng.integers(0, 3100, (15000, 2)) * spread
+    q[::7] += 1     # ids between the spread values (unknown unless spread == 1)
+    exp = oracle.bsi(oracle.encode(rp), oracle.encode(sp), q[:, 0], q[:, 1])
+    r = build_indexed(Relation.from_raw_pairs("R", rp))
+    s = build_indexed(Relation.from_raw_pairs("S", sp))
+    got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1])
+    assert np.array_equal(got, exp)
+    monkeypatch.setattr(bsi, "DIRECT_SPREAD", 0)
+    r._mmj_bsi_cache = None
+    got2 = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1])
+    assert np.array_equal(got2, exp)
+
+
+def test_bsi_tables_abi_errors():
+    from paper_2002_12459_b200 import _native as nat
+    nat.require_cuda()
+    lib = nat.load()
+    assert lib.mmj_bsi_direct_table(0, 0, 0, 0, 0, 0, 0) == nat.MMJ_ERR_ARG
+    assert lib.mmj_bsi_answer_tables(0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 4, 0, 0, 0, 0, 0, 0) == nat.MMJ_ERR_ARG
+
+
 def test_star_golden():
     from paper_2002_12459_b200.joinproject import star_join
     from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce_many
