@@ -712,7 +712,13 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     // 2-5 with bits 6-9 (quads stay contiguous for the 8-byte reads, the
     // lanes' runs spread over the banks during the expansion)
     uint16_t* gst = &sm.u.stage[0][0];
+#ifdef MMJ_CTA_QUADS
+    constexpr bool QUAD = true;    // 32-B stores; swizzle keeps quads contiguous
     auto sw = [](int k) { return k ^ (((k >> 6) & 15) << 2); };
+#else
+    constexpr bool QUAD = false;   // 16-B stores; k_emit_pf16's pair-preserving swizzle
+    auto sw = [](int k) { return k ^ (((k >> 5) & 31) << 1); };
+#endif
     const int segs_per_piece = cw >> 5;
     int64_t* const codes = f.codes + sm.prefix;
     for (int g0 = 0; g0 < nseg; g0 += NWARP) {
@@ -721,7 +727,7 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
       const int gend = (g0 + ng < nseg) ? s_segoff[g0 + ng] : agg;
       const int total = gend - goff;
       int64_t* const gout = codes + goff;
-      const int mis = (int)((reinterpret_cast<uintptr_t>(gout) >> 3) & 3);
+      const int mis = (int)((reinterpret_cast<uintptr_t>(gout) >> 3) & (QUAD ? 3 : 1));
       const int rr0 = g0 / segs_per_piece;
       const bool one_row = rr0 == (g0 + ng - 1) / segs_per_piece;
       const int si = g0 + warp;
@@ -759,24 +765,40 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
       }
       __syncthreads();
       if (total > 0) {
-        const int nq = (mis + total + 3) >> 2;
-        int64_t* const oa = gout - mis;   // 32-byte aligned
         const int64_t gbase =
             one_row ? (a.x0 + r0 + rr0) * a.dom_z + (c0w + (int64_t)(g0 - rr0 * segs_per_piece) * 32) * 32 : 0;
-        for (int q = tid; q < nq; q += NT) {
-          const uint2 raw = *reinterpret_cast<const uint2*>(gst + sw(4 * q));
-          const uint32_t v[4] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16};
-          int64_t cd[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            cd[i] = one_row ? gbase + (int64_t)v[i] : sm.gb[(v[i] >> 10) & (NWARP - 1)] + (int64_t)(v[i] & 1023u);
-          const int e0 = 4 * q;
-          if (e0 >= mis && e0 + 4 <= mis + total) {
-            st_v4(oa + e0, cd[0], cd[1], cd[2], cd[3]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (e0 + i >= mis && e0 + i < mis + total) oa[e0 + i] = cd[i];
+        auto code_of = [&](uint32_t v) -> int64_t {
+          return one_row ? gbase + (int64_t)v : sm.gb[(v >> 10) & (NWARP - 1)] + (int64_t)(v & 1023u);
+        };
+        int64_t* const oa = gout - mis;   // 32-byte (quads) / 16-byte (pairs) aligned
+        if (QUAD) {
+          const int nq = (mis + total + 3) >> 2;
+          for (int q = tid; q < nq; q += NT) {
+            const uint2 raw = *reinterpret_cast<const uint2*>(gst + sw(4 * q));
+            const int64_t c0 = code_of(raw.x & 0xFFFFu), c1 = code_of(raw.x >> 16);
+            const int64_t c2 = code_of(raw.y & 0xFFFFu), c3 = code_of(raw.y >> 16);
+            const int e0 = 4 * q;
+            if (e0 >= mis && e0 + 4 <= mis + total) {
+              st_v4(oa + e0, c0, c1, c2, c3);
+            } else {
+              if (e0 >= mis && e0 < mis + total) oa[e0] = c0;
+              if (e0 + 1 >= mis && e0 + 1 < mis + total) oa[e0 + 1] = c1;
+              if (e0 + 2 >= mis && e0 + 2 < mis + total) oa[e0 + 2] = c2;
+              if (e0 + 3 >= mis && e0 + 3 < mis + total) oa[e0 + 3] = c3;
+            }
+          }
+        } else {
+          const int np = (mis + total + 1) >> 1;
+          for (int p = tid; p < np; p += NT) {
+            const uint32_t two = *reinterpret_cast<const uint32_t*>(gst + sw(2 * p));
+            const int64_t c0 = code_of(two & 0xFFFFu), c1 = code_of(two >> 16);
+            const int e0 = 2 * p;
+            if (e0 >= mis && e0 + 2 <= mis + total) {
+              st_cs2(oa + e0, c0, c1);
+            } else {
+              if (e0 >= mis && e0 < mis + total) st_cs(oa + e0, c0);
+              if (e0 + 1 >= mis && e0 + 1 < mis + total) st_cs(oa + e0 + 1, c1);
+            }
           }
         }
       }
