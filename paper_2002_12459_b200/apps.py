@@ -113,20 +113,20 @@ def _compact_family(idx, c: int):
     dc = DeviceRelation()
     dc.fwd_ptr, dc.fwd_idx, dc.fwd_row, dc.left_deg = buf(dom + 1), buf(n), buf(n), buf(dom)
     dc.rev_ptr, dc.rev_idx, dc.right_deg = buf(dom_y + 1), buf(n), buf(dom_y)
-    sizes = torch.zeros(2, dtype=torch.int64, device="cuda")
+    sizes = torch.empty(2, dtype=torch.int64, device="cuda")   # written by mmj_compact_rows
     ws_buf, nb = IngestWorkspace().get(max(n, dom, dom_y))
     nat.call("mmj_compact_rows", nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.fwd_row), nat.ptr(dr.rev_ptr),
              nat.ptr(dr.rev_idx), nat.ptr(dr.left_deg), n, dom, dom_y, int(c), nat.ptr(new_id), nat.ptr(orig),
              nat.ptr(dc.fwd_ptr), nat.ptr(dc.fwd_idx), nat.ptr(dc.fwd_row), nat.ptr(dc.left_deg), nat.ptr(dc.rev_ptr),
              nat.ptr(dc.rev_idx), nat.ptr(dc.right_deg), nat.ptr(sizes), nat.ptr(ws_buf), nb, nat.stream_handle())
-    # the kept sets and tuples are known on the host already (the degrees the
-    # plan used): no device round trip for the sizes
-    dom_c, n_c = int(keep.sum()), int(ldeg[keep].sum())
+    # one small D2H brings back the compacted offsets (their last entry is n')
+    dom_c = nk
+    dc.fwd_ptr_host = dc.fwd_ptr[:dom_c + 1].cpu().numpy().astype(np.int64)
+    n_c = int(dc.fwd_ptr_host[-1])
     dc.n, dc.dom_left, dc.dom_right, dc.device, dc.h2d_bytes = n_c, dom_c, dom_y, dr.device, 0
     dc.fwd_ptr, dc.left_deg = dc.fwd_ptr[:dom_c + 1], dc.left_deg[:dom_c]
     dc.fwd_idx, dc.fwd_row, dc.rev_idx = dc.fwd_idx[:n_c], dc.fwd_row[:n_c], dc.rev_idx[:n_c]
-    dc.fwd_ptr_host = np.concatenate([[0], np.cumsum(ldeg[keep], dtype=np.int64)])
-    return dc, orig[:dom_c], ldeg[keep]
+    return dc, orig[:dom_c], np.diff(dc.fwd_ptr_host)
 
 
 def _decode_compact(codes, dom_c: int, orig, dom: int):
