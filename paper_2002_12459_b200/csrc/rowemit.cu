@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
         const int64_t gbase =
             one_row ? (a.x0 + r0 + rr0) * a.dom_z + (c0w + (int64_t)(g0 - rr0 * segs_per_piece) * 32) * 32 : 0;
         auto code_of = [&](uint32_t v) -> int64_t {
-          return one_row ? gbase + (int64_t)v : sm.gb[(v >> 10) & (NWARP - 1)] + (int64_t)(v & 1023u);
+          return one_row ? gbase + (int64_t)v : sm.gb[v >> 10] + (int64_t)(v & 1023u);
         };
         int64_t* const oa = gout - mis;   // 32-byte (quads) / 16-byte (pairs) aligned
         if (QUAD) {
