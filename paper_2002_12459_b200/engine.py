@@ -37,6 +37,24 @@ FUSED_SMEM_LIMIT = 200 * 1024
 SYNC_FUSED_CAP_BYTES = 4 << 30
 
 
+_HOST_MAX = {}
+
+
+def _host_max(arr) -> int:
+    """max of a host degree array, remembered per array object: the inputs
+    are immutable (as the reference's IndexedRelation), and engines for the
+    same relations (one per batch / shard / step) would otherwise rescan
+    them on the host (~0.3 ms per 500k-entry array on the GPU box)."""
+    hit = _HOST_MAX.get(id(arr))
+    if hit is not None and hit[0] is arr:
+        return hit[1]
+    m = int(np.asarray(arr).max(initial=0))
+    if len(_HOST_MAX) >= 64:
+        _HOST_MAX.clear()
+    _HOST_MAX[id(arr)] = (arr, m)   # the reference keeps the id from being reused
+    return m
+
+
 def _rup(a: int, b: int) -> int:
     return -(-a // b) * b
 
@@ -237,13 +255,11 @@ class TwoPathEngine:
     @staticmethod
     def _max_deg(host_deg, d: DeviceRelation) -> int:
         if host_deg is not None:
-            return int(np.asarray(host_deg).max(initial=0))
+            return _host_max(host_deg)
         return int(d.left_deg.max().item()) if d.left_deg.numel() else 0
 
     def _any_heavy(self, host_deg, d: DeviceRelation) -> bool:
-        if host_deg is not None:
-            return bool((np.asarray(host_deg) > self.d2).any())
-        return bool((d.left_deg > self.d2).any().item())
+        return self._max_deg(host_deg, d) > self.d2
 
     # ------------------------------------------------------------ chunks
     def chunk_bounds(self, x_begin: int = 0, x_end: Optional[int] = None):
