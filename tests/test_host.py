@@ -194,6 +194,35 @@ def test_capi_argument_errors_without_gpu():
     assert rc == 1 and b"unknown mode" in lib.mmj_last_error()
 
 
+def test_capi_new_entry_points_argument_errors_without_gpu():
+    """SSJ compaction / code decode / BSI direct tables: argument checks run
+    before any CUDA call."""
+    from paper_2002_12459_b200 import _native
+    if not _native.lib_path().exists():
+        pytest.skip("libmmjoin_b200.so not built")
+    lib = _native.load()
+    assert lib.mmj_compact_rows(*([None] * 6), 0, 0, 0, -1, *([None] * 11), 0, None) == 1
+    assert b"min_deg" in lib.mmj_last_error()
+    assert lib.mmj_compact_rows(*([None] * 6), -5, 0, 0, 2, *([None] * 11), 0, None) == 1
+    assert lib.mmj_decode_compact_codes(None, 4, 0, None, None, 10, None, None) == 1
+    assert b"domains" in lib.mmj_last_error()
+    assert lib.mmj_bsi_direct_table(None, None, 0, 0, 0, None, None) == 1
+    assert b"range" in lib.mmj_last_error()
+    assert lib.mmj_bsi_answer_tables(None, None, 1, None, 0, 1, None, 0, 1, None, None, 4, None, None, None, None,
+                                     None, None) == 1
+    assert b"direct tables" in lib.mmj_last_error()
+
+
+def test_engine_host_degree_max_memo():
+    from paper_2002_12459_b200.engine import _host_max
+    a = np.array([3, 9, 2], dtype=np.int64)
+    b = np.array([3, 9, 2], dtype=np.int64)
+    assert _host_max(a) == 9 and _host_max(a) == 9
+    assert _host_max(b) == 9
+    assert _host_max(np.empty(0, dtype=np.int64)) == 0
+    assert _host_max([1, 40, 7]) == 40          # list input (reference objects may hold lists)
+
+
 def test_product_fails_loudly_without_gpu():
     import torch
     if torch.cuda.is_available():
