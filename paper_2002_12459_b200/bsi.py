@@ -227,9 +227,14 @@ class BsiEngine:
                      nat.ptr(self.hpos), nat.ptr(lflag), nat.ptr(lpos), nat.ptr(lptr), nat.ptr(lidx),
                      nat.ptr(self.ws.scan_ws(sd.n)), st)
             self.sides.append((bits, lptr, lidx))
-        self.tables = [self._direct_table(tag, sd) for tag, sd in (("r", self.sR), ("s", self.sS))]
+        sides = (("r", self.sR), ("s", self.sS))
+        # both sides' smallest / largest raw ids in one device -> host copy
+        ends = [sd.sorted_vals[[0, sd.dom_left - 1]] for _, sd in sides
+                if sd.sorted_vals is not None and sd.dom_left > 0]
+        ends = iter(torch.cat(ends).cpu().tolist()) if ends else iter(())
+        self.tables = [self._direct_table(tag, sd, ends) for tag, sd in sides]
 
-    def _direct_table(self, tag, sd: BsiSide):
+    def _direct_table(self, tag, sd: BsiSide, ends):
         """(table, vmin, range) when the side's raw ids fill at most
         DIRECT_SPREAD x their count of a value range: each query id then
         resolves with one load instead of a binary search (cfg5: 4M ids in
@@ -237,8 +242,8 @@ class BsiEngine:
         if sd.sorted_vals is None or sd.dom_left == 0:
             return None
         torch = _torch()
-        ends = torch.stack([sd.sorted_vals[0], sd.sorted_vals[sd.dom_left - 1]]).cpu().tolist()
-        vmin, rng = int(ends[0]), int(ends[1]) - int(ends[0]) + 1
+        lo, hi = next(ends), next(ends)
+        vmin, rng = int(lo), int(hi) - int(lo) + 1
         if rng > DIRECT_SPREAD * sd.dom_left or rng >= (1 << 31) - 1:
             return None
         table = self.ws.get(f"direct_{tag}", rng, torch.int32)
