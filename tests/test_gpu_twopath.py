@@ -206,3 +206,29 @@ def test_triple_operand_count_boundary(pkg, oracle, deg_x0, monkeypatch):
     exp = oracle.two_path(R, S, oracle.OPlan("partitioned", 1, 1))
     assert np.array_equal(got[0], exp.codes)
     assert got[2].heavy_pairs == exp.stats["heavy_pairs"]
+
+
+@pytest.mark.parametrize("case", ["disjoint_y", "single_pair", "one_hub_y", "one_x_row", "skinny_z"])
+def test_two_path_edge_cases(pkg, oracle, case):
+    """Empty semi-join result, a single output pair, one y shared by every
+    tuple (K = 1 heavy column), a single output row, a single output column:
+    every plan, with and without counts, bit-exact vs the oracle."""
+    if case == "disjoint_y":
+        rp = [(x, 2 * x) for x in range(50)]
+        sp = [(z, 2 * z + 1) for z in range(50)]
+    elif case == "single_pair":
+        rp = [(7, 3), (8, 4)]
+        sp = [(9, 3), (10, 5)]
+    elif case == "one_hub_y":
+        rp = [(x, 0) for x in range(300)] + [(x, 1 + x % 7) for x in range(300)]
+        sp = [(z, 0) for z in range(260)] + [(z, 1 + z % 5) for z in range(0, 260, 3)]
+    elif case == "one_x_row":
+        rp = [(5, y) for y in range(200)]
+        sp = [(z, y % 200) for z in range(40) for y in range(z, z + 15)]
+    else:
+        rp = [(x, y) for x in range(120) for y in range(x % 9, x % 9 + 4)]
+        sp = [(3, y) for y in range(20)]
+    nn = max(len(rp), len(sp))
+    plans = [("partitioned", 1, 1), ("partitioned", 2, 1), ("partitioned", 3, 4), ("partitioned", nn, nn),
+             ("fulljoin", nn, nn)]
+    _check(pkg, oracle, rp, sp, plans)
