@@ -284,3 +284,25 @@ def test_ssj_ordered_and_scj_on_device(oracle):
     sa, sb = scj_join_project_arrays(fam)
     assert np.array_equal(sa, x[keep]) and np.array_equal(sb, z[keep])
     assert keep.sum() > 0
+
+
+@pytest.mark.parametrize("case", ["singletons", "identical_sets", "one_big_set"])
+def test_ssj_edge_families(oracle, case):
+    """All sets of size 1 (no pair reaches c >= 2), several identical sets
+    (every pair at overlap = |set|), one large set among singletons."""
+    from paper_2002_12459_b200.apps import SetFamily, ssj_mmjoin, ssj_mmjoin_arrays
+    from paper_2002_12459_b200.relation import Relation
+    if case == "singletons":
+        pairs = np.array([(a, a % 13) for a in range(200)], dtype=np.int64)
+    elif case == "identical_sets":
+        pairs = np.array([(a, e) for a in range(30) for e in range(10, 22)], dtype=np.int64)
+    else:
+        pairs = np.array([(0, e) for e in range(500)] + [(a, a * 3) for a in range(1, 150)], dtype=np.int64)
+    fam = SetFamily(Relation.from_raw_pairs("sets", pairs))
+    for c in (1, 2, 12):
+        ea, eb, en = oracle.ssj_arrays(oracle.encode(pairs), c)
+        a, b, n = ssj_mmjoin_arrays(fam, c)
+        assert np.array_equal(a, ea) and np.array_equal(b, eb) and np.array_equal(n, en), (case, c)
+    if case == "identical_sets":
+        got = ssj_mmjoin(fam, 12)
+        assert len(got) == 30 * 29 // 2 and set(got.values()) == {12}
