@@ -334,6 +334,9 @@ int mmj_compact_rows(const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32
  * compact codes back to the caller's dense-id codes; ascending stays ascending */
 int mmj_decode_compact_codes(const int64_t* in, int64_t n, int64_t dom_c, const int32_t* orig_l,
                              const int32_t* orig_r, int64_t dom_out, int64_t* out, void* stream);
+/* a[i] = codes[i] / dom, b[i] = codes[i] % dom (codes >= 0): the result pairs
+ * of SSJ / SCJ as two arrays (apps.py:57-62 unpacks codes the same way) */
+int mmj_split_codes(const int64_t* codes, int64_t n, int64_t dom, int64_t* a, int64_t* b, void* stream);
 int mmj_ingest_csr(const int32_t* rows, const int32_t* cols, int64_t n, int64_t dom_rows, int64_t dom_cols,
                    int32_t* ptr, int32_t* idx, int32_t* row_of, int32_t* deg, void* ws, size_t ws_bytes,
                    void* stream);

@@ -62,6 +62,7 @@ _SIGS = {
     "mmj_ingest_csr": (INT, [P, P, I64, I64, I64, P, P, P, P, P, SZ, P]),
     "mmj_compact_rows": (INT, [P, P, P, P, P, P, I64, I64, I64, I64] + [P] * 11 + [SZ, P]),
     "mmj_decode_compact_codes": (INT, [P, I64, I64, P, P, I64, P, P]),
+    "mmj_split_codes": (INT, [P, I64, I64, P, P, P]),
     "mmj_build_operand_pairs": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
     "mmj_build_operand_triple": (INT, [INT, P, P, I64, P, I64, P, P, I64, I64, I64, I64, P]),
     "mmj_light_z_csr": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P]),

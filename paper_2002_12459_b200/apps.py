@@ -174,12 +174,25 @@ def _split(codes: np.ndarray, dz: int):
     return codes // dz, codes % dz
 
 
+def _split_device(codes, dz: int):
+    """(codes // dz, codes % dz) computed on the device (mmj_split_codes) and
+    copied back: the host would otherwise divide ~2e8 int64 codes in numpy."""
+    import torch
+
+    from . import _native as nat
+    n = int(codes.numel())
+    a = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    b = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    nat.call("mmj_split_codes", nat.ptr(codes), n, int(dz), nat.ptr(a), nat.ptr(b), nat.stream_handle())
+    return a[:n].cpu().numpy(), b[:n].cpu().numpy()
+
+
 def ssj_mmjoin_arrays(family: SetFamily, c: int, plan: Optional[ThresholdPlan] = None,
                       chunk_rows: Optional[int] = None):
     """(a, b, overlap) int64 arrays of every unordered pair a < b (dense set
     ids) with |a n b| >= c, in ascending (a, b) order."""
     cd, cn = _ssj_device(family, c, plan, chunk_rows)
-    a, b = _split(cd.cpu().numpy(), family.indexed.rel.dom_left)
+    a, b = _split_device(cd, family.indexed.rel.dom_left)
     return a, b, cn.cpu().numpy().astype(np.int64)
 
 
@@ -210,7 +223,7 @@ def ssj_ordered_arrays(family: SetFamily, c: int, plan: Optional[ThresholdPlan] 
         nat.call("mmj_ingest_gather", nat.ptr(cd), 8, nat.ptr(order), n, nat.ptr(cd2), st)
         nat.call("mmj_ingest_gather", nat.ptr(cn), 4, nat.ptr(order), n, nat.ptr(cn2), st)
         cd, cn = cd2, cn2
-    a, b = _split(cd.cpu().numpy(), family.indexed.rel.dom_left)
+    a, b = _split_device(cd, family.indexed.rel.dom_left)
     return a, b, cn.cpu().numpy().astype(np.int64)
 
 
@@ -235,7 +248,7 @@ def scj_join_project_arrays(family: SetFamily, plan: Optional[ThresholdPlan] = N
     eng = TwoPathEngine(dr, dr, plan.strategy, d1, d2, True, off_diagonal=True, row_min=dr.left_deg,
                         host_left_deg_r=idx.left_deg, host_left_deg_s=idx.left_deg)
     cd, _ = _device_pairs(eng)
-    return _split(cd.cpu().numpy(), idx.rel.dom_left)
+    return _split_device(cd, idx.rel.dom_left)
 
 
 def scj_join_project(family: SetFamily) -> set:

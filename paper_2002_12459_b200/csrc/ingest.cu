@@ -374,6 +374,20 @@ __global__ void k_decode_codes(const int64_t* in, int64_t n, int64_t dom_c, doub
   }
 }
 
+// code -> (code / dom, code % dom): the (a, b) arrays of SSJ / SCJ results
+__global__ void k_split_codes(const int64_t* __restrict__ codes, int64_t n, int64_t dom, double inv,
+                              int64_t* __restrict__ a, int64_t* __restrict__ b) {
+  GRID_STRIDE(i, n) {
+    const int64_t c = codes[i];
+    int64_t q = (int64_t)((double)c * inv);
+    int64_t r = c - q * dom;
+    while (r < 0) { --q; r += dom; }
+    while (r >= dom) { ++q; r -= dom; }
+    a[i] = q;
+    b[i] = r;
+  }
+}
+
 struct Scratch {
   Bump w;
   int64_t *k0, *k1, *k2, *k3;
@@ -642,6 +656,18 @@ int mmj_decode_compact_codes(const int64_t* in, int64_t n, int64_t dom_c, const 
   if (n == 0) return MMJ_OK;
   k_decode_codes<<<grid1(n), TPB, 0, st>>>(in, n, dom_c, 1.0 / (double)dom_c, orig_l, orig_r, dom_out, out);
   MMJ_CHECK_LAUNCH("k_decode_codes");
+  return MMJ_OK;
+}
+
+int mmj_split_codes(const int64_t* codes, int64_t n, int64_t dom, int64_t* a, int64_t* b, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n < 0 || dom <= 0) {
+    set_error("split_codes: need n >= 0 and dom > 0 (got %lld, %lld)", (long long)n, (long long)dom);
+    return MMJ_ERR_ARG;
+  }
+  if (n == 0) return MMJ_OK;
+  k_split_codes<<<grid1(n), TPB, 0, st>>>(codes, n, dom, 1.0 / (double)dom, a, b);
+  MMJ_CHECK_LAUNCH("k_split_codes");
   return MMJ_OK;
 }
 

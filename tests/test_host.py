@@ -211,6 +211,8 @@ def test_capi_new_entry_points_argument_errors_without_gpu():
     assert lib.mmj_bsi_answer_tables(None, None, 1, None, 0, 1, None, 0, 1, None, None, 4, None, None, None, None,
                                      None, None) == 1
     assert b"direct tables" in lib.mmj_last_error()
+    assert lib.mmj_split_codes(None, 4, 0, None, None, None) == 1
+    assert b"split_codes" in lib.mmj_last_error()
 
 
 def test_engine_host_degree_max_memo():
