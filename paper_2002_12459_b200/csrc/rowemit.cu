@@ -210,13 +210,13 @@ __device__ __forceinline__ unsigned long long merge_light(
     int ti = 0;   // tuple of the current slot; slots grow, so the cursor only moves forward
     // MERGE_ILP slots per thread per step: their list loads are issued
     // together before the shared-memory atomics (the loads are the latency)
-    for (int s0 = tid; s0 < tot; s0 += MERGE_ILP * TM_THREADS) {
+    for (int s0 = tid; s0 < tot; s0 += MERGE_ILP * NT) {
       int32_t zv[MERGE_ILP];
       int rowv[MERGE_ILP];
       bool ok[MERGE_ILP];
 #pragma unroll
       for (int u = 0; u < MERGE_ILP; ++u) {
-        const int s = s0 + u * TM_THREADS;
+        const int s = s0 + u * NT;
         ok[u] = s < tot;
         rowv[u] = 0;
         zv[u] = 0;
