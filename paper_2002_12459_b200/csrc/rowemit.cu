@@ -1475,15 +1475,18 @@ int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int6
   if (fuse_persistent() && tw == 4096) return launch_merge_emit_p<4096, 8>(f, st);
   static int variant = -1;
   if (variant < 0) {
-    const char* e = getenv("MMJ_FUSE_VARIANT");   // A/B: 1 = (4096, 256 thr, 6 CTAs/SM), 2 = (16384, 512 thr)
+    const char* e = getenv("MMJ_FUSE_VARIANT");   // A/B: 1 = (4096, 256 thr, 6 CTAs/SM), 2 = (16384, 512 thr), 3 = (8192, 256 thr, 4)
     variant = e ? atoi(e) : 0;
   }
   if (variant == 1 && tw == 4096) return launch_merge_emit<4096, 256, 6>(f, st);
   if (variant == 2 && tw == 16384) return launch_merge_emit<16384, 512, 2>(f, st);
+  if (variant == 3 && tw == 8192) return launch_merge_emit<8192, 256, 4>(f, st);   // the round-1d..1f default
   switch (tw) {
     case 4096: return launch_merge_emit<4096, 256, 4>(f, st);
     case 16384: return launch_merge_emit<16384, 256, 2>(f, st);
-    default: return launch_merge_emit<8192, 256, 4>(f, st);
+    // 9 warps x 4 CTAs = 36 warps per SM at 54 registers (171.8 vs 173.1 ms
+    // per cfg2 step for 8 warps: more warps hide the look-back wait)
+    default: return launch_merge_emit<8192, 288, 4>(f, st);
   }
 }
 
