@@ -45,16 +45,10 @@ extern "C" {
 #define MMJ_MODE_BITMAP_PAIR 4 /* BITMAP over a z-pair B operand (mmj_build_operand_pairs): b_rows = pair
                                   rows, 2 bits per accumulator; needs every count < 128 (a side whose
                                   heavy degrees are <= 127); ld_out*16 >= b_rows rounded up to 256 */
-#define MMJ_MODE_BITMAP_TRIPLE 6 /* BITMAP over z-triple operands (mmj_build_operand_triple): K window = 2*kpad
-                                  of the builders' kpad, 3 bits per accumulator, 24 words per 256 B rows;
-                                  needs every count < 128; words at or past ld_out are not written */
 #define MMJ_MODE_COUNT16 5     /* exact counts as uint16 (caller guarantees every count < 65536); ld_out in
                                   uint16 elements, multiple of 8 */
 #define MMJ_MODE_UPPER 16      /* OR-flag: self-join, skip tiles whose columns are all <= their rows
                                   (cells there are left unwritten; consumers keep z > x only) */
-#define MMJ_MODE_COLOC 32      /* OR-flag for MMJ_MODE_BITMAP_PAIR: the co-resident build (<= 85
-                                  registers, 2-stage ring, ~97 KB shared memory) that fits on an SM
-                                  beside two CTAs of mmj_merge_emit */
 
 int mmj_abi_version(void);
 const char* mmj_last_error(void);
@@ -67,6 +61,11 @@ long long mmj_launch_count(void);
 size_t mmj_scan_workspace_bytes(int64_t n);
 /* out[i] = sum(in[0..i)), out[n] = total  (int32 in, int64 out) */
 int mmj_exclusive_scan_i32(const int32_t* in, int64_t* out, int64_t n, void* ws, void* stream);
+/* order-sensitive checksum of n codes (parity stamps of chunked outputs):
+ * out[0] += sum(codes[i]), out[1] += sum((base+i+1) * codes[i]), mod 2^64;
+ * out: 2 x uint64 on the device, accumulated (zero it first); additive over
+ * consecutive chunks when base = the number of codes before the chunk. */
+int mmj_code_checksum(const int64_t* codes, int64_t n, int64_t base, unsigned long long* out, void* stream);
 
 /* ---- degree split: joinproject.py:178-180 ----------------------------------
  * hpos[y] = rank of y among heavy y (deg_R(y) > delta1 or deg_S(y) > delta1),
@@ -86,16 +85,6 @@ int mmj_build_operand(const int32_t* rows, const int32_t* cols, int64_t n, const
 int mmj_build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
                             int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
                             int64_t kpad, void* stream);
-
-/* z-triple form for MMJ_MODE_BITMAP_TRIPLE (both operands have pitch 2*kpad,
- * zeroed first).  side 0 (A): row r = [R_h row | 128 x R_h row].  side 1 (B):
- * z = row0 + 96G + 32w + 8b + k (w < 3, b < 4, k < 8) goes to mat row
- * 32G + 8((4w+b)/3) + k, field (4w+b)%3: weight 1 / 128 in the first K half
- * for fields 0 / 1, weight 128 in the second half for field 2; mat_rows >=
- * ceil(nrows/96)*32. */
-int mmj_build_operand_triple(int side, const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
-                             int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
-                             int64_t mat_rows, int64_t kpad, void* stream);
 
 /* ---- light-z CSR of S for pass 3: joinproject.py:195-203 --------------------
  * lz_ptr[dom_y+1]/lz_idx: S.rev(y) restricted to z with deg_S(z) <= delta2.
@@ -175,17 +164,8 @@ int mmj_merge_emit(const uint32_t* bitmap, int has_heavy, int64_t x0, int64_t ro
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
                    const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
                    const int32_t* lz_idx, const int32_t* split_full, const int32_t* split_lz,
-                   const void* entries, unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws,
-                   size_t ws_bytes, void* stream);
-/* Optional per-(R tuple, column block) list ranges for mmj_merge_emit
- * (entries: n x ncb pairs of int32 (begin | 1<<31 for a light-z list, end),
- * ncb = mmj_merge_emit_col_blocks(wpr)); with them a tile reads one pair per
- * R tuple instead of the tuple -> y -> degrees -> list -> split chain.  The
- * split tables are required when ncb > 1, the light-z lists for a
- * partitioned plan. */
-int mmj_tuple_entries(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t n, const int32_t* rdeg_x,
-                      int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* lz_ptr,
-                      const int32_t* split_full, const int32_t* split_lz, int64_t wpr, void* entries, void* stream);
+                   unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws, size_t ws_bytes,
+                   void* stream);
 /* Column blocks per row of the fused kernel's tiles, and the optional list
  * split table it reads instead of bisecting every long list per tile:
  * split[y*(ncb+1)+j] = position in idx of list y's first entry >= the j-th

@@ -27,9 +27,7 @@ MODE_ACC64 = 2
 MODE_BITMAP_U8 = 3
 MODE_BITMAP_PAIR = 4
 MODE_COUNT16 = 5
-MODE_BITMAP_TRIPLE = 6
 MODE_UPPER = 16
-MODE_COLOC = 32
 
 P = C.c_void_p
 I64 = C.c_int64
@@ -45,6 +43,7 @@ _SIGS = {
     "mmj_launch_count": (C.c_longlong, []),
     "mmj_scan_workspace_bytes": (C.c_size_t, [I64]),
     "mmj_exclusive_scan_i32": (INT, [P, P, I64, P, P]),
+    "mmj_code_checksum": (INT, [P, I64, I64, P, P]),
     "mmj_heavy_y_positions": (INT, [P, P, I64, I64, P, P, P, P, P]),
     "mmj_build_operand": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
     "mmj_ingest_workspace_bytes": (SZ, [I64]),
@@ -64,7 +63,6 @@ _SIGS = {
     "mmj_decode_compact_codes": (INT, [P, I64, I64, P, P, I64, P, P]),
     "mmj_split_codes": (INT, [P, I64, I64, P, P, P]),
     "mmj_build_operand_pairs": (INT, [P, P, I64, P, I64, P, P, I64, I64, I64, P]),
-    "mmj_build_operand_triple": (INT, [INT, P, P, I64, P, I64, P, P, I64, I64, I64, I64, P]),
     "mmj_light_z_csr": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, P]),
     "mmj_light_lengths": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, I64, INT, P, P, P, P]),
     "mmj_light_expand": (INT, [P, P, I64, I64, P, I64, P, P, P, P, P, I64, INT, P, I64, INT, I64, P, I64, P]),
@@ -74,8 +72,7 @@ _SIGS = {
     "mmj_tile_merge": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P]),
     "mmj_emit_codes": (INT, [P, P, I64, I64, I64, I64, P, P]),
     "mmj_merge_emit_workspace_size": (SZ, [I64, I64]),
-    "mmj_merge_emit": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
-    "mmj_tuple_entries": (INT, [P, P, I64, P, I64, P, P, P, P, P, I64, P, P]),
+    "mmj_merge_emit": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "mmj_merge_emit_col_blocks": (INT, [I64]),
     "mmj_debug_timing_buffer": (None, [P]),
     "mmj_list_splits": (INT, [P, P, I64, I64, P, P]),

@@ -46,18 +46,29 @@ class BsiSide:
     h2d_bytes: int = 0
 
 
+def _int_values(vals):
+    """int64 array of a dictionary's raw values when every value is an
+    integer (an integer ndarray, or Python / numpy ints that are not bools),
+    else None: floats, numeric strings and bools must keep Python equality
+    semantics (1.5 != 1, '5' != 5), so they never go through an int cast."""
+    if isinstance(vals, np.ndarray):
+        if vals.dtype.kind in "iu":
+            return vals.astype(np.int64)
+        if vals.dtype.kind != "O":
+            return None
+    try:
+        if not all(isinstance(v, (int, np.integer)) and not isinstance(v, (bool, np.bool_)) for v in vals):
+            return None
+        return np.asarray(vals, dtype=np.int64)
+    except (OverflowError, TypeError, ValueError):
+        return None
+
+
 def _left_lookup_arrays(rel):
     """(sorted raw values, order) for int-valued dictionaries, else None."""
-    lv = rel.left_values
-    if isinstance(lv, np.ndarray) and lv.dtype.kind in "iu":
-        vals = lv.astype(np.int64)
-    else:
-        try:
-            if not all(isinstance(v, (int, np.integer)) and not isinstance(v, bool) for v in lv):
-                return None
-            vals = np.asarray(lv, dtype=np.int64)
-        except (OverflowError, TypeError, ValueError):
-            return None
+    vals = _int_values(rel.left_values)
+    if vals is None:
+        return None
     order = np.argsort(vals, kind="stable")
     return vals[order], order.astype(np.int32)
 
@@ -139,12 +150,13 @@ def prepare(r, s, pinned=False):
         sides = (_side(r, None, dom_y, pinned), _side(s, None, dom_y, pinned), dom_y)
     else:
         rv, sv = r.rel.right_values, s.rel.right_values
-        try:
-            ra = np.asarray(rv, dtype=np.int64)
-            sa = np.asarray(sv, dtype=np.int64)
+        ra, sa = _int_values(rv), _int_values(sv)
+        if ra is not None and sa is not None:
             allv = np.union1d(ra, sa)
             rmap, smap = np.searchsorted(allv, ra), np.searchsorted(allv, sa)
-        except (TypeError, ValueError, OverflowError):
+        else:
+            # any other values: one dictionary under Python equality, as the
+            # reference's raw-value comparison (apps.py:332-350)
             allv = {}
             for v in list(rv) + list(sv):
                 allv.setdefault(v, len(allv))
@@ -287,14 +299,15 @@ def answer_batch(r, s, batch_a, batch_b, heavy_bits: int = 256) -> np.ndarray:
     eng.build()
 
     def to_dev(rel, side, q):
-        try:
-            arr = np.asarray(q, dtype=np.int64)
-            if side.sorted_vals is not None:
+        # raw ids go to the device only when the side's dictionary is
+        # integer-valued AND every query id is an integer; anything else (5.5,
+        # '5', True) is resolved by the dictionary itself, so an id the
+        # relation does not hold answers None (apps.py:321-329)
+        if side.sorted_vals is not None:
+            arr = _int_values(q)
+            if arr is not None:
                 return torch.from_numpy(arr).to("cuda"), False
-            dense = _dense_queries(rel, q)
-        except (TypeError, ValueError, OverflowError):
-            dense = _dense_queries(rel, q)
-        return torch.from_numpy(dense).to("cuda"), True
+        return torch.from_numpy(_dense_queries(rel, q)).to("cuda"), True
 
     da, dense_a = to_dev(r.rel, sR, qa)
     db, dense_b = to_dev(s.rel, sS, qb)

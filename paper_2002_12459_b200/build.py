@@ -40,8 +40,18 @@ def sources():
     return sorted(CSRC.glob("*.cu"))
 
 
+STAMP = LIB.with_suffix(".flags")
+
+
+def _flag_line() -> str:
+    return " ".join(ARCH + FLAGS)
+
+
 def _stale() -> bool:
-    if not LIB.exists():
+    """Rebuild when a source / header is newer than the library, or when the
+    nvcc flags differ from the ones it was built with (an experiment build
+    with MMJ_NVCC_EXTRA=-D... must never be picked up silently)."""
+    if not LIB.exists() or not STAMP.exists() or STAMP.read_text() != _flag_line():
         return True
     t = LIB.stat().st_mtime
     deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
@@ -74,6 +84,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
     os.replace(tmp, LIB)
+    STAMP.write_text(_flag_line())
     return LIB
 
 

@@ -8,8 +8,6 @@ int heavy_y_positions(const int32_t*, const int32_t*, int64_t, int64_t, uint8_t*
                       cudaStream_t);
 int build_operand(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint8_t*, int64_t,
                   int64_t, int64_t, cudaStream_t);
-int build_operand_triple(int, const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*,
-                         uint8_t*, int64_t, int64_t, int64_t, int64_t, cudaStream_t);
 int build_operand_pairs(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint8_t*,
                         int64_t, int64_t, int64_t, cudaStream_t);
 int light_z_csr(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, uint8_t*, int32_t*,
@@ -36,10 +34,8 @@ int emit_codes(const uint32_t*, const int64_t*, int64_t, int64_t, int64_t, int64
 size_t merge_emit_ws_bytes(int64_t, int64_t);
 int merge_emit(const uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t*, const int32_t*, const int32_t*,
                int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*,
-               const int32_t*, const int32_t*, const void*, unsigned long long*, int64_t*, int64_t*, void*, size_t,
+               const int32_t*, const int32_t*, unsigned long long*, int64_t*, int64_t*, void*, size_t,
                cudaStream_t);
-int tuple_entries(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, const int32_t*,
-                  const int32_t*, const int32_t*, const int32_t*, int64_t, void*, cudaStream_t);
 int merge_emit_col_blocks(int64_t);
 extern unsigned long long* tdbg_buffer;
 int list_splits(const int32_t*, const int32_t*, int64_t, int64_t, int32_t*, cudaStream_t);
@@ -100,6 +96,10 @@ int mmj_exclusive_scan_i32(const int32_t* in, int64_t* out, int64_t n, void* ws,
   return mmj::scan_i32_i64(in, out, n, ws, ST(stream));
 }
 
+int mmj_code_checksum(const int64_t* codes, int64_t n, int64_t base, unsigned long long* out, void* stream) {
+  return mmj::code_checksum(codes, n, base, out, ST(stream));
+}
+
 int mmj_heavy_y_positions(const int32_t* rdeg_y, const int32_t* sdeg_y, int64_t dom_y, int64_t delta1,
                           uint8_t* flag_ws, int32_t* scan_out, int32_t* hpos, void* ws, void* stream) {
   if (delta1 < 1) {
@@ -118,13 +118,6 @@ int mmj_build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n,
                             int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
                             int64_t kpad, void* stream) {
   return mmj::build_operand_pairs(rows, cols, n, left_deg, delta2, hpos, mat, row0, nrows, kpad, ST(stream));
-}
-
-int mmj_build_operand_triple(int side, const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
-                             int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
-                             int64_t mat_rows, int64_t kpad, void* stream) {
-  return mmj::build_operand_triple(side, rows, cols, n, left_deg, delta2, hpos, mat, row0, nrows, mat_rows, kpad,
-                                   ST(stream));
 }
 
 int mmj_light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, int64_t dom_y,
@@ -158,11 +151,10 @@ int mmj_light_expand(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t t0,
 int mmj_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t b_rows, int64_t kpad, int64_t k_off,
                   int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out, int64_t ld_out,
                   unsigned long long* nnz, int max_ctas, void* stream) {
-  const int base_mode = mode & ~(MMJ_MODE_UPPER | MMJ_MODE_COLOC);
-  const int upper = mode & MMJ_MODE_UPPER, coloc = mode & MMJ_MODE_COLOC;
-  if (base_mode < 0 || base_mode > MMJ_MODE_BITMAP_TRIPLE ||
-      (upper && base_mode != MMJ_MODE_COUNT32 && base_mode != MMJ_MODE_COUNT16) ||
-      (coloc && base_mode != MMJ_MODE_BITMAP_PAIR)) {
+  const int base_mode = mode & ~MMJ_MODE_UPPER;
+  const int upper = mode & MMJ_MODE_UPPER;
+  if (base_mode < 0 || base_mode > MMJ_MODE_COUNT16 ||
+      (upper && base_mode != MMJ_MODE_COUNT32 && base_mode != MMJ_MODE_COUNT16)) {
     mmj::set_error("heavy_mma: unknown mode %d (MMJ_MODE_UPPER combines with the count modes only)", mode);
     return MMJ_ERR_ARG;
   }
@@ -201,18 +193,11 @@ int mmj_merge_emit(const uint32_t* bitmap, int has_heavy, int64_t x0, int64_t ro
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
                    const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
                    const int32_t* lz_idx, const int32_t* split_full, const int32_t* split_lz,
-                   const void* entries, unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws,
-                   size_t ws_bytes, void* stream) {
+                   unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws, size_t ws_bytes,
+                   void* stream) {
   return mmj::merge_emit(bitmap, has_heavy, x0, rows, wpr, dom_z, fwd_ptr, fwd_idx, rdeg_x, delta2, hpos, s_rev_ptr,
-                         s_rev_idx, lz_ptr, lz_idx, split_full, split_lz, entries, witnesses, codes, total, ws,
+                         s_rev_idx, lz_ptr, lz_idx, split_full, split_lz, witnesses, codes, total, ws,
                          ws_bytes, ST(stream));
-}
-
-int mmj_tuple_entries(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t n, const int32_t* rdeg_x,
-                      int64_t delta2, const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* lz_ptr,
-                      const int32_t* split_full, const int32_t* split_lz, int64_t wpr, void* entries, void* stream) {
-  return mmj::tuple_entries(fwd_row, fwd_idx, n, rdeg_x, delta2, hpos, s_rev_ptr, lz_ptr, split_full, split_lz, wpr,
-                            entries, ST(stream));
 }
 
 int mmj_merge_emit_col_blocks(int64_t wpr) { return mmj::merge_emit_col_blocks(wpr); }

@@ -20,11 +20,9 @@
 //                the generic multiply_counts backend);
 //       BITMAP_PAIR: B rows are z pairs weighted (1, 128) (mmj_build_operand_pairs),
 //                one accumulator = two cells: half the MMAs and half the TMEM
-//                read-out per output bit, 64 B per row/tile;
-//       BITMAP_TRIPLE: A = [R_h | 128 R_h] (K doubled), B rows hold three z
-//                weighted (1, 128 | 128): one accumulator = c0 + 128 c1 +
-//                16384 c2, three cells per TMEM word (the read-out bound),
-//                96 B per row/tile.
+//                read-out per output bit, 64 B per row/tile (a z-triple
+//                form, three 7-bit fields per accumulator, measured slower:
+//                35.1 vs 26.5 ms on cfg2, its packing is ALU-bound).
 //
 // Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
 // w3 idle, w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4) .. +31 and the
@@ -72,8 +70,7 @@ constexpr int SMEM_MAX = smem_bytes_for(3, true) > smem_bytes_for(STAGES, false)
 static_assert(SMEM_MAX <= 227 * 1024, "shared memory budget");
 constexpr int GROUP_M = 16;             // raster: sweep N for a band of 16 M blocks
 
-enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, BITMAP_PAIR = 4, COUNT16 = 5, BITMAP_TRIPLE = 6,
-                  MODE_UPPER = 16, MODE_COLOC = 32 };
+enum Mode : int { BITMAP = 0, COUNT32 = 1, ACC64 = 2, BITMAP_U8 = 3, BITMAP_PAIR = 4, COUNT16 = 5, MODE_UPPER = 16 };
 
 struct Params {
   int64_t m_begin;      // first A row of this launch (multiple of BM not required)
@@ -83,8 +80,7 @@ struct Params {
   int64_t n_cols;       // columns of the product (= rows of B)
   int num_kb;           // Kp / BK
   int stages;           // smem ring depth (2..STAGES)
-  int debug;            // 1: epilogue skips the bit packing (profiling experiment)
-  int alt;              // BITMAP_PAIR / BITMAP_TRIPLE: alternating epilogue warp groups (env MMJ_EPI_ALT)
+  int alt;              // BITMAP_PAIR: alternating epilogue warp groups
   int small_counts;     // BITMAP: every product entry < 256 (K window <= 255 nonzero columns)
   int mode;
   int shift;            // ACC64 only
@@ -260,32 +256,6 @@ __device__ __forceinline__ uint32_t pack_bits_pair(const uint32_t* r) {
   return w;   // register k's flags now sit at bits k, 8+k, 16+k, 24+k
 }
 
-// BITMAP_TRIPLE: a = c0 + 128 c1 + 16384 c2 with every c < 128.  a + (c1 << 7)
-// + 3 (c2 << 14) moves the fields to bytes 0, 1, 2; + 0x7F per byte sets each
-// byte's MSB iff its field is nonzero (no carry leaves a byte).
-__device__ __forceinline__ uint32_t triple_flags(uint32_t a) {
-  const uint32_t t1 = a & 0x3F80u, t2 = a & 0x1FC000u;
-  return (a + t1 + 0x7F7F7Fu + 3u * t2) & 0x808080u;
-}
-
-// 32 accumulators -> 3 bitmap words.  Accumulator 8q + k (q < 4, k < 8)
-// lands at bit k of bytes 0..2 of chain c[q] (fields 0..2); the 12 chain
-// bytes c0.b0 c0.b1 c0.b2 c1.b0 ... c3.b2 are the 3 words' 12 bytes in order.
-// The operand builder (mmj_build_operand_triples) places z accordingly.
-__device__ __forceinline__ void pack_bits_triple(const uint32_t* r, uint32_t* w) {
-  uint32_t c[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t v = triple_flags(r[8 * q]);
-#pragma unroll
-    for (int k = 1; k < 8; ++k) v = (v >> 1) | triple_flags(r[8 * q + k]);
-    c[q] = v;
-  }
-  w[0] = __byte_perm(c[0], c[1], 0x4210);
-  w[1] = __byte_perm(c[1], c[2], 0x5421);
-  w[2] = __byte_perm(c[2], c[3], 0x6542);
-}
-
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -328,12 +298,7 @@ __device__ __forceinline__ bool below_diagonal(const Params& p, TileCoord c) {
 }
 
 // ----------------------------------------------------------------- the kernel
-// MINB = 2: the co-resident build (<= 85 registers, used with a 2-stage ring,
-// ~97 KB of shared memory) that leaves room on every SM for two CTAs of the
-// fused projection tail, so a chunk's heavy product (TMEM-read-bound) runs
-// beside the previous chunk's emission (HBM-write-bound).
-template <int MINB>
-__global__ void __launch_bounds__(NUM_THREADS, MINB)
+__global__ void __launch_bounds__(NUM_THREADS, 1)
     heavy_mma_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -431,7 +396,7 @@ __global__ void __launch_bounds__(NUM_THREADS, MINB)
         if (++acc == ACC_STAGES) { acc = 0; acc_ph ^= 1; }
       }
     }
-  } else if (warp >= 4 && (MINB == 2 || p.alt)) {
+  } else if (warp >= 4 && p.alt) {
     // ------------------------------------------------------- epilogue, alternating groups
     // Warps 4-7 (group 0) take the CTA's even tiles (accumulator stage 0),
     // warps 8-11 (group 1) the odd ones (stage 1), each warp all 256 columns
@@ -454,41 +419,10 @@ __global__ void __launch_bounds__(NUM_THREADS, MINB)
       const int64_t row = (int64_t)c.m_blk * BM + q * 32 + lane;
       const bool row_ok = row < p.m_rows;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (MINB == 1 && p.mode == BITMAP_TRIPLE) {
-        constexpr int NWT = 3 * BN / 32;   // 24 words
-        uint32_t w[NWT];
-        // two 32-column loads in flight per wait (the TMEM load latency,
-        // not its bandwidth, bounds a warp that waits on every 32 columns)
-#pragma unroll
-        for (int j = 0; j < BN / 64; ++j) {
-          uint32_t r[64];
-          uint32_t* r1 = r + 32;
-          TMEM_LD_32x32b_X32(taddr + 64 * j, r);
-          TMEM_LD_32x32b_X32(taddr + 64 * j + 32, r1);
-          tmem_wait_ld();
-          if (j == BN / 64 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
-          pack_bits_triple(r, w + 6 * j);
-          pack_bits_triple(r1, w + 6 * j + 3);
-        }
-        if (row_ok) {
-          const int64_t wbase = (int64_t)c.n_blk * NWT;
-          uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + wbase;
-#pragma unroll
-          for (int k = 0; k < NWT; k += 4) {
-            if (wbase + k + 4 <= p.ld_out) {
-              *reinterpret_cast<uint4*>(dst + k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
-              my_nnz += __popc(w[k]) + __popc(w[k + 1]) + __popc(w[k + 2]) + __popc(w[k + 3]);
-            }
-          }
-        }
-      } else {   // BITMAP_PAIR
+      {   // BITMAP_PAIR
         constexpr int NW = BN / 16;        // 16 words
         uint32_t w[NW];
-        if (MINB == 1) {
+        {
 #pragma unroll
           for (int j = 0; j < BN / 128; ++j) {
             uint32_t r[64];
@@ -503,20 +437,6 @@ __global__ void __launch_bounds__(NUM_THREADS, MINB)
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) w[8 * j + k] = pack_bits_pair(r + 8 * k);
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < BN / 64; ++j) {
-            uint32_t r[32];
-            TMEM_LD_32x32b_X32_PACK16(taddr + 64 * j, r);
-            tmem_wait_ld();
-            if (j == BN / 64 - 1) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&tempty[acc]);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) w[4 * j + k] = pack_bits_pair(r + 8 * k);
           }
         }
         if (row_ok) {
@@ -535,7 +455,7 @@ __global__ void __launch_bounds__(NUM_THREADS, MINB)
       for (int o = 16; o > 0; o >>= 1) my_nnz += __shfl_xor_sync(0xffffffffu, my_nnz, o);
       if (lane == 0 && my_nnz) atomicAdd(p.nnz, my_nnz);
     }
-  } else if (MINB == 1 && warp >= 4) {
+  } else if (warp >= 4) {
     // ------------------------------------------------------- epilogue
     const int q = warp & 3;              // TMEM lane quadrant
     const int grp = (warp - 4) >> 2;     // CW-column group of the 256-column tile
@@ -573,8 +493,7 @@ __global__ void __launch_bounds__(NUM_THREADS, MINB)
         } else {
 #pragma unroll
           for (int k = 0; k < NW / 2; ++k) {
-            if (p.debug) w[k] = r[16 * k] | r[16 * k + 7];
-            else if (p.small_counts) w[k] = pack_bits_u8(r + 16 * k);    // counts < 256: PRMT + SWAR
+            if (p.small_counts) w[k] = pack_bits_u8(r + 16 * k);    // counts < 256: PRMT + SWAR
             else w[k] = pack_bits_u16(r + 16 * k);
           }
 #pragma unroll
@@ -596,39 +515,6 @@ __global__ void __launch_bounds__(NUM_THREADS, MINB)
           }
 #pragma unroll
           for (int k = 0; k < NW; ++k) my_nnz += __popc(w[k]);
-        }
-      } else if (p.mode == BITMAP_TRIPLE) {
-        // CW accumulators = 3*CW z -> 3*CW/32 words, 32-column chunks
-        constexpr int NWT = 3 * CW / 32;
-        constexpr int NC = CW / 32;
-        uint32_t w[NWT];
-        uint32_t ra[32], rb[32];
-        TMEM_LD_32x32b_X32(taddr, ra);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < NC; ++j) {
-          uint32_t* cur = (j & 1) ? rb : ra;
-          uint32_t* nxt = (j & 1) ? ra : rb;
-          if (j + 1 < NC) {
-            TMEM_LD_32x32b_X32(taddr + 32 * (j + 1), nxt);
-          } else {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
-          pack_bits_triple(cur, w + 3 * j);
-          if (j + 1 < NC) tmem_wait_ld();
-        }
-        if (row_ok) {
-          const int64_t wbase = (int64_t)c.n_blk * (3 * BN / 32) + grp * NWT;
-          uint32_t* dst = reinterpret_cast<uint32_t*>(p.out) + row * p.ld_out + wbase;
-#pragma unroll
-          for (int k = 0; k < NWT; k += 4) {
-            if (wbase + k + 4 <= p.ld_out) {   // the last tile of a row may pass its end
-              *reinterpret_cast<uint4*>(dst + k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
-              my_nnz += __popc(w[k]) + __popc(w[k + 1]) + __popc(w[k + 2]) + __popc(w[k + 3]);
-            }
-          }
         }
       } else if (p.mode == COUNT16) {
         // counts < 2^16 (caller's guarantee): pack::16b registers hold two
@@ -776,12 +662,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
                      int64_t k_off, int64_t k_len, int64_t m_begin, int64_t m_rows, int mode, int shift, void* out,
                      int64_t ld_out, unsigned long long* nnz, int max_ctas, cudaStream_t st) {
   const int upper = (mode & MODE_UPPER) ? 1 : 0;
-  const bool coloc = (mode & MODE_COLOC) != 0;
-  mode &= ~(MODE_UPPER | MODE_COLOC);
-  if (coloc && mode != BITMAP_PAIR) {
-    set_error("heavy_mma: MMJ_MODE_COLOC is built for MMJ_MODE_BITMAP_PAIR only");
-    return MMJ_ERR_ARG;
-  }
+  mode &= ~MODE_UPPER;
   if (kpad <= 0 || kpad % BK != 0 || k_off < 0 || k_len <= 0 || k_off % BK != 0 || k_len % BK != 0 ||
       k_off + k_len > kpad) {
     set_error("heavy_mma: K window [%lld,+%lld) of pitch %lld must be multiples of %d", (long long)k_off,
@@ -805,11 +686,6 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
     set_error("heavy_mma: pair-bitmap pitch %lld words too small / unaligned", (long long)ld_out);
     return MMJ_ERR_ARG;
   }
-  if (mode == BITMAP_TRIPLE && (ld_out % 4 != 0 || ceil_div(b_rows, BN) * (3 * BN / 32) < ld_out)) {
-    set_error("heavy_mma: triple-bitmap pitch %lld words unaligned or not covered by %lld B rows", (long long)ld_out,
-              (long long)b_rows);
-    return MMJ_ERR_ARG;
-  }
   if (mode == COUNT32 && ld_out % 4 != 0) {
     set_error("heavy_mma: count pitch must be a multiple of 4");
     return MMJ_ERR_ARG;
@@ -818,7 +694,7 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
     set_error("heavy_mma: uint16 count pitch must be a multiple of 8");
     return MMJ_ERR_ARG;
   }
-  if (mode < 0 || mode > BITMAP_TRIPLE) {
+  if (mode < 0 || mode > COUNT16) {
     set_error("heavy_mma: unknown mode %d", mode);
     return MMJ_ERR_ARG;
   }
@@ -838,64 +714,25 @@ int launch_heavy_mma(const uint8_t* a, int64_t a_rows, const uint8_t* b, int64_t
   p.n_cols = b_rows;
   p.num_kb = (int)(k_len / BK);
   p.stages = p.num_kb <= 2 ? 2 : STAGES;
-  {
-    static int st_env = -1;
-    if (st_env < 0) {
-      const char* e = getenv("MMJ_MMA_STAGES");
-      st_env = e ? atoi(e) : 0;
-    }
-    if (st_env >= 2 && st_env <= STAGES) p.stages = st_env;
-  }
   const bool staged = (mode == COUNT32 || mode == COUNT16);
   if (staged && p.stages > 3) p.stages = 3;   // room for the epilogue staging buffers
   p.small_counts = (mode == BITMAP_U8 || k_len <= 255) ? 1 : 0;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("MMJ_DEBUG_EPI");
-      dbg = (e && e[0] == '1') ? 1 : 0;
-    }
-    p.debug = dbg;
-    static int alt = -1;
-    if (alt < 0) {
-      const char* e = getenv("MMJ_EPI_ALT");
-      alt = (e && e[0] == '0') ? 0 : 1;
-    }
-    p.alt = (alt && (mode == BITMAP_PAIR || mode == BITMAP_TRIPLE)) ? 1 : 0;
-    static int bo = -1;
-    if (bo < 0) {
-      const char* e = getenv("MMJ_BACKOFF");
-      bo = (e && e[0] == '0') ? 0 : 1;
-    }
-    p.backoff = bo;
-  }
+  // alternating epilogue groups for the z-pair bitmap (one group packs while
+  // the other drains TMEM); the single-thread producer / issuer back off
+  // between barrier polls so they do not take issue slots from the epilogue
+  p.alt = mode == BITMAP_PAIR ? 1 : 0;
+  p.backoff = 1;
   p.mode = mode == BITMAP_U8 ? BITMAP : mode;
   p.shift = shift;
   p.out = out;
   p.ld_out = ld_out;
   p.nnz = nnz;
-  static bool attr_set = false;
-  if (!attr_set) {
-    MMJ_TRY(cuda_status(cudaFuncSetAttribute(heavy_mma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             SMEM_MAX),
-                        "cudaFuncSetAttribute(heavy_mma)"));
-    MMJ_TRY(cuda_status(cudaFuncSetAttribute(heavy_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem_bytes_for(2, false)),
-                        "cudaFuncSetAttribute(heavy_mma coloc)"));
-    attr_set = true;
-  }
-  if (coloc) {
-    p.stages = 2;
-    p.alt = 1;
-  }
+  MMJ_TRY(set_max_dynamic_smem((const void*)heavy_mma_kernel, SMEM_MAX, "heavy_mma_kernel"));
   const int64_t tiles = ceil_div(m_rows, BM) * ceil_div(b_rows, BN);
   int grid = sm_count();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   if (tiles < grid) grid = (int)tiles;
-  if (coloc)
-    heavy_mma_kernel<2><<<grid, NUM_THREADS, smem_bytes_for(p.stages, staged), st>>>(ma, mb, p);
-  else
-    heavy_mma_kernel<1><<<grid, NUM_THREADS, smem_bytes_for(p.stages, staged), st>>>(ma, mb, p);
+  heavy_mma_kernel<<<grid, NUM_THREADS, smem_bytes_for(p.stages, staged), st>>>(ma, mb, p);
   MMJ_CHECK_LAUNCH("heavy_mma_kernel");
   return MMJ_OK;
 }

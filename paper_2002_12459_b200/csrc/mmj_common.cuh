@@ -49,6 +49,11 @@ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 int sm_count();
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the CURRENT
+// device, set once per (device, function): the attribute is per device, so
+// a process driving several GPUs must set it on each (scan.cu).
+int set_max_dynamic_smem(const void* func, int bytes, const char* where);
+
 // ---- exclusive scans (scan.cu) --------------------------------------------
 // out[i] = sum(in[0..i)), out[n] = total.  `ws` must hold scan_ws_bytes(n).
 size_t scan_ws_bytes(int64_t n);
@@ -56,6 +61,7 @@ int scan_i32_i64(const int32_t* in, int64_t* out, int64_t n, void* ws, cudaStrea
 int scan_u8_i32(const uint8_t* in, int32_t* out, int64_t n, void* ws, cudaStream_t st);
 int scan_i64_i64(const int64_t* in, int64_t* out, int64_t n, void* ws, cudaStream_t st);
 int scan_i32_i32(const int32_t* in, int32_t* out, int64_t n, void* ws, cudaStream_t st);
+int code_checksum(const int64_t* codes, int64_t n, int64_t base, unsigned long long* out, cudaStream_t st);
 
 }  // namespace mmj
 

@@ -17,7 +17,7 @@
 //                 materialised keys), the merged tile is written back and the
 //                 popcount of every 32-word segment is recorded;
 //   (exclusive scan of the segment counts, scan.cu)
-//   k_emit(_pf)   one warp per segment (the CTA's 32 segments of bitmap words and
+//   k_emit_pf16   one warp per segment (the CTA's 32 segments of bitmap words and
 //                 offsets prefetched into shared memory first): prefix of the 32 word popcounts, the
 //                 lane's set bits staged as 32-bit cell offsets in a swizzled
 //                 shared buffer, then coalesced 16-byte streaming stores of
@@ -44,7 +44,7 @@ constexpr int SHORT_LIST = 96;          // lists up to this length are filtered,
 // per SM (40 / 32 registers) measured 1-4% slower than ptxas's 48 registers)
 constexpr int MERGE_ILP = 8;            // witness slots per thread per step of the merge
 constexpr int EM_WARPS = 8;
-constexpr int EM_SEGS = 64;             // segments per emission CTA (8 per warp: balances uneven row densities)
+constexpr int EM_SEGS = 32;             // segments per emission CTA (4 per warp)
 
 __device__ __forceinline__ void st_cs2(int64_t* p, int64_t a, int64_t b) {
   asm volatile("st.global.cs.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
@@ -119,8 +119,6 @@ struct TileArgs {
   // boundaries (full S.rev lists / light-z lists): replaces per-tile bisection
   const int32_t* split_full = nullptr;
   const int32_t* split_lz = nullptr;
-  // optional per-(R tuple, column block) list ranges (mmj_tuple_entries)
-  const int2* ent = nullptr;
 };
 
 // Light witnesses of one tile OR-ed into its shared-memory bitmap (rows
@@ -140,24 +138,7 @@ __device__ __forceinline__ unsigned long long merge_light(
     const int64_t t = tb + tid;
     int len = 0, row = 0, filt = 0;
     const int32_t* base = nullptr;
-    if (t < t_end && a.ent != nullptr) {
-      // precomputed (list begin | lz flag, list end) of tuple t in this column
-      // block (mmj_tuple_entries): one load instead of the dependent chain
-      // tuple -> y -> degrees / list pointers -> split table
-      const int2 en = a.ent[t * a.ncb + cbi];
-      if (a.G > 1) {
-        int64_t lo = xa, hi = xb;
-        while (hi - lo > 1) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (a.fwd_ptr[mid] <= t) lo = mid;
-          else hi = mid;
-        }
-        row = (int)(lo - xa);
-      }
-      const int32_t b = en.x & 0x7FFFFFFF;
-      base = ((en.x < 0) ? a.lz_idx : a.s_rev_idx) + b;
-      len = en.y - b;
-    } else if (t < t_end) {
+    if (t < t_end) {
       int64_t lo = xa, hi = xb;   // row of tuple t: last x with fwd_ptr[x] <= t
       while (hi - lo > 1) {
         const int64_t mid = (lo + hi) >> 1;
@@ -320,122 +301,14 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
 }
 
 // --------------------------------------------------------------- emission
-template <int SEGS>
-__global__ void __launch_bounds__(EM_WARPS * 32) k_emit(const uint32_t* __restrict__ bm, const int64_t* __restrict__ segoff,
-                                                        int64_t nseg, int64_t segs_per_row, int64_t x0, int64_t dom_z,
-                                                        int64_t* __restrict__ codes) {
-  __shared__ __align__(16) uint32_t stage_all[EM_WARPS][1024];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* stage = stage_all[warp];
-  // staging slot of the k-th code: lanes' runs start at unrelated offsets, so
-  // XOR-ing the bank bits with the 32-slot row index spreads their stores
-  auto sl = [](int k) { return k ^ ((k >> 5) & 31); };
-  const int64_t s0 = (int64_t)blockIdx.x * SEGS;
-  for (int si = warp; si < SEGS; si += EM_WARPS) {
-    const int64_t s = s0 + si;
-    if (s >= nseg) break;
-    uint32_t word = bm[s * 32 + lane];
-    const int c = __popc(word);
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int tot = __shfl_sync(0xffffffffu, incl, 31);
-    const int64_t row = s / segs_per_row;
-    const int64_t base = (x0 + row) * dom_z + (s - row * segs_per_row) * 1024;   // code of the segment's cell 0
-    const uint32_t off0 = lane * 32;
-    int k = incl - c;
-    while (word) {
-      const int b = __ffs(word) - 1;
-      stage[sl(k)] = off0 + b;
-      ++k;
-      word &= word - 1;
-    }
-    __syncwarp();
-    int64_t* out = codes + segoff[s];
-    const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
-    if (lane < h) st_cs(out + lane, base + stage[sl(lane)]);
-    const int np = (tot - h) >> 1;
-    for (int p = lane; p < np; p += 32) {
-      const int i = h + 2 * p;
-      st_cs2(out + i, base + stage[sl(i)], base + stage[sl(i + 1)]);
-    }
-    const int done = h + 2 * np;
-    if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(done + lane)]);
-    __syncwarp();
-  }
-}
-
-
-// Prefetching variant: the CTA's SEGS x 32 bitmap words and SEGS + 1 segment
-// offsets are loaded up front by all threads (8 independent loads each) into
-// shared memory, so no warp waits on a DRAM round trip per segment.
-template <int SEGS>
-__global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf(const uint32_t* __restrict__ bm,
-                                                           const int64_t* __restrict__ segoff, int64_t nseg,
-                                                           int64_t segs_per_row, int64_t x0, int64_t dom_z,
-                                                           int64_t* __restrict__ codes) {
-  __shared__ __align__(16) uint32_t stage_all[EM_WARPS][1024];
-  __shared__ __align__(16) uint32_t sbits[SEGS * 32];
-  __shared__ int64_t soff[SEGS + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* stage = stage_all[warp];
-  auto sl = [](int k) { return k ^ ((k >> 5) & 31); };
-  const int64_t s0 = (int64_t)blockIdx.x * SEGS;
-  const int64_t nhere = min((int64_t)SEGS, nseg - s0);
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(bm + s0 * 32);
-    uint4* dst = reinterpret_cast<uint4*>(sbits);
-    const int nq = (int)(nhere * 8);
-#pragma unroll 2
-    for (int i = threadIdx.x; i < nq; i += EM_WARPS * 32) dst[i] = __ldcs(src + i);
-    for (int i = threadIdx.x; i <= nhere; i += EM_WARPS * 32) soff[i] = segoff[s0 + i];
-  }
-  __syncthreads();
-  for (int si = warp; si < nhere; si += EM_WARPS) {
-    const int64_t s = s0 + si;
-    uint32_t word = sbits[si * 32 + lane];
-    const int c = __popc(word);
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int tot = __shfl_sync(0xffffffffu, incl, 31);
-    const int64_t row = s / segs_per_row;
-    const int64_t base = (x0 + row) * dom_z + (s - row * segs_per_row) * 1024;
-    const uint32_t off0 = lane * 32;
-    int k = incl - c;
-    while (word) {
-      const int b = __ffs(word) - 1;
-      stage[sl(k)] = off0 + b;
-      ++k;
-      word &= word - 1;
-    }
-    __syncwarp();
-    int64_t* out = codes + soff[si];
-    const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
-    if (lane < h) st_cs(out + lane, base + stage[sl(lane)]);
-    const int np = (tot - h) >> 1;
-    for (int p = lane; p < np; p += 32) {
-      const int i = h + 2 * p;
-      st_cs2(out + i, base + stage[sl(i)], base + stage[sl(i + 1)]);
-    }
-    const int done = h + 2 * np;
-    if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(done + lane)]);
-    __syncwarp();
-  }
-}
-
-// Same as k_emit_pf with 16-bit staging (cell offsets < 1024) and a
-// branch-free bit-slice expansion for dense words: half the
-// shared memory per CTA, so 8 CTAs (64 warps) fit per SM instead of 6.  Element
+// Emission of the three-kernel tail: the CTA's SEGS segments (bitmap words
+// and offsets) are prefetched into shared memory, then one warp per segment
+// stages its cells as 16-bit offsets (cell offsets < 1024) -- a branch-free
+// bit slice for dense words, an ffs loop for sparse ones -- and writes the
+// codes with 16-byte streaming stores (8 CTAs, 64 warps, per SM).  Element
 // i is staged at slot i + h (h = the output's 16-B misalignment) so every
 // stored pair is one aligned 32-bit shared load.
-template <int SEGS, bool BITSLICE>
+template <int SEGS>
 __global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf16(const uint32_t* __restrict__ bm,
                                                              const int64_t* __restrict__ segoff, int64_t nseg,
                                                              int64_t segs_per_row, int64_t x0, int64_t dom_z,
@@ -479,7 +352,7 @@ __global__ void __launch_bounds__(EM_WARPS * 32) k_emit_pf16(const uint32_t* __r
     int k = h + (incl - c);
     // dense words (the warp's fullest lane >= 10 bits): the branch-free bit
     // slice; sparse ones: the ffs loop (warp-uniform choice)
-    if (BITSLICE && __reduce_max_sync(0xffffffffu, (unsigned)c) >= 10u) {
+    if (__reduce_max_sync(0xffffffffu, (unsigned)c) >= 10u) {
       // branch-free: 32 predicated 16-bit stores, independent of the density
 #pragma unroll
       for (int b = 0; b < 32; ++b) {
@@ -530,7 +403,6 @@ struct FuseArgs {
   int64_t* total;           // chunk code count (written by the last tile)
   int64_t* codes;
   unsigned long long* tdbg;  // MMJ_DEBUG_TIMING: per-tile phase timestamps (8 per tile)
-  int dbg;                  // debug bisection flags (MMJ_DEBUG_BOUNDS builds)
 };
 
 #ifndef MMJ_LOOKBACK_SLEEP_NS
@@ -570,11 +442,10 @@ struct FuseSmem {
   int next_seg;
   unsigned int tile;
   long long prefix;
-  long long gb[NT / 32];   // CTA emission: code of cell 0 of each segment of a multi-row group
   __align__(8) uint64_t bar;
 };
 
-template <int TW, int NT, int MINB, bool CTA_EMIT>
+template <int TW, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
   constexpr int NWARP = NT / 32;
   constexpr int MAXSEG = TW / 32;
@@ -708,110 +579,6 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
 #ifdef MMJ_DEBUG_TIMING
   if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 4] = gtimer();
 #endif
-  if (CTA_EMIT) {
-    // CTA-cooperative emission: the NWARP segments of a group are expanded
-    // (one warp each) into ONE contiguous 16-bit staging run, then all NT
-    // threads write the group's codes -- a contiguous ~32 KB range of the
-    // output at half density -- with 32-byte stores.  Block-contiguous 32-B
-    // stores measured 7.6 TB/s on the box vs 5.5-6.4 TB/s for per-warp
-    // 16-B runs (tools/emit_lab.cu "blk 32KB" vs "V0").
-    // staged value v = (segment - g0) * 1024 + cell; slot swizzle XORs bits
-    // 2-5 with bits 6-9 (quads stay contiguous for the 8-byte reads, the
-    // lanes' runs spread over the banks during the expansion)
-    uint16_t* gst = &sm.u.stage[0][0];
-#ifdef MMJ_CTA_QUADS
-    constexpr bool QUAD = true;    // 32-B stores; swizzle keeps quads contiguous
-    auto sw = [](int k) { return k ^ (((k >> 6) & 15) << 2); };
-#else
-    constexpr bool QUAD = false;   // 16-B stores; k_emit_pf16's pair-preserving swizzle
-    auto sw = [](int k) { return k ^ (((k >> 5) & 31) << 1); };
-#endif
-    const int segs_per_piece = cw >> 5;
-    int64_t* const codes = f.codes + sm.prefix;
-    for (int g0 = 0; g0 < nseg; g0 += NWARP) {
-      const int ng = min(NWARP, nseg - g0);
-      const int goff = s_segoff[g0];
-      const int gend = (g0 + ng < nseg) ? s_segoff[g0 + ng] : agg;
-      const int total = gend - goff;
-      int64_t* const gout = codes + goff;
-      const int mis = (int)((reinterpret_cast<uintptr_t>(gout) >> 3) & (QUAD ? 3 : 1));
-      const int rr0 = g0 / segs_per_piece;
-      const bool one_row = rr0 == (g0 + ng - 1) / segs_per_piece;
-      const int si = g0 + warp;
-      if (si < nseg && total > 0) {
-        uint32_t word = sbm[si * 32 + lane];
-        const int c = __popc(word);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int vv = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += vv;
-        }
-        int k = mis + (s_segoff[si] - goff) + (incl - c);
-        const uint32_t off0 = (uint32_t)(warp * 1024 + lane * 32);
-        if (!one_row && lane == 0) {
-          const int rr = si / segs_per_piece;
-          sm.gb[warp] = (a.x0 + r0 + rr) * a.dom_z + (c0w + (int64_t)(si - rr * segs_per_piece) * 32) * 32;
-        }
-        if (__reduce_max_sync(0xffffffffu, (unsigned)c) >= 10u) {
-#pragma unroll
-          for (int b = 0; b < 32; ++b) {
-            if (word & (1u << b)) {
-              gst[sw(k)] = (uint16_t)(off0 + b);
-              ++k;
-            }
-          }
-        } else {
-          while (word) {
-            const int b = __ffs(word) - 1;
-            gst[sw(k)] = (uint16_t)(off0 + b);
-            ++k;
-            word &= word - 1;
-          }
-        }
-      }
-      __syncthreads();
-      if (total > 0) {
-        const int64_t gbase =
-            one_row ? (a.x0 + r0 + rr0) * a.dom_z + (c0w + (int64_t)(g0 - rr0 * segs_per_piece) * 32) * 32 : 0;
-        auto code_of = [&](uint32_t v) -> int64_t {
-          return one_row ? gbase + (int64_t)v : sm.gb[v >> 10] + (int64_t)(v & 1023u);
-        };
-        int64_t* const oa = gout - mis;   // 32-byte (quads) / 16-byte (pairs) aligned
-        if (QUAD) {
-          const int nq = (mis + total + 3) >> 2;
-          for (int q = tid; q < nq; q += NT) {
-            const uint2 raw = *reinterpret_cast<const uint2*>(gst + sw(4 * q));
-            const int64_t c0 = code_of(raw.x & 0xFFFFu), c1 = code_of(raw.x >> 16);
-            const int64_t c2 = code_of(raw.y & 0xFFFFu), c3 = code_of(raw.y >> 16);
-            const int e0 = 4 * q;
-            if (e0 >= mis && e0 + 4 <= mis + total) {
-              st_v4(oa + e0, c0, c1, c2, c3);
-            } else {
-              if (e0 >= mis && e0 < mis + total) oa[e0] = c0;
-              if (e0 + 1 >= mis && e0 + 1 < mis + total) oa[e0 + 1] = c1;
-              if (e0 + 2 >= mis && e0 + 2 < mis + total) oa[e0 + 2] = c2;
-              if (e0 + 3 >= mis && e0 + 3 < mis + total) oa[e0 + 3] = c3;
-            }
-          }
-        } else {
-          const int np = (mis + total + 1) >> 1;
-          for (int p = tid; p < np; p += NT) {
-            const uint32_t two = *reinterpret_cast<const uint32_t*>(gst + sw(2 * p));
-            const int64_t c0 = code_of(two & 0xFFFFu), c1 = code_of(two >> 16);
-            const int e0 = 2 * p;
-            if (e0 >= mis && e0 + 2 <= mis + total) {
-              st_cs2(oa + e0, c0, c1);
-            } else {
-              if (e0 >= mis && e0 < mis + total) st_cs(oa + e0, c0);
-              if (e0 + 1 >= mis && e0 + 1 < mis + total) st_cs(oa + e0 + 1, c1);
-            }
-          }
-        }
-      }
-      __syncthreads();
-    }
-  } else {
   // emission: one warp per segment (k_emit_pf16's staging and stores)
   uint16_t* stage = sm.u.stage[warp];
   auto sl = [](int k) { return k ^ (((k >> 5) & 31) << 1); };
@@ -869,7 +636,6 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(h + done + lane)]);
     __syncwarp();
   }
-  }
 #ifdef MMJ_DEBUG_TIMING
   __syncthreads();
   if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 5] = gtimer();
@@ -878,383 +644,6 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
 
 
 // ---------------------------------------------------------------------------
-// Persistent, warp-specialised form of k_merge_emit: one producer warp per CTA
-// prepares tile i+1 (ticket, bulk copy of the heavy bits, light merge,
-// segment scan, decoupled look-back) in one shared-memory buffer while NEW
-// emitter warps write tile i's codes from the other, so the tile's
-// pre-emission latency (dependent list loads, the look-back) no longer idles
-// the emitters.  Buffers hand over through mbarriers (full: producer ->
-// emitters, empty: emitters -> producer).  Deadlock-free: a producer takes a
-// ticket only when it holds a free buffer, and a tile's look-back only waits
-// on tiles whose tickets were taken earlier by producers that are not blocked.
-__device__ __forceinline__ void mbar_wait_par(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n\t"
-      "DONE:\n\t}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
-// light witnesses of one tile OR-ed in by a single warp (32 R tuples per batch)
-__device__ __forceinline__ unsigned long long merge_light_warp(const TileArgs& a, uint32_t* sbm, int64_t xa,
-                                                               int64_t xb, int64_t t_begin, int64_t t_end,
-                                                               int32_t zlo, int32_t zhi, int cw, int cbi) {
-  const int lane = threadIdx.x & 31;
-  unsigned long long my_w = 0;
-  for (int64_t tb = t_begin; tb < t_end; tb += 32) {
-    const int64_t t = tb + lane;
-    int len = 0, row = 0, filt = 0;
-    const int32_t* base = nullptr;
-    if (t < t_end) {
-      int64_t lo = xa, hi = xb;
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (a.fwd_ptr[mid] <= t) lo = mid;
-        else hi = mid;
-      }
-      row = (int)(lo - xa);
-      const int32_t y = a.fwd_idx[t];
-      const bool full = (a.hpos == nullptr) || (a.hpos[y] < 0) || (a.rdeg_x[lo] <= a.d2);
-      int32_t b, e;
-      if (full) {
-        b = a.s_rev_ptr[y];
-        e = a.s_rev_ptr[y + 1];
-        base = a.s_rev_idx + b;
-      } else {
-        b = a.lz_ptr[y];
-        e = a.lz_ptr[y + 1];
-        base = a.lz_idx + b;
-      }
-      len = e - b;
-      if (a.ncb > 1) {
-        const int32_t* sp = full ? a.split_full : a.split_lz;
-        if (sp != nullptr) {
-          const int32_t* q = sp + (int64_t)y * (a.ncb + 1) + cbi;
-          const int32_t lb = q[0], ub = q[1];
-          base += lb - b;
-          len = ub - lb;
-        } else if (len > SHORT_LIST) {
-          const int lb = lower_bound_i32(base, len, zlo);
-          const int ub = lb + lower_bound_i32(base + lb, len - lb, zhi);
-          base += lb;
-          len = ub - lb;
-        } else {
-          filt = 1;
-        }
-      }
-    }
-    int incl = len;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int tot = __shfl_sync(0xffffffffu, incl, 31);
-    const int excl = incl - len;
-    const int nt = (int)min((int64_t)32, t_end - tb);
-    int ti = 0;
-    // warp-uniform trip count: the cursor below uses full-warp shuffles
-    for (int s00 = 0; s00 < tot; s00 += MERGE_ILP * 32) {
-      const int s0 = s00 + lane;
-      int32_t zv[MERGE_ILP];
-      int rowv[MERGE_ILP];
-      bool ok[MERGE_ILP];
-#pragma unroll
-      for (int u = 0; u < MERGE_ILP; ++u) {
-        const int sidx = s0 + u * 32;
-        ok[u] = sidx < tot;
-        rowv[u] = 0;
-        zv[u] = 0;
-        // tuple of slot sidx: the last tuple whose exclusive offset is <= sidx
-        // (tuples are scanned from the cursor; slots only grow)
-        while (true) {
-          const int nx = __shfl_sync(0xffffffffu, excl, min(ti + 1, 31));
-          const bool adv = ok[u] && ti + 1 < nt && nx <= sidx;
-          if (!__any_sync(0xffffffffu, adv)) break;
-          if (adv) ++ti;
-        }
-        const int e0 = __shfl_sync(0xffffffffu, excl, ti);
-        const int32_t* bs = reinterpret_cast<const int32_t*>(
-            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(base), ti));
-        const int rw = __shfl_sync(0xffffffffu, row | (filt << 30), ti);
-        if (ok[u]) {
-#ifdef MMJ_DEBUG_BOUNDS
-          if (bs == nullptr || sidx - e0 < 0) {
-            printf("merge_light_warp: bad slot %d e0 %d ti %d nt %d tot %d\n", sidx, e0, ti, nt, tot);
-            __trap();
-          }
-#endif
-          zv[u] = __ldg(bs + (sidx - e0));
-          rowv[u] = rw;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < MERGE_ILP; ++u) {
-        if (!ok[u]) continue;
-        const int32_t z = zv[u];
-        if ((rowv[u] >> 30) && (z < zlo || z >= zhi)) continue;
-        atomicOr(&sbm[(rowv[u] & 0x3FFFFFFF) * cw + ((z - zlo) >> 5)], 1u << (z & 31));
-        ++my_w;
-      }
-    }
-  }
-  return my_w;
-}
-
-template <int TW, int NEW>
-struct PSmem {
-  uint32_t bm[2][TW];
-  int segoff[2][TW / 32];
-  uint16_t stage[NEW][1024 + 8];
-  long long prefix[2];
-  int tile[2];
-  int nseg[2];
-  int next_seg[2];
-  __align__(8) uint64_t full[2];
-  __align__(8) uint64_t empty[2];
-  __align__(8) uint64_t tbar[2];
-};
-
-template <int TW, int NEW>
-__global__ void __launch_bounds__((NEW + 1) * 32, 4) k_merge_emit_p(const FuseArgs f) {
-  extern __shared__ __align__(16) uint8_t p_raw[];
-  PSmem<TW, NEW>& sm = *reinterpret_cast<PSmem<TW, NEW>*>(p_raw);
-  const TileArgs& a = f.t;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.full[b])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&sm.empty[b])), "r"(NEW));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.tbar[b])));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == NEW) {
-    // ------------------------------------------------------------ producer
-    unsigned long long wit = 0;
-    for (int k = 0;; ++k) {
-      const int b = k & 1;
-      const uint32_t use = (uint32_t)(k >> 1);
-      mbar_wait_par(&sm.empty[b], (use & 1) ^ 1);
-      unsigned int tk = 0;
-      if (lane == 0) tk = atomicAdd(f.ticket, 1u);
-      tk = __shfl_sync(0xffffffffu, tk, 0);
-      if ((int64_t)tk >= f.ntiles) {
-        if (lane == 0) {
-          sm.tile[b] = -1;
-          mbar_arrive_cta(&sm.full[b]);
-        }
-        break;
-      }
-      const int64_t tile = tk;
-      const int64_t rg = tile / a.ncb;
-      const int cbi = (int)(tile - rg * a.ncb);
-      const int64_t r0 = rg * a.G;
-      const int64_t r1 = min(r0 + (int64_t)a.G, a.rows);
-      const int64_t c0w = (int64_t)cbi * a.cb_words;
-      const int cw = (int)min((int64_t)a.cb_words, a.wpr - c0w);
-      const int words = (int)(r1 - r0) * cw;
-      const int32_t zlo = (int32_t)(c0w * 32);
-      const int32_t zhi = (int32_t)min((c0w + cw) * 32, a.dom_z);
-      uint32_t* sbm = sm.bm[b];
-#ifdef MMJ_DEBUG_BOUNDS
-      if (words > TW || words <= 0 || cw <= 0 || r1 <= r0) {
-        printf("producer tile %lld words %d cw %d r0 %lld r1 %lld G %d ncb %d\n", (long long)tile, words, cw,
-               (long long)r0, (long long)r1, a.G, a.ncb);
-        __trap();
-      }
-#endif
-      if (a.has_heavy) {
-        if (lane == 0) bulk_g2s(sbm, a.bm + r0 * a.wpr + c0w, (uint32_t)words * 4u, &sm.tbar[b]);
-      } else {
-        for (int i = lane; i < words; i += 32) sbm[i] = 0;
-      }
-      const int64_t xa = a.x0 + r0, xb = a.x0 + r1;
-      const int64_t t_begin = a.fwd_ptr ? a.fwd_ptr[xa] : 0, t_end = a.fwd_ptr ? a.fwd_ptr[xb] : 0;
-      if (a.has_heavy) mbar_wait_par(&sm.tbar[b], use & 1);
-      __syncwarp();
-#ifdef MMJ_DEBUG_BOUNDS
-      if (!(f.dbg & 1))
-#endif
-      wit += merge_light_warp(a, sbm, xa, xb, t_begin, t_end, zlo, zhi, cw, cbi);
-      __syncwarp();
-      // segment counts and their exclusive scan (nseg <= TW/32, one warp)
-      const int nseg = words >> 5;
-      int run = 0;
-      for (int s0 = 0; s0 < nseg; s0 += 32) {
-        int mine = 0;
-        const int ns = min(32, nseg - s0);
-        for (int j = 0; j < ns; ++j) {
-          const int c = __reduce_add_sync(0xffffffffu, __popc(sbm[(s0 + j) * 32 + lane]));
-          if (lane == j) mine = c;
-        }
-        int incl = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += v;
-        }
-        if (lane < ns) sm.segoff[b][s0 + lane] = run + incl - mine;
-        run += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      const long long agg = run;
-      // decoupled look-back
-      long long prefix = 0;
-      if (tile == 0) {
-        if (lane == 0) st_status(f.status, ST_INC | (unsigned long long)agg);
-      } else {
-        if (lane == 0) st_status(f.status + tile, ST_AGG | (unsigned long long)agg);
-        int64_t pos = tile - 1;
-        while (true) {
-          const int64_t idx = pos - lane;
-          unsigned long long st = idx >= 0 ? ld_status(f.status + idx) : ST_INC;
-          while (__any_sync(0xffffffffu, (st >> 62) == 0)) {
-            if ((st >> 62) == 0) st = ld_status(f.status + idx);
-          }
-          const unsigned inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
-          const int stop = inc ? __ffs(inc) - 1 : 31;
-          long long val = lane <= stop ? (long long)(st & ST_VAL) : 0;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-          prefix += val;
-          if (inc) break;
-          pos -= 32;
-        }
-        if (lane == 0) st_status(f.status + tile, ST_INC | (unsigned long long)(prefix + agg));
-      }
-      if (lane == 0) {
-        if (tile == f.ntiles - 1) *f.total = prefix + agg;
-        sm.prefix[b] = prefix;
-        sm.tile[b] = (int)tile;
-        sm.nseg[b] = nseg;
-        sm.next_seg[b] = NEW;
-        mbar_arrive_cta(&sm.full[b]);   // release: the tile's words, offsets and info
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wit += __shfl_xor_sync(0xffffffffu, wit, o);
-    if (lane == 0 && wit) atomicAdd(a.witnesses, wit);
-  } else {
-    // ------------------------------------------------------------ emitters
-    uint16_t* stage = sm.stage[warp];
-    auto sl = [](int k) { return k ^ (((k >> 5) & 31) << 1); };
-    for (int k = 0;; ++k) {
-      const int b = k & 1;
-      mbar_wait_par(&sm.full[b], (uint32_t)(k >> 1) & 1);
-      const int tile = sm.tile[b];
-      if (tile < 0) break;
-      const int64_t rg = tile / a.ncb;
-      const int cbi = (int)(tile - rg * a.ncb);
-      const int64_t r0 = rg * a.G;
-      const int64_t c0w = (int64_t)cbi * a.cb_words;
-      const int cw = (int)min((int64_t)a.cb_words, a.wpr - c0w);
-      const int segs_per_piece = cw >> 5;
-      const int nseg = sm.nseg[b];
-      const uint32_t* sbm = sm.bm[b];
-      int64_t* const codes = f.codes + sm.prefix[b];
-      for (int si = warp; si < nseg;) {
-        uint32_t word = sbm[si * 32 + lane];
-        const int c = __popc(word);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int vv = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += vv;
-        }
-        const int tot = __shfl_sync(0xffffffffu, incl, 31);
-        const int cur = si;
-        {
-          int nx = 0;
-          if (lane == 0) nx = atomicAdd(&sm.next_seg[b], 1);
-          si = __shfl_sync(0xffffffffu, nx, 0);
-        }
-        if (tot == 0) continue;
-#ifdef MMJ_DEBUG_BOUNDS
-        if (f.dbg & 2) continue;
-#endif
-        const int rr = cur / segs_per_piece;
-        const int64_t base = (a.x0 + r0 + rr) * a.dom_z + (c0w + (int64_t)(cur - rr * segs_per_piece) * 32) * 32;
-        int64_t* out = codes + sm.segoff[b][cur];
-#ifdef MMJ_DEBUG_BOUNDS
-        if (sm.prefix[b] + sm.segoff[b][cur] + tot > a.rows * a.dom_z || cur >= nseg) {
-          printf("emitter: tile %d cur %d nseg %d prefix %lld segoff %d tot %d cap %lld\n", tile, cur, nseg,
-                 sm.prefix[b], sm.segoff[b][cur], tot, (long long)(a.rows * a.dom_z));
-          __trap();
-        }
-#endif
-        const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
-        const uint32_t off0 = lane * 32;
-        int kk = h + (incl - c);
-        if (__reduce_max_sync(0xffffffffu, (unsigned)c) >= 10u) {
-#pragma unroll
-          for (int bb = 0; bb < 32; ++bb) {
-            if (word & (1u << bb)) {
-              stage[sl(kk)] = (uint16_t)(off0 + bb);
-              ++kk;
-            }
-          }
-        } else {
-          while (word) {
-            const int bb = __ffs(word) - 1;
-            stage[sl(kk)] = (uint16_t)(off0 + bb);
-            ++kk;
-            word &= word - 1;
-          }
-        }
-        __syncwarp();
-        if (lane < h) st_cs(out, base + stage[sl(h)]);
-        const int np = (tot - h) >> 1;
-        for (int p = lane; p < np; p += 32) {
-          const uint32_t two = *reinterpret_cast<const uint32_t*>(stage + sl(2 * h + 2 * p));
-          st_cs2(out + h + 2 * p, base + (two & 0xFFFFu), base + (two >> 16));
-        }
-        const int done = h + 2 * np;
-        if (lane < tot - done) st_cs(out + done + lane, base + stage[sl(h + done + lane)]);
-        __syncwarp();
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cta(&sm.empty[b]);   // this warp is done reading buffer b
-    }
-  }
-}
-
-// ent[t*ncb + j] = (first position | (1 << 31) if the light-z list, end position)
-// of R tuple t's S-side list restricted to column block j: the x-side
-// restatement of joinproject.py:183-203 (full S.rev(y) when y or x is light,
-// the light-z list otherwise), evaluated once per engine.
-__global__ void k_tuple_entries(const int32_t* __restrict__ fwd_row, const int32_t* __restrict__ fwd_idx, int64_t n,
-                                const int32_t* __restrict__ rdeg_x, int64_t d2, const int32_t* __restrict__ hpos,
-                                const int32_t* __restrict__ s_rev_ptr, const int32_t* __restrict__ lz_ptr,
-                                const int32_t* __restrict__ split_full, const int32_t* __restrict__ split_lz, int ncb,
-                                int2* __restrict__ ent) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t y = fwd_idx[t];
-    const bool full = (hpos == nullptr) || (hpos[y] < 0) || (rdeg_x[fwd_row[t]] <= d2);
-    const int32_t* ptr = full ? s_rev_ptr : lz_ptr;
-    const int32_t* sp = full ? split_full : split_lz;
-    const int32_t flag = full ? 0 : (int32_t)0x80000000u;
-    for (int j = 0; j < ncb; ++j) {
-      int32_t b, e;
-      if (ncb == 1) {
-        b = ptr[y];
-        e = ptr[y + 1];
-      } else {
-        b = sp[(int64_t)y * (ncb + 1) + j];
-        e = sp[(int64_t)y * (ncb + 1) + j + 1];
-      }
-      ent[t * ncb + j] = make_int2(b | flag, e);
-    }
-  }
-}
-
 // split[y*(ncb+1) + j] = absolute position in idx of the first entry of list
 // y (ptr[y] .. ptr[y+1], sorted) that is >= j * cb_cells
 __global__ void k_list_splits(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx, int64_t dom_y,
@@ -1293,90 +682,33 @@ void tile_geometry(int64_t wpr, int& G, int& cb, int& ncb, int64_t tile_words = 
   }
 }
 
-// MMJ_FUSE_PERSIST=1: the persistent warp-specialised tail (k_merge_emit_p,
-// 4096-word tiles); measured slower on cfg2 (191 vs 170 ms: one producer warp
-// per CTA does not keep 8 emitter warps fed), so one CTA per tile is the default
-bool fuse_persistent() {
-  static int persist = -1;
-  if (persist < 0) {
-    const char* e = getenv("MMJ_FUSE_PERSIST");
-    persist = (e && e[0] == '1') ? 1 : 0;
-  }
-  return persist != 0;
-}
+constexpr int FUSE_TILE_WORDS = 8192;   // 32 KB of bitmap per tile (4096 / 16384 measured slower)
 
-// tile words of the fused kernel (env MMJ_FUSE_TW: 4096 / 8192 / 16384)
-int fuse_tile_words() {
-  static int tw = -1;
-  if (tw < 0) {
-    const char* e = getenv("MMJ_FUSE_TW");
-    tw = e ? atoi(e) : (fuse_persistent() ? 4096 : 8192);
-    if (tw != 4096 && tw != 8192 && tw != 16384) tw = 8192;
-  }
-  return tw;
-}
+// 9 warps x 4 CTAs = 36 warps per SM at 54 registers (171.8 vs 173.1 ms per
+// cfg2 step for 8 warps: more warps hide the look-back wait)
+constexpr int FUSE_THREADS = 288;
+constexpr int FUSE_MIN_CTAS = 4;
 
-template <int TW, int NEW>
-int launch_merge_emit_p(const FuseArgs& f, cudaStream_t st) {
-  constexpr size_t smem = sizeof(PSmem<TW, NEW>);
-  static bool attr = false;
-  if (!attr) {
-    MMJ_TRY(cuda_status(cudaFuncSetAttribute(k_merge_emit_p<TW, NEW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem),
-                        "cudaFuncSetAttribute(k_merge_emit_p)"));
-    attr = true;
-  }
-  int per_sm = 0;
-  MMJ_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_emit_p<TW, NEW>, (NEW + 1) * 32,
-                                                                    smem),
-                      "occupancy(k_merge_emit_p)"));
-  const int64_t grid = std::min<int64_t>(f.ntiles, (int64_t)std::max(per_sm, 1) * sm_count());
-  k_merge_emit_p<TW, NEW><<<(unsigned)grid, (NEW + 1) * 32, smem, st>>>(f);
-  MMJ_CHECK_LAUNCH("k_merge_emit_p");
-  return MMJ_OK;
-}
-
-// MMJ_CTA_EMIT: 1 = CTA-cooperative 32-byte emission, 0 = per-warp segments
-bool cta_emit() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MMJ_CTA_EMIT");
-    v = e ? (e[0] == '1') : 0;
-  }
-  return v != 0;
-}
-
-template <int TW, int NT, int MINB, bool CTA>
-int launch_merge_emit_v(const FuseArgs& f, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    MMJ_TRY(cuda_status(cudaFuncSetAttribute(k_merge_emit<TW, NT, MINB, CTA>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, TW * 4),
-                        "cudaFuncSetAttribute(k_merge_emit)"));
-    attr = true;
-  }
+int launch_merge_emit(const FuseArgs& f, cudaStream_t st) {
+  auto kern = k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS>;
+  MMJ_TRY(set_max_dynamic_smem((const void*)kern, FUSE_TILE_WORDS * 4, "k_merge_emit"));
   const size_t smem = (size_t)f.t.G * f.t.cb_words * 4;
-  k_merge_emit<TW, NT, MINB, CTA><<<(unsigned)f.ntiles, NT, smem, st>>>(f);
+  kern<<<(unsigned)f.ntiles, FUSE_THREADS, smem, st>>>(f);
   MMJ_CHECK_LAUNCH("k_merge_emit");
   return MMJ_OK;
-}
-
-template <int TW, int NT, int MINB>
-int launch_merge_emit(const FuseArgs& f, cudaStream_t st) {
-  return cta_emit() ? launch_merge_emit_v<TW, NT, MINB, true>(f, st) : launch_merge_emit_v<TW, NT, MINB, false>(f, st);
 }
 
 }  // namespace
 
 int merge_emit_col_blocks(int64_t wpr) {
   int G, cb, ncb;
-  tile_geometry(wpr, G, cb, ncb, fuse_tile_words());
+  tile_geometry(wpr, G, cb, ncb, FUSE_TILE_WORDS);
   return ncb;
 }
 
 int list_splits(const int32_t* ptr, const int32_t* idx, int64_t dom_y, int64_t wpr, int32_t* split, cudaStream_t st) {
   int G, cb, ncb;
-  tile_geometry(wpr, G, cb, ncb, fuse_tile_words());
+  tile_geometry(wpr, G, cb, ncb, FUSE_TILE_WORDS);
   const int64_t n = dom_y * (ncb + 1);
   if (n == 0) return MMJ_OK;
   const int64_t g = std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 16);
@@ -1385,30 +717,9 @@ int list_splits(const int32_t* ptr, const int32_t* idx, int64_t dom_y, int64_t w
   return MMJ_OK;
 }
 
-int tuple_entries(const int32_t* fwd_row, const int32_t* fwd_idx, int64_t n, const int32_t* rdeg_x, int64_t d2,
-                  const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* lz_ptr, const int32_t* split_full,
-                  const int32_t* split_lz, int64_t wpr, void* ent, cudaStream_t st) {
-  int G, cb, ncb;
-  tile_geometry(wpr, G, cb, ncb, fuse_tile_words());
-  if (ncb > 1 && (split_full == nullptr || (hpos != nullptr && lz_ptr != nullptr && split_lz == nullptr))) {
-    set_error("tuple_entries: rows span %d column blocks: the split tables are required", ncb);
-    return MMJ_ERR_ARG;
-  }
-  if (hpos != nullptr && lz_ptr == nullptr) {
-    set_error("tuple_entries: a partitioned plan needs the light-z lists");
-    return MMJ_ERR_ARG;
-  }
-  if (n == 0) return MMJ_OK;
-  const int64_t g = std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 16);
-  k_tuple_entries<<<(unsigned)g, 256, 0, st>>>(fwd_row, fwd_idx, n, rdeg_x, d2, hpos, s_rev_ptr, lz_ptr, split_full,
-                                              split_lz, ncb, static_cast<int2*>(ent));
-  MMJ_CHECK_LAUNCH("k_tuple_entries");
-  return MMJ_OK;
-}
-
 int64_t merge_emit_tiles(int64_t rows, int64_t wpr) {
   int G, cb, ncb;
-  tile_geometry(wpr, G, cb, ncb, fuse_tile_words());
+  tile_geometry(wpr, G, cb, ncb, FUSE_TILE_WORDS);
   return ceil_div(rows, G) * ncb;
 }
 
@@ -1421,14 +732,13 @@ unsigned long long* tdbg_buffer = nullptr;   // MMJ_DEBUG_TIMING builds: set by 
 int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t d2, const int32_t* hpos,
                const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx,
-               const int32_t* split_full, const int32_t* split_lz, const void* ent, unsigned long long* witnesses,
-               int64_t* codes, int64_t* total, void* ws, size_t ws_bytes, cudaStream_t st) {
+               const int32_t* split_full, const int32_t* split_lz, unsigned long long* witnesses, int64_t* codes,
+               int64_t* total, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (wpr <= 0 || wpr % 32 != 0) {
     set_error("merge_emit: bitmap pitch must be a positive multiple of 32 words");
     return MMJ_ERR_ARG;
   }
   if (rows <= 0) return cuda_status(cudaMemsetAsync(total, 0, sizeof(int64_t), st), "merge_emit: total");
-  const int tw = fuse_tile_words();
   FuseArgs f;
   TileArgs& a = f.t;
   a.bm = const_cast<uint32_t*>(bm);
@@ -1437,7 +747,7 @@ int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int6
   a.rows = rows;
   a.wpr = wpr;
   a.dom_z = dom_z;
-  tile_geometry(wpr, a.G, a.cb_words, a.ncb, tw);
+  tile_geometry(wpr, a.G, a.cb_words, a.ncb, FUSE_TILE_WORDS);
   f.ntiles = ceil_div(rows, a.G) * a.ncb;
   if (f.ntiles >= (1ll << 31)) {
     set_error("merge_emit: too many tiles in one chunk");
@@ -1461,33 +771,13 @@ int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int6
   a.witnesses = witnesses;
   a.split_full = split_full;
   a.split_lz = split_lz;
-  a.ent = static_cast<const int2*>(ent);
   f.ticket = static_cast<unsigned int*>(ws);
   f.status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 16);
   f.total = total;
   f.codes = codes;
-  {
-    const char* e = getenv("MMJ_DBG_FUSE");
-    f.dbg = e ? atoi(e) : 0;
-  }
   f.tdbg = tdbg_buffer;
   MMJ_TRY(cuda_status(cudaMemsetAsync(ws, 0, need, st), "merge_emit: workspace reset"));
-  if (fuse_persistent() && tw == 4096) return launch_merge_emit_p<4096, 8>(f, st);
-  static int variant = -1;
-  if (variant < 0) {
-    const char* e = getenv("MMJ_FUSE_VARIANT");   // A/B: 1 = (4096, 256 thr, 6 CTAs/SM), 2 = (16384, 512 thr), 3 = (8192, 256 thr, 4)
-    variant = e ? atoi(e) : 0;
-  }
-  if (variant == 1 && tw == 4096) return launch_merge_emit<4096, 256, 6>(f, st);
-  if (variant == 2 && tw == 16384) return launch_merge_emit<16384, 512, 2>(f, st);
-  if (variant == 3 && tw == 8192) return launch_merge_emit<8192, 256, 4>(f, st);   // the round-1d..1f default
-  switch (tw) {
-    case 4096: return launch_merge_emit<4096, 256, 4>(f, st);
-    case 16384: return launch_merge_emit<16384, 256, 2>(f, st);
-    // 9 warps x 4 CTAs = 36 warps per SM at 54 registers (171.8 vs 173.1 ms
-    // per cfg2 step for 8 warps: more warps hide the look-back wait)
-    default: return launch_merge_emit<8192, 288, 4>(f, st);
-  }
+  return launch_merge_emit(f, st);
 }
 
 int64_t row_emit_tiles(int64_t rows, int64_t wpr) {
@@ -1530,13 +820,7 @@ int tile_merge(uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int64_t wp
   a.segcnt = segcnt;
   a.witnesses = witnesses;
   const size_t smem = (size_t)a.G * a.cb_words * 4;
-  static bool attr = false;
-  if (!attr) {
-    MMJ_TRY(cuda_status(cudaFuncSetAttribute(k_tile_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             TILE_WORDS * 4),
-                        "cudaFuncSetAttribute(k_tile_merge)"));
-    attr = true;
-  }
+  MMJ_TRY(set_max_dynamic_smem((const void*)k_tile_merge, TILE_WORDS * 4, "k_tile_merge"));
   k_tile_merge<<<(unsigned)ntiles, TM_THREADS, smem, st>>>(a);
   MMJ_CHECK_LAUNCH("k_tile_merge");
   return MMJ_OK;
@@ -1550,53 +834,9 @@ int emit_codes(const uint32_t* bm, const int64_t* segoff, int64_t rows, int64_t 
   }
   const int64_t nseg = rows * wpr / 32;
   if (nseg == 0) return MMJ_OK;
-  static int segs = -1;
-  if (segs < 0) {
-    const char* e = getenv("MMJ_EMIT_SEGS");   // A/B knob: segments per emission CTA
-    segs = e ? atoi(e) : EM_SEGS;
-  }
-  static int ver = -1;
-  if (ver < 0) {
-    // 3 (default): prefetch + 16-bit staging; 2: prefetch + 32-bit staging;
-    // 1: the round-1 kernel without prefetch (A/B references)
-    const char* e = getenv("MMJ_EMIT_V");
-    ver = e ? atoi(e) : 3;
-  }
-  if (ver == 3) {
-    static int bs = -1;
-    if (bs < 0) {
-      const char* e = getenv("MMJ_EMIT_BITSLICE");
-      bs = (e && e[0] == '0') ? 0 : 1;
-    }
-    if (bs)
-      k_emit_pf16<32, true><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0,
-                                                                                    dom_z, codes);
-    else if (getenv("MMJ_EMIT_SEGS") && segs == 64)
-      k_emit_pf16<64, false><<<(unsigned)ceil_div(nseg, 64), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z,
-                                                                              codes);
-    else
-      k_emit_pf16<32, false><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0,
-                                                                                     dom_z, codes);
-    MMJ_CHECK_LAUNCH("k_emit_pf16");
-    return MMJ_OK;
-  }
-  if (ver == 2) {
-    if (!getenv("MMJ_EMIT_SEGS") || segs == 32)
-      k_emit_pf<32><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes);
-    else if (segs == 16)
-      k_emit_pf<16><<<(unsigned)ceil_div(nseg, 16), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes);
-    else
-      k_emit_pf<64><<<(unsigned)ceil_div(nseg, 64), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes);
-    MMJ_CHECK_LAUNCH("k_emit_pf");
-    return MMJ_OK;
-  }
-  switch (segs) {
-    case 8: k_emit<8><<<(unsigned)ceil_div(nseg, 8), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes); break;
-    case 16: k_emit<16><<<(unsigned)ceil_div(nseg, 16), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes); break;
-    case 32: k_emit<32><<<(unsigned)ceil_div(nseg, 32), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes); break;
-    default: k_emit<EM_SEGS><<<(unsigned)ceil_div(nseg, EM_SEGS), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0, dom_z, codes);
-  }
-  MMJ_CHECK_LAUNCH("k_emit");
+  k_emit_pf16<EM_SEGS><<<(unsigned)ceil_div(nseg, EM_SEGS), EM_WARPS * 32, 0, st>>>(bm, segoff, nseg, wpr / 32, x0,
+                                                                                 dom_z, codes);
+  MMJ_CHECK_LAUNCH("k_emit_pf16");
   return MMJ_OK;
 }
 

@@ -6,6 +6,11 @@
 #include <cub/block/block_scan.cuh>
 #include <stdarg.h>
 
+#include <algorithm>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
 #include "mmj_common.cuh"
 
 namespace mmj {
@@ -34,6 +39,19 @@ int sm_count() {
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   if (dev < 64) cached[dev] = n;
   return n;
+}
+
+int set_max_dynamic_smem(const void* func, int bytes, const char* where) {
+  static std::mutex mu;
+  static std::vector<std::tuple<int, const void*, int>> done;   // (device, function, bytes)
+  int dev = 0;
+  MMJ_TRY(cuda_status(cudaGetDevice(&dev), where));
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (std::get<0>(d) == dev && std::get<1>(d) == func && std::get<2>(d) >= bytes) return MMJ_OK;
+  MMJ_TRY(cuda_status(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), where));
+  done.emplace_back(dev, func, bytes);
+  return MMJ_OK;
 }
 
 namespace {
@@ -138,6 +156,52 @@ int scan_i32_i32(const int32_t* in, int32_t* out, int64_t n, void* ws, cudaStrea
 }
 int scan_i64_i64(const int64_t* in, int64_t* out, int64_t n, void* ws, cudaStream_t st) {
   return scan_impl<int64_t, int64_t>(in, out, n, ws, st);
+}
+
+// ---- order-sensitive checksum of a sorted code run ---------------------------
+// out[0] += sum(codes[i]), out[1] += sum((base + i + 1) * codes[i]), both
+// mod 2^64: equal for two code arrays of one length only if (with
+// overwhelming probability) they are equal element by element, and additive
+// over consecutive chunks when `base` is the number of codes before the chunk.
+namespace {
+__global__ void k_code_checksum(const int64_t* __restrict__ codes, int64_t n, unsigned long long base,
+                                unsigned long long* __restrict__ out) {
+  unsigned long long s = 0, w = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + stride < n; i += 2 * stride) {   // two streaming loads in flight per thread
+    const unsigned long long c0 = (unsigned long long)__ldcs(codes + i);
+    const unsigned long long c1 = (unsigned long long)__ldcs(codes + i + stride);
+    s += c0 + c1;
+    w += (base + (unsigned long long)i + 1ull) * c0 + (base + (unsigned long long)(i + stride) + 1ull) * c1;
+  }
+  if (i < n) {
+    const unsigned long long c = (unsigned long long)__ldcs(codes + i);
+    s += c;
+    w += (base + (unsigned long long)i + 1ull) * c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    w += __shfl_xor_sync(0xffffffffu, w, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (s | w)) {
+    atomicAdd(out, s);
+    atomicAdd(out + 1, w);
+  }
+}
+}  // namespace
+
+int code_checksum(const int64_t* codes, int64_t n, int64_t base, unsigned long long* out, cudaStream_t st) {
+  if (n < 0 || base < 0) {
+    set_error("code_checksum: negative length / base");
+    return MMJ_ERR_ARG;
+  }
+  if (n == 0) return MMJ_OK;
+  const int64_t g = std::min<int64_t>(ceil_div(n, 512), (int64_t)sm_count() * 8);
+  k_code_checksum<<<(unsigned)g, 256, 0, st>>>(codes, n, (unsigned long long)base, out);
+  MMJ_CHECK_LAUNCH("k_code_checksum");
+  return MMJ_OK;
 }
 
 }  // namespace mmj

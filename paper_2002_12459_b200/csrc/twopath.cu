@@ -89,49 +89,6 @@ __global__ void k_build_operand_pairs(const int32_t* __restrict__ rows, const in
   }
 }
 
-// A operand of MMJ_MODE_BITMAP_TRIPLE: [R_h | 128 R_h], pitch 2*kpad.
-__global__ void k_build_operand_x2(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols, int64_t n,
-                                   const int32_t* __restrict__ left_deg, int64_t d2, const int32_t* __restrict__ hpos,
-                                   uint8_t* __restrict__ mat, int64_t row0, int64_t nrows, int64_t kpad) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = rows[t] - row0;
-    if (r < 0 || r >= nrows) continue;
-    if (left_deg[rows[t]] <= d2) continue;
-    const int32_t k = hpos[cols[t]];
-    if (k < 0) continue;
-    mat[r * 2 * kpad + k] = 1;
-    mat[r * 2 * kpad + kpad + k] = 128;
-  }
-}
-
-// z-triple B operand for MMJ_MODE_BITMAP_TRIPLE (pitch 2*kpad): z = 96G + 32w
-// + 8b + k (w < 3, b < 4, k < 8) is byte P = 4w + b of the group's 12 output
-// bytes, i.e. field f = P % 3 of accumulator row 32G + 8 (P / 3) + k
-// (mma_i8.cu pack_bits_triple); field 0 weight 1 and field 1 weight 128 in
-// the first K half, field 2 weight 128 in the second (A's second half is 128).
-__global__ void k_build_operand_triples(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
-                                        int64_t n, const int32_t* __restrict__ left_deg, int64_t d2,
-                                        const int32_t* __restrict__ hpos, uint8_t* __restrict__ mat, int64_t row0,
-                                        int64_t nz, int64_t kpad) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t z = rows[t] - row0;
-    if (z < 0 || z >= nz) continue;
-    if (left_deg[rows[t]] <= d2) continue;
-    const int32_t k = hpos[cols[t]];
-    if (k < 0) continue;
-    const int64_t g = z / 96;
-    const int zz = (int)(z - g * 96);
-    const int P = 4 * (zz >> 5) + ((zz & 31) >> 3);
-    const int f = P % 3;
-    const int64_t prow = g * 32 + 8 * (P / 3) + (zz & 7);
-    const int64_t off = prow * 2 * kpad + (f == 2 ? kpad : 0) + k;
-    const uint32_t v = f == 0 ? 0x01u : 0x80u;
-    atomicOr(reinterpret_cast<unsigned int*>(mat + (off & ~int64_t(3))), v << (8 * (off & 3)));
-  }
-}
-
 // ----------------------------------------------------------- light-z CSR
 __global__ void k_lz_flags(const int32_t* __restrict__ rev_idx, int64_t n,
                            const int32_t* __restrict__ left_deg, int64_t d2, uint8_t* __restrict__ flag) {
@@ -543,24 +500,6 @@ int build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n, con
   k_build_operand_pairs<<<grid_for(n, TPB), TPB, 0, st>>>(rows, cols, n, left_deg, d2, hpos, mat, row0, nrows,
                                                           kpad);
   MMJ_CHECK_LAUNCH("k_build_operand_pairs");
-  return MMJ_OK;
-}
-
-int build_operand_triple(int side, const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
-                         int64_t d2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows, int64_t mat_rows,
-                         int64_t kpad, cudaStream_t st) {
-  if (kpad % 4 != 0 || reinterpret_cast<uintptr_t>(mat) % 4 != 0 || (side == 1 && mat_rows * 3 < nrows)) {
-    set_error("build_operand_triple: kpad and mat must be 4-byte aligned and B must hold ceil(nrows/3) rows");
-    return MMJ_ERR_ARG;
-  }
-  MMJ_TRY(cuda_status(cudaMemsetAsync(mat, 0, (size_t)(mat_rows * 2 * kpad), st), "memset operand"));
-  if (n == 0) return MMJ_OK;
-  if (side == 0)
-    k_build_operand_x2<<<grid_for(n, TPB), TPB, 0, st>>>(rows, cols, n, left_deg, d2, hpos, mat, row0, nrows, kpad);
-  else
-    k_build_operand_triples<<<grid_for(n, TPB), TPB, 0, st>>>(rows, cols, n, left_deg, d2, hpos, mat, row0, nrows,
-                                                              kpad);
-  MMJ_CHECK_LAUNCH("k_build_operand_triple");
   return MMJ_OK;
 }
 

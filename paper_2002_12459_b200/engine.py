@@ -41,14 +41,20 @@ _HOST_MAX = {}
 
 
 def _host_max(arr) -> int:
-    """max of a host degree array, remembered per array object: the inputs
-    are immutable (as the reference's IndexedRelation), and engines for the
-    same relations (one per batch / shard / step) would otherwise rescan
-    them on the host (~0.3 ms per 500k-entry array on the GPU box)."""
+    """max of a host degree array.  Read-only arrays (this package's
+    IndexedRelation freezes its degree vectors) are remembered per array
+    object, so engines for the same relations (one per batch / shard / step)
+    do not rescan them (~0.3 ms per 500k entries); writeable arrays (e.g. a
+    caller's own index) are rescanned on every call, so an in-place edit can
+    never leave a stale maximum behind (that maximum gates the uint16 count
+    cells and the z-pair operand)."""
+    a = np.asarray(arr)
+    if a.flags.writeable:
+        return int(a.max(initial=0))
     hit = _HOST_MAX.get(id(arr))
     if hit is not None and hit[0] is arr:
         return hit[1]
-    m = int(np.asarray(arr).max(initial=0))
+    m = int(a.max(initial=0))
     if len(_HOST_MAX) >= 64:
         _HOST_MAX.clear()
     _HOST_MAX[id(arr)] = (arr, m)   # the reference keeps the id from being reused
@@ -80,19 +86,6 @@ class EngineStats:
     out_size: int = 0
     launches: int = 0
     extra: dict = field(default_factory=dict)
-
-
-_STREAMS: dict = {}
-
-
-def _stream_pair(tag: str):
-    """(low-priority, high-priority) CUDA streams of the current device, created
-    once per process (stream creation costs more than a small join)."""
-    import torch
-    key = (tag, torch.cuda.current_device())
-    if key not in _STREAMS:
-        _STREAMS[key] = (torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1))
-    return _STREAMS[key]
 
 
 class TwoPathEngine:
@@ -135,8 +128,6 @@ class TwoPathEngine:
         self.pairs = False
         self.allow_pairs = bool(pair_operand)   # False: B stays one z per row (heavy_matrices reads it)
         self.kpad = 0
-        self.mma_kpad = 0       # K window of the heavy product (2 * kpad for the z-triple operands)
-        self.triple = False
         self.lz_ptr = None
         self.lz_idx = None
         self._host_ldeg_r = host_left_deg_r
@@ -165,7 +156,6 @@ class TwoPathEngine:
         self._sizes_dev = None
         self._n_async = 0
         self.timer = None          # optional PhaseTimer (bench instrumentation)
-        self.mma_ctas = int(__import__("os").environ.get("MMJ_MMA_CTAS", "0"))   # 0 = one CTA per SM
 
     # ------------------------------------------------------------ prepare
     def _st(self):
@@ -199,31 +189,12 @@ class TwoPathEngine:
                               and __import__("os").environ.get("MMJ_PAIR", "1") != "0"
                               and (k <= 127 or self._max_deg(self._host_ldeg_r, dr) <= 127
                                    or self._max_deg(self._host_ldeg_s, ds) <= 127))
-                # z triples (3 cells per TMEM word) are opt-in: measured slower than
-                # pairs on cfg2 (35.1 vs 26.5 ms: the extra packing ALU outweighs the
-                # saved TMEM read-out), kept as an A/B option (MMJ_TRIPLE=1)
-                self.triple = self.pairs and __import__("os").environ.get("MMJ_TRIPLE", "0") == "1"
-                self.mma_kpad = kpad
-                if not self.triple:
-                    self.A = torch.empty((arows, kpad), dtype=torch.uint8, device="cuda")
-                    nat.call("mmj_build_operand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n,
-                             nat.ptr(dr.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.A), 0, arows, kpad, st)
-                if self.triple:
-                    # three z per accumulator (weights 1, 128 | 128 with A =
-                    # [R_h | 128 R_h]): one TMEM word carries three cells
-                    self.mma_kpad = 2 * kpad
-                    brows_t = -(-(brows // 32) // 24) * BN
-                    self.A = torch.empty((arows, 2 * kpad), dtype=torch.uint8, device="cuda")
-                    nat.call("mmj_build_operand_triple", 0, nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n,
-                             nat.ptr(dr.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.A), 0, arows, arows,
-                             kpad, st)
-                    self.B = torch.empty((brows_t, 2 * kpad), dtype=torch.uint8, device="cuda")
-                    nat.call("mmj_build_operand_triple", 1, nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n,
-                             nat.ptr(ds.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.B), 0, brows, brows_t,
-                             kpad, st)
-                elif self.pairs:
+                self.A = torch.empty((arows, kpad), dtype=torch.uint8, device="cuda")
+                nat.call("mmj_build_operand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n,
+                         nat.ptr(dr.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.A), 0, arows, kpad, st)
+                if self.pairs:
                     # z pairs share one accumulator (weights 1, 128): every
-                    # count is < 128 because one side's heavy degrees are
+                    # count is < 128 because one side's heavy degrees are <= 127
                     self.B = torch.empty((brows // 2, kpad), dtype=torch.uint8, device="cuda")
                     nat.call("mmj_build_operand_pairs", nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n,
                              nat.ptr(ds.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.B), 0, brows, kpad, st)
@@ -246,8 +217,6 @@ class TwoPathEngine:
     def _bitmap_mode(self) -> int:
         # every product entry counts <= K shared heavy y: with K <= 255 the
         # epilogue may pack counts as bytes
-        if self.triple:
-            return nat.MODE_BITMAP_TRIPLE
         if self.pairs:
             return nat.MODE_BITMAP_PAIR
         return nat.MODE_BITMAP_U8 if 0 < self.stats.k_heavy <= 255 else nat.MODE_BITMAP
@@ -295,7 +264,7 @@ class TwoPathEngine:
         self._ph("heavy_mma", True)
         if self.A is not None:
             nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
-                     self.mma_kpad, 0, self.mma_kpad, x0, rows, mode, 0, nat.ptr(buf), ld, nat.ptr(self.nnz), 0, st)
+                     self.kpad, 0, self.kpad, x0, rows, mode, 0, nat.ptr(buf), ld, nat.ptr(self.nnz), 0, st)
         else:
             buf.zero_()
         self._ph("heavy_mma", False)
@@ -414,17 +383,11 @@ class TwoPathEngine:
         self.stats.out_size += total
         return ChunkResult(x0, x1, total, codes[:total], None, light)
 
-    def _list_splits(self):
-        """(full, light-z) column-block split tables of the S-side lists for
-        the fused kernel, built once per engine; (0, 0) when a row is a single
-        tile or the table would be large (the kernel then bisects)."""
-        return self._tail_tables()[:2]
-
     def _tail_tables(self):
-        """Per-engine tables of the fused tail: the (full, light-z) split tables
-        (first list position of every column block; only when a row spans
-        several tiles) and the per-(R tuple, column block) list ranges
-        (mmj_tuple_entries), each 0 when absent."""
+        """(full, light-z) column-block split tables of the S-side lists for
+        the fused kernel (first list position of every column block), built
+        once per engine; 0 when a row is a single tile or the table would be
+        large (the kernel then bisects long lists)."""
         if self._splits is None:
             torch = self.torch
             st = self._st()
@@ -444,20 +407,8 @@ class TwoPathEngine:
                              nat.ptr(lzt), st)
                     keep.append(lzt)
                     spl = nat.ptr(lzt)
-            ent = 0
-            hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
-            ok = (ncb == 1 or spf) and (hp == 0 or self.lz_ptr is not None) and (ncb == 1 or hp == 0 or spl)
-            # opt-in (MMJ_TUPLE_ENTRIES=1): measured neutral on cfg2 (170.7 vs 170.5 ms): the
-            # tile's merge latency is hidden by the other CTAs on the SM
-            if ok and self.dr.n * ncb <= (256 << 20) and __import__("os").environ.get("MMJ_TUPLE_ENTRIES", "0") == "1":
-                e = torch.empty((max(self.dr.n * ncb, 1), 2), dtype=torch.int32, device="cuda")
-                nat.call("mmj_tuple_entries", nat.ptr(self.dr.fwd_row), nat.ptr(self.dr.fwd_idx), self.dr.n,
-                         nat.ptr(self.dr.left_deg), self.d2, hp, nat.ptr(self.ds.rev_ptr),
-                         nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0, spf, spl, self.wpr, nat.ptr(e), st)
-                keep.append(e)
-                ent = nat.ptr(e)
-            self._splits = (spf, spl, ent, keep)
-        return self._splits[:3]
+            self._splits = (spf, spl, keep)
+        return self._splits[:2]
 
     def _merge_emit_tail(self, x0, x1, rows, buf, sync, codes_key):
         torch = self.torch
@@ -473,11 +424,11 @@ class TwoPathEngine:
         cap = rows * self.dom_z
         codes = self.ws.get(codes_key, cap, torch.int64)
         slot = self._async_slot()
-        spf, spl, ent = self._tail_tables()
+        spf, spl = self._tail_tables()
         self._ph("merge_emit", True)
         nat.call("mmj_merge_emit", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
                  nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp, nat.ptr(ds.rev_ptr),
-                 nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, ent, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(slot),
+                 nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(slot),
                  nat.ptr(ws), wsb, st)
         self._ph("merge_emit", False)
         self.stats.chunks += 1
@@ -488,191 +439,6 @@ class TwoPathEngine:
         light = int(self.wit.item()) - wit0
         self.stats.out_size += total
         return ChunkResult(x0, x1, total, codes[:total], None, light)
-
-    def run_mma_ahead(self, x_begin: int = 0, x_end: Optional[int] = None, timer=None):
-        """Projection with the heavy product of chunk i+1 running on a
-        high-priority side stream while chunk i's fused tail (mmj_merge_emit)
-        runs on a low-priority one.  The product uses the co-resident build
-        (MMJ_MODE_COLOC: <= 85 registers, 2-stage ring) when the operand is in
-        z-pair form, so each SM hosts one product CTA beside two tail CTAs:
-        the TMEM-read-bound product overlaps the HBM-write-bound emission.
-        Chunk bitmaps are double-buffered; codes go to one reused buffer
-        (streaming consumer).  Without the fused tail (MMJ_FUSED_EMIT=0) the
-        three-kernel tail is used."""
-        if not self.fused:
-            raise ValueError("run_mma_ahead needs the bitmap (no counts) path")
-        torch = self.torch
-        self.prepare()
-        dr, ds = self.dr, self.ds
-        caller = torch.cuda.current_stream()
-        if getattr(self, "_mma_stream", None) is None:
-            lo, hi = _stream_pair("mma_ahead")
-            self._mma_stream, self._main_stream = hi, lo
-        ms = self._mma_stream
-        main = self._main_stream
-        main.wait_stream(caller)
-        ms.wait_stream(caller)
-        hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
-        lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
-        lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
-        mst, sst = main.cuda_stream, ms.cuda_stream
-        rows_max = self.chunk_rows
-        codes = self.ws.get("codes", rows_max * self.dom_z, torch.int64)
-        bounds = list(self.chunk_bounds(x_begin, x_end))
-        bufs = [self.ws.get(f"bm{b}", rows_max * self.wpr, torch.int32) for b in (0, 1)]
-        freed = [None, None]
-        mma_done = {}
-        coloc = self.pairs and not self.triple and __import__("os").environ.get("MMJ_COLOC", "1") != "0"
-        mode = self._bitmap_mode() | (nat.MODE_COLOC if coloc else 0)
-        spf, spl, ent = self._tail_tables() if self.one_kernel_tail else (0, 0, 0)
-        wsb = int(self.lib.mmj_merge_emit_workspace_size(rows_max, self.wpr))
-        fws = self.ws.get("fuse_ws", wsb, torch.uint8)
-
-        def issue_mma(i):
-            x0, x1 = bounds[i]
-            b = i & 1
-            if freed[b] is not None:
-                ms.wait_event(freed[b])
-            if timer is not None:
-                timer.start("heavy_mma", ms)
-            if self.A is not None:
-                nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
-                         self.mma_kpad, 0, self.mma_kpad, x0, x1 - x0, mode, 0, nat.ptr(bufs[b]), self.wpr,
-                         nat.ptr(self.nnz), self.mma_ctas, sst)
-            if timer is not None:
-                timer.stop("heavy_mma", ms)
-            ev = torch.cuda.Event()
-            ev.record(ms)
-            mma_done[i] = ev
-
-        if bounds:
-            issue_mma(0)
-        for i, (x0, x1) in enumerate(bounds):
-            if i + 1 < len(bounds):
-                issue_mma(i + 1)
-            b = i & 1
-            rows = x1 - x0
-            buf = bufs[b]
-            main.wait_event(mma_done.pop(i))
-            with torch.cuda.stream(main):
-                slot = self._async_slot()
-            if self.one_kernel_tail:
-                if timer is not None:
-                    timer.start("merge_emit", main)
-                nat.call("mmj_merge_emit", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
-                         nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp,
-                         nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, ent, nat.ptr(self.wit),
-                         nat.ptr(codes), nat.ptr(slot), nat.ptr(fws), wsb, mst)
-                if timer is not None:
-                    timer.stop("merge_emit", main)
-            else:
-                nseg = rows * self.wpr // 32
-                segcnt = self.ws.get("segcnt", rows_max * self.wpr // 32, torch.int32)
-                segoff = self.ws.get("segoff", rows_max * self.wpr // 32 + 1, torch.int64)
-                if timer is not None:
-                    timer.start("light_merge", main)
-                nat.call("mmj_tile_merge", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
-                         nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp,
-                         nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(self.wit), mst)
-                if timer is not None:
-                    timer.stop("light_merge", main)
-                    timer.start("segments", main)
-                nat.call("mmj_exclusive_scan_i32", nat.ptr(segcnt), nat.ptr(segoff), nseg,
-                         nat.ptr(self.ws.scan_ws(rows_max * self.wpr // 32)), mst)
-                if timer is not None:
-                    timer.stop("segments", main)
-                    timer.start("emit", main)
-                nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dom_z,
-                         nat.ptr(codes), mst)
-                if timer is not None:
-                    timer.stop("emit", main)
-                with torch.cuda.stream(main):
-                    slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(main)
-            freed[b] = ev
-            self.stats.chunks += 1
-        caller.wait_stream(ms)
-        caller.wait_stream(main)
-        return codes
-
-    def run_pipelined(self, x_begin: int = 0, x_end: Optional[int] = None, timer=None):
-        """Projection over [x_begin, x_end) with two streams: chunk i's
-        emission (HBM-write bound) runs on a side stream while chunk i+1's
-        heavy product + light merge + scan (SM bound) run on the current
-        stream.  Chunk bitmaps / segment offsets are double-buffered; codes
-        land in one device buffer (a streaming consumer).  No host sync
-        until :meth:`finish`."""
-        if not self.fused:
-            raise ValueError("run_pipelined needs the bitmap (no counts) path")
-        torch = self.torch
-        self.prepare()
-        dr, ds = self.dr, self.ds
-        caller = torch.cuda.current_stream()
-        if getattr(self, "_emit_stream", None) is None:
-            # emission (HBM-bound, floods the SMs with short CTAs) on a
-            # low-priority stream; the heavy product / merge / scan chain of
-            # the next chunk on a high-priority one, so its CTAs are placed
-            # first whenever emission CTAs retire
-            self._emit_stream, self._work_stream = _stream_pair("pipelined")
-        es = self._emit_stream
-        main = self._work_stream
-        main.wait_stream(caller)
-        es.wait_stream(caller)
-        freed = [None, None]
-        hp = nat.ptr(self.hpos) if self.strategy == PARTITIONED else 0
-        lzp = nat.ptr(self.lz_ptr) if self.lz_ptr is not None else 0
-        lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
-        mst, est = main.cuda_stream, es.cuda_stream
-        rows_max = self.chunk_rows
-        codes = self.ws.get("codes", rows_max * self.dom_z, torch.int64)
-        for i, (x0, x1) in enumerate(self.chunk_bounds(x_begin, x_end)):
-            b = i & 1
-            rows = x1 - x0
-            nseg = rows * self.wpr // 32
-            buf = self.ws.get(f"bm{b}", rows_max * self.wpr, torch.int32)
-            segcnt = self.ws.get(f"segcnt{b}", rows_max * self.wpr // 32, torch.int32)
-            segoff = self.ws.get(f"segoff{b}", rows_max * self.wpr // 32 + 1, torch.int64)
-            if freed[b] is not None:
-                main.wait_event(freed[b])
-            if timer is not None:
-                timer.start("heavy_mma", main)
-            if self.A is not None:
-                nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
-                         self.mma_kpad, 0, self.mma_kpad, x0, rows, self._bitmap_mode(), 0, nat.ptr(buf), self.wpr,
-                         nat.ptr(self.nnz), 0, mst)
-            if timer is not None:
-                timer.stop("heavy_mma", main)
-                timer.start("light_merge", main)
-            nat.call("mmj_tile_merge", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
-                     nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp,
-                     nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(self.wit), mst)
-            if timer is not None:
-                timer.stop("light_merge", main)
-                timer.start("segments", main)
-            nat.call("mmj_exclusive_scan_i32", nat.ptr(segcnt), nat.ptr(segoff), nseg,
-                     nat.ptr(self.ws.scan_ws(rows_max * self.wpr // 32)), mst)
-            if timer is not None:
-                timer.stop("segments", main)
-            ready = torch.cuda.Event()
-            ready.record(main)
-            es.wait_event(ready)
-            if timer is not None:
-                timer.start("emit", es)
-            nat.call("mmj_emit_codes", nat.ptr(buf), nat.ptr(segoff), rows, self.wpr, x0, self.dom_z,
-                     nat.ptr(codes), est)
-            if timer is not None:
-                timer.stop("emit", es)
-            with torch.cuda.stream(es):
-                slot = self._async_slot()
-                slot[0:1].copy_(segoff[nseg:nseg + 1], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(es)
-            freed[b] = ev
-            self.stats.chunks += 1
-        caller.wait_stream(main)
-        caller.wait_stream(es)
-        return codes
 
     def _async_slot(self):
         """Device slot (2 x int64) receiving one async chunk's (size, light)."""

@@ -214,6 +214,8 @@ class DeviceIndexedRelation:
         self._mmj_device_cache = {torch.cuda.current_device(): dr}
         self.left_deg = ldeg.cpu().numpy().astype(np.int64)
         self.right_deg = rdeg.cpu().numpy().astype(np.int64)
+        self.left_deg.flags.writeable = False
+        self.right_deg.flags.writeable = False
         self.rel = _DeviceRel(self, name, n, left_values_dev.cpu().numpy(), right_values_host, right_ids)
         self._host = {}
 

@@ -207,11 +207,8 @@ def optimize_thresholds(stats_r, stats_s, dom_x: int, out_join: int, consts: Cos
 # ---------------------------------------------------------------------------
 # Light witnesses cost one L2 atomic each; the heavy product costs 2*U*W ops
 # per heavy y on the int8 tensor cores, and the bitmap it writes is the same
-# for every plan.  Rates are per-B200 planning constants (measured orders of
-# magnitude, refined by bench runs), not correctness parameters.
-LIGHT_WITNESS_RATE = 2.0e11        # light witnesses / s (bitmap atomicOr, L2 resident)
-LIGHT_COUNT_RATE = 2.0e10          # light witnesses / s (int32 count atomics over a chunk larger than L2)
-MMA_OPS_RATE = 2.0e15              # int8 ops / s sustained (K is padded to 128)
+# for every plan.  The per-B200 constants live in GpuCosts (measured by
+# measure_gpu_costs); they are planning inputs, not correctness parameters.
 K_BLOCK = 128
 
 

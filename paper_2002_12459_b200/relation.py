@@ -306,6 +306,10 @@ class IndexedRelation:
         self.rev_indptr, self.rev_indices = _csr(b, a, rel.dom_right)
         self.left_deg = np.diff(self.fwd_indptr)
         self.right_deg = np.diff(self.rev_indptr)
+        # immutable like the reference's index (engines remember their maxima)
+        for arr in (self.fwd_indptr, self.fwd_indices, self.rev_indptr, self.rev_indices, self.left_deg,
+                    self.right_deg):
+            arr.flags.writeable = False
 
     def fwd(self, a: int) -> np.ndarray:
         return self.fwd_indices[self.fwd_indptr[a]:self.fwd_indptr[a + 1]]

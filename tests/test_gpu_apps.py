@@ -157,6 +157,35 @@ def test_bsi_string_ids_and_heavy_bits(oracle):
             assert g == bool(radj[a] & sadj[b])
 
 
+def test_bsi_float_values_and_mixed_query_ids():
+    """Raw values keep Python equality (apps.py:321-350): float y-values
+    never collapse onto their integer part (R y 1.5 / 2.5 vs S y 1.7 share
+    nothing), an integer-valued y equal to a float one (2 == 2.0) still
+    matches, and query ids 5.0 / True resolve like dict.get while 5.5 and
+    '5' are unknown (None)."""
+    from paper_2002_12459_b200.apps import bsi_answer_batch
+    from paper_2002_12459_b200.relation import Relation, build_indexed
+    rng = np.random.default_rng(45)
+    rp = [(int(a), float(y) + 0.5) for a, y in random_pairs(rng, 300, 40, 25)] + [(1, 1.5), (5, 2.0)]
+    sp = [(int(b), float(y) + 0.7) for b, y in random_pairs(rng, 300, 40, 25)] + [(3, 1.7), (6, 2)]
+    r = build_indexed(Relation.from_raw_pairs("R", rp))
+    s = build_indexed(Relation.from_raw_pairs("S", sp))
+    batch = [(int(a), int(b)) for a, b in rng.integers(0, 45, (200, 2))]
+    batch += [(1, 3), (5, 6), (5.0, 6), (True, 3), (5.5, 6), ("5", 6), (5, 6.0)]
+    got = bsi_answer_batch(r, s, batch)
+    radj, sadj = {}, {}
+    for a, y in rp:
+        radj.setdefault(a, set()).add(y)
+    for b, y in sp:
+        sadj.setdefault(b, set()).add(y)
+    for (a, b), g in zip(batch, got):
+        if radj.get(a) is None or sadj.get(b) is None:
+            assert g is None, (a, b)
+        else:
+            assert g == bool(radj[a] & sadj[b]), (a, b)
+    assert got[-7:-4] == [False, True, True] and got[-3:-1] == [None, None]
+
+
 @pytest.mark.parametrize("heavy_bits", [128, 512])
 def test_bsi_zipf_vs_oracle(oracle, heavy_bits):
     from paper_2002_12459_b200.apps import bsi_answer_batch_arrays

@@ -28,13 +28,10 @@ def _wide(seed, nx, nr, nz, ns, dom_y, s_exp):
     return r_pairs, s_zy
 
 
-@pytest.mark.parametrize("triple,entries", [("0", "0"), ("1", "0"), ("0", "1")])
 @pytest.mark.parametrize("plan", [("partitioned", 40, 1), ("partitioned", 8, 3), ("fulljoin", 0, 0)])
-def test_wide_rows_match_oracle(oracle, plan, triple, entries, monkeypatch):
+def test_wide_rows_match_oracle(oracle, plan):
     from paper_2002_12459_b200.joinproject import two_path_join
     from paper_2002_12459_b200.optimizer import ThresholdPlan
-    monkeypatch.setenv("MMJ_TRIPLE", triple)   # z-pair (default) and z-triple heavy operands
-    monkeypatch.setenv("MMJ_TUPLE_ENTRIES", entries)   # per-tuple list ranges precomputed (opt-in)
     r_pairs, s_pairs = _wide(71, 32, 4_000, 3_000_000, 1_000_000, 3000, 1.1)
     r, s = _rels(r_pairs, s_pairs)
     assert s.rel.dom_left > 3 * 8192 * 32     # four column blocks per row (dom_z ~ 790k)
@@ -82,44 +79,3 @@ def test_fused_equals_three_kernel_path_on_cfg2_chunks():
         assert three.n == n > 0
         assert torch.equal(fused_codes, three.codes)
         assert w1 - w0 == w2 - w1 == three.light
-
-
-@pytest.mark.parametrize("coloc", ["1", "0"])
-def test_mma_ahead_schedule_equals_serial(coloc, monkeypatch):
-    """The two-stream schedule (heavy product of chunk i+1 beside chunk i's
-    fused tail, co-resident MMA build) produces the serial schedule's chunk
-    sizes, statistics and codes."""
-    import torch
-
-    from paper_2002_12459_b200 import datagen
-    from paper_2002_12459_b200.device import device_relation
-    from paper_2002_12459_b200.engine import TwoPathEngine
-    from paper_2002_12459_b200.optimizer import gpu_plan
-    monkeypatch.setenv("MMJ_COLOC", coloc)
-    wl = datagen.config("cfg2")
-    r, s = _rels(wl.relations[0], wl.relations[1])
-    plan = gpu_plan(r, s)
-    dr, ds = device_relation(r), device_relation(s)
-
-    def engine():
-        return TwoPathEngine(dr, ds, plan.strategy, plan.delta1, plan.delta2, False, chunk_rows=2048,
-                             host_left_deg_r=r.left_deg, host_left_deg_s=s.left_deg)
-    lo, hi = 100_000, 100_000 + 3 * 2048 - 5
-    ser = engine()
-    ser.prepare()
-    sizes, last = [], None
-    for x0, x1 in ser.chunk_bounds(lo, hi):
-        ch = ser.run_chunk(x0, x1, sync=False, codes_key="ser")
-        n = int(ch.total_dev.item())
-        sizes.append(n)
-        last = ch.codes[:n].clone()
-    st_ser = ser.finish()
-    eng = engine()
-    codes = eng.run_mma_ahead(lo, hi)
-    torch.cuda.synchronize()
-    per_chunk = [int(v) for v in eng._sizes_dev[: eng._n_async, 0].tolist()]
-    st = eng.finish()
-    assert per_chunk == sizes and len(sizes) == 3
-    assert st.out_size == st_ser.out_size == sum(sizes)
-    assert st.heavy_pairs == st_ser.heavy_pairs and st.light_intermediate == st_ser.light_intermediate
-    assert torch.equal(codes[: sizes[-1]], last)

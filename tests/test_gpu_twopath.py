@@ -180,34 +180,6 @@ def test_pair_operand_count_boundary(pkg, oracle, deg_x0):
     assert np.array_equal(got[0], exp.codes)
 
 
-@pytest.mark.parametrize("deg_x0", [126, 127, 128])
-def test_triple_operand_count_boundary(pkg, oracle, deg_x0, monkeypatch):
-    """BITMAP_TRIPLE packs three cells as c0 + 128*c1 + 16384*c2: with z 1..95
-    reaching every heavy y of x0, every field of 32 accumulators holds the
-    count deg_x0 (127 -> the accumulator's maximum 2^21 - 1, no carry between
-    fields); at 128 the packed forms switch off."""
-    from paper_2002_12459_b200.joinproject import _collect, _engine
-    from paper_2002_12459_b200.optimizer import ThresholdPlan
-    monkeypatch.setenv("MMJ_TRIPLE", "1")      # opt-in operand form
-    rng = np.random.default_rng(1000 + deg_x0)
-    n_y = 300
-    rp = [(0, y) for y in range(deg_x0)]
-    sp = [(0, y) for y in range(n_y)] + [(z, y) for z in range(1, 96) for y in range(deg_x0)]
-    for y in range(n_y):
-        rp += [(1 + int(rng.integers(0, 400)), y), (401 + y, y)]
-        sp += [(96 + int(rng.integers(0, 400)), y), (500 + y, y)]
-    rp, sp = sorted(set(rp)), sorted(set(sp))
-    r, s = _mine(pkg, rp, sp)
-    eng = _engine(r, s, ThresholdPlan("partitioned", 1, 1), False)
-    eng.prepare()
-    assert eng.triple == eng.pairs == (deg_x0 <= 127)
-    got = _collect(eng)
-    R, S = _oracle_rels(oracle, rp, sp)
-    exp = oracle.two_path(R, S, oracle.OPlan("partitioned", 1, 1))
-    assert np.array_equal(got[0], exp.codes)
-    assert got[2].heavy_pairs == exp.stats["heavy_pairs"]
-
-
 @pytest.mark.parametrize("case", ["disjoint_y", "single_pair", "one_hub_y", "one_x_row", "skinny_z"])
 def test_two_path_edge_cases(pkg, oracle, case):
     """Empty semi-join result, a single output pair, one y shared by every

@@ -183,14 +183,14 @@ def test_capi_argument_errors_without_gpu():
     lib = _native.load()
     # a pitch that is not a multiple of 32 words
     rc = lib.mmj_merge_emit(None, 0, 0, 4, 33, 1000, None, None, None, 1, None, None, None, None, None, None, None,
-                            None, None, None, None, None, 0, None)
+                            None, None, None, None, 0, None)
     assert rc == 1 and b"multiple of 32" in lib.mmj_last_error()
     # a workspace smaller than mmj_merge_emit_workspace_size
     rc = lib.mmj_merge_emit(None, 0, 0, 4, 32, 1000, None, None, None, 1, None, None, None, None, None, None, None,
-                            None, None, None, None, ctypes.c_void_p(16), 8, None)
+                            None, None, None, ctypes.c_void_p(16), 8, None)
     assert rc == 5 and b"workspace" in lib.mmj_last_error()
     # heavy product modes outside the enum
-    rc = lib.mmj_heavy_mma(None, 256, None, 256, 128, 0, 128, 0, 128, 7, 0, None, 8, None, 0, None)
+    rc = lib.mmj_heavy_mma(None, 256, None, 256, 128, 0, 128, 0, 128, 6, 0, None, 8, None, 0, None)
     assert rc == 1 and b"unknown mode" in lib.mmj_last_error()
 
 

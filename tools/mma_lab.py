@@ -1,5 +1,5 @@
 """Heavy-product kernel in isolation (cfg2-like shapes): time per launch for
-the bitmap / count epilogues, optionally with MMJ_DEBUG_EPI=1 (no packing).
+the bitmap / count epilogues.
 
     python tools/mma_lab.py [rows] [ncols] [kpad]
 """
@@ -55,7 +55,7 @@ def main():
             cells = rows * ncols
             tiles = (rows // 128) * (ncols // 256)   # per 32K output cells
             clk = 1.965e9
-            print(f"{name} debug={os.environ.get('MMJ_DEBUG_EPI', '0')} rows={rows} ncols={ncols} k={kpad}: "
+            print(f"{name} rows={rows} ncols={ncols} k={kpad}: "
                   f"{ms:.3f} ms  {cells / ms / 1e9:.2f} Tcell/s  {ms * 1e-3 * clk * 148 / tiles:.0f} clk/tile/SM  "
                   f"{2 * cells * kpad / ms / 1e9:.0f} TOPS  out {rows * wpr * 4 / ms / 1e6:.0f} GB/s")
 
