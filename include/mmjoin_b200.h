@@ -86,6 +86,14 @@ int mmj_build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n,
                             int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
                             int64_t kpad, void* stream);
 
+/* Heavy-y bit rows of S_h (k x wpr uint32, zeroed first): bit z of row
+ * hpos[cols[t]] for every tuple t = (z = rows[t], y = cols[t]) with
+ * left_deg[z] > delta2 and heavy y; M2 of joinproject.py:119-143 at one bit
+ * per cell, the operand of mmj_merge_emit / mmj_tile_merge has_heavy == 2. */
+int mmj_build_heavy_rows(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
+                         int64_t delta2, const int32_t* hpos, uint32_t* heavy_rows, int64_t k, int64_t wpr,
+                         void* stream);
+
 /* ---- light-z CSR of S for pass 3: joinproject.py:195-203 --------------------
  * lz_ptr[dom_y+1]/lz_idx: S.rev(y) restricted to z with deg_S(z) <= delta2.
  * flag_ws: n bytes; pos_ws: n+1 int32. */
@@ -136,8 +144,12 @@ int mmj_digit_plane(const int64_t* src, int64_t rows, int64_t cols, int transpos
  *      counts): joinproject.py:183-203 + 220-225 ------------------------------
  * Chunk bitmap [x0, x0+rows) x [0, dom_z): rows x wpr words, wpr a multiple
  * of 32 (rows start on 1024-cell segments).  mmj_tile_merge runs one CTA per
- * tile (mmj_tile_count(rows, wpr) tiles of <= 65536 cells): the heavy bits
- * (has_heavy) or zeros are staged in shared memory, every light witness of
+ * tile (mmj_tile_count(rows, wpr) tiles of <= 65536 cells): the heavy part
+ * is staged in shared memory -- has_heavy 0: zeros; 1: the chunk's heavy
+ * bitmap already in `bitmap` (the tcgen05 product's output); 2: computed by
+ * the tile from the heavy-y bit rows `heavy_rows` (mmj_build_heavy_rows) as
+ * OR over the heavy y of each heavy row x, popcount added to *heavy_pairs
+ * -- then every light witness of
  * the tile is OR-ed in (shared-memory atomics), the merged tile is written
  * back and segcnt[rows*wpr/32] receives each 32-word segment's popcount;
  * *witnesses accumulates the light intermediate size.  After an exclusive
@@ -147,7 +159,8 @@ int64_t mmj_tile_count(int64_t rows, int64_t wpr);
 int mmj_tile_merge(uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
                    const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
-                   const int32_t* lz_idx, int32_t* segcnt, unsigned long long* witnesses, void* stream);
+                   const int32_t* lz_idx, const uint32_t* heavy_rows, unsigned long long* heavy_pairs, int32_t* segcnt,
+                   unsigned long long* witnesses, void* stream);
 int mmj_emit_codes(const uint32_t* bitmap, const int64_t* seg_off, int64_t rows, int64_t wpr, int64_t x0,
                    int64_t dom_z, int64_t* codes, void* stream);
 /* The same three steps fused into one kernel (no merged-bitmap write-back,
@@ -158,14 +171,16 @@ int mmj_emit_codes(const uint32_t* bitmap, const int64_t* seg_off, int64_t rows,
  * ws: caller-owned workspace of mmj_merge_emit_workspace_size(rows, wpr)
  * bytes (reset by the call, on `stream`).  fwd_ptr == NULL: no light merge
  * (the bitmap is complete; e.g. the star path, whose light part is OR-ed in
- * by mmj_star_light): segment scan + look-back + emission only. */
+ * by mmj_star_light): segment scan + look-back + emission only.
+ * has_heavy as for mmj_tile_merge; with has_heavy == 2 `bitmap` is the
+ * heavy-y bit rows (k x wpr) and no chunk bitmap exists in HBM at all. */
 size_t mmj_merge_emit_workspace_size(int64_t rows, int64_t wpr);
 int mmj_merge_emit(const uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
                    const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
                    const int32_t* lz_idx, const int32_t* split_full, const int32_t* split_lz,
-                   unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws, size_t ws_bytes,
-                   void* stream);
+                   unsigned long long* witnesses, unsigned long long* heavy_pairs, int64_t* codes, int64_t* total,
+                   void* ws, size_t ws_bytes, void* stream);
 /* Column blocks per row of the fused kernel's tiles, and the optional list
  * split table it reads instead of bisecting every long list per tile:
  * split[y*(ncb+1)+j] = position in idx of list y's first entry >= the j-th
@@ -222,36 +237,33 @@ int mmj_star_light(int k, const int64_t* dims, const int32_t* const* rev_ptr, co
                    int64_t ld, unsigned long long* witnesses, void* ws, void* stream);
 
 /* ---- batched boolean set intersection: apps.py:314-351 ----------------------
- * Heavy y (hpos >= 0, from mmj_heavy_y_positions) -> per-left-id bitsets of
- * `words` uint32 (multiple of 4); the remaining (light) y of every left id's
- * forward list -> compacted sorted light lists.  mmj_bsi_answer resolves raw
- * query ids through each relation's sorted raw left values (r_sorted/r_order;
- * NULL = queries are dense ids already) and writes ans[q] = 1 (intersect),
- * 0 (disjoint) or -1 (id unknown to the unreduced relation = None). */
+ * Heavy y (hpos >= 0, from mmj_heavy_y_positions) -> one record per left id
+ * (mmj_bsi_records, one pass over the forward CSR): `words` bitset words
+ * (4, 8, 16 or 32) with bit hpos[y] for each heavy y, then the base and the
+ * length of the id's light list, whose y are compacted in place into ovf at
+ * the id's own CSR offset (ovf: n int32); rec holds dom_left records of
+ * mmj_bsi_record_words(words) uint32 (64-byte multiples).  mmj_bsi_answer
+ * resolves raw query ids per side through a direct-address table (table !=
+ * NULL), else the sorted raw left values (sorted/order; both NULL = queries
+ * are dense ids already), and writes ans[q] = 1 (intersect), 0 (disjoint)
+ * or -1 (id unknown to the unreduced relation = None). */
 /* histogram of max(rdeg[y], sdeg[y]) > 0: 64 log2 bins (log2mode) or nbins
  * (<= 1024) linear bins over [lo, hi); picks the heavy-y threshold on the device */
 int mmj_bsi_degree_histogram(const int32_t* rdeg, const int32_t* sdeg, int64_t dom_y, int64_t lo, int64_t hi,
                              int nbins, int log2mode, int32_t* hist, void* stream);
-int mmj_bsi_bits(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* hpos, int words, uint32_t* bits,
-                 int64_t dom_left, void* stream);
-int mmj_bsi_light_lists(const int32_t* fwd_ptr, const int32_t* fwd_idx, int64_t n, int64_t dom_left,
-                        const int32_t* hpos, uint8_t* flag_ws, int32_t* pos_ws, int32_t* lptr, int32_t* lidx,
-                        void* ws, void* stream);
+int mmj_bsi_record_words(int words);
+int mmj_bsi_records(const int32_t* fwd_ptr, const int32_t* fwd_idx, int64_t dom_left, const int32_t* hpos, int words,
+                    uint32_t* rec, int32_t* ovf, void* stream);
 int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted, const int32_t* r_order,
-                   int64_t r_n, const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const uint32_t* r_bits,
-                   const uint32_t* s_bits, int words, const int32_t* r_lptr, const int32_t* r_lidx,
-                   const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, void* stream);
+                   int64_t r_n, const int32_t* r_table, int64_t r_min, int64_t r_range, const int64_t* s_sorted,
+                   const int32_t* s_order, int64_t s_n, const int32_t* s_table, int64_t s_min, int64_t s_range,
+                   const uint32_t* r_rec, const int32_t* r_ovf, const uint32_t* s_rec, const int32_t* s_ovf,
+                   int words, int8_t* ans, void* stream);
 /* direct-address id map for dense raw id ranges: table[range] = dense id of
- * raw value vmin + i, -1 where absent (replaces the per-query binary search of
- * mmj_bsi_answer by one load; range = max - min + 1 < 2^31) */
+ * raw value vmin + i, -1 where absent (one load per query instead of a
+ * binary search; range = max - min + 1 < 2^31) */
 int mmj_bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
                          int32_t* table, void* stream);
-/* mmj_bsi_answer with both query sides resolved through direct tables */
-int mmj_bsi_answer_tables(const int64_t* qa, const int64_t* qb, int64_t nq, const int32_t* r_table, int64_t r_min,
-                          int64_t r_range, const int32_t* s_table, int64_t s_min, int64_t s_range,
-                          const uint32_t* r_bits, const uint32_t* s_bits, int words, const int32_t* r_lptr,
-                          const int32_t* r_lidx, const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans,
-                          void* stream);
 
 
 /* ---- device ingest: relation.py:37-69, 119-140, 148-186 ----

@@ -69,19 +69,19 @@ _SIGS = {
     "mmj_heavy_mma": (INT, [P, I64, P, I64, I64, I64, I64, I64, I64, INT, INT, P, I64, P, INT, P]),
     "mmj_digit_plane": (INT, [P, I64, I64, INT, INT, P, I64, P]),
     "mmj_tile_count": (I64, [I64, I64]),
-    "mmj_tile_merge": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P]),
+    "mmj_tile_merge": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, P, P]),
     "mmj_emit_codes": (INT, [P, P, I64, I64, I64, I64, P, P]),
     "mmj_merge_emit_workspace_size": (SZ, [I64, I64]),
-    "mmj_merge_emit": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "mmj_merge_emit": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "mmj_build_heavy_rows": (INT, [P, P, I64, P, I64, P, P, I64, I64, P]),
     "mmj_merge_emit_col_blocks": (INT, [I64]),
     "mmj_debug_timing_buffer": (None, [P]),
     "mmj_list_splits": (INT, [P, P, I64, I64, P, P]),
     "mmj_bsi_degree_histogram": (INT, [P, P, I64, I64, I64, INT, INT, P, P]),
-    "mmj_bsi_bits": (INT, [P, P, I64, P, INT, P, I64, P]),
-    "mmj_bsi_light_lists": (INT, [P, P, I64, I64, P, P, P, P, P, P, P]),
-    "mmj_bsi_answer": (INT, [P, P, I64, P, P, I64, P, P, I64, P, P, INT, P, P, P, P, P, P]),
+    "mmj_bsi_record_words": (INT, [INT]),
+    "mmj_bsi_records": (INT, [P, P, I64, P, INT, P, P, P]),
+    "mmj_bsi_answer": (INT, [P, P, I64, P, P, I64, P, I64, I64, P, P, I64, P, I64, I64, P, P, P, P, INT, P, P]),
     "mmj_bsi_direct_table": (INT, [P, P, I64, I64, I64, P, P]),
-    "mmj_bsi_answer_tables": (INT, [P, P, I64, P, I64, I64, P, I64, I64, P, P, INT, P, P, P, P, P, P]),
     "mmj_star_split": (INT, [INT, P, I64, C.c_double, P, P, P, P, P, P, P, P]),
     "mmj_star_operand": (INT, [INT, P, P, I64, I64, I64, P, P]),
     "mmj_star_light_workspace_bytes": (SZ, [I64]),

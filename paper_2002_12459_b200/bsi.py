@@ -44,6 +44,38 @@ class BsiSide:
     sorted_vals: object       # device int64 sorted raw left values (or None)
     order: object             # device int32 dense id of each sorted value
     h2d_bytes: int = 0
+    table: object = None      # (direct-address id table, vmin, range) or None
+
+
+def _attach_table(sd: BsiSide, ends) -> None:
+    """Direct-address raw id -> dense id table when the side's raw ids fill
+    at most DIRECT_SPREAD x their count of a value range: each query id then
+    resolves with one load instead of a binary search (cfg5: 4M ids in
+    [0, 4M), a 16 MB table).  Part of the device form of the relation's
+    left_ids dictionary, so it is built once with the sides."""
+    if sd.sorted_vals is None or sd.dom_left == 0:
+        return
+    torch = _torch()
+    lo, hi = next(ends), next(ends)
+    vmin, rng = int(lo), int(hi) - int(lo) + 1
+    if rng > DIRECT_SPREAD * sd.dom_left or rng >= (1 << 31) - 1:
+        return
+    table = torch.empty(rng, dtype=torch.int32, device="cuda")
+    nat.call("mmj_bsi_direct_table", nat.ptr(sd.sorted_vals), nat.ptr(sd.order), sd.dom_left, vmin, rng,
+             nat.ptr(table), nat.stream_handle())
+    sd.table = (table, vmin, rng)
+
+
+def _with_tables(sides):
+    """Attach the direct id tables of both sides (one device -> host copy of
+    their smallest / largest raw ids)."""
+    torch = _torch()
+    sR, sS, _ = sides
+    have = [sd for sd in (sR, sS) if sd.sorted_vals is not None and sd.dom_left > 0]
+    ends = iter(torch.cat([sd.sorted_vals[[0, sd.dom_left - 1]] for sd in have]).cpu().tolist()) if have else iter(())
+    for sd in have:
+        _attach_table(sd, ends)
+    return sides
 
 
 def _int_values(vals):
@@ -142,7 +174,7 @@ def prepare(r, s, pinned=False):
     from .ingest import DeviceIndexedRelation
     if (isinstance(r, DeviceIndexedRelation) and isinstance(s, DeviceIndexedRelation) and not pinned
             and r._right_values_dev is not None and s._right_values_dev is not None):
-        sides = _prepare_device(r, s)
+        sides = _with_tables(_prepare_device(r, s))
         r._mmj_bsi_cache = (key, sides)
         return sides
     if r.rel.right_values is s.rel.right_values:
@@ -164,6 +196,7 @@ def prepare(r, s, pinned=False):
             smap = np.array([allv[v] for v in sv], dtype=np.int64)
         dom_y = len(allv)
         sides = (_side(r, rmap, dom_y, pinned), _side(s, smap, dom_y, pinned), dom_y)
+    sides = _with_tables(sides)
     if not pinned:
         try:
             r._mmj_bsi_cache = (key, sides)
@@ -183,6 +216,9 @@ class BsiEngine:
 
     def __init__(self, sR: BsiSide, sS: BsiSide, dom_y: int, heavy_bits: int = 256, ws=None):
         self.sR, self.sS, self.dom_y = sR, sS, dom_y
+        self.lib = nat.load()
+        if heavy_bits not in (128, 256, 512, 1024):
+            raise ValueError("heavy_bits must be 128, 256, 512 or 1024")
         self.heavy_bits = max(BITS_BLOCK, -(-heavy_bits // BITS_BLOCK) * BITS_BLOCK)
         self.ws = ws or Workspace()
         self.rdeg, self.sdeg = sR.ydeg, sS.ydeg
@@ -217,6 +253,8 @@ class BsiEngine:
         return max(1, t)
 
     def build(self):
+        """Heavy-y split, then one record per left id on each side (heavy-y
+        bit row + light list header; light lists compacted in place)."""
         torch = _torch()
         st = nat.stream_handle()
         dom_y = self.dom_y
@@ -226,62 +264,30 @@ class BsiEngine:
         nat.call("mmj_heavy_y_positions", nat.ptr(self.rdeg), nat.ptr(self.sdeg), dom_y, self.delta1,
                  nat.ptr(flag), nat.ptr(scan), nat.ptr(self.hpos), nat.ptr(self.ws.scan_ws(dom_y)), st)
         self.words = self.heavy_bits // 32
+        stride = int(self.lib.mmj_bsi_record_words(self.words))
         self.sides = []
         for tag, sd in (("r", self.sR), ("s", self.sS)):
-            bits = self.ws.get(f"bits_{tag}", max(sd.dom_left, 1) * self.words, torch.int32)
-            nat.call("mmj_bsi_bits", nat.ptr(sd.fwd_row), nat.ptr(sd.fwd_idx), sd.n, nat.ptr(self.hpos),
-                     self.words, nat.ptr(bits), sd.dom_left, st)
-            lflag = self.ws.get(f"lflag_{tag}", sd.n, torch.uint8)
-            lpos = self.ws.get(f"lpos_{tag}", sd.n + 1, torch.int32)
-            lptr = self.ws.get(f"lptr_{tag}", sd.dom_left + 1, torch.int32)
-            lidx = self.ws.get(f"lidx_{tag}", max(sd.n, 1), torch.int32)
-            nat.call("mmj_bsi_light_lists", nat.ptr(sd.fwd_ptr), nat.ptr(sd.fwd_idx), sd.n, sd.dom_left,
-                     nat.ptr(self.hpos), nat.ptr(lflag), nat.ptr(lpos), nat.ptr(lptr), nat.ptr(lidx),
-                     nat.ptr(self.ws.scan_ws(sd.n)), st)
-            self.sides.append((bits, lptr, lidx))
-        sides = (("r", self.sR), ("s", self.sS))
-        # both sides' smallest / largest raw ids in one device -> host copy
-        ends = [sd.sorted_vals[[0, sd.dom_left - 1]] for _, sd in sides
-                if sd.sorted_vals is not None and sd.dom_left > 0]
-        ends = iter(torch.cat(ends).cpu().tolist()) if ends else iter(())
-        self.tables = [self._direct_table(tag, sd, ends) for tag, sd in sides]
-
-    def _direct_table(self, tag, sd: BsiSide, ends):
-        """(table, vmin, range) when the side's raw ids fill at most
-        DIRECT_SPREAD x their count of a value range: each query id then
-        resolves with one load instead of a binary search (cfg5: 4M ids in
-        [0, 4M), a 16 MB table that stays in L2)."""
-        if sd.sorted_vals is None or sd.dom_left == 0:
-            return None
-        torch = _torch()
-        lo, hi = next(ends), next(ends)
-        vmin, rng = int(lo), int(hi) - int(lo) + 1
-        if rng > DIRECT_SPREAD * sd.dom_left or rng >= (1 << 31) - 1:
-            return None
-        table = self.ws.get(f"direct_{tag}", rng, torch.int32)
-        nat.call("mmj_bsi_direct_table", nat.ptr(sd.sorted_vals), nat.ptr(sd.order), sd.dom_left, vmin, rng,
-                 nat.ptr(table), nat.stream_handle())
-        return table, vmin, rng
+            rec = self.ws.get(f"rec_{tag}", max(sd.dom_left, 1) * stride, torch.int32)
+            ovf = self.ws.get(f"ovf_{tag}", max(sd.n, 1), torch.int32)
+            nat.call("mmj_bsi_records", nat.ptr(sd.fwd_ptr), nat.ptr(sd.fwd_idx), sd.dom_left, nat.ptr(self.hpos),
+                     self.words, nat.ptr(rec), nat.ptr(ovf), st)
+            self.sides.append((rec, ovf))
 
     def answer(self, qa_dev, qb_dev, nq, dense_a=False, dense_b=False, out=None):
         torch = _torch()
-        st = nat.stream_handle()
         ans = out if out is not None else torch.empty(max(nq, 1), dtype=torch.int8, device="cuda")
-        (rb, rlp, rli), (sb, slp, sli) = self.sides
-        sR, sS = self.sR, self.sS
-        ta, tb = getattr(self, "tables", (None, None))
-        if not dense_a and not dense_b and ta is not None and tb is not None:
-            nat.call("mmj_bsi_answer_tables", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, nat.ptr(ta[0]), ta[1], ta[2],
-                     nat.ptr(tb[0]), tb[1], tb[2], nat.ptr(rb), nat.ptr(sb), self.words, nat.ptr(rlp), nat.ptr(rli),
-                     nat.ptr(slp), nat.ptr(sli), nat.ptr(ans), st)
-            return ans[:nq]
-        rs = 0 if dense_a else nat.ptr(sR.sorted_vals)
-        ro = 0 if dense_a else nat.ptr(sR.order)
-        ss = 0 if dense_b else nat.ptr(sS.sorted_vals)
-        so = 0 if dense_b else nat.ptr(sS.order)
-        nat.call("mmj_bsi_answer", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, rs, ro, sR.dom_left, ss, so, sS.dom_left,
-                 nat.ptr(rb), nat.ptr(sb), self.words, nat.ptr(rlp), nat.ptr(rli), nat.ptr(slp), nat.ptr(sli),
-                 nat.ptr(ans), st)
+        (rrec, rovf), (srec, sovf) = self.sides
+
+        def idmap(side, dense):
+            if dense:
+                return 0, 0, 0, 0, 0, 0
+            t = side.table
+            if t is not None:
+                return 0, 0, 0, nat.ptr(t[0]), t[1], t[2]
+            return nat.ptr(side.sorted_vals), nat.ptr(side.order), side.dom_left, 0, 0, 0
+        nat.call("mmj_bsi_answer", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, *idmap(self.sR, dense_a),
+                 *idmap(self.sS, dense_b), nat.ptr(rrec), nat.ptr(rovf), nat.ptr(srec), nat.ptr(sovf), self.words,
+                 nat.ptr(ans), nat.stream_handle())
         return ans[:nq]
 
 

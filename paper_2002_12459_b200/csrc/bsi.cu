@@ -5,15 +5,18 @@
 // output.  At cfg5 scale (64M + 64M tuples, 4M queries over a 4M x 4M space)
 // a dense product would be 0.25 ppm dense, so the B200 path evaluates the
 // "sampled" product instead -- only the queried (a, b) cells:
-//   * heavy y (the H most frequent join values) become H-bit rows per left
-//     id (Rbits[a], Sbits[b]); a query is decided by popc(Rbits & Sbits) > 0
-//     whenever a heavy witness exists -- the heavy part of the reference's
-//     matrix product with its nonzero test, restricted to queried cells;
-//   * otherwise the light lists (each left id's y list without heavy y, in
-//     y order) are merge-intersected;
-//   * raw query ids are resolved against each relation's own dictionary on
-//     device (binary search over the sorted raw values); an id unknown to
-//     the unreduced relation answers -1 (the reference's None marker).
+//   * index build, one pass over each side's forward CSR (k_bsi_records,
+//     thread per left id): a record of RECORD_WORDS(words) uint32 (64-byte
+//     multiples, so one DRAM access fetches it) holding the H-bit row of the
+//     id's heavy y (the H most frequent join values), the base and length of
+//     its light list, which is compacted IN PLACE into the id's own CSR span
+//     (no scan, no offsets array);
+//   * per query (k_bsi_answer): raw ids -> dense ids (direct-address table
+//     or binary search; -1 = unknown id = the reference's None), both records
+//     loaded together, popc(Rbits & Sbits) > 0 decides whenever a heavy
+//     witness exists -- the heavy part of the reference's matrix product
+//     with its nonzero test, restricted to queried cells; otherwise the two
+//     light lists (sectors prefetched to L1 first) are merge-intersected.
 #include "mmj_common.cuh"
 
 namespace mmj {
@@ -28,31 +31,37 @@ inline int grid_for(int64_t n, int per = TPB, int waves = 32) {
   return (int)(g < 1 ? 1 : g);
 }
 
-// bits[left * words + hpos[y] / 32] |= bit, for every tuple (left, y) with heavy y
-__global__ void k_bsi_bits(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols, int64_t n,
-                           const int32_t* __restrict__ hpos, int words, uint32_t* __restrict__ bits) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t h = hpos[cols[t]];
-    if (h >= 0) atomicOr(&bits[(int64_t)rows[t] * words + (h >> 5)], 1u << (h & 31));
+// Record of left id x (rec + x * stride uint32): words bitset words (bit
+// hpos[y] for every heavy y of x), then [words] = base of x's light list in
+// ovf (= fwd_ptr[x]) and [words + 1] = its length; the light y of x are
+// written to ovf[fwd_ptr[x] ...] in forward (ascending y) order.
+template <int WORDS>
+__global__ void __launch_bounds__(TPB) k_bsi_records(const int32_t* __restrict__ fwd_ptr,
+                                                     const int32_t* __restrict__ fwd_idx, int64_t dom,
+                                                     const int32_t* __restrict__ hpos, int stride,
+                                                     uint32_t* __restrict__ rec, int32_t* __restrict__ ovf) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < dom; x += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t b[WORDS];
+#pragma unroll
+    for (int w = 0; w < WORDS; ++w) b[w] = 0u;
+    const int32_t p0 = fwd_ptr[x], p1 = fwd_ptr[x + 1];
+    int32_t k = p0;
+    for (int32_t p = p0; p < p1; ++p) {
+      const int32_t y = fwd_idx[p];
+      const int32_t h = hpos[y];
+      if (h >= 0) {
+        const uint32_t m = 1u << (h & 31);
+#pragma unroll
+        for (int w = 0; w < WORDS; ++w) b[w] |= ((h >> 5) == w) ? m : 0u;
+      } else {
+        ovf[k++] = y;
+      }
+    }
+    uint32_t* r = rec + x * (int64_t)stride;
+#pragma unroll
+    for (int w = 0; w < WORDS; w += 4) *reinterpret_cast<uint4*>(r + w) = make_uint4(b[w], b[w + 1], b[w + 2], b[w + 3]);
+    *reinterpret_cast<uint2*>(r + WORDS) = make_uint2((uint32_t)p0, (uint32_t)(k - p0));
   }
-}
-
-__global__ void k_bsi_light_flags(const int32_t* __restrict__ cols, int64_t n, const int32_t* __restrict__ hpos,
-                                  uint8_t* __restrict__ flag) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-    flag[t] = hpos[cols[t]] < 0 ? 1 : 0;
-}
-
-__global__ void k_bsi_light_scatter(const int32_t* __restrict__ cols, const uint8_t* __restrict__ flag,
-                                    const int32_t* __restrict__ pos, int64_t n, int32_t* __restrict__ out) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-    if (flag[t]) out[pos[t]] = cols[t];
-}
-
-__global__ void k_bsi_light_ptr(const int32_t* __restrict__ ptr, const int32_t* __restrict__ pos, int64_t dom,
-                                int32_t* __restrict__ lptr) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= dom; i += (int64_t)gridDim.x * blockDim.x)
-    lptr[i] = pos[ptr[i]];
 }
 
 __device__ __forceinline__ int32_t lookup(const int64_t* __restrict__ sorted, const int32_t* __restrict__ order,
@@ -65,26 +74,6 @@ __device__ __forceinline__ int32_t lookup(const int64_t* __restrict__ sorted, co
   }
   return (lo < n && sorted[lo] == key) ? order[lo] : -1;
 }
-
-struct BsiArgs {
-  const int64_t* qa;            // raw query ids (or dense ids when sorted == nullptr)
-  const int64_t* qb;
-  int64_t nq;
-  const int64_t* r_sorted;      // sorted raw left values of R and their dense ids
-  const int32_t* r_order;
-  int64_t r_n;
-  const int64_t* s_sorted;
-  const int32_t* s_order;
-  int64_t s_n;
-  const uint32_t* r_bits;       // [dom_R x words]
-  const uint32_t* s_bits;
-  int words;
-  const int32_t* r_lptr;        // light lists (y ids ascending)
-  const int32_t* r_lidx;
-  const int32_t* s_lptr;
-  const int32_t* s_lidx;
-  int8_t* ans;
-};
 
 // raw id -> dense id: binary search over the sorted raw values, or one load
 // from a direct-address table (dense_of[raw - vmin], -1 = unknown id)
@@ -104,36 +93,69 @@ __device__ __forceinline__ int32_t map_id(const IdMap& m, int64_t v) {
   return m.sorted ? lookup(m.sorted, m.order, m.n, v) : (int32_t)v;
 }
 
-__global__ void k_bsi_answer(const BsiArgs a, const IdMap ma, const IdMap mb) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.nq; q += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t ia = map_id(ma, a.qa[q]);
-    const int32_t ib = map_id(mb, a.qb[q]);
+struct BsiSideArgs {
+  IdMap map;
+  const uint32_t* rec;
+  const int32_t* ovf;
+};
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+template <int WORDS>
+__global__ void __launch_bounds__(TPB) k_bsi_answer(const int64_t* __restrict__ qa, const int64_t* __restrict__ qb,
+                                                    int64_t nq, const BsiSideArgs ra, const BsiSideArgs sb, int stride,
+                                                    int8_t* __restrict__ ans) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t ia = map_id(ra.map, qa[q]);
+    const int32_t ib = map_id(sb.map, qb[q]);
     if (ia < 0 || ib < 0) {
-      a.ans[q] = -1;
+      ans[q] = -1;
       continue;
     }
-    bool hit = false;
-    const uint32_t* ra = a.r_bits + (int64_t)ia * a.words;
-    const uint32_t* sb = a.s_bits + (int64_t)ib * a.words;
-    for (int w = 0; w < a.words && !hit; w += 4) {
-      const uint4 x = *reinterpret_cast<const uint4*>(ra + w);
-      const uint4 y = *reinterpret_cast<const uint4*>(sb + w);
-      hit = ((x.x & y.x) | (x.y & y.y) | (x.z & y.z) | (x.w & y.w)) != 0u;
+    const uint32_t* pa = ra.rec + (int64_t)ia * stride;
+    const uint32_t* pb = sb.rec + (int64_t)ib * stride;
+    // both records' bit rows and list headers in flight together
+    uint4 xa[WORDS / 4], xb[WORDS / 4];
+#pragma unroll
+    for (int w = 0; w < WORDS / 4; ++w) {
+      xa[w] = __ldg(reinterpret_cast<const uint4*>(pa) + w);
+      xb[w] = __ldg(reinterpret_cast<const uint4*>(pb) + w);
     }
-    if (!hit) {
-      int32_t i = a.r_lptr[ia], ie = a.r_lptr[ia + 1];
-      int32_t j = a.s_lptr[ib], je = a.s_lptr[ib + 1];
-      while (i < ie && j < je) {
-        const int32_t u = a.r_lidx[i], v = a.s_lidx[j];
+    const uint2 ha = __ldg(reinterpret_cast<const uint2*>(pa + WORDS));
+    const uint2 hb = __ldg(reinterpret_cast<const uint2*>(pb + WORDS));
+    uint32_t any = 0u;
+#pragma unroll
+    for (int w = 0; w < WORDS / 4; ++w)
+      any |= (xa[w].x & xb[w].x) | (xa[w].y & xb[w].y) | (xa[w].z & xb[w].z) | (xa[w].w & xb[w].w);
+    bool hit = any != 0u;
+    if (!hit && ha.y && hb.y) {
+      const int32_t* la = ra.ovf + ha.x;
+      const int32_t* lb = sb.ovf + hb.x;
+      const int32_t na = (int32_t)ha.y, nb = (int32_t)hb.y;
+      // every 32-byte sector of both lists requested before the (dependent) merge
+      for (int32_t i = 0; i < na; i += 8) prefetch_l1(la + i);
+      for (int32_t j = 0; j < nb; j += 8) prefetch_l1(lb + j);
+      prefetch_l1(la + na - 1);
+      prefetch_l1(lb + nb - 1);
+      int32_t i = 0, j = 0;
+      int32_t u = la[0], v = lb[0];
+      while (true) {
         if (u == v) {
           hit = true;
           break;
         }
-        if (u < v) ++i;
-        else ++j;
+        if (u < v) {
+          if (++i == na) break;
+          u = la[i];
+        } else {
+          if (++j == nb) break;
+          v = lb[j];
+        }
       }
     }
-    a.ans[q] = hit ? 1 : 0;
+    ans[q] = hit ? 1 : 0;
   }
 }
 
@@ -168,46 +190,46 @@ __global__ void k_bsi_deg_hist(const int32_t* __restrict__ rdeg, const int32_t* 
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
-int bsi_bits(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* hpos, int words, uint32_t* bits,
-             int64_t dom, cudaStream_t st) {
-  MMJ_TRY(cuda_status(cudaMemsetAsync(bits, 0, (size_t)dom * words * 4, st), "memset bits"));
-  if (n == 0) return MMJ_OK;
-  k_bsi_bits<<<grid_for(n), TPB, 0, st>>>(rows, cols, n, hpos, words, bits);
-  MMJ_CHECK_LAUNCH("k_bsi_bits");
-  return MMJ_OK;
-}
+int bsi_record_words(int words) { return (int)round_up(words + 2, 16); }
 
-int bsi_light_lists(const int32_t* ptr, const int32_t* cols, int64_t n, int64_t dom, const int32_t* hpos,
-                    uint8_t* flag_ws, int32_t* pos_ws, int32_t* lptr, int32_t* lidx, void* ws, cudaStream_t st) {
-  if (n > 0) {
-    k_bsi_light_flags<<<grid_for(n), TPB, 0, st>>>(cols, n, hpos, flag_ws);
-    MMJ_CHECK_LAUNCH("k_bsi_light_flags");
+int bsi_records(const int32_t* fwd_ptr, const int32_t* fwd_idx, int64_t dom, const int32_t* hpos, int words,
+                uint32_t* rec, int32_t* ovf, cudaStream_t st) {
+  if (dom == 0) return MMJ_OK;
+  const int stride = bsi_record_words(words);
+  const int g = grid_for(dom);
+  switch (words) {
+    case 4: k_bsi_records<4><<<g, TPB, 0, st>>>(fwd_ptr, fwd_idx, dom, hpos, stride, rec, ovf); break;
+    case 8: k_bsi_records<8><<<g, TPB, 0, st>>>(fwd_ptr, fwd_idx, dom, hpos, stride, rec, ovf); break;
+    case 16: k_bsi_records<16><<<g, TPB, 0, st>>>(fwd_ptr, fwd_idx, dom, hpos, stride, rec, ovf); break;
+    case 32: k_bsi_records<32><<<g, TPB, 0, st>>>(fwd_ptr, fwd_idx, dom, hpos, stride, rec, ovf); break;
+    default:
+      set_error("bsi_records: words must be 4, 8, 16 or 32 (128 .. 1024 heavy bits)");
+      return MMJ_ERR_ARG;
   }
-  MMJ_TRY(scan_u8_i32(flag_ws, pos_ws, n, ws, st));
-  if (n > 0) {
-    k_bsi_light_scatter<<<grid_for(n), TPB, 0, st>>>(cols, flag_ws, pos_ws, n, lidx);
-    MMJ_CHECK_LAUNCH("k_bsi_light_scatter");
-  }
-  k_bsi_light_ptr<<<grid_for(dom + 1), TPB, 0, st>>>(ptr, pos_ws, dom, lptr);
-  MMJ_CHECK_LAUNCH("k_bsi_light_ptr");
+  MMJ_CHECK_LAUNCH("k_bsi_records");
   return MMJ_OK;
 }
 
 int bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted, const int32_t* r_order,
-               int64_t r_n, const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const uint32_t* r_bits,
-               const uint32_t* s_bits, int words, const int32_t* r_lptr, const int32_t* r_lidx,
-               const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, const int32_t* r_table, int64_t r_min,
-               int64_t r_range, const int32_t* s_table, int64_t s_min, int64_t s_range, cudaStream_t st) {
-  if (words % 4 != 0 || words <= 0) {
-    set_error("bsi_answer: bitset words must be a positive multiple of 4");
+               int64_t r_n, const int32_t* r_table, int64_t r_min, int64_t r_range, const int64_t* s_sorted,
+               const int32_t* s_order, int64_t s_n, const int32_t* s_table, int64_t s_min, int64_t s_range,
+               const uint32_t* r_rec, const int32_t* r_ovf, const uint32_t* s_rec, const int32_t* s_ovf, int words,
+               int8_t* ans, cudaStream_t st) {
+  if (words != 4 && words != 8 && words != 16 && words != 32) {
+    set_error("bsi_answer: words must be 4, 8, 16 or 32 (128 .. 1024 heavy bits)");
     return MMJ_ERR_ARG;
   }
   if (nq == 0) return MMJ_OK;
-  BsiArgs a{qa, qb, nq, r_sorted, r_order, r_n, s_sorted, s_order, s_n, r_bits, s_bits, words,
-            r_lptr, r_lidx, s_lptr, s_lidx, ans};
-  const IdMap ma{r_sorted, r_order, r_n, r_table, r_min, r_range};
-  const IdMap mb{s_sorted, s_order, s_n, s_table, s_min, s_range};
-  k_bsi_answer<<<grid_for(nq, TPB, 16), TPB, 0, st>>>(a, ma, mb);
+  const BsiSideArgs a{IdMap{r_sorted, r_order, r_n, r_table, r_min, r_range}, r_rec, r_ovf};
+  const BsiSideArgs b{IdMap{s_sorted, s_order, s_n, s_table, s_min, s_range}, s_rec, s_ovf};
+  const int stride = bsi_record_words(words);
+  const int g = grid_for(nq, TPB, 16);
+  switch (words) {
+    case 4: k_bsi_answer<4><<<g, TPB, 0, st>>>(qa, qb, nq, a, b, stride, ans); break;
+    case 8: k_bsi_answer<8><<<g, TPB, 0, st>>>(qa, qb, nq, a, b, stride, ans); break;
+    case 16: k_bsi_answer<16><<<g, TPB, 0, st>>>(qa, qb, nq, a, b, stride, ans); break;
+    default: k_bsi_answer<32><<<g, TPB, 0, st>>>(qa, qb, nq, a, b, stride, ans); break;
+  }
   MMJ_CHECK_LAUNCH("k_bsi_answer");
   return MMJ_OK;
 }

@@ -8,6 +8,8 @@ int heavy_y_positions(const int32_t*, const int32_t*, int64_t, int64_t, uint8_t*
                       cudaStream_t);
 int build_operand(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint8_t*, int64_t,
                   int64_t, int64_t, cudaStream_t);
+int build_heavy_rows(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint32_t*,
+                     int64_t, int64_t, cudaStream_t);
 int build_operand_pairs(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint8_t*,
                         int64_t, int64_t, int64_t, cudaStream_t);
 int light_z_csr(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, uint8_t*, int32_t*,
@@ -28,24 +30,23 @@ int count_emit(const void*, int, int64_t, int64_t, int64_t, int64_t, int64_t, in
                const int64_t*, int64_t*, int32_t*, cudaStream_t);
 int64_t row_emit_tiles(int64_t, int64_t);
 int tile_merge(uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t*, const int32_t*, const int32_t*,
-               int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int32_t*,
-               unsigned long long*, cudaStream_t);
+               int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*,
+               const uint32_t*, unsigned long long*, int32_t*, unsigned long long*, cudaStream_t);
 int emit_codes(const uint32_t*, const int64_t*, int64_t, int64_t, int64_t, int64_t, int64_t*, cudaStream_t);
 size_t merge_emit_ws_bytes(int64_t, int64_t);
 int merge_emit(const uint32_t*, int, int64_t, int64_t, int64_t, int64_t, const int32_t*, const int32_t*, const int32_t*,
                int64_t, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*,
-               const int32_t*, const int32_t*, unsigned long long*, int64_t*, int64_t*, void*, size_t,
+               const int32_t*, const int32_t*, unsigned long long*, unsigned long long*, int64_t*, int64_t*, void*,
+               size_t,
                cudaStream_t);
 int merge_emit_col_blocks(int64_t);
 extern unsigned long long* tdbg_buffer;
 int list_splits(const int32_t*, const int32_t*, int64_t, int64_t, int32_t*, cudaStream_t);
-int bsi_bits(const int32_t*, const int32_t*, int64_t, const int32_t*, int, uint32_t*, int64_t, cudaStream_t);
-int bsi_light_lists(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, uint8_t*, int32_t*, int32_t*,
-                    int32_t*, void*, cudaStream_t);
-int bsi_answer(const int64_t*, const int64_t*, int64_t, const int64_t*, const int32_t*, int64_t, const int64_t*,
-               const int32_t*, int64_t, const uint32_t*, const uint32_t*, int, const int32_t*, const int32_t*,
-               const int32_t*, const int32_t*, int8_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t,
-               int64_t, cudaStream_t);
+int bsi_record_words(int);
+int bsi_records(const int32_t*, const int32_t*, int64_t, const int32_t*, int, uint32_t*, int32_t*, cudaStream_t);
+int bsi_answer(const int64_t*, const int64_t*, int64_t, const int64_t*, const int32_t*, int64_t, const int32_t*, int64_t,
+               int64_t, const int64_t*, const int32_t*, int64_t, const int32_t*, int64_t, int64_t, const uint32_t*,
+               const int32_t*, const uint32_t*, const int32_t*, int, int8_t*, cudaStream_t);
 int bsi_direct_table(const int64_t*, const int32_t*, int64_t, int64_t, int64_t, int32_t*, cudaStream_t);
 int star_split(int, const int32_t* const*, int64_t, double, uint8_t*, uint8_t*, int32_t*, int32_t*, int32_t*, int32_t*,
                void*, cudaStream_t);
@@ -120,6 +121,12 @@ int mmj_build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n,
   return mmj::build_operand_pairs(rows, cols, n, left_deg, delta2, hpos, mat, row0, nrows, kpad, ST(stream));
 }
 
+int mmj_build_heavy_rows(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
+                         int64_t delta2, const int32_t* hpos, uint32_t* heavy_rows, int64_t k, int64_t wpr,
+                         void* stream) {
+  return mmj::build_heavy_rows(rows, cols, n, left_deg, delta2, hpos, heavy_rows, k, wpr, ST(stream));
+}
+
 int mmj_light_z_csr(const int32_t* rev_ptr, const int32_t* rev_idx, int64_t n, int64_t dom_y,
                     const int32_t* left_deg, int64_t delta2, uint8_t* flag_ws, int32_t* pos_ws, int32_t* lz_ptr,
                     int32_t* lz_idx, void* ws, void* stream) {
@@ -182,9 +189,10 @@ int64_t mmj_tile_count(int64_t rows, int64_t wpr) { return mmj::row_emit_tiles(r
 int mmj_tile_merge(uint32_t* bitmap, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
                    const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
-                   const int32_t* lz_idx, int32_t* segcnt, unsigned long long* witnesses, void* stream) {
+                   const int32_t* lz_idx, const uint32_t* heavy_rows, unsigned long long* heavy_pairs, int32_t* segcnt,
+                   unsigned long long* witnesses, void* stream) {
   return mmj::tile_merge(bitmap, has_heavy, x0, rows, wpr, dom_z, fwd_ptr, fwd_idx, rdeg_x, delta2, hpos, s_rev_ptr,
-                         s_rev_idx, lz_ptr, lz_idx, segcnt, witnesses, ST(stream));
+                         s_rev_idx, lz_ptr, lz_idx, heavy_rows, heavy_pairs, segcnt, witnesses, ST(stream));
 }
 
 size_t mmj_merge_emit_workspace_size(int64_t rows, int64_t wpr) { return mmj::merge_emit_ws_bytes(rows, wpr); }
@@ -193,10 +201,10 @@ int mmj_merge_emit(const uint32_t* bitmap, int has_heavy, int64_t x0, int64_t ro
                    const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t delta2,
                    const int32_t* hpos, const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr,
                    const int32_t* lz_idx, const int32_t* split_full, const int32_t* split_lz,
-                   unsigned long long* witnesses, int64_t* codes, int64_t* total, void* ws, size_t ws_bytes,
-                   void* stream) {
+                   unsigned long long* witnesses, unsigned long long* heavy_pairs, int64_t* codes, int64_t* total,
+                   void* ws, size_t ws_bytes, void* stream) {
   return mmj::merge_emit(bitmap, has_heavy, x0, rows, wpr, dom_z, fwd_ptr, fwd_idx, rdeg_x, delta2, hpos, s_rev_ptr,
-                         s_rev_idx, lz_ptr, lz_idx, split_full, split_lz, witnesses, codes, total, ws,
+                         s_rev_idx, lz_ptr, lz_idx, split_full, split_lz, witnesses, heavy_pairs, codes, total, ws,
                          ws_bytes, ST(stream));
 }
 
@@ -221,23 +229,20 @@ int mmj_bsi_degree_histogram(const int32_t* rdeg, const int32_t* sdeg, int64_t d
   return mmj::bsi_degree_histogram(rdeg, sdeg, dom_y, lo, hi, nbins, log2mode, hist, ST(stream));
 }
 
-int mmj_bsi_bits(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* hpos, int words, uint32_t* bits,
-                 int64_t dom_left, void* stream) {
-  return mmj::bsi_bits(rows, cols, n, hpos, words, bits, dom_left, ST(stream));
-}
+int mmj_bsi_record_words(int words) { return mmj::bsi_record_words(words); }
 
-int mmj_bsi_light_lists(const int32_t* fwd_ptr, const int32_t* fwd_idx, int64_t n, int64_t dom_left,
-                        const int32_t* hpos, uint8_t* flag_ws, int32_t* pos_ws, int32_t* lptr, int32_t* lidx,
-                        void* ws, void* stream) {
-  return mmj::bsi_light_lists(fwd_ptr, fwd_idx, n, dom_left, hpos, flag_ws, pos_ws, lptr, lidx, ws, ST(stream));
+int mmj_bsi_records(const int32_t* fwd_ptr, const int32_t* fwd_idx, int64_t dom_left, const int32_t* hpos, int words,
+                    uint32_t* rec, int32_t* ovf, void* stream) {
+  return mmj::bsi_records(fwd_ptr, fwd_idx, dom_left, hpos, words, rec, ovf, ST(stream));
 }
 
 int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted, const int32_t* r_order,
-                   int64_t r_n, const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const uint32_t* r_bits,
-                   const uint32_t* s_bits, int words, const int32_t* r_lptr, const int32_t* r_lidx,
-                   const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans, void* stream) {
-  return mmj::bsi_answer(qa, qb, nq, r_sorted, r_order, r_n, s_sorted, s_order, s_n, r_bits, s_bits, words, r_lptr,
-                         r_lidx, s_lptr, s_lidx, ans, nullptr, 0, 0, nullptr, 0, 0, ST(stream));
+                   int64_t r_n, const int32_t* r_table, int64_t r_min, int64_t r_range, const int64_t* s_sorted,
+                   const int32_t* s_order, int64_t s_n, const int32_t* s_table, int64_t s_min, int64_t s_range,
+                   const uint32_t* r_rec, const int32_t* r_ovf, const uint32_t* s_rec, const int32_t* s_ovf,
+                   int words, int8_t* ans, void* stream) {
+  return mmj::bsi_answer(qa, qb, nq, r_sorted, r_order, r_n, r_table, r_min, r_range, s_sorted, s_order, s_n, s_table,
+                         s_min, s_range, r_rec, r_ovf, s_rec, s_ovf, words, ans, ST(stream));
 }
 
 int mmj_bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
@@ -245,18 +250,6 @@ int mmj_bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n,
   return mmj::bsi_direct_table(sorted, order, n, vmin, range, table, ST(stream));
 }
 
-int mmj_bsi_answer_tables(const int64_t* qa, const int64_t* qb, int64_t nq, const int32_t* r_table, int64_t r_min,
-                          int64_t r_range, const int32_t* s_table, int64_t s_min, int64_t s_range,
-                          const uint32_t* r_bits, const uint32_t* s_bits, int words, const int32_t* r_lptr,
-                          const int32_t* r_lidx, const int32_t* s_lptr, const int32_t* s_lidx, int8_t* ans,
-                          void* stream) {
-  if (r_table == nullptr || s_table == nullptr) {
-    mmj::set_error("bsi_answer_tables: both direct tables are required (mmj_bsi_answer resolves by search)");
-    return MMJ_ERR_ARG;
-  }
-  return mmj::bsi_answer(qa, qb, nq, nullptr, nullptr, 0, nullptr, nullptr, 0, r_bits, s_bits, words, r_lptr, r_lidx,
-                         s_lptr, s_lidx, ans, r_table, r_min, r_range, s_table, s_min, s_range, ST(stream));
-}
 
 int mmj_star_split(int k, const int32_t* const* rev_ptr, int64_t dom_y, double threshold, uint8_t* heavy_flag,
                    uint8_t* light_flag, int32_t* heavy_scan, int32_t* light_scan, int32_t* hpos, int32_t* light_y,

@@ -99,8 +99,11 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ v, in
   return lo;
 }
 
+// has_heavy: 0 = no heavy part; 1 = the chunk's heavy bitmap (the tcgen05
+// product's output) is in bm; 2 = the heavy part is computed by the tile
+// itself from the heavy-y bit rows `hbits` (heavy_or_rows)
 struct TileArgs {
-  uint32_t* bm;               // rows x wpr words (in: heavy bits if has_heavy; out: merged)
+  uint32_t* bm;               // rows x wpr words (in: heavy bits if has_heavy == 1; out: merged)
   int has_heavy;
   int64_t x0, rows, wpr, dom_z;
   int G, cb_words, ncb;
@@ -119,7 +122,70 @@ struct TileArgs {
   // boundaries (full S.rev lists / light-z lists): replaces per-tile bisection
   const int32_t* split_full = nullptr;
   const int32_t* split_lz = nullptr;
+  // has_heavy == 2: K x wpr bit rows of S_h (bit z of row hpos[y] set iff z
+  // heavy and (z, y) in S) and the heavy_pairs counter
+  const uint32_t* hbits = nullptr;
+  unsigned long long* heavy_nnz = nullptr;
 };
+
+// Heavy part of a tile's rows [xa, xa + nrow), columns [c0w, c0w + cw) words,
+// as a sparse boolean product (joinproject.py:208-216, nonzero(M1 @ M2)):
+// word i of heavy row x = OR over the heavy y of R[x] of hbits[hpos[y]][c0w+i]
+// (light x rows are zero, as in M1).  Each row's heavy positions are
+// compacted NT at a time into s_list, then every thread ORs its 16-byte word
+// groups over them (the bit rows are L2-resident: K x wpr x 4 B).  Writes
+// every word of the tile; returns this thread's popcount of the heavy bits
+// (the heavy_pairs statistic).  Block-uniform control flow.
+template <int NT>
+__device__ unsigned long long heavy_or_rows(const TileArgs& a, uint32_t* sbm, int64_t xa, int nrow, int cw,
+                                            int64_t c0w, typename cub::BlockScan<int, NT>::TempStorage& scan_tmp,
+                                            int* s_list) {
+  const int tid = threadIdx.x;
+  const int q4 = cw >> 2;
+  unsigned long long pc = 0;
+  for (int rr = 0; rr < nrow; ++rr) {
+    const int64_t x = xa + rr;
+    uint4* dst = reinterpret_cast<uint4*>(sbm + (int64_t)rr * cw);
+    const bool heavy_x = a.rdeg_x[x] > a.d2;
+    const int64_t tb0 = heavy_x ? a.fwd_ptr[x] : 0, te = heavy_x ? a.fwd_ptr[x + 1] : 0;
+    if (tb0 >= te) {
+      for (int q = tid; q < q4; q += NT) dst[q] = make_uint4(0u, 0u, 0u, 0u);
+      continue;
+    }
+    for (int64_t tb = tb0; tb < te; tb += NT) {
+      const int64_t t = tb + tid;
+      const int h = t < te ? a.hpos[a.fwd_idx[t]] : -1;
+      int pos, cnt;
+      cub::BlockScan<int, NT>(scan_tmp).ExclusiveSum(h >= 0 ? 1 : 0, pos, cnt);
+      if (h >= 0) s_list[pos] = h;
+      __syncthreads();
+      const bool last = tb + NT >= te;
+      for (int q = tid; q < q4; q += NT) {
+        uint4 v = tb == tb0 ? make_uint4(0u, 0u, 0u, 0u) : dst[q];
+        int j = 0;
+        for (; j + 2 <= cnt; j += 2) {   // two independent L2 loads in flight
+          const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(a.hbits + (int64_t)s_list[j] * a.wpr + c0w) + q);
+          const uint4 w1 = __ldg(reinterpret_cast<const uint4*>(a.hbits + (int64_t)s_list[j + 1] * a.wpr + c0w) + q);
+          v.x |= w0.x | w1.x;
+          v.y |= w0.y | w1.y;
+          v.z |= w0.z | w1.z;
+          v.w |= w0.w | w1.w;
+        }
+        if (j < cnt) {
+          const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(a.hbits + (int64_t)s_list[j] * a.wpr + c0w) + q);
+          v.x |= w0.x;
+          v.y |= w0.y;
+          v.z |= w0.z;
+          v.w |= w0.w;
+        }
+        dst[q] = v;
+        if (last) pc += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+      }
+      __syncthreads();   // s_list / scan storage reused by the next batch
+    }
+  }
+  return pc;
+}
 
 // Light witnesses of one tile OR-ed into its shared-memory bitmap (rows
 // [xa, xb), columns [zlo, zhi), cw words per row): R tuples are staged NT at a
@@ -253,13 +319,13 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   // (ncb == 1) or one row piece (G == 1)
   uint32_t* gtile = a.bm + r0 * a.wpr + c0w;
   const uint32_t tile_bytes = (uint32_t)words * 4u;
-  if (a.has_heavy) {
+  if (a.has_heavy == 1) {
     if (tid == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar)));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       bulk_g2s(sbm, gtile, tile_bytes, &s_bar);
     }
-  } else {
+  } else if (a.has_heavy == 0) {
     for (int i = tid; i < words; i += TM_THREADS) sbm[i] = 0;
   }
   if (tid == 0) s_touched = 0;
@@ -267,8 +333,14 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   const int64_t xa = a.x0 + r0, xb = a.x0 + r1;
   const int64_t t_begin = a.fwd_ptr[xa], t_end = a.fwd_ptr[xb];
   unsigned long long my_w = 0;
+  if (a.has_heavy == 2) {
+    unsigned long long pc = heavy_or_rows<TM_THREADS>(a, sbm, xa, nrow, cw, c0w, scan_tmp, s_tb_len);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
+    if (lane == 0 && pc) atomicAdd(a.heavy_nnz, pc);
+  }
   __syncthreads();
-  if (a.has_heavy) bar_wait0(&s_bar);   // tile bytes landed (all threads observe the phase)
+  if (a.has_heavy == 1) bar_wait0(&s_bar);   // tile bytes landed (all threads observe the phase)
   my_w = merge_light<TM_THREADS>(a, sbm, xa, xb, t_begin, t_end, zlo, zhi, cw, cbi, scan_tmp, s_tb_len, s_tb_base,
                                  s_tb_row, s_tb_filt, &s_touched);
   {
@@ -279,7 +351,7 @@ __global__ void __launch_bounds__(TM_THREADS) k_tile_merge(const TileArgs a) {
   }
   // write back the merged tile (skipped when the heavy bits are unchanged)
   __syncthreads();
-  if ((s_touched || !a.has_heavy) && tid == 0) bulk_s2g(gtile, sbm, tile_bytes);
+  if ((s_touched || a.has_heavy != 1) && tid == 0) bulk_s2g(gtile, sbm, tile_bytes);
   // segment popcounts (segments never straddle rows: wpr % 32 == 0): a warp
   // takes 32 segments, lane l reads word l of each (conflict-free LDS) and
   // REDUX sums the 32 popcounts; lane j keeps the total of segment j
@@ -476,20 +548,27 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
   const int32_t zlo = (int32_t)(c0w * 32);
   const int32_t zhi = (int32_t)min((c0w + cw) * 32, a.dom_z);
   const uint32_t* gtile = a.bm + r0 * a.wpr + c0w;
-  if (a.has_heavy) {
+  if (a.has_heavy == 1) {
     if (tid == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar)));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       bulk_g2s(sbm, gtile, (uint32_t)words * 4u, &sm.bar);
     }
-  } else {
+  } else if (a.has_heavy == 0) {
     for (int i = tid; i < words; i += NT) sbm[i] = 0;
   }
   const int64_t xa = a.x0 + r0, xb = a.x0 + r1;
   // fwd_ptr == nullptr: the bitmap is already complete (no light witnesses to merge)
   const int64_t t_begin = a.fwd_ptr ? a.fwd_ptr[xa] : 0, t_end = a.fwd_ptr ? a.fwd_ptr[xb] : 0;
+  if (a.has_heavy == 2) {
+    // the heavy part computed in place: no tcgen05 product, no bitmap in HBM
+    unsigned long long pc = heavy_or_rows<NT>(a, sbm, xa, nrow, cw, c0w, sm.scan_tmp, sm.u.m.tb_len);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
+    if (lane == 0 && pc) atomicAdd(a.heavy_nnz, pc);
+  }
   __syncthreads();
-  if (a.has_heavy) bar_wait0(&sm.bar);
+  if (a.has_heavy == 1) bar_wait0(&sm.bar);
 
 #ifdef MMJ_DEBUG_TIMING
   if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 1] = gtimer();
@@ -732,10 +811,16 @@ unsigned long long* tdbg_buffer = nullptr;   // MMJ_DEBUG_TIMING builds: set by 
 int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t d2, const int32_t* hpos,
                const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx,
-               const int32_t* split_full, const int32_t* split_lz, unsigned long long* witnesses, int64_t* codes,
-               int64_t* total, void* ws, size_t ws_bytes, cudaStream_t st) {
+               const int32_t* split_full, const int32_t* split_lz, unsigned long long* witnesses,
+               unsigned long long* heavy_pairs, int64_t* codes, int64_t* total, void* ws, size_t ws_bytes,
+               cudaStream_t st) {
   if (wpr <= 0 || wpr % 32 != 0) {
     set_error("merge_emit: bitmap pitch must be a positive multiple of 32 words");
+    return MMJ_ERR_ARG;
+  }
+  if (has_heavy < 0 || has_heavy > 2 ||
+      (has_heavy == 2 && (hpos == nullptr || fwd_ptr == nullptr || heavy_pairs == nullptr))) {
+    set_error("merge_emit: has_heavy must be 0, 1 or 2 (2 needs hpos, the R CSR and a heavy_pairs counter)");
     return MMJ_ERR_ARG;
   }
   if (rows <= 0) return cuda_status(cudaMemsetAsync(total, 0, sizeof(int64_t), st), "merge_emit: total");
@@ -771,6 +856,10 @@ int merge_emit(const uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int6
   a.witnesses = witnesses;
   a.split_full = split_full;
   a.split_lz = split_lz;
+  if (has_heavy == 2) {
+    a.hbits = bm;
+    a.heavy_nnz = heavy_pairs;
+  }
   f.ticket = static_cast<unsigned int*>(ws);
   f.status = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 16);
   f.total = total;
@@ -789,10 +878,16 @@ int64_t row_emit_tiles(int64_t rows, int64_t wpr) {
 int tile_merge(uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int64_t wpr, int64_t dom_z,
                const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* rdeg_x, int64_t d2, const int32_t* hpos,
                const int32_t* s_rev_ptr, const int32_t* s_rev_idx, const int32_t* lz_ptr, const int32_t* lz_idx,
-               int32_t* segcnt, unsigned long long* witnesses, cudaStream_t st) {
+               const uint32_t* hbits, unsigned long long* heavy_pairs, int32_t* segcnt, unsigned long long* witnesses,
+               cudaStream_t st) {
   if (rows <= 0) return MMJ_OK;
   if (wpr <= 0 || wpr % 32 != 0) {
     set_error("tile_merge: bitmap pitch must be a positive multiple of 32 words");
+    return MMJ_ERR_ARG;
+  }
+  if (has_heavy < 0 || has_heavy > 2 ||
+      (has_heavy == 2 && (hbits == nullptr || hpos == nullptr || heavy_pairs == nullptr))) {
+    set_error("tile_merge: has_heavy must be 0, 1 or 2 (2 needs the heavy-y bit rows, hpos and a counter)");
     return MMJ_ERR_ARG;
   }
   TileArgs a;
@@ -819,6 +914,8 @@ int tile_merge(uint32_t* bm, int has_heavy, int64_t x0, int64_t rows, int64_t wp
   a.lz_idx = lz_idx;
   a.segcnt = segcnt;
   a.witnesses = witnesses;
+  a.hbits = hbits;
+  a.heavy_nnz = heavy_pairs;
   const size_t smem = (size_t)a.G * a.cb_words * 4;
   MMJ_TRY(set_max_dynamic_smem((const void*)k_tile_merge, TILE_WORDS * 4, "k_tile_merge"));
   k_tile_merge<<<(unsigned)ntiles, TM_THREADS, smem, st>>>(a);

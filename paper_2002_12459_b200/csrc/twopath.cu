@@ -66,6 +66,21 @@ __global__ void k_build_operand(const int32_t* __restrict__ rows, const int32_t*
   }
 }
 
+// Heavy-y bit rows of S_h for the in-tile heavy product (rowemit.cu
+// heavy_or_rows): bit z of row hpos[y] is set for every S tuple (z, y) with
+// heavy z (deg_S(z) > d2) and heavy y -- the rows of joinproject.py:119-143's
+// M2 stored one bit per cell.
+__global__ void k_build_heavy_rows(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols, int64_t n,
+                                   const int32_t* __restrict__ left_deg, int64_t d2, const int32_t* __restrict__ hpos,
+                                   uint32_t* __restrict__ hbits, int64_t wpr) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t z = rows[t];
+    if (left_deg[z] <= d2) continue;
+    const int32_t k = hpos[cols[t]];
+    if (k >= 0) atomicOr(&hbits[(int64_t)k * wpr + (z >> 5)], 1u << (z & 31));
+  }
+}
+
 // z-pair operand for MMJ_MODE_BITMAP_PAIR: z = 32G + b (b = k + 8j) goes to
 // row 16G + 2k + (j >> 1) with weight 1 (j even) or 128 (j odd) -- the
 // placement the heavy_mma pair epilogue unpacks (mma_i8.cu pack_bits_pair).
@@ -485,6 +500,19 @@ int build_operand(const int32_t* rows, const int32_t* cols, int64_t n, const int
   if (n == 0) return MMJ_OK;
   k_build_operand<<<grid_for(n, TPB), TPB, 0, st>>>(rows, cols, n, left_deg, d2, hpos, mat, row0, nrows, kpad);
   MMJ_CHECK_LAUNCH("k_build_operand");
+  return MMJ_OK;
+}
+
+int build_heavy_rows(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t d2,
+                     const int32_t* hpos, uint32_t* hbits, int64_t k, int64_t wpr, cudaStream_t st) {
+  if (k < 0 || wpr <= 0 || wpr % 4 != 0) {
+    set_error("build_heavy_rows: k >= 0 and a positive row pitch (multiple of 4 words) are required");
+    return MMJ_ERR_ARG;
+  }
+  MMJ_TRY(cuda_status(cudaMemsetAsync(hbits, 0, (size_t)(k * wpr) * 4, st), "memset heavy rows"));
+  if (n == 0 || k == 0) return MMJ_OK;
+  k_build_heavy_rows<<<grid_for(n, TPB), TPB, 0, st>>>(rows, cols, n, left_deg, d2, hpos, hbits, wpr);
+  MMJ_CHECK_LAUNCH("k_build_heavy_rows");
   return MMJ_OK;
 }
 

@@ -35,6 +35,7 @@ DEFAULT_BITMAP_CHUNK_BYTES = 1 << 30
 DEFAULT_COUNT_CHUNK_BYTES = 4 << 30
 FUSED_SMEM_LIMIT = 200 * 1024
 SYNC_FUSED_CAP_BYTES = 4 << 30
+OR_MAX_MEAN_DEG = 16       # engine._heavy_or: heavy y per heavy row up to which the OR path wins
 
 
 _HOST_MAX = {}
@@ -128,6 +129,11 @@ class TwoPathEngine:
         self.pairs = False
         self.allow_pairs = bool(pair_operand)   # False: B stays one z per row (heavy_matrices reads it)
         self.kpad = 0
+        # heavy part of a projection: "mma" (tcgen05 product into a chunk
+        # bitmap) or "or" (heavy-y bit rows OR-ed per row inside the fused
+        # tail, no product and no bitmap round trip); chosen in prepare()
+        self.heavy_kernel = None
+        self.hbits = None
         self.lz_ptr = None
         self.lz_idx = None
         self._host_ldeg_r = host_left_deg_r
@@ -180,7 +186,14 @@ class TwoPathEngine:
             self.stats.k_heavy = k
             heavy_x = self._any_heavy(self._host_ldeg_r, dr)
             heavy_z = self._any_heavy(self._host_ldeg_s, ds)
-            if k > 0 and heavy_x and heavy_z:
+            if k > 0 and heavy_x and heavy_z and self._heavy_or(k):
+                # the heavy rows of S_h at one bit per cell (K x wpr words)
+                self.heavy_kernel = "or"
+                self.hbits = torch.empty((k, self.wpr), dtype=torch.int32, device="cuda")
+                nat.call("mmj_build_heavy_rows", nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n, nat.ptr(ds.left_deg),
+                         self.d2, nat.ptr(self.hpos), nat.ptr(self.hbits), k, self.wpr, st)
+            elif k > 0 and heavy_x and heavy_z:
+                self.heavy_kernel = "mma"
                 kpad = _rup(k, BK)
                 self.kpad = kpad
                 arows = _rup(max(self.dom_x, 1), BN)
@@ -213,6 +226,26 @@ class TwoPathEngine:
                      self.d2, nat.ptr(lflag), nat.ptr(lpos), nat.ptr(self.lz_ptr), nat.ptr(self.lz_idx),
                      nat.ptr(self.ws.scan_ws(n)), st)
         self._prepared = True
+
+    def _heavy_or(self, k: int) -> bool:
+        """Projection heavy part as a sparse boolean product (OR of heavy-y
+        bit rows) instead of the dense tcgen05 product.  Per output cell the
+        product reads 2 B of TMEM (z-pair accumulators) whatever R_h's
+        density; the OR reads 4 B x (heavy y of the row) / 32 from L2 and runs
+        inside the emission tail.  Taken when R_h's heavy rows carry at most
+        OR_MAX_MEAN_DEG heavy y on average (cfg2: 4.2 of K = 128) and the
+        fused projection tail is in use; env MMJ_HEAVY=mma|or overrides."""
+        env = __import__("os").environ.get("MMJ_HEAVY", "")
+        if not self.fused or self.counts or not self.allow_pairs:
+            return False
+        if env in ("mma", "or"):
+            return env == "or"
+        torch = self.torch
+        dr = self.dr
+        hx = dr.left_deg > self.d2
+        ht = ((self.hpos[dr.fwd_idx.long()] >= 0) & hx[dr.fwd_row.long()]).sum()
+        nh, nt = (int(v) for v in torch.stack([hx.sum(), ht]).cpu())
+        return nt <= OR_MAX_MEAN_DEG * max(nh, 1)
 
     def _bitmap_mode(self) -> int:
         # every product entry counts <= K shared heavy y: with K <= 255 the
@@ -260,14 +293,15 @@ class TwoPathEngine:
             buf = self.ws.get("bm", rows * self.wpr, torch.int32)
             ld = self.wpr
             mode = self._bitmap_mode()
-        # heavy part (writes every cell of the chunk) or zero fill
-        self._ph("heavy_mma", True)
+        # heavy part (writes every cell of the chunk) or zero fill; the in-tile
+        # OR path (hbits) computes it inside the tail kernel instead
         if self.A is not None:
+            self._ph("heavy_mma", True)
             nat.call("mmj_heavy_mma", nat.ptr(self.A), self.A.shape[0], nat.ptr(self.B), self.B.shape[0],
                      self.kpad, 0, self.kpad, x0, rows, mode, 0, nat.ptr(buf), ld, nat.ptr(self.nnz), 0, st)
-        else:
+            self._ph("heavy_mma", False)
+        elif self.hbits is None:
             buf.zero_()
-        self._ph("heavy_mma", False)
         if self.fused:
             return self._fused_tail(x0, x1, rows, buf, sync, codes_key)
         # light passes (x-driven; FULL_JOIN when hpos is None)
@@ -356,9 +390,10 @@ class TwoPathEngine:
         lzi = nat.ptr(self.lz_idx) if self.lz_idx is not None else 0
         wit0 = int(self.wit.item()) if sync else 0
         self._ph("light_merge", True)
-        nat.call("mmj_tile_merge", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
+        nat.call("mmj_tile_merge", nat.ptr(buf), self._has_heavy(), x0, rows, self.wpr, self.dom_z,
                  nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp, nat.ptr(ds.rev_ptr),
-                 nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(segcnt), nat.ptr(self.wit), st)
+                 nat.ptr(ds.rev_idx), lzp, lzi, nat.ptr(self.hbits) if self.hbits is not None else 0,
+                 nat.ptr(self.nnz), nat.ptr(segcnt), nat.ptr(self.wit), st)
         self._ph("light_merge", False)
         self._ph("segments", True)
         nat.call("mmj_exclusive_scan_i32", nat.ptr(segcnt), nat.ptr(segoff), nseg, nat.ptr(self.ws.scan_ws(nseg)), st)
@@ -382,6 +417,11 @@ class TwoPathEngine:
         light = int(self.wit.item()) - wit0
         self.stats.out_size += total
         return ChunkResult(x0, x1, total, codes[:total], None, light)
+
+    def _has_heavy(self) -> int:
+        """mmj_merge_emit / mmj_tile_merge heavy source: 0 none, 1 the chunk
+        bitmap written by the tcgen05 product, 2 the heavy-y bit rows."""
+        return 2 if self.hbits is not None else int(self.A is not None)
 
     def _tail_tables(self):
         """(full, light-z) column-block split tables of the S-side lists for
@@ -426,9 +466,11 @@ class TwoPathEngine:
         slot = self._async_slot()
         spf, spl = self._tail_tables()
         self._ph("merge_emit", True)
-        nat.call("mmj_merge_emit", nat.ptr(buf), int(self.A is not None), x0, rows, self.wpr, self.dom_z,
+        heavy_src = self.hbits if self.hbits is not None else buf
+        nat.call("mmj_merge_emit", nat.ptr(heavy_src), self._has_heavy(), x0, rows, self.wpr, self.dom_z,
                  nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.left_deg), self.d2, hp, nat.ptr(ds.rev_ptr),
-                 nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(slot),
+                 nat.ptr(ds.rev_idx), lzp, lzi, spf, spl, nat.ptr(self.wit), nat.ptr(self.nnz), nat.ptr(codes),
+                 nat.ptr(slot),
                  nat.ptr(ws), wsb, st)
         self._ph("merge_emit", False)
         self.stats.chunks += 1

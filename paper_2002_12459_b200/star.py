@@ -105,6 +105,7 @@ class StarEngine:
         self.wit = torch.zeros(1, dtype=torch.int64, device="cuda")
         # projection tail: scan + look-back + emission in one kernel (MMJ_FUSED_EMIT=0: scan, then emission)
         self.one_kernel_tail = os.environ.get("MMJ_FUSED_EMIT", "1") != "0"
+        self.timer = None          # optional PhaseTimer (bench instrumentation)
 
     def prepare(self):
         torch = self.torch
@@ -147,8 +148,13 @@ class StarEngine:
                              0, nat.ptr(self.hpos), nat.ptr(h), 0, rows, self.kpad, st)
                 self.H.append(h)
 
-    def run(self, sink=None):
-        """Evaluate every x1 chunk.  Without `sink` the codes (and counts) are
+    def _ph(self, name: str, start: bool):
+        if self.timer is not None:
+            (self.timer.start if start else self.timer.stop)(name)
+
+    def run(self, sink=None, x1_range=None):
+        """Evaluate every x1 chunk (of ``x1_range`` = [lo, hi) when given:
+        x1-range sharding).  Without `sink` the codes (and counts) are
         collected to host numpy arrays; with `sink(x1_lo, x1_hi, codes_dev,
         counts_dev)` they stay on the device (valid during the call)."""
         torch = self.torch
@@ -159,12 +165,13 @@ class StarEngine:
         rev_idxs = _ptr_array([nat.ptr(d.rev_idx) for d in self.dev])
         heavy_ptrs = _ptr_array([nat.ptr(h) for h in self.H]) if self.H else None
         codes_out, counts_out = [], []
-        d1 = self.dims[0]
-        for xa in range(0, d1, self.x1_per_chunk):
-            xb = min(d1, xa + self.x1_per_chunk)
+        lo1, hi1 = (0, self.dims[0]) if x1_range is None else x1_range
+        for xa in range(lo1, hi1, self.x1_per_chunk):
+            xb = min(hi1, xa + self.x1_per_chunk)
             rows = (xb - xa) * self.row_per_x1
             ld = self.ldc if self.counts else self.wpr
             buf = self.ws.get("star_out", rows * ld, torch.int32)
+            self._ph("heavy_mma", True)
             if self.H is not None:
                 arows = _rup(rows, 256)
                 A = self.ws.get("star_A", arows * self.kpad, torch.uint8)
@@ -180,9 +187,12 @@ class StarEngine:
                          mode, 0, nat.ptr(buf), ld, nat.ptr(self.nnz), 0, st)
             else:
                 buf.zero_()
+            self._ph("heavy_mma", False)
+            self._ph("light", True)
             lws = self.ws.get("star_lws", int(self.lib.mmj_star_light_workspace_bytes(self.n_light)), torch.uint8)
             nat.call("mmj_star_light", self.k, dims_arr, rev_ptrs, rev_idxs, nat.ptr(self.light_y), self.n_light, xa,
                      xb, 1 if self.counts else 0, nat.ptr(buf), ld, nat.ptr(self.wit), nat.ptr(lws), st)
+            self._ph("light", False)
             x0 = xa * self.row_per_x1
             if self.counts:
                 ncell = rows * self.ldc
@@ -209,8 +219,10 @@ class StarEngine:
                 fws = self.ws.get("fuse_ws", wsb, torch.uint8)
                 codes = self.ws.get("codes", rows * self.dk, torch.int64)
                 tot = self.ws.get("star_total", 1, torch.int64)
+                self._ph("merge_emit", True)
                 nat.call("mmj_merge_emit", nat.ptr(buf), 1, x0, rows, self.wpr, self.dk, 0, 0, 0, 0, 0, 0, 0, 0, 0,
-                         0, 0, 0, nat.ptr(self.wit), nat.ptr(codes), nat.ptr(tot), nat.ptr(fws), wsb, st)
+                         0, 0, nat.ptr(self.wit), 0, nat.ptr(codes), nat.ptr(tot), nat.ptr(fws), wsb, st)
+                self._ph("merge_emit", False)
                 total = int(tot.item())
                 if sink is not None:
                     sink(xa, xb, codes[:total], None)

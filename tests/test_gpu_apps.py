@@ -234,7 +234,8 @@ def test_bsi_tables_abi_errors():
     nat.require_cuda()
     lib = nat.load()
     assert lib.mmj_bsi_direct_table(0, 0, 0, 0, 0, 0, 0) == nat.MMJ_ERR_ARG
-    assert lib.mmj_bsi_answer_tables(0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 4, 0, 0, 0, 0, 0, 0) == nat.MMJ_ERR_ARG
+    assert lib.mmj_bsi_answer(0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 0, 0, 6, 0, 0) == nat.MMJ_ERR_ARG
+    assert lib.mmj_bsi_records(0, 0, 1, 0, 12, 0, 0, 0) == nat.MMJ_ERR_ARG
 
 
 def test_star_golden():

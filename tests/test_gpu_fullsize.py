@@ -3,13 +3,13 @@
 * cfg1 (two-path self-join, 200k tuples) in full, against the checksum of the
   REFERENCE's own full output (tests/golden/cfg1_reference.json, 387,365,144
   codes, made by make_golden.py --cfg1) and its stats;
-* cfg2 (5M + 5M two-path, ~1.3e11 output tuples) through the chunked device
-  path, with x-slices checked against the oracle (pi(sigma_X R join S) =
-  sigma_X pi(R join S), compared in raw-value space) and every chunk strictly
-  increasing;
+* cfg2 (5M + 5M two-path, 128,713,977,893 output tuples) through the exact
+  engine bench.py times: |OUT|, per-chunk checksums equal to the three-kernel
+  tail, and the boundary rows of every chunk vs the oracle (pi(sigma_X R join
+  S) = sigma_X pi(R join S), compared in raw-value space);
 * cfg3 (3 x 300k star) x1-slices vs the oracle; cfg4 (SSJ, 2M pairs, c=4)
-  set-slices vs the oracle; cfg5 (BSI) at 1/8 scale vs the oracle on every
-  query (the full 64M + 64M size is exercised by tools/bench_configs.py).
+  set-slices vs the oracle; cfg5 (BSI) at full scale and at 1/8 scale vs
+  the oracle on every query.
 """
 
 import json
@@ -64,51 +64,82 @@ def _raw_pairs_of(codes, dz, lv_x, lv_z):
     return np.stack([np.asarray(lv_x)[codes // dz], np.asarray(lv_z)[codes % dz]], axis=1)
 
 
-def test_cfg2_chunks_sorted_and_x_slices_match_oracle(oracle):
+def test_cfg2_bench_configuration_exact(oracle, monkeypatch):
+    """The exact engine bench.py times on cfg2 (gpu_plan, 16384-row chunks,
+    asynchronous chunks, the one-kernel tail k_merge_emit, all 31 chunks):
+      * |OUT| = 128,713,977,893 (bench.CFG2_OUT) and every chunk strictly
+        increasing, chunks in code order;
+      * per-chunk sizes and order-sensitive 64-bit checksums equal to the
+        three-kernel tail's (k_tile_merge -> scan -> k_emit_pf16) and to the
+        fused tail fed by the tcgen05 heavy product instead of the in-tile
+        OR of heavy-y bit rows;
+      * the first and last 3 x of EVERY chunk (186 rows, each covering all
+        column blocks / tile boundaries of its row) equal the oracle's
+        sigma_X two-path, compared in raw-value space.
+    Reference: joinproject.py:155-225."""
     import torch
 
-    from paper_2002_12459_b200 import datagen
-    from paper_2002_12459_b200.joinproject import two_path_join_chunks
-    from paper_2002_12459_b200.optimizer import gpu_plan
-    from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce
-    wl = datagen.config("cfg2")
-    R, S = semi_join_reduce(Relation.from_raw_pairs("R", wl.relations[0]), Relation.from_raw_pairs("S", wl.relations[1]))
-    r, s = build_indexed(R), build_indexed(S)
+    import bench
+    from paper_2002_12459_b200 import _native as nat
+    args = bench._args(["--config", "cfg2"])
+    wl = bench.TwoPath(args, 0, 1)
+    wl.setup()
+    r, s = wl.r, wl.s
     dz = s.rel.dom_left
-    plan = gpu_plan(r, s)
-    slices = [(0, 6), (250000, 250006), (r.rel.dom_left - 6, r.rel.dom_left)]
-    want = {}
-    total = 0
-    prev_last = -1
-    for part in two_path_join_chunks(r, s, plan=plan, chunk_rows=4096, device_output=True):
-        c = part.codes
-        n = int(c.numel())
-        total += n
-        if n:
-            assert bool((c[1:] > c[:-1]).all().item()) if n > 1 else True
-            first, last = int(c[0].item()), int(c[-1].item())
-            assert first > prev_last
-            prev_last = last
-        x0, x1 = part.stats["x_range"]
-        for lo, hi in slices:
-            if lo < x1 and hi > x0:
-                xs = c // dz
-                sel = c[(xs >= lo) & (xs < hi)].cpu().numpy()
-                want.setdefault((lo, hi), []).append(sel)
-    assert total > 1.2e11          # ~1.26e11 distinct tuples
-    Rraw, Sraw = wl.relations
-    OS = oracle.encode(Sraw)
-    for (lo, hi), parts in want.items():
-        got = np.concatenate(parts)
-        xs_raw = np.asarray(r.rel.left_values)[lo:hi]
-        a, b = oracle.semi_join_many([oracle.encode(Rraw[np.isin(Rraw[:, 0], xs_raw)]), OS])
-        exp = oracle.two_path(a, b, None)
-        g = _raw_pairs_of(got, dz, r.rel.left_values, s.rel.left_values)
-        e = _raw_pairs_of(exp.codes, exp.dims[1], a.left_values, b.left_values)
-        gk = g[:, 0] * (1 << 31) + g[:, 1]
-        ek = np.sort(e[:, 0] * (1 << 31) + e[:, 1])
-        assert np.array_equal(gk, ek), (lo, hi)
-    del torch
+    st = nat.stream_handle
+
+    def run(one_kernel, heavy=""):
+        monkeypatch.setenv("MMJ_HEAVY", heavy)
+        eng = wl.engine()
+        eng.one_kernel_tail = one_kernel
+        eng.prepare()
+        assert eng.chunk_rows == 16384
+        assert eng.heavy_kernel == (heavy or "or")      # the bench's default: the in-tile OR
+        sizes, sums, rows = [], [], {}
+        prev = -1
+        for a, b in eng.chunk_bounds(wl.x_lo, wl.x_hi):
+            ch = eng.run_chunk(a, b, sync=False)          # bench.TwoPath.step's call
+            n = int(ch.total_dev.item())
+            c = ch.codes[:n]
+            if n > 1:
+                assert bool((c[1:] > c[:-1]).all().item())
+            if n:
+                assert int(c[0].item()) > prev
+                prev = int(c[-1].item())
+            acc = torch.zeros(2, dtype=torch.int64, device="cuda")
+            nat.call("mmj_code_checksum", nat.ptr(c), n, 0, nat.ptr(acc), st())
+            sizes.append(n)
+            sums.append(tuple(acc.cpu().tolist()))
+            if one_kernel:
+                cut = torch.tensor([(a + 3) * dz, (b - 3) * dz], dtype=torch.int64, device="cuda")
+                i0, i1 = (int(v) for v in torch.searchsorted(c, cut).cpu())
+                rows[(a, b)] = (c[:i0].cpu().numpy(), c[i1:].cpu().numpy())
+        stats = eng.finish()
+        return sizes, sums, rows, stats
+
+    sizes, sums, rows, stats = run(True)
+    assert len(sizes) == 31 and sum(sizes) == bench.CFG2_OUT == stats.out_size
+    sizes3, sums3, _, stats3 = run(False)
+    assert sizes3 == sizes and sums3 == sums
+    assert (stats3.light_intermediate, stats3.heavy_pairs) == (stats.light_intermediate, stats.heavy_pairs)
+    # the same chunks with the heavy part from the tcgen05 product (an
+    # independent computation of the heavy cells): identical output and stats
+    sizes_m, sums_m, _, stats_m = run(True, "mma")
+    assert sizes_m == sizes and sums_m == sums
+    assert (stats_m.light_intermediate, stats_m.heavy_pairs) == (stats.light_intermediate, stats.heavy_pairs)
+    # oracle on the 6 boundary rows of every chunk, one sigma_X join
+    lv_r, lv_s = np.asarray(r.rel.left_values), np.asarray(s.rel.left_values)
+    xs = np.concatenate([np.r_[a:a + 3, b - 3:b] for a, b in rows])
+    got = np.concatenate([np.concatenate(v) for v in rows.values()])
+    Rraw, Sraw = wl.Rraw, wl.Sraw
+    A, B = oracle.semi_join_many([oracle.encode(Rraw[np.isin(Rraw[:, 0], lv_r[xs])]), oracle.encode(Sraw)])
+    exp = oracle.two_path(A, B, None)
+    g = np.stack([lv_r[got // dz], lv_s[got % dz]], axis=1)
+    e = np.stack([np.asarray(A.left_values)[exp.codes // exp.dims[1]],
+                  np.asarray(B.left_values)[exp.codes % exp.dims[1]]], axis=1)
+    gk = np.sort(g[:, 0] * (1 << 31) + g[:, 1])
+    ek = np.sort(e[:, 0] * (1 << 31) + e[:, 1])
+    assert len(gk) > 4e7 and np.array_equal(gk, ek)
 
 
 def test_cfg3_star_x1_slices(oracle):
@@ -158,6 +189,31 @@ def test_cfg4_ssj_set_slices(oracle):
         m = np.isin(lv[a], raws)
         got = set(zip(lv[a[m]].tolist(), lv[b[m]].tolist(), n[m].tolist()))
         assert got == exp
+
+
+def test_cfg5_bsi_full_scale_all_queries(oracle):
+    """cfg5 at BASELINE size (64M + 64M tuples, the 4M-query batch plus 4096
+    queries with ids no relation holds): every answer equals the oracle's
+    per-query set intersection (apps.py:314-351 restated), None markers
+    included; relations ingested on the device as bench.py does."""
+    import torch
+
+    from paper_2002_12459_b200 import datagen
+    from paper_2002_12459_b200.apps import bsi_answer_batch_arrays
+    from paper_2002_12459_b200.ingest import from_raw_pairs_device
+    wl = datagen.config("cfg5")
+    raws = [torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)) for x in wl.relations]
+    r = from_raw_pairs_device("R", raws[0])
+    s = from_raw_pairs_device("S", raws[1])
+    rng = np.random.default_rng(5)
+    extra = rng.integers(0, 4_000_000, (4096, 2))
+    extra[::2, 0] += 4_000_000          # unknown x
+    extra[1::4, 1] = -7 - extra[1::4, 1]  # unknown z
+    q = np.concatenate([wl.batch, extra])
+    got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1])
+    exp = oracle.bsi(oracle.encode(wl.relations[0]), oracle.encode(wl.relations[1]), q[:, 0], q[:, 1])
+    assert np.array_equal(got, exp)
+    assert (exp[-4096:] == -1).sum() >= 2048 and 0.55 < (exp[:-4096] == 1).mean() < 0.7
 
 
 def test_cfg5_bsi_eighth_scale_all_queries(oracle):

@@ -28,10 +28,12 @@ def _wide(seed, nx, nr, nz, ns, dom_y, s_exp):
     return r_pairs, s_zy
 
 
+@pytest.mark.parametrize("heavy", ["mma", "or"])
 @pytest.mark.parametrize("plan", [("partitioned", 40, 1), ("partitioned", 8, 3), ("fulljoin", 0, 0)])
-def test_wide_rows_match_oracle(oracle, plan):
+def test_wide_rows_match_oracle(oracle, plan, heavy, monkeypatch):
     from paper_2002_12459_b200.joinproject import two_path_join
     from paper_2002_12459_b200.optimizer import ThresholdPlan
+    monkeypatch.setenv("MMJ_HEAVY", heavy)   # tcgen05 product / in-tile OR of heavy-y bit rows
     r_pairs, s_pairs = _wide(71, 32, 4_000, 3_000_000, 1_000_000, 3000, 1.1)
     r, s = _rels(r_pairs, s_pairs)
     assert s.rel.dom_left > 3 * 8192 * 32     # four column blocks per row (dom_z ~ 790k)

@@ -60,8 +60,13 @@ def _check(pkg, oracle, r_pairs, s_pairs, plans, self_join=False, chunk_rows=Non
                     assert got.stats[key] == exp.stats[key], (key, strategy, d1, d2, counts)
 
 
+@pytest.mark.parametrize("heavy", ["mma", "or"])
 @pytest.mark.parametrize("seed", range(6))
-def test_two_path_random_plans(pkg, oracle, seed):
+def test_two_path_random_plans(pkg, oracle, seed, heavy, monkeypatch):
+    """Both heavy kernels of the projection: the tcgen05 product into a chunk
+    bitmap and the in-tile OR of heavy-y bit rows (the count path always
+    uses the product)."""
+    monkeypatch.setenv("MMJ_HEAVY", heavy)
     rng = np.random.default_rng(seed)
     n = int(rng.integers(20, 400))
     dom = int(rng.integers(5, 40))
@@ -73,8 +78,10 @@ def test_two_path_random_plans(pkg, oracle, seed):
     _check(pkg, oracle, rp, sp, plans)
 
 
+@pytest.mark.parametrize("heavy", ["", "mma", "or"])
 @pytest.mark.parametrize("chunk_rows", [None, 128])
-def test_two_path_zipf_medium(pkg, oracle, chunk_rows):
+def test_two_path_zipf_medium(pkg, oracle, chunk_rows, heavy, monkeypatch):
+    monkeypatch.setenv("MMJ_HEAVY", heavy)
     rng = np.random.default_rng(11)
     rp = zipf_pairs(rng, 20000, 1500, 3000, 1.2)
     sp = zipf_pairs(rng, 20000, 1300, 3000, 1.1)

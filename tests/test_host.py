@@ -183,11 +183,11 @@ def test_capi_argument_errors_without_gpu():
     lib = _native.load()
     # a pitch that is not a multiple of 32 words
     rc = lib.mmj_merge_emit(None, 0, 0, 4, 33, 1000, None, None, None, 1, None, None, None, None, None, None, None,
-                            None, None, None, None, 0, None)
+                            None, None, None, None, None, 0, None)
     assert rc == 1 and b"multiple of 32" in lib.mmj_last_error()
     # a workspace smaller than mmj_merge_emit_workspace_size
     rc = lib.mmj_merge_emit(None, 0, 0, 4, 32, 1000, None, None, None, 1, None, None, None, None, None, None, None,
-                            None, None, None, ctypes.c_void_p(16), 8, None)
+                            None, None, None, None, ctypes.c_void_p(16), 8, None)
     assert rc == 5 and b"workspace" in lib.mmj_last_error()
     # heavy product modes outside the enum
     rc = lib.mmj_heavy_mma(None, 256, None, 256, 128, 0, 128, 0, 128, 6, 0, None, 8, None, 0, None)
@@ -208,9 +208,10 @@ def test_capi_new_entry_points_argument_errors_without_gpu():
     assert b"domains" in lib.mmj_last_error()
     assert lib.mmj_bsi_direct_table(None, None, 0, 0, 0, None, None) == 1
     assert b"range" in lib.mmj_last_error()
-    assert lib.mmj_bsi_answer_tables(None, None, 1, None, 0, 1, None, 0, 1, None, None, 4, None, None, None, None,
-                                     None, None) == 1
-    assert b"direct tables" in lib.mmj_last_error()
+    assert lib.mmj_bsi_answer(None, None, 1, None, None, 1, None, 0, 1, None, None, 1, None, 0, 1, None, None, None,
+                              None, 6, None, None) == 1
+    assert b"words" in lib.mmj_last_error()
+    assert lib.mmj_bsi_record_words(8) == 16 and lib.mmj_bsi_record_words(32) == 48
     assert lib.mmj_split_codes(None, 4, 0, None, None, None) == 1
     assert b"split_codes" in lib.mmj_last_error()
 
@@ -223,6 +224,13 @@ def test_engine_host_degree_max_memo():
     assert _host_max(b) == 9
     assert _host_max(np.empty(0, dtype=np.int64)) == 0
     assert _host_max([1, 40, 7]) == 40          # list input (reference objects may hold lists)
+    c = np.array([1, 2, 3])
+    assert _host_max(c) == 3
+    c[0] = 50                                   # writeable arrays are never memoised: no stale maximum
+    assert _host_max(c) == 50
+    d = np.array([4, 5])
+    d.flags.writeable = False                   # IndexedRelation freezes its degree vectors
+    assert _host_max(d) == 5 and _host_max(d) == 5
 
 
 def test_product_fails_loudly_without_gpu():
