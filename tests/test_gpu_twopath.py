@@ -168,10 +168,14 @@ def _pair_boundary_pairs(rng, deg_x0, n_y=300):
 
 
 @pytest.mark.parametrize("deg_x0", [126, 127, 128])
-def test_pair_operand_count_boundary(pkg, oracle, deg_x0):
+@pytest.mark.parametrize("heavy", ["mma", "or"])
+def test_pair_operand_count_boundary(pkg, oracle, deg_x0, heavy, monkeypatch):
     """BITMAP_PAIR packs two cells as c0 + 128*c1 (engine.py: on iff one
     side's heavy degrees are <= 127): counts of exactly 127 on both slots must
-    not carry, and 128 must switch the pair form off."""
+    not carry, and 128 must switch the pair form off.  The tcgen05 product is
+    forced (MMJ_HEAVY=mma; the default picks the in-tile OR for these sparse
+    heavy rows, which has no pair operand) and the OR path checked too."""
+    monkeypatch.setenv("MMJ_HEAVY", heavy)
     from paper_2002_12459_b200.joinproject import _collect, _engine
     from paper_2002_12459_b200.optimizer import ThresholdPlan
     rng = np.random.default_rng(deg_x0)
@@ -180,7 +184,9 @@ def test_pair_operand_count_boundary(pkg, oracle, deg_x0):
     plan = ThresholdPlan("partitioned", 1, 1)
     eng = _engine(r, s, plan, False)
     eng.prepare()
-    assert eng.pairs == (deg_x0 <= 127 or int(np.max(s.left_deg)) <= 127)
+    assert eng.heavy_kernel == heavy
+    if heavy == "mma":
+        assert eng.pairs == (deg_x0 <= 127 or int(np.max(s.left_deg)) <= 127)
     got = _collect(eng)
     R, S = _oracle_rels(oracle, rp, sp)
     exp = oracle.two_path(R, S, oracle.OPlan("partitioned", 1, 1))
