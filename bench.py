@@ -332,11 +332,16 @@ class TwoPath:
             base += n
             sizes.append(n)
         st = eng.finish()
+        from paper_2002_12459_b200.shard import combine_checksums
         s, w = (int(v) & (2 ** 64 - 1) for v in acc.cpu().tolist())
-        out = {"out": base, "sum": s, "wsum": w, "max_chunk": max(sizes) if sizes else 0,
+        # whole-job stamp: the rank-order concatenation of every shard's codes
+        n_all, s, w = combine_checksums(base, s, w)
+        out = {"out": n_all, "sum": s, "wsum": w, "max_chunk": max(sizes) if sizes else 0,
                "light_intermediate": st.light_intermediate, "heavy_pairs": st.heavy_pairs}
-        if self.args.config == "cfg2" and self.world == 1 and not self.args.x_limit:
-            out["out_matches_pinned"] = base == CFG2_OUT
+        if self.world > 1:
+            out["scope"] = f"all {self.world} ranks (rank-order concatenation); statistics rank 0's"
+        if self.args.config == "cfg2" and not self.args.x_limit:
+            out["out_matches_pinned"] = n_all == CFG2_OUT
         return out
 
     def report(self, phases, t_step, out_local, int8_peak):
@@ -921,8 +926,13 @@ class Bsi:
         return self.nq
 
     def verify(self):
-        a = self.ans[: self.nq].cpu().numpy()
-        return {"answers": int(self.nq), "true": int((a == 1).sum()), "false": int((a == 0).sum()),
+        """Whole-batch stamp: every rank's slice gathered back into batch
+        order (shard.gather_batch_answers), then counts and an order-sensitive
+        checksum -- identical for any number of ranks."""
+        from paper_2002_12459_b200.shard import gather_batch_answers
+        nq_all = len(self.wl.batch)
+        a = gather_batch_answers(self.ans[: self.nq], nq_all).cpu().numpy()
+        return {"answers": int(len(a)), "true": int((a == 1).sum()), "false": int((a == 0).sum()),
                 "none": int((a == -1).sum()),
                 "checksum": int((np.arange(1, len(a) + 1, dtype=np.uint64) * (a.astype(np.int64) + 2).astype(np.uint64))
                                 .sum(dtype=np.uint64))}

@@ -49,6 +49,65 @@ def batch_slice(nq: int, rank: int, world: int) -> tuple:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+def combine_checksums(n_local: int, s_local: int, w_local: int, group=None) -> tuple:
+    """Whole-output (|OUT|, sum, weighted sum) of the rank-order concatenation
+    of the shards' code runs, every rank computing its own with base 0
+    (mmj_code_checksum: s = sum c_i, w = sum (base + i + 1) c_i mod 2^64, so a
+    run shifted by `base` codes adds base * s).  One all-gather of three
+    words per rank; every rank returns the same triple."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return int(n_local), int(s_local) & _M64, int(w_local) & _M64
+    dev = _group_device(group)
+    mine = torch.tensor([_i64(n_local), _i64(s_local), _i64(w_local)], dtype=torch.int64, device=dev)
+    parts = [torch.empty(3, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    n = s = w = 0
+    for p in parts:
+        pn, ps, pw = (int(v) & _M64 for v in p.cpu().tolist())
+        w = (w + pw + n * ps) & _M64
+        s = (s + ps) & _M64
+        n += pn
+    return n, s, w
+
+
+def gather_batch_answers(ans_local, nq: int, group=None):
+    """Answers of a position-sharded BSI batch back in batch order on every
+    rank: rank r holds the int8 answers of batch_slice(nq, r, world); slices
+    are padded to the longest for the all-gather (NCCL needs equal sizes) and
+    cut back in rank order.  Returns a tensor of nq answers on ans_local's
+    device."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return ans_local[:nq]
+    rank = dist.get_rank(group)
+    lo, hi = batch_slice(nq, rank, world)
+    if int(ans_local.numel()) < hi - lo:
+        raise ValueError(f"rank {rank}: {ans_local.numel()} answers for the {hi - lo}-query slice")
+    width = max(hi_ - lo_ for lo_, hi_ in (batch_slice(nq, k, world) for k in range(world)))
+    width = max(width, 1)
+    dev = _group_device(group)
+    pad = torch.full((width,), -2, dtype=torch.int8, device=dev)
+    pad[: hi - lo] = ans_local[: hi - lo].to(dev)
+    parts = [torch.empty(width, dtype=torch.int8, device=dev) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    out = torch.cat([parts[k][: b - a] for k, (a, b) in enumerate(batch_slice(nq, k, world) for k in range(world))])
+    return out.to(ans_local.device)
+
+
+_M64 = (1 << 64) - 1
+
+
+def _i64(v: int) -> int:
+    """uint64 bit pattern as a signed int64 (torch has no uint64 all-gather)."""
+    v = int(v) & _M64
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
 def two_path_join_shard(r, s, plan=None, rank: int = 0, world: int = 1, want_counts: bool = False,
                         chunk_rows=None):
     """This rank's part of two_path_join: an OutputSet over its x range

@@ -139,3 +139,80 @@ def test_gloo_replicate_relation_and_global_degrees():
     for p in procs:
         p.join(timeout=60)
     assert res == [(0, True), (1, True)]
+
+
+# ---- bench.py's rank orchestration (shard.combine_checksums /
+# shard.gather_batch_answers, the calls bench.py's verify() makes on every
+# rank) with the CPU oracle standing in for the per-rank kernel call only
+
+M64 = (1 << 64) - 1
+
+
+def host_checksum(codes):
+    """numpy restatement of mmj_code_checksum with base 0 (scan.cu)."""
+    c = np.asarray(codes, dtype=np.int64).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        s = int(c.sum(dtype=np.uint64))
+        w = int((np.arange(1, len(c) + 1, dtype=np.uint64) * c).sum(dtype=np.uint64))
+    return len(c), s & M64, w & M64
+
+
+def _orch_worker(rank, world, port, out):
+    try:
+        out.put((rank, _orch_body(rank, world, port)))
+    except Exception as e:  # noqa: BLE001 - report to the parent
+        import traceback
+        out.put((rank, traceback.format_exc() + repr(e)))
+
+
+def _orch_body(rank, world, port):
+    import torch
+
+    from oracle import mmjoin_oracle as o
+    from paper_2002_12459_b200 import shard
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    res = {}
+    # two-path (cfg2's orchestration): witness-balanced x range -> this rank's
+    # sorted codes -> whole-job (|OUT|, sum, wsum) stamp
+    rp, sp, r, s = _rels(7)
+    lo, hi = shard.shard_of(r, s, rank, world)
+    OR, OS = o.semi_join_many([o.encode(rp), o.encode(sp)])
+    full = o.two_path(OR, OS, None)
+    x = full.codes // full.dims[1]
+    mine = full.codes[(x >= lo) & (x < hi)]                 # stand-in for the engine's chunks
+    stamp = shard.combine_checksums(*host_checksum(mine))
+    res["two_path"] = stamp == host_checksum(full.codes)
+    res["nonempty"] = len(mine) > 0
+    # BSI (cfg5's orchestration): contiguous batch slice -> answers -> batch
+    # order on every rank, uneven slice lengths included
+    rng = np.random.default_rng(11)
+    ra = np.array(random_pairs(rng, 3000, 400, 300), dtype=np.int64)
+    sa = np.array(random_pairs(rng, 3000, 400, 300), dtype=np.int64)
+    OR5, OS5 = o.encode(ra), o.encode(sa)
+    nq = 1001 + world                                        # not a multiple of world
+    qa = rng.integers(-5, 410, nq)
+    qb = rng.integers(-5, 410, nq)
+    qlo, qhi = shard.batch_slice(nq, rank, world)
+    local = torch.from_numpy(o.bsi(OR5, OS5, qa[qlo:qhi], qb[qlo:qhi]))
+    got = shard.gather_batch_answers(local, nq).numpy()
+    exp = o.bsi(OR5, OS5, qa, qb)
+    res["bsi"] = bool(np.array_equal(got, exp)) and (exp == -1).any() and (exp == 1).any()
+    dist.destroy_process_group()
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_bench_orchestration_two_path_and_bsi(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_orch_worker, args=(k, world, port, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=240) for _ in procs), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, r in res:
+        assert isinstance(r, dict), r
+        assert r == {"two_path": True, "nonempty": True, "bsi": True}, (rank, r)
