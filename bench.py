@@ -71,6 +71,8 @@ def _args(argv=None):
     ap.add_argument("--no-verify", action="store_true", help="skip the untimed checksum pass")
     ap.add_argument("--no-light-work", action="store_true", help="skip the light-pass byte count (diagnostic)")
     ap.add_argument("--x-limit", type=int, default=0, help="debug: only the first X output rows")
+    ap.add_argument("--bsi-form", default="auto", choices=["auto", "lists", "records"],
+                    help="cfg5 device algorithm (bsi.BsiEngine); answers are identical")
     return ap.parse_args(argv)
 
 
@@ -911,7 +913,7 @@ class Bsi:
         sR, sS, dom_y = self.sides
         if timer is not None:
             timer.start("build")
-        eng = BsiEngine(sR, sS, dom_y, 256)
+        eng = BsiEngine(sR, sS, dom_y, 256, form=self.args.bsi_form)
         eng.build()
         if timer is not None:
             timer.stop("build")
@@ -953,6 +955,7 @@ class Bsi:
                 "algorithmic": "B_bsi = 8 B per input tuple + 9 B per query (SURVEY 8(d) lower bound) / step time"}
         cfg = {"workload": self.wl.description + " (BASELINE configs[4])", "config_name": "cfg5",
                "queries_this_rank": self.nq, "batch_slice": [self.qlo, self.qhi], "heavy_bits": 256,
+               "bsi_form": self.eng.form,
                "index": "replicated on every rank (built from the device CSR inside every timed step)",
                "l2": "256 MiB L2 flush before every timed step"}
         return roof, info, cfg

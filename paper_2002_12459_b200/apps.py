@@ -264,11 +264,13 @@ def bsi_batch_size(rate: float, n: int) -> int:
     return math.ceil((rate * n) ** 0.6)
 
 
-def bsi_answer_batch_arrays(r, s, batch_a, batch_b, heavy_bits: int = 256) -> np.ndarray:
+def bsi_answer_batch_arrays(r, s, batch_a, batch_b, heavy_bits: int = 256, form: str = "auto") -> np.ndarray:
     """int8 answers per query: 1 = sets intersect, 0 = disjoint, -1 = an id
-    unknown to the (unreduced) relation (apps.py:321-329)."""
+    unknown to the (unreduced) relation (apps.py:321-329).  `form` picks the
+    device algorithm (bsi.BsiEngine: "records", "lists" or "auto"); the
+    answers are the same."""
     from .bsi import answer_batch
-    return answer_batch(r, s, batch_a, batch_b, heavy_bits=heavy_bits)
+    return answer_batch(r, s, batch_a, batch_b, heavy_bits=heavy_bits, form=form)
 
 
 def bsi_answer_batch(r, s, batch: Sequence[tuple]) -> list:

@@ -1,13 +1,15 @@
 """Host orchestration of batched boolean set intersection on the B200
 (apps.py:314-351).  See csrc/bsi.cu for the device algorithm.
 
-Steps (all kernels of libmmjoin_b200.so):
+Steps (all kernels of libmmjoin_b200.so), "records" form:
   1. degree split of y over both relations (mmj_heavy_y_positions) with
      delta1 chosen so that at most `heavy_bits` y are heavy;
-  2. heavy-y bitsets per left id of R and S (mmj_bsi_bits);
-  3. light lists per left id (mmj_bsi_light_lists);
-  4. per query: raw id -> dense id through each relation's own (unreduced)
+  2. one record per left id of R and S: heavy-y bitset + light list header,
+     light lists compacted in place (mmj_bsi_records);
+  3. per query: raw id -> dense id through each relation's own (unreduced)
      dictionary, bitset test, light merge intersection (mmj_bsi_answer).
+"lists" form (short lists, BsiEngine): step 3 alone, merging the two ids'
+full forward lists (mmj_bsi_answer_lists).
 If R and S do not share a right dictionary, their y ids are first mapped to
 a common raw-value space on the host (input preparation, as the reference's
 semi_join_reduce does) -- left ids, hence "known" ids, stay those of the
@@ -24,6 +26,7 @@ from . import _native as nat
 from .device import Workspace
 
 BITS_BLOCK = 128     # bitset width granularity (4 words)
+LIST_MAX_MEAN = 64   # "lists" form when both sides' mean list length is at most this
 DIRECT_SPREAD = 4    # direct id table when max - min + 1 <= 4 x the number of ids
 
 
@@ -212,17 +215,36 @@ def _dense_queries(rel, q):
 
 
 class BsiEngine:
-    """Index build + answering for one (R, S) pair (reusable across batches)."""
+    """Index build + answering for one (R, S) pair (reusable across batches).
 
-    def __init__(self, sR: BsiSide, sS: BsiSide, dom_y: int, heavy_bits: int = 256, ws=None):
+    Two exact forms of the same answers:
+      "records"  heavy-y split + one record per left id (bitset of its heavy
+                 y, then its light list): popc(bits_a & bits_b) decides any
+                 query with a heavy witness, the light lists the rest -- the
+                 heavy part of the reference's product restricted to the
+                 queried cells (apps.py:332-350 -> joinproject.py:208-216);
+      "lists"    no index build: the queried ids' forward lists are
+                 merge-intersected (mmj_bsi_answer_lists).
+    "auto" takes "lists" when both sides' mean list length is at most
+    LIST_MAX_MEAN: a record is 64 B, as many DRAM sectors as a 16-entry list,
+    so for short lists the records only add their build pass (cfg5: 16 y per
+    id; the build was 1.34 of the 2.0 ms step, r2b)."""
+
+    def __init__(self, sR: BsiSide, sS: BsiSide, dom_y: int, heavy_bits: int = 256, ws=None, form: str = "auto"):
         self.sR, self.sS, self.dom_y = sR, sS, dom_y
         self.lib = nat.load()
         if heavy_bits not in (128, 256, 512, 1024):
             raise ValueError("heavy_bits must be 128, 256, 512 or 1024")
+        if form not in ("auto", "lists", "records"):
+            raise ValueError("form must be 'auto', 'lists' or 'records'")
+        if form == "auto":
+            short = all(sd.n <= LIST_MAX_MEAN * max(sd.dom_left, 1) for sd in (sR, sS))
+            form = "lists" if short else "records"
+        self.form = form
         self.heavy_bits = max(BITS_BLOCK, -(-heavy_bits // BITS_BLOCK) * BITS_BLOCK)
         self.ws = ws or Workspace()
         self.rdeg, self.sdeg = sR.ydeg, sS.ydeg
-        self.delta1 = self._threshold()
+        self.delta1 = self._threshold() if form == "records" else None
         self.k = 0
 
     def _threshold(self) -> int:
@@ -254,7 +276,10 @@ class BsiEngine:
 
     def build(self):
         """Heavy-y split, then one record per left id on each side (heavy-y
-        bit row + light list header; light lists compacted in place)."""
+        bit row + light list header; light lists compacted in place).  The
+        "lists" form has nothing to build."""
+        if self.form == "lists":
+            return
         torch = _torch()
         st = nat.stream_handle()
         dom_y = self.dom_y
@@ -276,7 +301,6 @@ class BsiEngine:
     def answer(self, qa_dev, qb_dev, nq, dense_a=False, dense_b=False, out=None):
         torch = _torch()
         ans = out if out is not None else torch.empty(max(nq, 1), dtype=torch.int8, device="cuda")
-        (rrec, rovf), (srec, sovf) = self.sides
 
         def idmap(side, dense):
             if dense:
@@ -285,13 +309,19 @@ class BsiEngine:
             if t is not None:
                 return 0, 0, 0, nat.ptr(t[0]), t[1], t[2]
             return nat.ptr(side.sorted_vals), nat.ptr(side.order), side.dom_left, 0, 0, 0
+        if self.form == "lists":
+            nat.call("mmj_bsi_answer_lists", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, *idmap(self.sR, dense_a),
+                     *idmap(self.sS, dense_b), nat.ptr(self.sR.fwd_ptr), nat.ptr(self.sR.fwd_idx),
+                     nat.ptr(self.sS.fwd_ptr), nat.ptr(self.sS.fwd_idx), nat.ptr(ans), nat.stream_handle())
+            return ans[:nq]
+        (rrec, rovf), (srec, sovf) = self.sides
         nat.call("mmj_bsi_answer", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, *idmap(self.sR, dense_a),
                  *idmap(self.sS, dense_b), nat.ptr(rrec), nat.ptr(rovf), nat.ptr(srec), nat.ptr(sovf), self.words,
                  nat.ptr(ans), nat.stream_handle())
         return ans[:nq]
 
 
-def answer_batch(r, s, batch_a, batch_b, heavy_bits: int = 256) -> np.ndarray:
+def answer_batch(r, s, batch_a, batch_b, heavy_bits: int = 256, form: str = "auto") -> np.ndarray:
     """int8 answers (1 / 0 / -1 for None) for raw query ids."""
     torch = _torch()
     nat.require_cuda()
@@ -301,7 +331,7 @@ def answer_batch(r, s, batch_a, batch_b, heavy_bits: int = 256) -> np.ndarray:
     if nq == 0:
         return np.empty(0, dtype=np.int8)
     sR, sS, dom_y = prepare(r, s)
-    eng = BsiEngine(sR, sS, dom_y, heavy_bits)
+    eng = BsiEngine(sR, sS, dom_y, heavy_bits, form=form)
     eng.build()
 
     def to_dev(rel, side, q):

@@ -159,6 +159,60 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer(const int64_t* __restrict__ 
   }
 }
 
+// Sorted-list intersection of the two queried ids' forward lists (both
+// sorted by the shared y id): the index IS the relations' CSR, so nothing is
+// built per batch.  Taken when the lists are short (cfg5: 16 y per id on
+// average), where a bitset record (64 B) costs as many DRAM sectors as the
+// list itself and its build pass would be the larger part of the step.  Both
+// lists' 32-byte sectors are requested before the (dependent) merge.
+__global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restrict__ qa,
+                                                          const int64_t* __restrict__ qb, int64_t nq, const IdMap ma,
+                                                          const IdMap mb, const int32_t* __restrict__ pa_ptr,
+                                                          const int32_t* __restrict__ pa_idx,
+                                                          const int32_t* __restrict__ pb_ptr,
+                                                          const int32_t* __restrict__ pb_idx, int8_t* __restrict__ ans) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t ia = map_id(ma, __ldcs(qa + q));
+    const int32_t ib = map_id(mb, __ldcs(qb + q));
+    if (ia < 0 || ib < 0) {
+      ans[q] = -1;
+      continue;
+    }
+    const int2 ra = make_int2(__ldg(pa_ptr + ia), __ldg(pa_ptr + ia + 1));
+    const int2 rb = make_int2(__ldg(pb_ptr + ib), __ldg(pb_ptr + ib + 1));
+    const int32_t na = ra.y - ra.x, nb = rb.y - rb.x;
+    bool hit = false;
+    if (na > 0 && nb > 0) {
+      const int32_t* la = pa_idx + ra.x;
+      const int32_t* lb = pb_idx + rb.x;
+      for (int32_t i = 0; i < na; i += 8) prefetch_l1(la + i);
+      for (int32_t j = 0; j < nb; j += 8) prefetch_l1(lb + j);
+      prefetch_l1(la + na - 1);
+      prefetch_l1(lb + nb - 1);
+      // disjoint value ranges: no merge at all
+      const int32_t a0 = __ldg(la), a1 = __ldg(la + na - 1), b0 = __ldg(lb), b1 = __ldg(lb + nb - 1);
+      if (a1 >= b0 && b1 >= a0) {
+        int32_t i = 0, j = 0;
+        int32_t u = a0, v = b0;
+        while (true) {
+          if (u == v) {
+            hit = true;
+            break;
+          }
+          if (u < v) {
+            if (++i == na) break;
+            u = __ldg(la + i);
+          } else {
+            if (++j == nb) break;
+            v = __ldg(lb + j);
+          }
+        }
+      }
+    }
+    ans[q] = hit ? 1 : 0;
+  }
+}
+
 __global__ void k_direct_table(const int64_t* __restrict__ sorted, const int32_t* __restrict__ order, int64_t n,
                                int64_t vmin, int64_t range, int32_t* __restrict__ table) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -231,6 +285,24 @@ int bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* 
     default: k_bsi_answer<32><<<g, TPB, 0, st>>>(qa, qb, nq, a, b, stride, ans); break;
   }
   MMJ_CHECK_LAUNCH("k_bsi_answer");
+  return MMJ_OK;
+}
+
+int bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted,
+                     const int32_t* r_order, int64_t r_n, const int32_t* r_table, int64_t r_min, int64_t r_range,
+                     const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const int32_t* s_table,
+                     int64_t s_min, int64_t s_range, const int32_t* r_fwd_ptr, const int32_t* r_fwd_idx,
+                     const int32_t* s_fwd_ptr, const int32_t* s_fwd_idx, int8_t* ans, cudaStream_t st) {
+  if (nq == 0) return MMJ_OK;
+  if (r_fwd_ptr == nullptr || s_fwd_ptr == nullptr) {
+    set_error("bsi_answer_lists: both forward CSRs are required");
+    return MMJ_ERR_ARG;
+  }
+  const IdMap a{r_sorted, r_order, r_n, r_table, r_min, r_range};
+  const IdMap b{s_sorted, s_order, s_n, s_table, s_min, s_range};
+  k_bsi_answer_lists<<<grid_for(nq, TPB, 16), TPB, 0, st>>>(qa, qb, nq, a, b, r_fwd_ptr, r_fwd_idx, s_fwd_ptr,
+                                                             s_fwd_idx, ans);
+  MMJ_CHECK_LAUNCH("k_bsi_answer_lists");
   return MMJ_OK;
 }
 

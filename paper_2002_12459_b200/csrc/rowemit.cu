@@ -99,6 +99,43 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ v, in
   return lo;
 }
 
+// Emission of one 1024-cell segment (32 bitmap words) by one warp in output
+// order without shared-memory staging: step i takes word i, lane l owns its
+// bit l (cell 32 i + l) and, when set, writes the code to out[excl_i +
+// popc(word_i & lanemask_lt)] -- the active lanes of each store cover one
+// contiguous run, so every store is a single coalesced request.  `pw` is the
+// warp's 32-entry (word, exclusive code prefix) table, filled by the caller
+// (broadcast LDS.128 reads: two words per load).  ~7.5 instructions per word
+// against ~19 for the staged 16-bit offset path (ncu r2b source page).
+// Returns false when the segment's low code word could carry (the caller
+// takes the 64-bit path): code = seg_base + cell with seg_base's low 32 bits
+// <= 2^32 - 1025.
+__device__ __forceinline__ bool emit_segment_rr(const uint2* __restrict__ pw, int64_t* out, int64_t seg_base,
+                                                int lane) {
+  if ((uint32_t)seg_base > 0xFFFFFFFFu - 1024u) return false;
+  const uint32_t bit = 1u << lane, lt = bit - 1u;
+  const uint32_t lo0 = (uint32_t)seg_base + (uint32_t)lane;
+  const uint32_t hi = (uint32_t)((uint64_t)seg_base >> 32);
+  int64_t* ob;
+  asm("mov.b64 %0, %1;" : "=l"(ob) : "l"(out));   // opaque base: one IMAD.WIDE per address
+#pragma unroll 4
+  for (int i = 0; i < 32; i += 2) {
+    const uint4 q = *reinterpret_cast<const uint4*>(pw + i);
+    int64_t* p0 = ob + (q.y + __popc(q.x & lt));
+    int64_t* p1 = ob + (q.w + __popc(q.z & lt));
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p st.global.cs.v2.b32 [%0], {%2, %3};\n\t}" ::"l"(p0),
+                 "r"(q.x & bit), "r"(lo0 + 32u * i), "r"(hi)
+                 : "memory");
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p st.global.cs.v2.b32 [%0], {%2, %3};\n\t}" ::"l"(p1),
+                 "r"(q.z & bit), "r"(lo0 + 32u * (i + 1)), "r"(hi)
+                 : "memory");
+  }
+  return true;
+}
+
+// segments with fewer codes than this take the staged sparse path
+constexpr int RR_MIN_CODES = 128;
+
 // has_heavy: 0 = no heavy part; 1 = the chunk's heavy bitmap (the tcgen05
 // product's output) is in bm; 2 = the heavy part is computed by the tile
 // itself from the heavy-y bit rows `hbits` (heavy_or_rows)
@@ -501,7 +538,7 @@ __device__ __forceinline__ void st_status(unsigned long long* p, unsigned long l
 template <int NT>
 struct FuseSmem {
   typename cub::BlockScan<int, NT>::TempStorage scan_tmp;
-  union {
+  union __align__(16) {
     struct {
       int tb_len[NT + 1];
       const int32_t* tb_base[NT];
@@ -517,7 +554,7 @@ struct FuseSmem {
   __align__(8) uint64_t bar;
 };
 
-template <int TW, int NT, int MINB>
+template <int TW, int NT, int MINB, int RR>
 __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
   constexpr int NWARP = NT / 32;
   constexpr int MAXSEG = TW / 32;
@@ -685,6 +722,22 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     const int rr = cur / segs_per_piece;
     const int64_t base = (a.x0 + r0 + rr) * a.dom_z + (c0w + (int64_t)(cur - rr * segs_per_piece) * 32) * 32;
     int64_t* out = codes + s_segoff[cur];
+    if (RR && tot == 1024) {
+      // full segment: codes base .. base + 1023, 16-byte stores
+      const int hh = (int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1);
+      if (lane == 0 && hh) st_cs(out, base);
+      for (int p = hh + 2 * lane; p + 1 < 1024; p += 64) st_cs2(out + p, base + p, base + p + 1);
+      if (lane == 0 && hh) st_cs(out + 1023, base + 1023);
+      continue;
+    }
+    if (RR && tot >= RR_MIN_CODES) {
+      uint2* pw = reinterpret_cast<uint2*>(stage);
+      pw[lane] = make_uint2(word, (uint32_t)(incl - c));
+      __syncwarp();
+      const bool done_rr = emit_segment_rr(pw, out, base, lane);
+      __syncwarp();
+      if (done_rr) continue;
+    }
     const int h = min((int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1), tot);
     const uint32_t off0 = lane * 32;
     int k = h + (incl - c);
@@ -769,7 +822,12 @@ constexpr int FUSE_THREADS = 288;
 constexpr int FUSE_MIN_CTAS = 4;
 
 int launch_merge_emit(const FuseArgs& f, cudaStream_t st) {
-  auto kern = k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS>;
+  static const bool rr = [] {
+    const char* e = getenv("MMJ_EMIT_RR");
+    return e == nullptr || e[0] != '0';
+  }();
+  auto kern = rr ? k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS, 1>
+                 : k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS, 0>;
   MMJ_TRY(set_max_dynamic_smem((const void*)kern, FUSE_TILE_WORDS * 4, "k_merge_emit"));
   const size_t smem = (size_t)f.t.G * f.t.cb_words * 4;
   kern<<<(unsigned)f.ntiles, FUSE_THREADS, smem, st>>>(f);

@@ -186,8 +186,8 @@ def test_bsi_float_values_and_mixed_query_ids():
     assert got[-7:-4] == [False, True, True] and got[-3:-1] == [None, None]
 
 
-@pytest.mark.parametrize("heavy_bits", [128, 512])
-def test_bsi_zipf_vs_oracle(oracle, heavy_bits):
+@pytest.mark.parametrize("heavy_bits,form", [(128, "records"), (512, "records"), (256, "lists"), (256, "auto")])
+def test_bsi_zipf_vs_oracle(oracle, heavy_bits, form):
     from paper_2002_12459_b200.apps import bsi_answer_batch_arrays
     from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce
     rng = np.random.default_rng(heavy_bits)
@@ -198,7 +198,7 @@ def test_bsi_zipf_vs_oracle(oracle, heavy_bits):
     # unshared dictionaries (mapped on the host) and pre-reduced shared ones
     r = build_indexed(Relation.from_raw_pairs("R", rp))
     s = build_indexed(Relation.from_raw_pairs("S", sp))
-    got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], heavy_bits=heavy_bits)
+    got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], heavy_bits=heavy_bits, form=form)
     assert np.array_equal(got, exp)
     assert (exp == -1).any() and (exp == 1).any() and (exp == 0).any()
 
@@ -221,12 +221,14 @@ def test_bsi_direct_table_vs_search(oracle, spread, monkeypatch):
     exp = oracle.bsi(oracle.encode(rp), oracle.encode(sp), q[:, 0], q[:, 1])
     r = build_indexed(Relation.from_raw_pairs("R", rp))
     s = build_indexed(Relation.from_raw_pairs("S", sp))
-    got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1])
-    assert np.array_equal(got, exp)
+    for form in ("lists", "records"):
+        got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], form=form)
+        assert np.array_equal(got, exp)
     monkeypatch.setattr(bsi, "DIRECT_SPREAD", 0)
     r._mmj_bsi_cache = None
-    got2 = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1])
-    assert np.array_equal(got2, exp)
+    for form in ("lists", "records"):
+        got2 = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], form=form)
+        assert np.array_equal(got2, exp)
 
 
 def test_bsi_tables_abi_errors():

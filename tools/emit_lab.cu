@@ -203,6 +203,41 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const uint32_t* __restrict_
         const int i = done + lane;
         st_cs(out + i, base + st16[2 * sl32(i >> 1) + (i & 1)]);
       }
+    } else if (V == 13 || V == 14) {  // round robin, no staging: word i's codes by all lanes (lane = bit)
+      __shared__ __align__(16) uint2 pairs_all[WARPS][32];
+      uint2* pairs = pairs_all[warp];
+      pairs[lane] = make_uint2(word, (uint32_t)(incl - c));
+      __syncwarp();
+      const uint32_t bit = 1u << lane, lt = bit - 1u;
+      const int64_t cv = base + lane;
+      const uint32_t lo0 = (uint32_t)cv, hi = (uint32_t)((uint64_t)cv >> 32);
+      if (V == 13 && (uint32_t)base <= 0xFFFFFFFFu - 1024u) {
+        // no carry out of the low word inside the segment: 32-bit code arithmetic
+        int64_t* ob;
+        asm("mov.b64 %0, %1;" : "=l"(ob) : "l"(out));   // opaque base: one IMAD.WIDE per address
+#pragma unroll 4
+        for (int i = 0; i < 32; i += 2) {
+          const uint4 q = *reinterpret_cast<const uint4*>(pairs + i);
+          int64_t* p0 = ob + (q.y + __popc(q.x & lt));
+          int64_t* p1 = ob + (q.w + __popc(q.z & lt));
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p st.global.cs.v2.b32 [%0], {%2, %3};\n\t}"
+                       ::"l"(p0), "r"(q.x & bit), "r"(lo0 + 32u * i), "r"(hi) : "memory");
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p st.global.cs.v2.b32 [%0], {%2, %3};\n\t}"
+                       ::"l"(p1), "r"(q.z & bit), "r"(lo0 + 32u * (i + 1)), "r"(hi) : "memory");
+        }
+      } else
+#pragma unroll 4
+      for (int i = 0; i < 32; i += 2) {
+        const uint4 q = *reinterpret_cast<const uint4*>(pairs + i);
+        if ((q.x | q.z) == 0) continue;
+        if (V == 13) {
+          if (q.x & bit) st_cs(out + q.y + __popc(q.x & lt), cv + 32 * i);
+          if (q.z & bit) st_cs(out + q.w + __popc(q.z & lt), cv + 32 * (i + 1));
+        } else {
+          if (q.x & bit) out[q.y + __popc(q.x & lt)] = cv + 32 * i;
+          if (q.z & bit) out[q.w + __popc(q.z & lt)] = cv + 32 * (i + 1);
+        }
+      }
     } else if (V == 4) {  // no staging: each lane writes its own run (uncoalesced)
       int k = incl - c;
       while (word) {
@@ -489,6 +524,23 @@ int main(int argc, char** argv) {
       if (ms < best) best = ms;
     }
     printf("%-24s %8.3f ms  %7.1f GB/s\n", "V12 CTA-staged int64", best, bytes / (best * 1e-3) / 1e9);
+  }
+  {
+    const float r0 = run<13>(dbm, dso, nseg, dout), r1 = run<14>(dbm, dso, nseg, dout);
+    const float r2 = run<13, 8>(dbm, dso, nseg, dout), r3 = run<0, 8>(dbm, dso, nseg, dout);
+    const float r4 = run<13, 256, 1>(dbm, dso, nseg, dout);
+    printf("%-24s %8.3f ms  %7.1f GB/s\n", "V13 round robin cs", r0, bytes / (r0 * 1e-3) / 1e9);
+    printf("%-24s %8.3f ms  %7.1f GB/s\n", "V14 round robin wb", r1, bytes / (r1 * 1e-3) / 1e9);
+    printf("%-24s %8.3f ms  %7.1f GB/s\n", "V13 segs 8", r2, bytes / (r2 * 1e-3) / 1e9);
+    printf("%-24s %8.3f ms  %7.1f GB/s\n", "V0 segs 8", r3, bytes / (r3 * 1e-3) / 1e9);
+    printf("%-24s %8.3f ms  %7.1f GB/s\n", "V13 256 contiguous/warp", r4, bytes / (r4 * 1e-3) / 1e9);
+    // parity of V13 vs V0
+    std::vector<int64_t> o0(acc), o1(acc);
+    run<0>(dbm, dso, nseg, dout);
+    CK(cudaMemcpy(o0.data(), dout, acc * 8, cudaMemcpyDeviceToHost));
+    run<13>(dbm, dso, nseg, dout);
+    CK(cudaMemcpy(o1.data(), dout, acc * 8, cudaMemcpyDeviceToHost));
+    printf("V13 == V0: %s\n", o0 == o1 ? "yes" : "NO");
   }
   const float t8 = run<8>(dbm, dso, nseg, dout);
   printf("%-24s %8.3f ms  %7.1f GB/s\n", "V8 xor5 + 32B quads", t8, bytes / (t8 * 1e-3) / 1e9);
