@@ -343,6 +343,28 @@ int mmj_ingest_csr(const int32_t* rows, const int32_t* cols, int64_t n, int64_t 
                    int32_t* ptr, int32_t* idx, int32_t* row_of, int32_t* deg, void* ws, size_t ws_bytes,
                    void* stream);
 
+/* ---- result text formats: cli.py:129-136, 154-161, 180-182, 205-206 -----
+ * Lines "v0 v1 [v2 [v3]] [count]" of raw dictionary strings, sorted as
+ * Python sorts the strings, joined by '\n'.  Columns: ncode code columns
+ * (codes mixed radix over dims, as OutputSet.tuples) plus, when counts !=
+ * NULL, the count column.  Per column (host arrays of device pointers):
+ * rank[c][v] = position of value v's string among the column's sorted
+ * strings (nrank[c] entries; count column indexed by the count), soff[c]
+ * (nrank[c] + 1 int64 offsets) and blob[c] (UTF-8 bytes).
+ *   mmj_format_keys     key[t] = mixed-radix rank tuple (sort it: the line
+ *                       order); *bad = 1 if a value is outside its table
+ *   mmj_format_lengths  len[p] of line p (tuple order[p], or p if order is
+ *                       NULL), separators and the newline included
+ *   mmj_format_write    the bytes, line p at line_off[p] (exclusive scan of
+ *                       the lengths, mmj_exclusive_scan_i32) */
+int mmj_format_keys(const int64_t* codes, const int64_t* counts, int64_t n, int ncode, const int64_t* dims,
+                    const int32_t* const* rank, const int64_t* nrank, int64_t* key, int* bad, void* stream);
+int mmj_format_lengths(const int64_t* codes, const int64_t* counts, const int32_t* order, int64_t n, int ncode,
+                       const int64_t* dims, const int64_t* const* soff, int32_t* len, void* stream);
+int mmj_format_write(const int64_t* codes, const int64_t* counts, const int32_t* order, int64_t n, int ncode,
+                     const int64_t* dims, const int64_t* const* soff, const uint8_t* const* blob,
+                     const int64_t* line_off, uint8_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -3,6 +3,10 @@
 #include "mmj_common.cuh"
 
 namespace mmj {
+// format.cu (FmtArgs: mmj_common.cuh)
+int fmt_keys(const FmtArgs&, int64_t*, int*, cudaStream_t);
+int fmt_lengths(const FmtArgs&, int32_t*, cudaStream_t);
+int fmt_write(const FmtArgs&, const int64_t*, uint8_t*, cudaStream_t);
 // twopath.cu
 int heavy_y_positions(const int32_t*, const int32_t*, int64_t, int64_t, uint8_t*, int32_t*, int32_t*, void*,
                       cudaStream_t);
@@ -330,3 +334,60 @@ int mmj_count_emit(const void* cnt, int cell_bytes, int64_t nrows, int64_t ld, i
 }
 
 }  // extern "C"
+
+
+// ---- result text formats (cli.py:129-136, 154-161, 180-182, 205-206) ----
+static int fmt_args(mmj::FmtArgs& f, const int64_t* codes, const int64_t* counts, const int32_t* order, int64_t n,
+                    int ncode, const int64_t* dims, const int32_t* const* rank, const int64_t* nrank,
+                    const int64_t* const* soff, const uint8_t* const* blob) {
+  const int ncol = ncode + (counts ? 1 : 0);
+  if (ncode < 1 || ncol > 5 || n < 0 || (n > 0 && codes == nullptr)) {
+    mmj::set_error("format: 1 <= code columns, columns (+ count) <= 5, n >= 0");
+    return MMJ_ERR_ARG;
+  }
+  f.codes = codes;
+  f.counts = counts;
+  f.order = order;
+  f.n = n;
+  f.ncode = ncode;
+  for (int c = 0; c < 5; ++c) {
+    f.dims[c] = c < ncode ? dims[c] : 1;
+    f.rank[c] = (c < ncol && rank) ? rank[c] : nullptr;
+    f.nrank[c] = (c < ncol && nrank) ? nrank[c] : 1;
+    f.soff[c] = (c < ncol && soff) ? soff[c] : nullptr;
+    f.blob[c] = (c < ncol && blob) ? blob[c] : nullptr;
+    if (c < ncode && f.dims[c] < 1) {
+      mmj::set_error("format: dims must be >= 1");
+      return MMJ_ERR_ARG;
+    }
+  }
+  return MMJ_OK;
+}
+
+int mmj_format_keys(const int64_t* codes, const int64_t* counts, int64_t n, int ncode, const int64_t* dims,
+                    const int32_t* const* rank, const int64_t* nrank, int64_t* key, int* bad, void* stream) {
+  mmj::FmtArgs f;
+  MMJ_TRY(fmt_args(f, codes, counts, nullptr, n, ncode, dims, rank, nrank, nullptr, nullptr));
+  double span = 1.0;
+  for (int c = 0; c < ncode + (counts ? 1 : 0); ++c) span *= (double)f.nrank[c];
+  if (span >= 9.2e18) {
+    mmj::set_error("format_keys: the columns' rank product exceeds int64");
+    return MMJ_ERR_ARG;
+  }
+  return mmj::fmt_keys(f, key, bad, ST(stream));
+}
+
+int mmj_format_lengths(const int64_t* codes, const int64_t* counts, const int32_t* order, int64_t n, int ncode,
+                       const int64_t* dims, const int64_t* const* soff, int32_t* len, void* stream) {
+  mmj::FmtArgs f;
+  MMJ_TRY(fmt_args(f, codes, counts, order, n, ncode, dims, nullptr, nullptr, soff, nullptr));
+  return mmj::fmt_lengths(f, len, ST(stream));
+}
+
+int mmj_format_write(const int64_t* codes, const int64_t* counts, const int32_t* order, int64_t n, int ncode,
+                     const int64_t* dims, const int64_t* const* soff, const uint8_t* const* blob,
+                     const int64_t* line_off, uint8_t* out, void* stream) {
+  mmj::FmtArgs f;
+  MMJ_TRY(fmt_args(f, codes, counts, order, n, ncode, dims, nullptr, nullptr, soff, blob));
+  return mmj::fmt_write(f, line_off, out, ST(stream));
+}

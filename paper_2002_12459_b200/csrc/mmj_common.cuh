@@ -63,6 +63,21 @@ int scan_i64_i64(const int64_t* in, int64_t* out, int64_t n, void* ws, cudaStrea
 int scan_i32_i32(const int32_t* in, int32_t* out, int64_t n, void* ws, cudaStream_t st);
 int code_checksum(const int64_t* codes, int64_t n, int64_t base, unsigned long long* out, cudaStream_t st);
 
+// result text formats (format.cu): up to 4 code columns + the count column
+constexpr int MMJ_FMT_COLS = 5;
+struct FmtArgs {
+  const int64_t* codes;           // n mixed-radix codes over dims[0 .. ncode)
+  const int64_t* counts;          // n counts (the last column) or nullptr
+  const int32_t* order;           // line -> tuple (nullptr = identity)
+  int64_t n;
+  int ncode;                      // code columns
+  int64_t dims[MMJ_FMT_COLS];
+  const int32_t* rank[MMJ_FMT_COLS];
+  int64_t nrank[MMJ_FMT_COLS];    // table sizes (count column: max count + 1)
+  const int64_t* soff[MMJ_FMT_COLS];  // string offsets into blob, nrank + 1 entries
+  const uint8_t* blob[MMJ_FMT_COLS];
+};
+
 }  // namespace mmj
 
 // ---- device helpers ----------------------------------------------------------

@@ -814,7 +814,8 @@ void tile_geometry(int64_t wpr, int& G, int& cb, int& ncb, int64_t tile_words = 
   }
 }
 
-constexpr int FUSE_TILE_WORDS = 8192;   // 32 KB of bitmap per tile (4096 / 16384 measured slower)
+// 32 KB of bitmap per tile (2048 / 4096 / 16384 measured slower: r2f 198 / 179 / - vs 175 ms)
+constexpr int FUSE_TILE_WORDS = 8192;
 
 // 9 warps x 4 CTAs = 36 warps per SM at 54 registers (171.8 vs 173.1 ms per
 // cfg2 step for 8 warps: more warps hide the look-back wait)
