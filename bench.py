@@ -1126,7 +1126,7 @@ def run_b200(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * t_step_g, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": cfg, "roofline": roof, "phases": info, "check": check, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clk,
+            "gpu_launches": int(launches), "clocks": clk, "step_ms": [round(1e3 * t, 3) for t in times],
             "int8_peak_cublaslt_tops": (int8_peak / 1e12) if int8_peak else None,
         }
         print(json.dumps(line), flush=True)

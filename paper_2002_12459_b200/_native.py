@@ -12,7 +12,10 @@ from pathlib import Path
 
 from .errors import MatrixOverflowError
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libmmjoin_b200.so"
+# MMJ_LIB_VARIANT=check loads the bounds-checked build (MMJ_DCHECK compiled
+# in, build.py --check) instead of the product library
+_LIB_PATH = Path(__file__).resolve().parent / "_lib" / (
+    "libmmjoin_b200_check.so" if os.environ.get("MMJ_LIB_VARIANT") == "check" else "libmmjoin_b200.so")
 
 MMJ_OK = 0
 MMJ_ERR_ARG = 1

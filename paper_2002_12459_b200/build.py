@@ -42,33 +42,44 @@ def sources():
 
 STAMP = LIB.with_suffix(".flags")
 
+# the bounds-checked variant (MMJ_DCHECK compiled in): loaded instead of the
+# product library when MMJ_LIB_VARIANT=check (tests/test_gpu_checked.py)
+CHECK_LIB = LIBDIR / "libmmjoin_b200_check.so"
 
-def _flag_line() -> str:
-    return " ".join(ARCH + FLAGS)
+
+def _variant(check: bool):
+    if check:
+        return CHECK_LIB, CHECK_LIB.with_suffix(".flags"), LIBDIR / "obj_check", FLAGS + ["-DMMJ_DEBUG_CHECKS"]
+    return LIB, STAMP, LIBDIR / "obj", FLAGS
 
 
-def _stale() -> bool:
+def _flag_line(flags=None) -> str:
+    return " ".join(ARCH + (FLAGS if flags is None else flags))
+
+
+def _stale(check: bool = False) -> bool:
     """Rebuild when a source / header is newer than the library, or when the
     nvcc flags differ from the ones it was built with (an experiment build
     with MMJ_NVCC_EXTRA=-D... must never be picked up silently)."""
-    if not LIB.exists() or not STAMP.exists() or STAMP.read_text() != _flag_line():
+    lib, stamp, _, flags = _variant(check)
+    if not lib.exists() or not stamp.exists() or stamp.read_text() != _flag_line(flags):
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, check: bool = False) -> Path:
+    lib, stamp, objdir, flags = _variant(check)
+    if not force and not _stale(check):
+        return lib
     LIBDIR.mkdir(exist_ok=True)
-    objdir = LIBDIR / "obj"
     objdir.mkdir(exist_ok=True)
     nvcc = _nvcc()
     objs = []
     for src in sources():
         obj = objdir / (src.stem + ".o")
-        cmd = [nvcc, *ARCH, *FLAGS, "-I", str(CSRC), "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *ARCH, *flags, "-I", str(CSRC), "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
@@ -77,16 +88,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             sys.stderr.write(res.stderr)
         (objdir / (src.stem + ".ptxas.txt")).write_text(res.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    STAMP.write_text(_flag_line())
-    return LIB
+    os.replace(tmp, lib)
+    stamp.write_text(_flag_line(flags))
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, check="--check" in sys.argv))

@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restr
     const int2 ra = make_int2(__ldg(pa_ptr + ia), __ldg(pa_ptr + ia + 1));
     const int2 rb = make_int2(__ldg(pb_ptr + ib), __ldg(pb_ptr + ib + 1));
     const int32_t na = ra.y - ra.x, nb = rb.y - rb.x;
+    MMJ_DCHECK(ra.x >= 0 && rb.x >= 0, "list bounds");
     bool hit = false;
     if (na > 0 && nb > 0) {
       const int32_t* la = pa_idx + ra.x;

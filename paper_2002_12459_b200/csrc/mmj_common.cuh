@@ -44,6 +44,26 @@ long long launch_count();
     if (_st) return _st;         \
   } while (0)
 
+// Device-side bounds checks, compiled in only for the checked library
+// variant (libmmjoin_b200_check.so, -DMMJ_DEBUG_CHECKS; build.py): a failed
+// check prints the site and traps, so a bad index surfaces as a launch error
+// instead of a silent out-of-bounds access.  The stand-in for
+// compute-sanitizer, which this GPU pool does not run.
+#ifdef MMJ_DEBUG_CHECKS
+#define MMJ_DCHECK(cond, what)                                                                         \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("MMJ_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,          \
+             (int)blockIdx.x, (int)threadIdx.x);                                                      \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define MMJ_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 

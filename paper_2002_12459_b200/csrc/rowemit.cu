@@ -194,6 +194,7 @@ __device__ unsigned long long heavy_or_rows(const TileArgs& a, uint32_t* sbm, in
       const int h = t < te ? a.hpos[a.fwd_idx[t]] : -1;
       int pos, cnt;
       cub::BlockScan<int, NT>(scan_tmp).ExclusiveSum(h >= 0 ? 1 : 0, pos, cnt);
+      MMJ_DCHECK(pos <= NT, "heavy list position");
       if (h >= 0) s_list[pos] = h;
       __syncthreads();
       const bool last = tb + NT >= te;
@@ -315,6 +316,7 @@ __device__ __forceinline__ unsigned long long merge_light(
         if (!ok[u]) continue;
         const int32_t z = zv[u];
         if ((rowv[u] >> 30) && (z < zlo || z >= zhi)) continue;
+        MMJ_DCHECK(z >= zlo && z < zhi && (rowv[u] & 0x3FFFFFFF) < (int)(xb - xa), "light witness outside the tile");
         atomicOr(&sbm[(rowv[u] & 0x3FFFFFFF) * cw + ((z - zlo) >> 5)], 1u << (z & 31));
         ++kept;
       }
@@ -554,7 +556,7 @@ struct FuseSmem {
   __align__(8) uint64_t bar;
 };
 
-template <int TW, int NT, int MINB, int RR>
+template <int TW, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
   constexpr int NWARP = NT / 32;
   constexpr int MAXSEG = TW / 32;
@@ -667,6 +669,7 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
       int64_t pos = tile - 1;
       while (true) {
         const int64_t idx = pos - lane;
+        MMJ_DCHECK(idx < f.ntiles, "look-back status index");
         unsigned long long st = idx >= 0 ? ld_status(f.status + idx) : ST_INC;
         while (__any_sync(0xffffffffu, (st >> 62) == 0)) {
           // back off between polls: the spinning warp otherwise takes issue
@@ -695,7 +698,12 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
 #ifdef MMJ_DEBUG_TIMING
   if (tid == 0 && f.tdbg) f.tdbg[(int64_t)sm.tile * 8 + 4] = gtimer();
 #endif
-  // emission: one warp per segment (k_emit_pf16's staging and stores)
+  // emission: one warp per 1024-cell segment -- round robin over its words
+  // straight to global memory (emit_segment_rr); full segments as one
+  // 16-byte store run; sparse segments (< RR_MIN_CODES codes) through the
+  // 16-bit shared staging of k_emit_pf16.  (Measured and not adopted, r2h /
+  // r2i: TMA bulk stores of ~1.7 KB staged pieces 224 vs 175 ms; moving
+  // segment boundaries to 128-byte lines so one warp writes each line 206 ms.)
   uint16_t* stage = sm.u.stage[warp];
   auto sl = [](int k) { return k ^ (((k >> 5) & 31) << 1); };
   const int segs_per_piece = cw >> 5;
@@ -722,7 +730,8 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
     const int rr = cur / segs_per_piece;
     const int64_t base = (a.x0 + r0 + rr) * a.dom_z + (c0w + (int64_t)(cur - rr * segs_per_piece) * 32) * 32;
     int64_t* out = codes + s_segoff[cur];
-    if (RR && tot == 1024) {
+    MMJ_DCHECK(s_segoff[cur] >= 0 && s_segoff[cur] + tot <= agg, "segment codes outside the tile's output range");
+    if (tot == 1024) {
       // full segment: codes base .. base + 1023, 16-byte stores
       const int hh = (int)((reinterpret_cast<uintptr_t>(out) >> 3) & 1);
       if (lane == 0 && hh) st_cs(out, base);
@@ -730,7 +739,7 @@ __global__ void __launch_bounds__(NT, MINB) k_merge_emit(const FuseArgs f) {
       if (lane == 0 && hh) st_cs(out + 1023, base + 1023);
       continue;
     }
-    if (RR && tot >= RR_MIN_CODES) {
+    if (tot >= RR_MIN_CODES) {
       uint2* pw = reinterpret_cast<uint2*>(stage);
       pw[lane] = make_uint2(word, (uint32_t)(incl - c));
       __syncwarp();
@@ -823,12 +832,7 @@ constexpr int FUSE_THREADS = 288;
 constexpr int FUSE_MIN_CTAS = 4;
 
 int launch_merge_emit(const FuseArgs& f, cudaStream_t st) {
-  static const bool rr = [] {
-    const char* e = getenv("MMJ_EMIT_RR");
-    return e == nullptr || e[0] != '0';
-  }();
-  auto kern = rr ? k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS, 1>
-                 : k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS, 0>;
+  auto kern = k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS>;
   MMJ_TRY(set_max_dynamic_smem((const void*)kern, FUSE_TILE_WORDS * 4, "k_merge_emit"));
   const size_t smem = (size_t)f.t.G * f.t.cb_words * 4;
   kern<<<(unsigned)f.ntiles, FUSE_THREADS, smem, st>>>(f);

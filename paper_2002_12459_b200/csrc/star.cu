@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_star_light_expand(StarRels s, co
       int64_t row = xv[0] - x1_begin;
       for (int j = 1; j <= s.k - 2; ++j) row = row * s.dims[j] + xv[j];
       const int32_t col = xv[s.k - 1];
+      MMJ_DCHECK(row >= 0 && col >= 0 && (mode == 0 ? (col >> 5) < ld : col < ld), "star witness outside its block");
       if (mode == 0)
         atomicOr(reinterpret_cast<uint32_t*>(out) + row * ld + (col >> 5), 1u << (col & 31));
       else

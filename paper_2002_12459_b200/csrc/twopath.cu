@@ -77,6 +77,7 @@ __global__ void k_build_heavy_rows(const int32_t* __restrict__ rows, const int32
     const int32_t z = rows[t];
     if (left_deg[z] <= d2) continue;
     const int32_t k = hpos[cols[t]];
+    MMJ_DCHECK(z >= 0 && (z >> 5) < wpr, "heavy row bit outside the row pitch");
     if (k >= 0) atomicOr(&hbits[(int64_t)k * wpr + (z >> 5)], 1u << (z & 31));
   }
 }
@@ -222,6 +223,8 @@ __global__ void __launch_bounds__(EXP_THREADS) k_light_expand(LightArgs a, const
       const int32_t z = base[s - offs[i]];
       const int64_t row = (int64_t)x - x0;
       if (a.upper_only == 1 && z <= x) continue;  // SSJ keeps a < b only (apps.py:60)
+      MMJ_DCHECK(row >= 0 && z >= 0 && (MODE == 0 ? (z >> 5) < ld : (MODE == 1 ? z < ld : (z >> 1) < (ld >> 1))),
+                 "light witness outside the chunk's output block");
       if (MODE == 0) {
         atomicOr(reinterpret_cast<uint32_t*>(out) + row * ld + (z >> 5), 1u << (z & 31));
       } else if (MODE == 1) {

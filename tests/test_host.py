@@ -241,3 +241,18 @@ def test_product_fails_loudly_without_gpu():
     r = rl.build_indexed(rl.Relation.from_raw_pairs("R", [(1, 2), (2, 2)]))
     with pytest.raises(RuntimeError, match="CUDA"):
         two_path_join(r, r)
+
+
+def test_checked_variant_exports_and_has_checks():
+    """The bounds-checked build (build.py --check) exports the same C ABI and
+    carries the MMJ_DCHECK trap sites (their message is in its device code)."""
+    from paper_2002_12459_b200 import build
+    path = build.CHECK_LIB
+    if not path.exists():
+        pytest.skip("libmmjoin_b200_check.so not built")
+    lib = ctypes.CDLL(str(path))
+    missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+    blob = path.read_bytes()
+    assert b"MMJ_DCHECK failed" in blob
+    assert b"MMJ_DCHECK failed" not in build.LIB.read_bytes()

@@ -36,6 +36,8 @@ def main():
     from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce
 
     torch.cuda.set_device(0)
+    from paper_2002_12459_b200 import _native
+    print(f"library: {_native._LIB_PATH.name}", flush=True)
     rng = np.random.default_rng(3)
     # dom_z large enough for two column blocks of the fused tail (8192 words = 262144 cells)
     rp = np.array(zipf_pairs(rng, 30000, 600, 2000, 1.0))
