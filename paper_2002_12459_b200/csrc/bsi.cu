@@ -190,6 +190,16 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restr
       // 32-byte sectors on demand (an L1 line prefetch of every list moved
       // 613 B of DRAM per query, r2f ncu: whole 128-B lines for 64-B lists)
       const int32_t a0 = __ldg(la), b0 = __ldg(lb);
+      // and the next three 32-byte sectors of each (lists up to 32 entries)
+      // with real loads, so the merge's later steps hit L1 instead of
+      // waiting on one DRAM round trip per sector
+      int32_t warm = 0;
+#pragma unroll
+      for (int k = 1; k < 4; ++k) {
+        if (8 * k < na) warm += __ldg(la + 8 * k);
+        if (8 * k < nb) warm += __ldg(lb + 8 * k);
+      }
+      asm volatile("" ::"r"(warm));
       {
         int32_t i = 0, j = 0;
         int32_t u = a0, v = b0;

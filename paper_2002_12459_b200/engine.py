@@ -182,11 +182,14 @@ class TwoPathEngine:
             self.hpos = torch.empty(max(dom_y, 1), dtype=torch.int32, device="cuda")
             nat.call("mmj_heavy_y_positions", nat.ptr(dr.right_deg), nat.ptr(ds.right_deg), dom_y, self.d1,
                      nat.ptr(flag), nat.ptr(scan), nat.ptr(self.hpos), nat.ptr(self.ws.scan_ws(dom_y)), st)
-            k = int(scan[dom_y].item())
+            # one device -> host copy for K and the heavy-part choice's counts
+            or_stats = self._heavy_or_stats()
+            vals = torch.cat([scan[dom_y:dom_y + 1].long()] + ([or_stats] if or_stats is not None else [])).cpu()
+            k = int(vals[0])
             self.stats.k_heavy = k
             heavy_x = self._any_heavy(self._host_ldeg_r, dr)
             heavy_z = self._any_heavy(self._host_ldeg_s, ds)
-            if k > 0 and heavy_x and heavy_z and self._heavy_or(k):
+            if k > 0 and heavy_x and heavy_z and self._heavy_or(vals[1:].tolist()):
                 # the heavy rows of S_h at one bit per cell (K x wpr words)
                 self.heavy_kernel = "or"
                 self.hbits = torch.empty((k, self.wpr), dtype=torch.int32, device="cuda")
@@ -227,24 +230,38 @@ class TwoPathEngine:
                      nat.ptr(self.ws.scan_ws(n)), st)
         self._prepared = True
 
-    def _heavy_or(self, k: int) -> bool:
+    def _or_candidate(self):
+        """The projection's heavy part may take the in-tile OR form (fused
+        tail, no counts); None when forced by env MMJ_HEAVY=mma|or."""
+        if not self.fused or self.counts or not self.allow_pairs:
+            return False
+        env = __import__("os").environ.get("MMJ_HEAVY", "")
+        return (env == "or") if env in ("mma", "or") else None
+
+    def _heavy_or_stats(self):
+        """Device int64 [#heavy x, #heavy-x tuples with heavy y] for the OR
+        choice (launched, not synchronised), or None if not needed."""
+        if self._or_candidate() is not None:
+            return None
+        torch = self.torch
+        dr = self.dr
+        hx = dr.left_deg > self.d2
+        ht = ((self.hpos[dr.fwd_idx.long()] >= 0) & hx[dr.fwd_row.long()]).sum()
+        return torch.stack([hx.sum(), ht])
+
+    def _heavy_or(self, stats) -> bool:
         """Projection heavy part as a sparse boolean product (OR of heavy-y
         bit rows) instead of the dense tcgen05 product.  Per output cell the
         product reads 2 B of TMEM (z-pair accumulators) whatever R_h's
         density; the OR reads 4 B x (heavy y of the row) / 32 from L2 and runs
         inside the emission tail.  Taken when R_h's heavy rows carry at most
         OR_MAX_MEAN_DEG heavy y on average (cfg2: 4.2 of K = 128) and the
-        fused projection tail is in use; env MMJ_HEAVY=mma|or overrides."""
-        env = __import__("os").environ.get("MMJ_HEAVY", "")
-        if not self.fused or self.counts or not self.allow_pairs:
-            return False
-        if env in ("mma", "or"):
-            return env == "or"
-        torch = self.torch
-        dr = self.dr
-        hx = dr.left_deg > self.d2
-        ht = ((self.hpos[dr.fwd_idx.long()] >= 0) & hx[dr.fwd_row.long()]).sum()
-        nh, nt = (int(v) for v in torch.stack([hx.sum(), ht]).cpu())
+        fused projection tail is in use; env MMJ_HEAVY=mma|or overrides.
+        `stats` = the host values of _heavy_or_stats()."""
+        forced = self._or_candidate()
+        if forced is not None:
+            return forced
+        nh, nt = (int(v) for v in stats)
         return nt <= OR_MAX_MEAN_DEG * max(nh, 1)
 
     def _bitmap_mode(self) -> int:
