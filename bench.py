@@ -89,6 +89,7 @@ class ClockSampler:
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.q, self.dev = q, dev_index
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={dev_index}", f"--query-gpu={q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -105,6 +106,17 @@ class ClockSampler:
         self.f.seek(0)
         rows = [ln.strip().split(", ") for ln in self.f if ln.strip()]
         os.unlink(self.f.name)
+        when = "during the timed steps (100 ms period)"
+        if not rows:
+            # a timed region shorter than the sampling period: one sample
+            # right after it (the GPU is still at its under-load clocks)
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+                rows = [ln.strip().split(", ") for ln in out.stdout.splitlines() if ln.strip()]
+                when = "one sample right after the timed steps (shorter than the 100 ms sampling period)"
+            except (OSError, subprocess.SubprocessError):
+                rows = []
         sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -116,7 +128,7 @@ class ClockSampler:
                 if r[5 + i].strip().lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "sampled": when}
 
 
 class PhaseTimer:
@@ -338,7 +350,7 @@ class TwoPath:
         s, w = (int(v) & (2 ** 64 - 1) for v in acc.cpu().tolist())
         # whole-job stamp: the rank-order concatenation of every shard's codes
         n_all, s, w = combine_checksums(base, s, w)
-        out = {"out": n_all, "sum": s, "wsum": w, "max_chunk": max(sizes) if sizes else 0,
+        out = {"out": n_all, "sum": s, "wsum": w, "max_chunk": max(sizes) if sizes else 0, "chunk_codes": sizes,
                "light_intermediate": st.light_intermediate, "heavy_pairs": st.heavy_pairs}
         if self.world > 1:
             out["scope"] = f"all {self.world} ranks (rank-order concatenation); statistics rank 0's"
@@ -388,7 +400,7 @@ class TwoPath:
                     "peak_kind": hbm_kind,
                     "algorithmic": "8 B per distinct output code (SURVEY 8(d)) x |OUT| / the kernel's summed "
                                    "CUDA-event time over the step's chunks"}
-        roof["traffic"] = _ncu_traffic(dominant, 8.0 * out_local / max(st.chunks, 1))
+        roof["traffic"], roof["traffic_detail"] = _ncu_traffic(dominant)
         eng = self.eng
         if eng.heavy_kernel == "or":
             # heavy part inside k_merge_emit: every heavy row ORs its heavy-y
@@ -532,18 +544,21 @@ class TwoPath:
                 "api": "joinproject.two_path_join_chunks(upload='fresh', host_buffer=(pinned, pinned))"}
 
 
-def _ncu_traffic(kernel_phase, alg_bytes_per_launch):
-    """DRAM bytes per launch of the dominant kernel from the committed
-    `ncu --set full` capture (profiles/ncu_traffic.json: its measured DRAM /
-    algorithmic ratio), applied to this run's algorithmic bytes per launch."""
+def _ncu_traffic(kernel_phase):
+    """(traffic, detail) of the dominant kernel from the committed `ncu --set
+    full` capture (profiles/ncu_traffic.json): the captured launch's own
+    dram__bytes_read.sum + dram__bytes_write.sum, unscaled, with that launch's
+    algorithmic bytes and their ratio beside it."""
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(tpath):
-        return None
+        return None, None
     with open(tpath) as f:
         t = json.load(f).get(kernel_phase)
-    if isinstance(t, dict) and "traffic_over_algorithmic" in t:
-        return t["traffic_over_algorithmic"] * alg_bytes_per_launch
-    return None
+    if not isinstance(t, dict) or "dram_bytes_per_launch" not in t:
+        return None, None
+    detail = {k: t[k] for k in ("kernel", "algorithmic_bytes_per_launch", "traffic_over_algorithmic", "source", "note")
+              if k in t}
+    return t["dram_bytes_per_launch"], detail
 
 
 class Star:
@@ -598,8 +613,10 @@ class Star:
             base[0] += n
         self.eng.timer = None
         self.eng.run(sink, x1_range=self.x1)
+        from paper_2002_12459_b200.shard import combine_checksums
         s, w = (int(v) & (2 ** 64 - 1) for v in acc.cpu().tolist())
-        return {"out": base[0], "sum": s, "wsum": w, "full_cube": base[0] == 5000 ** 3 if self.world == 1 else None}
+        n, s, w = combine_checksums(base[0], s, w)      # the whole job (rank-order x1 ranges)
+        return {"out": n, "sum": s, "wsum": w, "full_cube": n == 5000 ** 3}
 
     def report(self, phases, t_step, out_local, int8_peak):
         hbm, hbm_kind = _peaks()
@@ -761,9 +778,12 @@ class Ssj:
             nat.call("mmj_code_checksum", nat.ptr(cnt), ch.n, base[0], nat.ptr(acc2), nat.stream_handle())
             base[0] += ch.n
         eng.run(sink, self.xr[0], self.xr[1])
+        from paper_2002_12459_b200.shard import combine_checksums
         s, w = (int(v) & (2 ** 64 - 1) for v in acc.cpu().tolist())
         cs, cw = (int(v) & (2 ** 64 - 1) for v in acc2.cpu().tolist())
-        return {"out": base[0], "sum": s, "wsum": w, "count_sum": cs, "count_wsum": cw}
+        n, s, w = combine_checksums(base[0], s, w)      # the whole job (rank-order row ranges)
+        _, cs, cw = combine_checksums(base[0], cs, cw)
+        return {"out": n, "sum": s, "wsum": w, "count_sum": cs, "count_wsum": cw}
 
     def report(self, phases, t_step, out_local, int8_peak):
         hbm, hbm_kind = _peaks()
