@@ -971,8 +971,9 @@ class Bsi:
             info["answer"].update(answers_per_s=self.nq / t_ans, bytes_lower_bound=9.0 * self.nq)
         ach = b_bsi / t_step / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "kernel": "bsi build + answer (whole step)", "peak_kind": hbm_kind, "traffic": None,
+                "kernel": "bsi build + answer (whole step)", "peak_kind": hbm_kind,
                 "algorithmic": "B_bsi = 8 B per input tuple + 9 B per query (SURVEY 8(d) lower bound) / step time"}
+        roof["traffic"], roof["traffic_detail"] = _ncu_traffic("bsi_answer") if self.eng.form == "lists" else (None, None)
         cfg = {"workload": self.wl.description + " (BASELINE configs[4])", "config_name": "cfg5",
                "queries_this_rank": self.nq, "batch_slice": [self.qlo, self.qhi], "heavy_bits": 256,
                "bsi_form": self.eng.form,
@@ -1113,19 +1114,31 @@ def run_b200(args):
     clocks = ClockSampler(local)
     launches0 = lib.mmj_launch_count()
     times = []
+    host_ms = []        # host time to issue each step (diagnostic: the GPU idles when it exceeds the step)
     units = 0
+    # no cyclic-GC pause inside a timed step (the step's host thread enqueues
+    # every chunk; a collection there leaves the GPU idle): collect between steps
+    import gc
+    gc_was = gc.isenabled()
     for _ in range(args.steps):
+        gc.enable()
+        gc.collect()
+        gc.disable()
         flush.random_(0, 127)          # 256 MiB write > 126 MB L2
         _barrier(world)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        th = time.perf_counter()
         h = wl.step(timer)
+        host_ms.append(round(1e3 * (time.perf_counter() - th), 3))
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / 1e3)
         units = wl.units(h)
         _barrier(world)
+    if gc_was:
+        gc.enable()
     launches = lib.mmj_launch_count() - launches0
     clk = clocks.stop()
     phases = {k: v / 1e3 / args.steps for k, v in timer.totals().items()}
@@ -1147,6 +1160,7 @@ def run_b200(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": cfg, "roofline": roof, "phases": info, "check": check, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk, "step_ms": [round(1e3 * t, 3) for t in times],
+            "host_issue_ms": host_ms,
             "int8_peak_cublaslt_tops": (int8_peak / 1e12) if int8_peak else None,
         }
         print(json.dumps(line), flush=True)

@@ -832,10 +832,17 @@ constexpr int FUSE_THREADS = 288;
 constexpr int FUSE_MIN_CTAS = 4;
 
 int launch_merge_emit(const FuseArgs& f, cudaStream_t st) {
-  auto kern = k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS>;
+  static const int var = [] {
+    const char* e = getenv("MMJ_FUSE_SHAPE");   // temporary A/B: 1 = 576 x 2, 2 = 448 x 2
+    return e ? atoi(e) : 0;
+  }();
+  auto kern = var == 1 ? k_merge_emit<FUSE_TILE_WORDS, 576, 2>
+              : var == 2 ? k_merge_emit<FUSE_TILE_WORDS, 448, 2>
+                         : k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS>;
+  const int nt = var == 1 ? 576 : var == 2 ? 448 : FUSE_THREADS;
   MMJ_TRY(set_max_dynamic_smem((const void*)kern, FUSE_TILE_WORDS * 4, "k_merge_emit"));
   const size_t smem = (size_t)f.t.G * f.t.cb_words * 4;
-  kern<<<(unsigned)f.ntiles, FUSE_THREADS, smem, st>>>(f);
+  kern<<<(unsigned)f.ntiles, nt, smem, st>>>(f);
   MMJ_CHECK_LAUNCH("k_merge_emit");
   return MMJ_OK;
 }
