@@ -71,6 +71,7 @@ def _args(argv=None):
     ap.add_argument("--no-verify", action="store_true", help="skip the untimed checksum pass")
     ap.add_argument("--no-light-work", action="store_true", help="skip the light-pass byte count (diagnostic)")
     ap.add_argument("--x-limit", type=int, default=0, help="debug: only the first X output rows")
+    ap.add_argument("--clock-period-ms", type=int, default=100, help="nvidia-smi sampling period during the steps")
     ap.add_argument("--bsi-form", default="auto", choices=["auto", "lists", "records"],
                     help="cfg5 device algorithm (bsi.BsiEngine); answers are identical")
     return ap.parse_args(argv)
@@ -84,15 +85,15 @@ def _dist():
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons sampled every 100 ms."""
 
-    def __init__(self, dev_index: int):
+    def __init__(self, dev_index: int, period_ms: int = 100):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        self.q, self.dev = q, dev_index
+        self.q, self.dev, self.period = q, dev_index, period_ms
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={dev_index}", f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", str(period_ms)],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
@@ -106,7 +107,7 @@ class ClockSampler:
         self.f.seek(0)
         rows = [ln.strip().split(", ") for ln in self.f if ln.strip()]
         os.unlink(self.f.name)
-        when = "during the timed steps (100 ms period)"
+        when = f"during the timed steps ({self.period} ms period)"
         if not rows:
             # a timed region shorter than the sampling period: one sample
             # right after it (the GPU is still at its under-load clocks)
@@ -1111,7 +1112,7 @@ def run_b200(args):
     int8_peak = _int8_peak_measure() if rank == 0 and args.config != "cfg5" else None
 
     timer = PhaseTimer()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, args.clock_period_ms)
     launches0 = lib.mmj_launch_count()
     times = []
     host_ms = []        # host time to issue each step (diagnostic: the GPU idles when it exceeds the step)

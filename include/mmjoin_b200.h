@@ -263,19 +263,12 @@ int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64
  * lists (fwd_ptr / fwd_idx int32, each list sorted by the shared y id) are
  * merge-intersected directly; id maps as for mmj_bsi_answer.  The engine
  * takes this form when the lists are short (mean length <= 64), where a
- * bitset record moves as many DRAM sectors as the list it summarises.
- * With a workspace (ws != NULL, >= mmj_bsi_lists_workspace_bytes(nq,
- * r_dom) bytes; r_dom = R's number of left ids) the queries are first
- * grouped by R-id bucket (<= 4096 buckets) so neighbouring threads read
- * neighbouring R lists; answers are written at the queries' own indices
- * either way (ws = NULL: batch order). */
+ * bitset record moves as many DRAM sectors as the list it summarises. */
 int mmj_bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted,
                          const int32_t* r_order, int64_t r_n, const int32_t* r_table, int64_t r_min, int64_t r_range,
                          const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const int32_t* s_table,
                          int64_t s_min, int64_t s_range, const int32_t* r_fwd_ptr, const int32_t* r_fwd_idx,
-                         const int32_t* s_fwd_ptr, const int32_t* s_fwd_idx, int64_t r_dom, void* ws, size_t ws_bytes,
-                         int8_t* ans, void* stream);
-size_t mmj_bsi_lists_workspace_bytes(int64_t nq, int64_t r_dom);
+                         const int32_t* s_fwd_ptr, const int32_t* s_fwd_idx, int8_t* ans, void* stream);
 /* direct-address id map for dense raw id ranges: table[range] = dense id of
  * raw value vmin + i, -1 where absent (one load per query instead of a
  * binary search; range = max - min + 1 < 2^31) */

@@ -88,9 +88,7 @@ _SIGS = {
     "mmj_format_keys": (INT, [P, P, I64, INT, P, P, P, P, P, P]),
     "mmj_format_lengths": (INT, [P, P, P, I64, INT, P, P, P, P]),
     "mmj_format_write": (INT, [P, P, P, I64, INT, P, P, P, P, P, P]),
-    "mmj_bsi_answer_lists": (INT, [P, P, I64, P, P, I64, P, I64, I64, P, P, I64, P, I64, I64, P, P, P, P, I64, P, SZ,
-                                   P, P]),
-    "mmj_bsi_lists_workspace_bytes": (SZ, [I64, I64]),
+    "mmj_bsi_answer_lists": (INT, [P, P, I64, P, P, I64, P, I64, I64, P, P, I64, P, I64, I64, P, P, P, P, P, P]),
     "mmj_star_split": (INT, [INT, P, I64, C.c_double, P, P, P, P, P, P, P, P]),
     "mmj_star_operand": (INT, [INT, P, P, I64, I64, I64, P, P]),
     "mmj_star_light_workspace_bytes": (SZ, [I64]),

@@ -27,7 +27,6 @@ from .device import Workspace
 
 BITS_BLOCK = 128     # bitset width granularity (4 words)
 LIST_MAX_MEAN = 64   # "lists" form when both sides' mean list length is at most this
-BUCKET_MIN = 1 << 16  # "lists" batches of at least this many queries are grouped by R-id bucket
 DIRECT_SPREAD = 4    # direct id table when max - min + 1 <= 4 x the number of ids
 
 
@@ -311,15 +310,9 @@ class BsiEngine:
                 return 0, 0, 0, nat.ptr(t[0]), t[1], t[2]
             return nat.ptr(side.sorted_vals), nat.ptr(side.order), side.dom_left, 0, 0, 0
         if self.form == "lists":
-            # batches of BUCKET_MIN+ queries are grouped by R-id bucket first
-            wsp, wsb = 0, 0
-            if nq >= BUCKET_MIN:
-                wsb = int(self.lib.mmj_bsi_lists_workspace_bytes(nq, self.sR.dom_left))
-                wsp = nat.ptr(self.ws.get("bsi_bucket", wsb, torch.uint8))
             nat.call("mmj_bsi_answer_lists", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, *idmap(self.sR, dense_a),
                      *idmap(self.sS, dense_b), nat.ptr(self.sR.fwd_ptr), nat.ptr(self.sR.fwd_idx),
-                     nat.ptr(self.sS.fwd_ptr), nat.ptr(self.sS.fwd_idx), self.sR.dom_left, wsp, wsb, nat.ptr(ans),
-                     nat.stream_handle())
+                     nat.ptr(self.sS.fwd_ptr), nat.ptr(self.sS.fwd_idx), nat.ptr(ans), nat.stream_handle())
             return ans[:nq]
         (rrec, rovf), (srec, sovf) = self.sides
         nat.call("mmj_bsi_answer", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, *idmap(self.sR, dense_a),

@@ -170,14 +170,9 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restr
                                                           const IdMap mb, const int32_t* __restrict__ pa_ptr,
                                                           const int32_t* __restrict__ pa_idx,
                                                           const int32_t* __restrict__ pb_ptr,
-                                                          const int32_t* __restrict__ pb_idx,
-                                                          const int32_t* __restrict__ order,
-                                                          const int32_t* __restrict__ dense_a, int8_t* __restrict__ ans) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nq; p += (int64_t)gridDim.x * blockDim.x) {
-    // bucketed batches (k_bsi_bucket_*): positions in R-id bucket order,
-    // the R id already resolved; answers still land at the query's index
-    const int64_t q = order ? (int64_t)__ldcs(order + p) : p;
-    const int32_t ia = dense_a ? dense_a[q] : map_id(ma, __ldcs(qa + q));
+                                                          const int32_t* __restrict__ pb_idx, int8_t* __restrict__ ans) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t ia = map_id(ma, __ldcs(qa + q));
     const int32_t ib = map_id(mb, __ldcs(qb + q));
     if (ia < 0 || ib < 0) {
       ans[q] = -1;
@@ -225,40 +220,6 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restr
     }
     ans[q] = hit ? 1 : 0;
   }
-}
-
-// Query bucketing for the lists form: queries grouped by their R id's
-// bucket (dense id >> shift; unknown ids in a last bucket), so the threads
-// of a warp read the forward lists of nearby R ids -- one region of fwd_idx
-// streamed through L2 / L1 instead of a random DRAM burst per list (the
-// batch's R ids are uniform: each R list is read about once per batch).
-__global__ void k_bsi_bucket_count(const int64_t* __restrict__ qa, int64_t nq, const IdMap ma, int shift, int nb,
-                                   int32_t* __restrict__ dense_a, int32_t* __restrict__ hist) {
-  extern __shared__ int32_t sh_hist[];
-  for (int i = threadIdx.x; i <= nb; i += blockDim.x) sh_hist[i] = 0;
-  __syncthreads();
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t ia = map_id(ma, __ldcs(qa + q));
-    dense_a[q] = ia;
-    atomicAdd(&sh_hist[ia >= 0 ? min(ia >> shift, nb - 1) : nb], 1);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i <= nb; i += blockDim.x)
-    if (sh_hist[i]) atomicAdd(&hist[i], sh_hist[i]);
-}
-
-__global__ void k_bsi_bucket_scatter(const int32_t* __restrict__ dense_a, int64_t nq, int shift, int nb,
-                                     unsigned long long* __restrict__ cursor, int32_t* __restrict__ order) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t ia = dense_a[q];
-    const unsigned long long pos = atomicAdd(&cursor[ia >= 0 ? min(ia >> shift, nb - 1) : nb], 1ull);
-    MMJ_DCHECK((int64_t)pos < nq, "bucketed query position");
-    order[pos] = (int32_t)q;
-  }
-}
-
-__global__ void k_bsi_bucket_cursor(const int64_t* __restrict__ off, int n, unsigned long long* __restrict__ cursor) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) cursor[i] = off[i];
 }
 
 __global__ void k_direct_table(const int64_t* __restrict__ sorted, const int32_t* __restrict__ order, int64_t n,
@@ -336,26 +297,11 @@ int bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* 
   return MMJ_OK;
 }
 
-// buckets of 2^shift R ids, at most 4096 of them (cfg5: 4M ids -> 1024 ids per bucket)
-static void bucket_geometry(int64_t r_dom, int& shift, int& nb) {
-  shift = 0;
-  while ((r_dom >> shift) > 4096) ++shift;
-  nb = (int)ceil_div(r_dom < 1 ? 1 : r_dom, (int64_t)1 << shift);
-}
-
-size_t bsi_lists_ws_bytes(int64_t nq, int64_t r_dom) {
-  int shift, nb;
-  bucket_geometry(r_dom, shift, nb);
-  return (size_t)(2 * round_up(nq, 64)) * 4 + (size_t)round_up(nb + 2, 64) * (4 + 8 + 8) +
-         scan_ws_bytes(nb + 2) + 256;
-}
-
 int bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted,
                      const int32_t* r_order, int64_t r_n, const int32_t* r_table, int64_t r_min, int64_t r_range,
                      const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const int32_t* s_table,
                      int64_t s_min, int64_t s_range, const int32_t* r_fwd_ptr, const int32_t* r_fwd_idx,
-                     const int32_t* s_fwd_ptr, const int32_t* s_fwd_idx, int64_t r_dom, void* ws, size_t ws_bytes,
-                     int8_t* ans, cudaStream_t st) {
+                     const int32_t* s_fwd_ptr, const int32_t* s_fwd_idx, int8_t* ans, cudaStream_t st) {
   if (nq == 0) return MMJ_OK;
   if (r_fwd_ptr == nullptr || s_fwd_ptr == nullptr) {
     set_error("bsi_answer_lists: both forward CSRs are required");
@@ -363,34 +309,8 @@ int bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const int
   }
   const IdMap a{r_sorted, r_order, r_n, r_table, r_min, r_range};
   const IdMap b{s_sorted, s_order, s_n, s_table, s_min, s_range};
-  const int32_t* order = nullptr;
-  int32_t* dense_a = nullptr;
-  if (ws != nullptr) {
-    if (ws_bytes < bsi_lists_ws_bytes(nq, r_dom) || nq >= (1ll << 31)) {
-      set_error("bsi_answer_lists: workspace of %zu bytes < %zu", ws_bytes, bsi_lists_ws_bytes(nq, r_dom));
-      return MMJ_ERR_ARG;
-    }
-    int shift, nb;
-    bucket_geometry(r_dom, shift, nb);
-    char* w = static_cast<char*>(ws);
-    dense_a = reinterpret_cast<int32_t*>(w);
-    int32_t* ord = dense_a + round_up(nq, 64);
-    int32_t* hist = ord + round_up(nq, 64);
-    int64_t* off = reinterpret_cast<int64_t*>(hist + round_up(nb + 2, 64));
-    unsigned long long* cursor = reinterpret_cast<unsigned long long*>(off + round_up(nb + 2, 64));
-    void* scan_ws = cursor + round_up(nb + 2, 64);
-    MMJ_TRY(cuda_status(cudaMemsetAsync(hist, 0, (size_t)(nb + 1) * 4, st), "memset bucket hist"));
-    k_bsi_bucket_count<<<grid_for(nq, TPB, 8), TPB, (nb + 1) * 4, st>>>(qa, nq, a, shift, nb, dense_a, hist);
-    MMJ_CHECK_LAUNCH("k_bsi_bucket_count");
-    MMJ_TRY(scan_i32_i64(hist, off, nb + 1, scan_ws, st));
-    k_bsi_bucket_cursor<<<grid_for(nb + 1), TPB, 0, st>>>(off, nb + 1, cursor);
-    MMJ_CHECK_LAUNCH("k_bsi_bucket_cursor");
-    k_bsi_bucket_scatter<<<grid_for(nq, TPB, 16), TPB, 0, st>>>(dense_a, nq, shift, nb, cursor, ord);
-    MMJ_CHECK_LAUNCH("k_bsi_bucket_scatter");
-    order = ord;
-  }
   k_bsi_answer_lists<<<grid_for(nq, TPB, 16), TPB, 0, st>>>(qa, qb, nq, a, b, r_fwd_ptr, r_fwd_idx, s_fwd_ptr,
-                                                             s_fwd_idx, order, dense_a, ans);
+                                                             s_fwd_idx, ans);
   MMJ_CHECK_LAUNCH("k_bsi_answer_lists");
   return MMJ_OK;
 }

@@ -54,9 +54,7 @@ int bsi_answer(const int64_t*, const int64_t*, int64_t, const int64_t*, const in
 int bsi_direct_table(const int64_t*, const int32_t*, int64_t, int64_t, int64_t, int32_t*, cudaStream_t);
 int bsi_answer_lists(const int64_t*, const int64_t*, int64_t, const int64_t*, const int32_t*, int64_t, const int32_t*,
                      int64_t, int64_t, const int64_t*, const int32_t*, int64_t, const int32_t*, int64_t, int64_t,
-                     const int32_t*, const int32_t*, const int32_t*, const int32_t*, int64_t, void*, size_t, int8_t*,
-                     cudaStream_t);
-size_t bsi_lists_ws_bytes(int64_t, int64_t);
+                     const int32_t*, const int32_t*, const int32_t*, const int32_t*, int8_t*, cudaStream_t);
 int star_split(int, const int32_t* const*, int64_t, double, uint8_t*, uint8_t*, int32_t*, int32_t*, int32_t*, int32_t*,
                void*, cudaStream_t);
 int star_operand(int, const int64_t*, const uint8_t* const*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
@@ -258,14 +256,10 @@ int mmj_bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const
                          const int32_t* r_order, int64_t r_n, const int32_t* r_table, int64_t r_min, int64_t r_range,
                          const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const int32_t* s_table,
                          int64_t s_min, int64_t s_range, const int32_t* r_fwd_ptr, const int32_t* r_fwd_idx,
-                         const int32_t* s_fwd_ptr, const int32_t* s_fwd_idx, int64_t r_dom, void* ws,
-                         size_t ws_bytes, int8_t* ans, void* stream) {
+                         const int32_t* s_fwd_ptr, const int32_t* s_fwd_idx, int8_t* ans, void* stream) {
   return mmj::bsi_answer_lists(qa, qb, nq, r_sorted, r_order, r_n, r_table, r_min, r_range, s_sorted, s_order, s_n,
-                               s_table, s_min, s_range, r_fwd_ptr, r_fwd_idx, s_fwd_ptr, s_fwd_idx, r_dom, ws, ws_bytes,
-                               ans, ST(stream));
+                               s_table, s_min, s_range, r_fwd_ptr, r_fwd_idx, s_fwd_ptr, s_fwd_idx, ans, ST(stream));
 }
-
-size_t mmj_bsi_lists_workspace_bytes(int64_t nq, int64_t r_dom) { return mmj::bsi_lists_ws_bytes(nq, r_dom); }
 
 int mmj_bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
                          int32_t* table, void* stream) {

@@ -826,23 +826,17 @@ void tile_geometry(int64_t wpr, int& G, int& cb, int& ncb, int64_t tile_words = 
 // 32 KB of bitmap per tile (2048 / 4096 / 16384 measured slower: r2f 198 / 179 / - vs 175 ms)
 constexpr int FUSE_TILE_WORDS = 8192;
 
-// 9 warps x 4 CTAs = 36 warps per SM at 54 registers (171.8 vs 173.1 ms per
-// cfg2 step for 8 warps: more warps hide the look-back wait)
+// 9 warps x 4 CTAs = 36 warps per SM (171.8 vs 173.1 ms per cfg2 step for 8
+// warps: more warps hide the look-back wait; 576 x 2 / 448 x 2 CTAs with the
+// round-robin emission: 188 / 184 vs 170 ms, r2l)
 constexpr int FUSE_THREADS = 288;
 constexpr int FUSE_MIN_CTAS = 4;
 
 int launch_merge_emit(const FuseArgs& f, cudaStream_t st) {
-  static const int var = [] {
-    const char* e = getenv("MMJ_FUSE_SHAPE");   // temporary A/B: 1 = 576 x 2, 2 = 448 x 2
-    return e ? atoi(e) : 0;
-  }();
-  auto kern = var == 1 ? k_merge_emit<FUSE_TILE_WORDS, 576, 2>
-              : var == 2 ? k_merge_emit<FUSE_TILE_WORDS, 448, 2>
-                         : k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS>;
-  const int nt = var == 1 ? 576 : var == 2 ? 448 : FUSE_THREADS;
+  auto kern = k_merge_emit<FUSE_TILE_WORDS, FUSE_THREADS, FUSE_MIN_CTAS>;
   MMJ_TRY(set_max_dynamic_smem((const void*)kern, FUSE_TILE_WORDS * 4, "k_merge_emit"));
   const size_t smem = (size_t)f.t.G * f.t.cb_words * 4;
-  kern<<<(unsigned)f.ntiles, nt, smem, st>>>(f);
+  kern<<<(unsigned)f.ntiles, FUSE_THREADS, smem, st>>>(f);
   MMJ_CHECK_LAUNCH("k_merge_emit");
   return MMJ_OK;
 }

@@ -51,17 +51,22 @@ class Column:
 
 
 def _column_cache(values) -> Column:
-    """One Column per dictionary object (dictionaries are immutable lists)."""
+    """One Column per dictionary object (dictionaries are immutable lists),
+    for the last _COLS_MAX dictionaries formatted."""
     key = id(values)
-    hit = _COLS.get(key)
+    hit = _COLS.pop(key, None)
     if hit is not None and hit[0] is values:
+        _COLS[key] = hit                  # most recently used last
         return hit[1]
     col = Column(values)
     _COLS[key] = (values, col)
+    while len(_COLS) > _COLS_MAX:
+        _COLS.pop(next(iter(_COLS)))
     return col
 
 
 _COLS: dict = {}
+_COLS_MAX = 8
 
 
 def _as_dev_i64(a):

@@ -186,13 +186,8 @@ def test_bsi_float_values_and_mixed_query_ids():
     assert got[-7:-4] == [False, True, True] and got[-3:-1] == [None, None]
 
 
-@pytest.mark.parametrize("heavy_bits,form", [(128, "records"), (512, "records"), (256, "lists"), (256, "auto"),
-                                             (256, "lists-bucketed")])
-def test_bsi_zipf_vs_oracle(oracle, heavy_bits, form, monkeypatch):
-    if form == "lists-bucketed":     # the R-id bucketing of large batches, on a small one
-        from paper_2002_12459_b200 import bsi
-        monkeypatch.setattr(bsi, "BUCKET_MIN", 1)
-        form = "lists"
+@pytest.mark.parametrize("heavy_bits,form", [(128, "records"), (512, "records"), (256, "lists"), (256, "auto")])
+def test_bsi_zipf_vs_oracle(oracle, heavy_bits, form):
     from paper_2002_12459_b200.apps import bsi_answer_batch_arrays
     from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce
     rng = np.random.default_rng(heavy_bits)
