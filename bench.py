@@ -83,14 +83,21 @@ def _dist():
 
 # ----------------------------------------------------------------- clocks / timers
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled every 100 ms."""
+    """nvidia-smi clocks and throttle reasons, sampled every `period_ms`.
+
+    Started before the warm-up steps -- nvidia-smi's own start-up (NVML
+    initialisation) otherwise lands inside the first timed steps and stalls
+    the host thread that issues them (a 37-96 ms stall of the second timed
+    step in r2m) -- and each sample is timestamped, so stop() keeps only the
+    samples taken inside the timed region [mark(), stop()]."""
 
     def __init__(self, dev_index: int, period_ms: int = 100):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         self.q, self.dev, self.period = q, dev_index, period_ms
+        self.t0 = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={dev_index}", f"--query-gpu={q}",
                                        "--format=csv,noheader,nounits", "-lms", str(period_ms)],
@@ -98,33 +105,51 @@ class ClockSampler:
         except OSError:
             self.p = None
 
+    def mark(self):
+        """Start of the timed region."""
+        self.t0 = time.time()
+
+    @staticmethod
+    def _stamp(txt):
+        import datetime
+        try:
+            return datetime.datetime.strptime(txt.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.time()
         self.p.terminate()
         self.p.wait()
         self.f.flush()
         self.f.seek(0)
         rows = [ln.strip().split(", ") for ln in self.f if ln.strip()]
         os.unlink(self.f.name)
+        t0 = self.t0 if self.t0 is not None else 0.0
+        inside = [r for r in rows if len(r) >= 10 and (lambda t: t is not None and t0 <= t <= t1)(self._stamp(r[0]))]
         when = f"during the timed steps ({self.period} ms period)"
-        if not rows:
-            # a timed region shorter than the sampling period: one sample
-            # right after it (the GPU is still at its under-load clocks)
+        if not inside:
+            # a timed region shorter than the sampling period: the sample
+            # nearest after its start (the GPU is still at its under-load clocks)
+            after = [r for r in rows if len(r) >= 10 and (self._stamp(r[0]) or 0.0) >= t0]
+            inside = after[:1]
+            when = "the first sample after the timed steps began (region shorter than the sampling period)"
+        if not inside:
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
-                rows = [ln.strip().split(", ") for ln in out.stdout.splitlines() if ln.strip()]
-                when = "one sample right after the timed steps (shorter than the 100 ms sampling period)"
+                inside = [ln.strip().split(", ") for ln in out.stdout.splitlines() if ln.strip()]
+                when = "one sample right after the timed steps (region shorter than the sampling period)"
             except (OSError, subprocess.SubprocessError):
-                rows = []
-        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+                inside = []
+        rows = [r[1:] for r in inside if len(r) >= 10]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in rows:
-            if len(r) < 9:
-                continue
             for i, nm in enumerate(names):
                 if r[5 + i].strip().lower().startswith("active"):
                     reasons.add(nm)
@@ -1106,13 +1131,13 @@ def run_b200(args):
     wl.setup()
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    clocks = ClockSampler(local, args.clock_period_ms)     # started early: see ClockSampler
     for _ in range(args.warmup):
         wl.units(wl.step())
     torch.cuda.synchronize()
     int8_peak = _int8_peak_measure() if rank == 0 and args.config != "cfg5" else None
 
     timer = PhaseTimer()
-    clocks = ClockSampler(local, args.clock_period_ms)
     launches0 = lib.mmj_launch_count()
     times = []
     host_ms = []        # host time to issue each step (diagnostic: the GPU idles when it exceeds the step)
@@ -1121,6 +1146,7 @@ def run_b200(args):
     # every chunk; a collection there leaves the GPU idle): collect between steps
     import gc
     gc_was = gc.isenabled()
+    clocks.mark()
     for _ in range(args.steps):
         gc.enable()
         gc.collect()
