@@ -93,6 +93,11 @@ int mmj_build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n,
 int mmj_build_heavy_rows(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,
                          int64_t delta2, const int32_t* hpos, uint32_t* heavy_rows, int64_t k, int64_t wpr,
                          void* stream);
+/* stats[0] = #heavy left ids (left_deg > delta2, over dom ids), stats[1] =
+ * #tuples with a heavy left id and a heavy y: the mean heavy-y count of a
+ * heavy row, which picks the projection's heavy form (engine.py) */
+int mmj_heavy_row_stats(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t dom,
+                        int64_t delta2, const int32_t* hpos, int64_t* stats, void* stream);
 
 /* ---- light-z CSR of S for pass 3: joinproject.py:195-203 --------------------
  * lz_ptr[dom_y+1]/lz_idx: S.rev(y) restricted to z with deg_S(z) <= delta2.

@@ -77,6 +77,7 @@ _SIGS = {
     "mmj_merge_emit_workspace_size": (SZ, [I64, I64]),
     "mmj_merge_emit": (INT, [P, INT, I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "mmj_build_heavy_rows": (INT, [P, P, I64, P, I64, P, P, I64, I64, P]),
+    "mmj_heavy_row_stats": (INT, [P, P, I64, P, I64, I64, P, P, P]),
     "mmj_merge_emit_col_blocks": (INT, [I64]),
     "mmj_debug_timing_buffer": (None, [P]),
     "mmj_list_splits": (INT, [P, P, I64, I64, P, P]),

@@ -14,6 +14,8 @@ int build_operand(const int32_t*, const int32_t*, int64_t, const int32_t*, int64
                   int64_t, int64_t, cudaStream_t);
 int build_heavy_rows(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint32_t*,
                      int64_t, int64_t, cudaStream_t);
+int heavy_row_stats(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, int64_t, const int32_t*,
+                    int64_t*, cudaStream_t);
 int build_operand_pairs(const int32_t*, const int32_t*, int64_t, const int32_t*, int64_t, const int32_t*, uint8_t*,
                         int64_t, int64_t, int64_t, cudaStream_t);
 int light_z_csr(const int32_t*, const int32_t*, int64_t, int64_t, const int32_t*, int64_t, uint8_t*, int32_t*,
@@ -126,6 +128,11 @@ int mmj_build_operand_pairs(const int32_t* rows, const int32_t* cols, int64_t n,
                             int64_t delta2, const int32_t* hpos, uint8_t* mat, int64_t row0, int64_t nrows,
                             int64_t kpad, void* stream) {
   return mmj::build_operand_pairs(rows, cols, n, left_deg, delta2, hpos, mat, row0, nrows, kpad, ST(stream));
+}
+
+int mmj_heavy_row_stats(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t dom,
+                        int64_t delta2, const int32_t* hpos, int64_t* stats, void* stream) {
+  return mmj::heavy_row_stats(rows, cols, n, left_deg, dom, delta2, hpos, stats, ST(stream));
 }
 
 int mmj_build_heavy_rows(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg,

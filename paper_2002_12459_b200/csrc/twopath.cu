@@ -506,6 +506,37 @@ int build_operand(const int32_t* rows, const int32_t* cols, int64_t n, const int
   return MMJ_OK;
 }
 
+// stats[0] = #{x : left_deg[x] > d2}, stats[1] = #{tuples (x, y) : left_deg[x] > d2 and hpos[y] >= 0}
+// (the engine's choice between the tcgen05 product and the in-tile OR)
+__global__ void k_heavy_row_stats(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols, int64_t n,
+                                  const int32_t* __restrict__ left_deg, int64_t dom, int64_t d2,
+                                  const int32_t* __restrict__ hpos, unsigned long long* __restrict__ stats) {
+  unsigned long long nh = 0, nt = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dom; i += stride) nh += left_deg[i] > d2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += stride)
+    nt += (left_deg[rows[t]] > d2) && hpos[cols[t]] >= 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nh += __shfl_xor_sync(0xffffffffu, nh, o);
+    nt += __shfl_xor_sync(0xffffffffu, nt, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (nh | nt)) {
+    atomicAdd(stats, nh);
+    atomicAdd(stats + 1, nt);
+  }
+}
+
+int heavy_row_stats(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t dom,
+                    int64_t d2, const int32_t* hpos, int64_t* stats, cudaStream_t st) {
+  MMJ_TRY(cuda_status(cudaMemsetAsync(stats, 0, 2 * sizeof(int64_t), st), "memset heavy row stats"));
+  if (n == 0 && dom == 0) return MMJ_OK;
+  k_heavy_row_stats<<<grid_for(n > dom ? n : dom, TPB), TPB, 0, st>>>(
+      rows, cols, n, left_deg, dom, d2, hpos, reinterpret_cast<unsigned long long*>(stats));
+  MMJ_CHECK_LAUNCH("k_heavy_row_stats");
+  return MMJ_OK;
+}
+
 int build_heavy_rows(const int32_t* rows, const int32_t* cols, int64_t n, const int32_t* left_deg, int64_t d2,
                      const int32_t* hpos, uint32_t* hbits, int64_t k, int64_t wpr, cudaStream_t st) {
   if (k < 0 || wpr <= 0 || wpr % 4 != 0) {

@@ -245,9 +245,10 @@ class TwoPathEngine:
             return None
         torch = self.torch
         dr = self.dr
-        hx = dr.left_deg > self.d2
-        ht = ((self.hpos[dr.fwd_idx.long()] >= 0) & hx[dr.fwd_row.long()]).sum()
-        return torch.stack([hx.sum(), ht])
+        stats = torch.empty(2, dtype=torch.int64, device="cuda")
+        nat.call("mmj_heavy_row_stats", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n, nat.ptr(dr.left_deg),
+                 dr.dom_left, self.d2, nat.ptr(self.hpos), nat.ptr(stats), self._st())
+        return stats
 
     def _heavy_or(self, stats) -> bool:
         """Projection heavy part as a sparse boolean product (OR of heavy-y
@@ -513,14 +514,20 @@ class TwoPathEngine:
         return slot
 
     def finish(self):
-        self.stats.heavy_pairs = int(self.nnz.item())     # synchronises the stream
-        if self.fused:
-            self.stats.light_intermediate = int(self.wit.item())
+        # one device -> host copy (synchronises the stream): heavy pairs,
+        # witnesses and the asynchronous chunks' (size, light) sums
+        torch = self.torch
+        parts = [self.nnz, self.wit]
         if self._n_async:
-            tot = self._sizes_dev[: self._n_async].sum(dim=0).cpu()
-            self.stats.out_size += int(tot[0])
+            parts.append(self._sizes_dev[: self._n_async].sum(dim=0))
+        vals = torch.cat(parts).cpu().tolist()
+        self.stats.heavy_pairs = int(vals[0])
+        if self.fused:
+            self.stats.light_intermediate = int(vals[1])
+        if self._n_async:
+            self.stats.out_size += int(vals[2])
             if not self.fused:
-                self.stats.light_intermediate += int(tot[1])
+                self.stats.light_intermediate += int(vals[3])
             self._n_async = 0
         return self.stats
 
