@@ -342,12 +342,27 @@ class TwoPath:
                              host_left_deg_r=self.r.left_deg, host_left_deg_s=self.s.left_deg)
 
     def step(self, timer=None):
+        diag = os.environ.get("MMJ_BENCH_DIAG") and timer is not None
+        if diag:
+            import torch
+            t = [time.perf_counter()]
+            m0 = torch.cuda.memory_stats().get("num_device_alloc", 0)
         eng = self.engine()
         self.eng = eng
         eng.timer = timer
+        if diag:
+            t.append(time.perf_counter())
         eng.prepare()
+        if diag:
+            t.append(time.perf_counter())
         for a, b in eng.chunk_bounds(self.x_lo, self.x_hi):
             eng.run_chunk(a, b, sync=False)
+        if diag:
+            t.append(time.perf_counter())
+            self.diag = getattr(self, "diag", []) + [
+                {"engine_ms": round(1e3 * (t[1] - t[0]), 3), "prepare_ms": round(1e3 * (t[2] - t[1]), 3),
+                 "chunks_ms": round(1e3 * (t[3] - t[2]), 3),
+                 "cuda_mallocs": torch.cuda.memory_stats().get("num_device_alloc", 0) - m0}]
         return eng
 
     def units(self, eng):
@@ -1191,6 +1206,7 @@ def run_b200(args):
             "gpu_launches": int(launches), "clocks": clk, "step_ms": [round(1e3 * t, 3) for t in times],
             "host_issue_ms": host_ms,
             "int8_peak_cublaslt_tops": (int8_peak / 1e12) if int8_peak else None,
+            **({"diag": getattr(wl, "diag", None)} if os.environ.get("MMJ_BENCH_DIAG") else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -119,9 +119,10 @@ def _compact_family(idx, c: int):
              nat.ptr(dr.rev_idx), nat.ptr(dr.left_deg), n, dom, dom_y, int(c), nat.ptr(new_id), nat.ptr(orig),
              nat.ptr(dc.fwd_ptr), nat.ptr(dc.fwd_idx), nat.ptr(dc.fwd_row), nat.ptr(dc.left_deg), nat.ptr(dc.rev_ptr),
              nat.ptr(dc.rev_idx), nat.ptr(dc.right_deg), nat.ptr(sizes), nat.ptr(ws_buf), nb, nat.stream_handle())
-    # one small D2H brings back the compacted offsets (their last entry is n')
+    # the compacted offsets follow from the host degrees (kept sets keep their
+    # order and their whole rows): no device -> host copy, no sync
     dom_c = nk
-    dc.fwd_ptr_host = dc.fwd_ptr[:dom_c + 1].cpu().numpy().astype(np.int64)
+    dc.fwd_ptr_host = np.concatenate([[0], np.cumsum(ldeg[keep], dtype=np.int64)])
     n_c = int(dc.fwd_ptr_host[-1])
     dc.n, dc.dom_left, dc.dom_right, dc.device, dc.h2d_bytes = n_c, dom_c, dom_y, dr.device, 0
     dc.fwd_ptr, dc.left_deg = dc.fwd_ptr[:dom_c + 1], dc.left_deg[:dom_c]

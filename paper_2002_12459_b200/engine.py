@@ -179,7 +179,9 @@ class TwoPathEngine:
             dom_y = self.dom_y
             flag = self.ws.get("yflag", dom_y, torch.uint8)
             scan = self.ws.get("yscan", dom_y + 1, torch.int32)
-            self.hpos = torch.empty(max(dom_y, 1), dtype=torch.int32, device="cuda")
+            # engine buffers come from the workspace: an engine re-created for
+            # every step (bench.py) reuses them instead of allocating
+            self.hpos = self.ws.get("e_hpos", max(dom_y, 1), torch.int32)
             nat.call("mmj_heavy_y_positions", nat.ptr(dr.right_deg), nat.ptr(ds.right_deg), dom_y, self.d1,
                      nat.ptr(flag), nat.ptr(scan), nat.ptr(self.hpos), nat.ptr(self.ws.scan_ws(dom_y)), st)
             # one device -> host copy for K and the heavy-part choice's counts
@@ -192,7 +194,7 @@ class TwoPathEngine:
             if k > 0 and heavy_x and heavy_z and self._heavy_or(vals[1:].tolist()):
                 # the heavy rows of S_h at one bit per cell (K x wpr words)
                 self.heavy_kernel = "or"
-                self.hbits = torch.empty((k, self.wpr), dtype=torch.int32, device="cuda")
+                self.hbits = self.ws.get("e_hbits", k * self.wpr, torch.int32).view(k, self.wpr)
                 nat.call("mmj_build_heavy_rows", nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n, nat.ptr(ds.left_deg),
                          self.d2, nat.ptr(self.hpos), nat.ptr(self.hbits), k, self.wpr, st)
             elif k > 0 and heavy_x and heavy_z:
@@ -205,17 +207,17 @@ class TwoPathEngine:
                               and __import__("os").environ.get("MMJ_PAIR", "1") != "0"
                               and (k <= 127 or self._max_deg(self._host_ldeg_r, dr) <= 127
                                    or self._max_deg(self._host_ldeg_s, ds) <= 127))
-                self.A = torch.empty((arows, kpad), dtype=torch.uint8, device="cuda")
+                self.A = self.ws.get("e_A", arows * kpad, torch.uint8).view(arows, kpad)
                 nat.call("mmj_build_operand", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n,
                          nat.ptr(dr.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.A), 0, arows, kpad, st)
                 if self.pairs:
                     # z pairs share one accumulator (weights 1, 128): every
                     # count is < 128 because one side's heavy degrees are <= 127
-                    self.B = torch.empty((brows // 2, kpad), dtype=torch.uint8, device="cuda")
+                    self.B = self.ws.get("e_B", (brows // 2) * kpad, torch.uint8).view(brows // 2, kpad)
                     nat.call("mmj_build_operand_pairs", nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n,
                              nat.ptr(ds.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.B), 0, brows, kpad, st)
                 else:
-                    self.B = torch.empty((brows, kpad), dtype=torch.uint8, device="cuda")
+                    self.B = self.ws.get("e_B", brows * kpad, torch.uint8).view(brows, kpad)
                     nat.call("mmj_build_operand", nat.ptr(ds.fwd_row), nat.ptr(ds.fwd_idx), ds.n,
                              nat.ptr(ds.left_deg), self.d2, nat.ptr(self.hpos), nat.ptr(self.B), 0, brows, kpad, st)
             self.stats.kpad = self.kpad
@@ -223,8 +225,8 @@ class TwoPathEngine:
             n = ds.n
             lflag = self.ws.get("lzflag", n, torch.uint8)
             lpos = self.ws.get("lzpos", n + 1, torch.int32)
-            self.lz_ptr = torch.empty(dom_y + 1, dtype=torch.int32, device="cuda")
-            self.lz_idx = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+            self.lz_ptr = self.ws.get("e_lz_ptr", dom_y + 1, torch.int32)
+            self.lz_idx = self.ws.get("e_lz_idx", max(n, 1), torch.int32)
             nat.call("mmj_light_z_csr", nat.ptr(ds.rev_ptr), nat.ptr(ds.rev_idx), n, dom_y, nat.ptr(ds.left_deg),
                      self.d2, nat.ptr(lflag), nat.ptr(lpos), nat.ptr(self.lz_ptr), nat.ptr(self.lz_idx),
                      nat.ptr(self.ws.scan_ws(n)), st)
@@ -245,7 +247,7 @@ class TwoPathEngine:
             return None
         torch = self.torch
         dr = self.dr
-        stats = torch.empty(2, dtype=torch.int64, device="cuda")
+        stats = self.ws.get("e_orstats", 2, torch.int64)
         nat.call("mmj_heavy_row_stats", nat.ptr(dr.fwd_row), nat.ptr(dr.fwd_idx), dr.n, nat.ptr(dr.left_deg),
                  dr.dom_left, self.d2, nat.ptr(self.hpos), nat.ptr(stats), self._st())
         return stats
@@ -454,13 +456,13 @@ class TwoPathEngine:
             keep = []
             spf = spl = 0
             if ncb > 1 and n <= (64 << 20):
-                full = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+                full = self.ws.get("e_split_full", max(n, 1), torch.int32)
                 nat.call("mmj_list_splits", nat.ptr(self.ds.rev_ptr), nat.ptr(self.ds.rev_idx), self.dom_y, self.wpr,
                          nat.ptr(full), st)
                 keep.append(full)
                 spf = nat.ptr(full)
                 if self.lz_ptr is not None:
-                    lzt = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+                    lzt = self.ws.get("e_split_lz", max(n, 1), torch.int32)
                     nat.call("mmj_list_splits", nat.ptr(self.lz_ptr), nat.ptr(self.lz_idx), self.dom_y, self.wpr,
                              nat.ptr(lzt), st)
                     keep.append(lzt)
