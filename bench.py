@@ -557,7 +557,9 @@ class TwoPath:
         import torch
 
         from paper_2002_12459_b200.joinproject import two_path_join_chunks
-        rows = 2048
+        # 2048-row chunks on one GPU; smaller per rank when N ranks pin their
+        # double buffers on one host (2 x the largest chunk's codes each)
+        rows = max(256, 2048 // max(self.world, 1))
         # two pinned buffers sized by the largest 2048-row chunk's output
         # (untimed sizing pass), not by the chunk's rows x dom_z cells
         cap = 0
@@ -777,7 +779,9 @@ class Ssj:
         self.setup_host()
         self.idx = self.fam.indexed
         self.plan = _ssj_plan(self.idx, None, 4)
-        self.make = lambda: _ssj_engine(self.idx, 4, self.plan, compact=True)
+        from paper_2002_12459_b200.device import Workspace
+        self.ws = Workspace()
+        self.make = lambda: _ssj_engine(self.idx, 4, self.plan, compact=True, ws=self.ws)
         eng, _ = self.make()
         # triangle work balance: rows a own the cells z > a
         dom = eng.dom_x

@@ -84,7 +84,7 @@ def _device_pairs(eng):
 COMPACT_MAX_KEPT = 0.9
 
 
-def _compact_family(idx, c: int):
+def _compact_family(idx, c: int, ws=None):
     """Sets with fewer than ``c`` elements reach no overlap >= c (the
     ``cnt >= c`` filter of apps.py:61-62), so their rows and columns of the
     count matrix are dead work: drop them on the device and renumber the kept
@@ -107,14 +107,22 @@ def _compact_family(idx, c: int):
     dr = device_relation(idx)
     n, dom, dom_y = dr.n, dr.dom_left, dr.dom_right
 
-    def buf(k):
+    def buf(k, key):
+        if ws is not None:
+            return ws.get("cf_" + key, max(k, 1), torch.int32)
         return torch.empty(max(k, 1), dtype=torch.int32, device="cuda")
-    new_id, orig = buf(dom), buf(dom)
+    new_id, orig = buf(dom, "new_id"), buf(dom, "orig")
     dc = DeviceRelation()
-    dc.fwd_ptr, dc.fwd_idx, dc.fwd_row, dc.left_deg = buf(dom + 1), buf(n), buf(n), buf(dom)
-    dc.rev_ptr, dc.rev_idx, dc.right_deg = buf(dom_y + 1), buf(n), buf(dom_y)
-    sizes = torch.empty(2, dtype=torch.int64, device="cuda")   # written by mmj_compact_rows
-    ws_buf, nb = IngestWorkspace().get(max(n, dom, dom_y))
+    dc.fwd_ptr, dc.fwd_idx, dc.fwd_row, dc.left_deg = (buf(dom + 1, "fptr"), buf(n, "fidx"), buf(n, "frow"),
+                                                       buf(dom, "ldeg"))
+    dc.rev_ptr, dc.rev_idx, dc.right_deg = buf(dom_y + 1, "rptr"), buf(n, "ridx"), buf(dom_y, "rdeg")
+    sizes = (ws.get("cf_sizes", 2, torch.int64) if ws is not None
+             else torch.empty(2, dtype=torch.int64, device="cuda"))   # written by mmj_compact_rows
+    if ws is not None:
+        nb = int(nat.load().mmj_ingest_workspace_bytes(int(max(n, dom, dom_y))))
+        ws_buf = ws.get("cf_ingest", nb, torch.uint8)
+    else:
+        ws_buf, nb = IngestWorkspace().get(max(n, dom, dom_y))
     nat.call("mmj_compact_rows", nat.ptr(dr.fwd_ptr), nat.ptr(dr.fwd_idx), nat.ptr(dr.fwd_row), nat.ptr(dr.rev_ptr),
              nat.ptr(dr.rev_idx), nat.ptr(dr.left_deg), n, dom, dom_y, int(c), nat.ptr(new_id), nat.ptr(orig),
              nat.ptr(dc.fwd_ptr), nat.ptr(dc.fwd_idx), nat.ptr(dc.fwd_row), nat.ptr(dc.left_deg), nat.ptr(dc.rev_ptr),
@@ -139,14 +147,18 @@ def _decode_compact(codes, dom_c: int, orig, dom: int):
     return codes
 
 
-def _ssj_engine(idx, c: int, plan: ThresholdPlan, chunk_rows: Optional[int] = None, compact: bool = True):
+def _ssj_engine(idx, c: int, plan: ThresholdPlan, chunk_rows: Optional[int] = None, compact: bool = True,
+                ws=None):
     """(engine, decode) for the SSJ count join over ``idx``: the engine runs on
     the compacted family when sets below ``c`` are a large share, and
-    ``decode(codes)`` maps its codes back to ``idx``'s dense ids."""
+    ``decode(codes)`` maps its codes back to ``idx``'s dense ids.  ``ws``: a
+    workspace reused across calls (the compacted family and the engine's
+    buffers live in it; one call at a time)."""
     from .joinproject import _engine
-    comp = _compact_family(idx, c) if (compact and c > 1) else None
+    comp = _compact_family(idx, c, ws) if (compact and c > 1) else None
     if comp is None:
-        return _engine(idx, idx, plan, True, min_count=c, upper_only=True, chunk_rows=chunk_rows), (lambda x: x)
+        return (_engine(idx, idx, plan, True, min_count=c, upper_only=True, chunk_rows=chunk_rows, ws=ws),
+                (lambda x: x))
     from .engine import TwoPathEngine
     dc, orig, hdeg = comp
     if plan.strategy == PARTITIONED:
@@ -154,7 +166,7 @@ def _ssj_engine(idx, c: int, plan: ThresholdPlan, chunk_rows: Optional[int] = No
     else:
         d1 = d2 = max(dc.n, 1)
     eng = TwoPathEngine(dc, dc, plan.strategy, d1, d2, True, min_count=c, upper_only=True, chunk_rows=chunk_rows,
-                        host_left_deg_r=hdeg, host_left_deg_s=hdeg)
+                        host_left_deg_r=hdeg, host_left_deg_s=hdeg, ws=ws)
     dom = int(idx.rel.dom_left)
     return eng, (lambda x: _decode_compact(x, dc.dom_left, orig, dom))
 
