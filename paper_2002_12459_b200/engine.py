@@ -162,14 +162,20 @@ class TwoPathEngine:
         self._sizes_dev = None
         self._n_async = 0
         self.timer = None          # optional PhaseTimer (bench instrumentation)
+        self._stream = None
 
     # ------------------------------------------------------------ prepare
     def _st(self):
-        return nat.stream_handle()
+        # the launching stream, looked up once per prepare() (a
+        # torch.cuda.current_stream() call costs ~17 us of host time)
+        if self._stream is None:
+            self._stream = nat.stream_handle()
+        return self._stream
 
     def prepare(self):
         if self._prepared:
             return
+        self._stream = None
         torch = self.torch
         st = self._st()
         dr, ds = self.dr, self.ds
