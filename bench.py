@@ -441,7 +441,7 @@ class TwoPath:
                     "peak_kind": hbm_kind,
                     "algorithmic": "8 B per distinct output code (SURVEY 8(d)) x |OUT| / the kernel's summed "
                                    "CUDA-event time over the step's chunks"}
-        roof["traffic"], roof["traffic_detail"] = _ncu_traffic(dominant)
+        roof["traffic"], roof["traffic_detail"] = _ncu_traffic(dominant, self.args.config)
         eng = self.eng
         if eng.heavy_kernel == "or":
             # heavy part inside k_merge_emit: every heavy row ORs its heavy-y
@@ -587,7 +587,7 @@ class TwoPath:
                 "api": "joinproject.two_path_join_chunks(upload='fresh', host_buffer=(pinned, pinned))"}
 
 
-def _ncu_traffic(kernel_phase):
+def _ncu_traffic(kernel_phase, config=None):
     """(traffic, detail) of the dominant kernel from the committed `ncu --set
     full` capture (profiles/ncu_traffic.json): the captured launch's own
     dram__bytes_read.sum + dram__bytes_write.sum, unscaled, with that launch's
@@ -599,6 +599,8 @@ def _ncu_traffic(kernel_phase):
         t = json.load(f).get(kernel_phase)
     if not isinstance(t, dict) or "dram_bytes_per_launch" not in t:
         return None, None
+    if config is not None and t.get("config") not in (None, config):
+        return None, None           # the capture is of another config's launch
     detail = {k: t[k] for k in ("kernel", "algorithmic_bytes_per_launch", "traffic_over_algorithmic", "source", "note")
               if k in t}
     return t["dram_bytes_per_launch"], detail
@@ -1018,7 +1020,7 @@ class Bsi:
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                 "kernel": "bsi build + answer (whole step)", "peak_kind": hbm_kind,
                 "algorithmic": "B_bsi = 8 B per input tuple + 9 B per query (SURVEY 8(d) lower bound) / step time"}
-        roof["traffic"], roof["traffic_detail"] = _ncu_traffic("bsi_answer") if self.eng.form == "lists" else (None, None)
+        roof["traffic"], roof["traffic_detail"] = _ncu_traffic("bsi_answer", "cfg5") if self.eng.form == "lists" else (None, None)
         cfg = {"workload": self.wl.description + " (BASELINE configs[4])", "config_name": "cfg5",
                "queries_this_rank": self.nq, "batch_slice": [self.qlo, self.qhi], "heavy_bits": 256,
                "bsi_form": self.eng.form,
