@@ -93,6 +93,34 @@ __device__ __forceinline__ int32_t map_id(const IdMap& m, int64_t v) {
   return m.sorted ? lookup(m.sorted, m.order, m.n, v) : (int32_t)v;
 }
 
+// L2 eviction-priority hints for the lists form: the id tables and list
+// offsets (4 x 16 MB at cfg5, every 64-byte granule read ~16 times per batch)
+// are kept (evict_last) while the lists themselves (each read about once)
+// stream through (evict_first) -- otherwise the lists push the tables out and
+// every 4-byte table / offset read costs a DRAM granule.
+__device__ __forceinline__ uint64_t l2_keep() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_stream() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int32_t ld_pol(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int32_t map_id_pol(const IdMap& m, int64_t v, uint64_t pol) {
+  if (m.table) {
+    const int64_t o = v - m.vmin;
+    return (o >= 0 && o < m.range) ? ld_pol(m.table + o, pol) : -1;
+  }
+  return m.sorted ? lookup(m.sorted, m.order, m.n, v) : (int32_t)v;
+}
+
 struct BsiSideArgs {
   IdMap map;
   const uint32_t* rec;
@@ -171,15 +199,16 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restr
                                                           const int32_t* __restrict__ pa_idx,
                                                           const int32_t* __restrict__ pb_ptr,
                                                           const int32_t* __restrict__ pb_idx, int8_t* __restrict__ ans) {
+  const uint64_t keep = l2_keep(), stream = l2_stream();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t ia = map_id(ma, __ldcs(qa + q));
-    const int32_t ib = map_id(mb, __ldcs(qb + q));
+    const int32_t ia = map_id_pol(ma, __ldcs(qa + q), keep);
+    const int32_t ib = map_id_pol(mb, __ldcs(qb + q), keep);
     if (ia < 0 || ib < 0) {
       ans[q] = -1;
       continue;
     }
-    const int2 ra = make_int2(__ldg(pa_ptr + ia), __ldg(pa_ptr + ia + 1));
-    const int2 rb = make_int2(__ldg(pb_ptr + ib), __ldg(pb_ptr + ib + 1));
+    const int2 ra = make_int2(ld_pol(pa_ptr + ia, keep), ld_pol(pa_ptr + ia + 1, keep));
+    const int2 rb = make_int2(ld_pol(pb_ptr + ib, keep), ld_pol(pb_ptr + ib + 1, keep));
     const int32_t na = ra.y - ra.x, nb = rb.y - rb.x;
     MMJ_DCHECK(ra.x >= 0 && rb.x >= 0, "list bounds");
     bool hit = false;
@@ -189,15 +218,15 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restr
       // both lists' first sectors requested together; the merge then walks
       // 32-byte sectors on demand (an L1 line prefetch of every list moved
       // 613 B of DRAM per query, r2f ncu: whole 128-B lines for 64-B lists)
-      const int32_t a0 = __ldg(la), b0 = __ldg(lb);
+      const int32_t a0 = ld_pol(la, stream), b0 = ld_pol(lb, stream);
       // and the next three 32-byte sectors of each (lists up to 32 entries)
       // with real loads, so the merge's later steps hit L1 instead of
       // waiting on one DRAM round trip per sector
       int32_t warm = 0;
 #pragma unroll
       for (int k = 1; k < 4; ++k) {
-        if (8 * k < na) warm += __ldg(la + 8 * k);
-        if (8 * k < nb) warm += __ldg(lb + 8 * k);
+        if (8 * k < na) warm += ld_pol(la + 8 * k, stream);
+        if (8 * k < nb) warm += ld_pol(lb + 8 * k, stream);
       }
       asm volatile("" ::"r"(warm));
       {
