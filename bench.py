@@ -72,7 +72,7 @@ def _args(argv=None):
     ap.add_argument("--no-light-work", action="store_true", help="skip the light-pass byte count (diagnostic)")
     ap.add_argument("--x-limit", type=int, default=0, help="debug: only the first X output rows")
     ap.add_argument("--clock-period-ms", type=int, default=100, help="nvidia-smi sampling period during the steps")
-    ap.add_argument("--bsi-form", default="auto", choices=["auto", "lists", "records"],
+    ap.add_argument("--bsi-form", default="auto", choices=["auto", "lists", "records", "walk"],
                     help="cfg5 device algorithm (bsi.BsiEngine); answers are identical")
     return ap.parse_args(argv)
 

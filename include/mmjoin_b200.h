@@ -266,7 +266,8 @@ int mmj_bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64
                    int words, int8_t* ans, void* stream);
 /* the same answers without any index build: the two queried ids' forward
  * lists (fwd_ptr / fwd_idx int32, each list sorted by the shared y id) are
- * merge-intersected directly; id maps as for mmj_bsi_answer.  The engine
+ * intersected directly (a warp per 32 queries, lists loaded coalesced into
+ * registers, shuffle binary search); id maps as for mmj_bsi_answer.  The engine
  * takes this form when the lists are short (mean length <= 64), where a
  * bitset record moves as many DRAM sectors as the list it summarises. */
 int mmj_bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted,
@@ -279,6 +280,20 @@ int mmj_bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const
  * binary search; range = max - min + 1 < 2^31) */
 int mmj_bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
                          int32_t* table, void* stream);
+/* span table for dense raw id ranges: table[range] uint32 = (forward-list
+ * offset << len_bits) | min(list length, 2^len_bits - 1) of raw value
+ * vmin + i, 0xFFFFFFFF where absent; needs n_tuples < 2^(32 - len_bits) - 1.
+ * mmj_bsi_answer_spans resolves each query id with that one load (a
+ * saturated length falls back to a binary search of the offset in fwd_ptr)
+ * and intersects the two forward lists: the left_ids.get() probes and set
+ * intersection of apps.py:321-350, same answers as mmj_bsi_answer_lists */
+int mmj_bsi_span_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
+                       const int32_t* fwd_ptr, int64_t n_tuples, int len_bits, uint32_t* table, void* stream);
+int mmj_bsi_answer_spans(const int64_t* qa, const int64_t* qb, int64_t nq, const uint32_t* r_span, int64_t r_min,
+                         int64_t r_range, int r_len_bits, const int32_t* r_fwd_ptr, int64_t r_dom,
+                         const int32_t* r_fwd_idx, const uint32_t* s_span, int64_t s_min, int64_t s_range,
+                         int s_len_bits, const int32_t* s_fwd_ptr, int64_t s_dom, const int32_t* s_fwd_idx,
+                         int8_t* ans, void* stream);
 
 
 /* ---- device ingest: relation.py:37-69, 119-140, 148-186 ----

@@ -28,6 +28,9 @@ from .device import Workspace
 BITS_BLOCK = 128     # bitset width granularity (4 words)
 LIST_MAX_MEAN = 64   # "lists" form when both sides' mean list length is at most this
 DIRECT_SPREAD = 4    # direct id table when max - min + 1 <= 4 x the number of ids
+SPAN_MAX_LEN_BITS = 16
+SPAN_MIN_LEN_BITS = 4  # span table only when a 32-bit entry leaves >= 4 length bits ...
+SPAN_MEAN_FRAC = 2     # ... and the mean list is at most half the largest length they hold
 
 
 def _torch():
@@ -48,6 +51,7 @@ class BsiSide:
     order: object             # device int32 dense id of each sorted value
     h2d_bytes: int = 0
     table: object = None      # (direct-address id table, vmin, range) or None
+    span: object = None       # (span table, vmin, range, len_bits) or None
 
 
 def _attach_table(sd: BsiSide, ends) -> None:
@@ -67,6 +71,15 @@ def _attach_table(sd: BsiSide, ends) -> None:
     nat.call("mmj_bsi_direct_table", nat.ptr(sd.sorted_vals), nat.ptr(sd.order), sd.dom_left, vmin, rng,
              nat.ptr(table), nat.stream_handle())
     sd.table = (table, vmin, rng)
+    # span table: raw id -> (list offset, length) in one 32-bit entry, when
+    # the tuple count leaves enough length bits for the typical list (a
+    # saturated length costs the query a binary search over fwd_ptr)
+    len_bits = min(SPAN_MAX_LEN_BITS, 32 - (sd.n + 1).bit_length())
+    if len_bits >= SPAN_MIN_LEN_BITS and sd.n * SPAN_MEAN_FRAC <= ((1 << len_bits) - 1) * sd.dom_left:
+        span = torch.empty(rng, dtype=torch.int32, device="cuda")
+        nat.call("mmj_bsi_span_table", nat.ptr(sd.sorted_vals), nat.ptr(sd.order), sd.dom_left, vmin, rng,
+                 nat.ptr(sd.fwd_ptr), sd.n, len_bits, nat.ptr(span), nat.stream_handle())
+        sd.span = (span, vmin, rng, len_bits)
 
 
 def _with_tables(sides):
@@ -235,8 +248,13 @@ class BsiEngine:
         self.lib = nat.load()
         if heavy_bits not in (128, 256, 512, 1024):
             raise ValueError("heavy_bits must be 128, 256, 512 or 1024")
-        if form not in ("auto", "lists", "records"):
-            raise ValueError("form must be 'auto', 'lists' or 'records'")
+        if form not in ("auto", "lists", "records", "walk"):
+            raise ValueError("form must be 'auto', 'lists', 'records' or 'walk'")
+        # "walk" = the lists form resolving ids through the id table and
+        # fwd_ptr even where span tables exist (A/B and parity of the two)
+        self.use_spans = form != "walk"
+        if form == "walk":
+            form = "lists"
         if form == "auto":
             short = all(sd.n <= LIST_MAX_MEAN * max(sd.dom_left, 1) for sd in (sR, sS))
             form = "lists" if short else "records"
@@ -309,6 +327,14 @@ class BsiEngine:
             if t is not None:
                 return 0, 0, 0, nat.ptr(t[0]), t[1], t[2]
             return nat.ptr(side.sorted_vals), nat.ptr(side.order), side.dom_left, 0, 0, 0
+        if self.form == "lists" and not (dense_a or dense_b) and self.sR.span and self.sS.span and self.use_spans:
+            # raw id -> list span in one load per side (cfg5)
+            def span(side):
+                t = side.span
+                return (nat.ptr(t[0]), t[1], t[2], t[3], nat.ptr(side.fwd_ptr), side.dom_left, nat.ptr(side.fwd_idx))
+            nat.call("mmj_bsi_answer_spans", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, *span(self.sR), *span(self.sS),
+                     nat.ptr(ans), nat.stream_handle())
+            return ans[:nq]
         if self.form == "lists":
             nat.call("mmj_bsi_answer_lists", nat.ptr(qa_dev), nat.ptr(qb_dev), nq, *idmap(self.sR, dense_a),
                      *idmap(self.sS, dense_b), nat.ptr(self.sR.fwd_ptr), nat.ptr(self.sR.fwd_idx),

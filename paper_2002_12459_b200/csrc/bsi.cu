@@ -18,6 +18,7 @@
 //     with its nonzero test, restricted to queried cells; otherwise the two
 //     light lists (sectors prefetched to L1 first) are merge-intersected.
 #include "mmj_common.cuh"
+#include <cstdlib>
 
 namespace mmj {
 namespace {
@@ -187,67 +188,190 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer(const int64_t* __restrict__ 
   }
 }
 
-// Sorted-list intersection of the two queried ids' forward lists (both
-// sorted by the shared y id): the index IS the relations' CSR, so nothing is
-// built per batch.  Taken when the lists are short (cfg5: 16 y per id on
-// average), where a bitset record (64 B) costs as many DRAM sectors as the
-// list itself and its build pass would be the larger part of the step.  Both
-// lists' 32-byte sectors are requested before the (dependent) merge.
-__global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restrict__ qa,
-                                                          const int64_t* __restrict__ qb, int64_t nq, const IdMap ma,
-                                                          const IdMap mb, const int32_t* __restrict__ pa_ptr,
-                                                          const int32_t* __restrict__ pa_idx,
-                                                          const int32_t* __restrict__ pb_ptr,
-                                                          const int32_t* __restrict__ pb_idx, int8_t* __restrict__ ans) {
-  const uint64_t keep = l2_keep(), stream = l2_stream();
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t ia = map_id_pol(ma, __ldcs(qa + q), keep);
-    const int32_t ib = map_id_pol(mb, __ldcs(qb + q), keep);
-    if (ia < 0 || ib < 0) {
-      ans[q] = -1;
-      continue;
-    }
-    const int2 ra = make_int2(ld_pol(pa_ptr + ia, keep), ld_pol(pa_ptr + ia + 1, keep));
-    const int2 rb = make_int2(ld_pol(pb_ptr + ib, keep), ld_pol(pb_ptr + ib + 1, keep));
-    const int32_t na = ra.y - ra.x, nb = rb.y - rb.x;
-    MMJ_DCHECK(ra.x >= 0 && rb.x >= 0, "list bounds");
-    bool hit = false;
-    if (na > 0 && nb > 0) {
-      const int32_t* la = pa_idx + ra.x;
-      const int32_t* lb = pb_idx + rb.x;
-      // both lists' first sectors requested together; the merge then walks
-      // 32-byte sectors on demand (an L1 line prefetch of every list moved
-      // 613 B of DRAM per query, r2f ncu: whole 128-B lines for 64-B lists)
-      const int32_t a0 = ld_pol(la, stream), b0 = ld_pol(lb, stream);
-      // and the next three 32-byte sectors of each (lists up to 32 entries)
-      // with real loads, so the merge's later steps hit L1 instead of
-      // waiting on one DRAM round trip per sector
-      int32_t warm = 0;
-#pragma unroll
-      for (int k = 1; k < 4; ++k) {
-        if (8 * k < na) warm += ld_pol(la + 8 * k, stream);
-        if (8 * k < nb) warm += ld_pol(lb + 8 * k, stream);
+// ---- "lists" form: warp-cooperative intersection of the forward lists ------
+// Both lists of a query are sorted by the shared y id, so the index IS the
+// relations' CSR and nothing is built per batch.  Taken when the lists are
+// short (cfg5: 16 y per id on average), where a bitset record (64 B) costs as
+// many DRAM granules as the list itself.
+//
+// A warp takes 32 queries: every lane resolves its own query's two list spans
+// (the table loads of 32 queries in flight together), then the warp walks the
+// queries, PIPE at a time: lane l loads element l of each list (one coalesced
+// request per list, every sector fetched once, straight into registers), and
+// the two 32-entry chunks are intersected by a shuffle binary search (5
+// steps) + ballot.  Lists longer than 32 take a chunked merge.  The
+// thread-per-query merge this replaces (r3b: 0.48 ms per 4M queries, 0.64 ms
+// before the span tables) ran 0.41 ms at PIPE = 2 (r3d/r3e; PIPE = 1 / 3 / 4 /
+// 8: 0.46 / 0.48 / 0.47 / 0.54 ms -- occupancy beats a deeper pipeline).
+//
+// Raw id -> list, three ways per side (ListSide):
+//   * span table (mmj_bsi_span_table): table[raw - vmin] = (offset <<
+//     len_bits) | min(length, 2^len_bits - 1), 0xFFFFFFFF for an id the
+//     relation does not hold -- one 4-byte load instead of the id table ->
+//     fwd_ptr[id], fwd_ptr[id + 1] chain (two more DRAM granules per side);
+//     a saturated length field sends the query to a binary search of its
+//     offset in fwd_ptr;
+//   * direct id table or binary search over the sorted raw ids, then fwd_ptr;
+//   * dense ids already (map all null).
+struct ListSide {
+  IdMap map;                // raw id -> dense id (when span == nullptr)
+  const uint32_t* span;     // raw id -> packed (offset, length), or nullptr
+  int64_t vmin, range;      // span table window
+  int len_bits;             // length bits of a span entry
+  const int32_t* fwd_ptr;   // dom + 1 CSR offsets (searched when a span's length saturates)
+  int64_t dom;
+  const int32_t* lists;     // fwd_idx
+};
+
+__device__ __forceinline__ uint32_t ld_pol_u32(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// (first entry index in s.lists, length) of raw id v's list; length -1 for an unknown id
+__device__ __forceinline__ int2 resolve_list(const ListSide& s, int64_t v, uint64_t keep) {
+  if (s.span) {
+    const int64_t o = v - s.vmin;
+    if (o < 0 || o >= s.range) return make_int2(0, -1);
+    const uint32_t e = ld_pol_u32(s.span + o, keep);
+    if (e == 0xFFFFFFFFu) return make_int2(0, -1);
+    const uint32_t cap = (1u << s.len_bits) - 1u;
+    const int32_t off = (int32_t)(e >> s.len_bits);
+    int32_t len = (int32_t)(e & cap);
+    if (len == (int32_t)cap) {
+      // saturated: the (non-empty) list's id is the last i with fwd_ptr[i] <= off
+      int64_t lo = 0, hi = s.dom;          // answer in [lo, hi)
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(s.fwd_ptr + mid) <= off) lo = mid;
+        else hi = mid;
       }
-      asm volatile("" ::"r"(warm));
-      {
-        int32_t i = 0, j = 0;
-        int32_t u = a0, v = b0;
-        while (true) {
-          if (u == v) {
-            hit = true;
-            break;
-          }
-          if (u < v) {
-            if (++i == na) break;
-            u = __ldg(la + i);
-          } else {
-            if (++j == nb) break;
-            v = __ldg(lb + j);
-          }
+      len = __ldg(s.fwd_ptr + lo + 1) - off;
+      MMJ_DCHECK(__ldg(s.fwd_ptr + lo) == off && len >= (int32_t)cap, "span escape");
+    }
+    return make_int2(off, len);
+  }
+  const int32_t id = map_id_pol(s.map, v, keep);
+  if (id < 0) return make_int2(0, -1);
+  const int32_t p0 = ld_pol(s.fwd_ptr + id, keep), p1 = ld_pol(s.fwd_ptr + id + 1, keep);
+  MMJ_DCHECK(p0 >= 0 && p1 >= p0, "list bounds");
+  return make_int2(p0, p1 - p0);
+}
+
+constexpr int32_t PAD_Y = 0x7FFFFFFF;   // beyond every y id (dom_y < 2^31 - 1)
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+// does any of the first ca values of `a` (one per lane) occur among the first
+// cb values of `b` (ascending, padded with PAD_Y)?  warp-uniform result
+__device__ __forceinline__ bool chunk_match(int32_t a, int32_t b, int ca, int cb, int lane) {
+  int lo = 0;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const int32_t v = __shfl_sync(FULL, b, lo + s - 1);
+    if (v < a) lo += s;
+  }
+  const int32_t v = __shfl_sync(FULL, b, lo);
+  return __any_sync(FULL, lane < ca && lo < cb && v == a);
+}
+
+// lists of any length, 32-entry chunks of each side; the chunk with the
+// smaller last value advances
+__device__ __noinline__ bool long_intersect(const int32_t* __restrict__ la, int na, const int32_t* __restrict__ lb,
+                                            int nb, int lane) {
+  int ia = 0, ib = 0;
+  int32_t a = lane < na ? __ldg(la + lane) : PAD_Y;
+  int32_t b = lane < nb ? __ldg(lb + lane) : PAD_Y;
+  while (true) {
+    const int ca = min(32, na - ia), cb = min(32, nb - ib);
+    if (chunk_match(a, b, ca, cb, lane)) return true;
+    const int32_t amax = __shfl_sync(FULL, a, ca - 1), bmax = __shfl_sync(FULL, b, cb - 1);
+    if (amax <= bmax) {
+      ia += ca;
+      if (ia >= na) return false;
+      a = ia + lane < na ? __ldg(la + ia + lane) : PAD_Y;
+    }
+    if (bmax <= amax) {
+      ib += cb;
+      if (ib >= nb) return false;
+      b = ib + lane < nb ? __ldg(lb + ib + lane) : PAD_Y;
+    }
+  }
+}
+
+constexpr int PIPE = 2;   // queries whose list loads are in flight together per warp
+
+template <bool MATCH>
+__global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restrict__ qa,
+                                                          const int64_t* __restrict__ qb, int64_t nq,
+                                                          const ListSide sa, const ListSide sb,
+                                                          int8_t* __restrict__ ans) {
+  // L2 hints: tables and offsets are re-read across the batch (evict_last),
+  // the lists are read about once (evict_first)
+  const uint64_t keep = l2_keep(), stream = l2_stream();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * 32; base < nq; base += nwarps * 32) {
+    const int64_t q = base + lane;
+    int2 ra = make_int2(0, -1), rb = make_int2(0, -1);
+    if (q < nq) {
+      ra = resolve_list(sa, __ldcs(qa + q), keep);
+      rb = resolve_list(sb, __ldcs(qb + q), keep);
+    }
+    int res = (ra.y < 0 || rb.y < 0) ? -1 : 0;
+    unsigned todo = __ballot_sync(FULL, ra.y > 0 && rb.y > 0);
+    while (todo) {
+      int j[PIPE], na[PIPE], nb[PIPE], oa[PIPE], ob[PIPE];
+      int32_t a[PIPE], b[PIPE];
+#pragma unroll
+      for (int p = 0; p < PIPE; ++p) {
+        j[p] = todo ? __ffs(todo) - 1 : -1;
+        todo &= todo - 1;            // 0 stays 0
+        const int src = j[p] & 31;
+        oa[p] = __shfl_sync(FULL, ra.x, src);
+        na[p] = j[p] >= 0 ? __shfl_sync(FULL, ra.y, src) : 0;
+        ob[p] = __shfl_sync(FULL, rb.x, src);
+        nb[p] = j[p] >= 0 ? __shfl_sync(FULL, rb.y, src) : 0;
+        if (MATCH && na[p] + nb[p] <= 32) {
+          // both lists in one register row: lanes [0, na) hold A, [na, na + nb) hold B
+          const int32_t* src = lane < na[p] ? sa.lists + oa[p] + lane : sb.lists + ob[p] + (lane - na[p]);
+          a[p] = lane < na[p] + nb[p] ? ld_pol(src, stream) : -1 - lane;
+          b[p] = 0;
+        } else {
+          a[p] = lane < na[p] ? ld_pol(sa.lists + oa[p] + lane, stream) : PAD_Y;
+          b[p] = lane < nb[p] ? ld_pol(sb.lists + ob[p] + lane, stream) : PAD_Y;
         }
       }
+#pragma unroll
+      for (int p = 0; p < PIPE; ++p) {
+        if (j[p] < 0) continue;      // warp-uniform
+        bool hit;
+        if (MATCH && na[p] + nb[p] <= 32) {
+          // a list holds no value twice, so two equal lanes are one y in both lists
+          const unsigned same = __match_any_sync(FULL, a[p]);
+          hit = __any_sync(FULL, (same & (same - 1)) != 0u);
+        } else if (na[p] <= 32 && nb[p] <= 32) hit = chunk_match(a[p], b[p], na[p], nb[p], lane);
+        else hit = long_intersect(sa.lists + oa[p], na[p], sb.lists + ob[p], nb[p], lane);
+        if (lane == j[p]) res = hit ? 1 : 0;
+      }
     }
-    ans[q] = hit ? 1 : 0;
+    if (q < nq) ans[q] = (int8_t)res;
+  }
+}
+
+// span entry of every held raw id: (fwd_ptr[dense] << len_bits) | min(length, cap)
+__global__ void k_span_table(const int64_t* __restrict__ sorted, const int32_t* __restrict__ order, int64_t n,
+                             int64_t vmin, int64_t range, const int32_t* __restrict__ fwd_ptr, int len_bits,
+                             uint32_t* __restrict__ table) {
+  const uint32_t cap = (1u << len_bits) - 1u;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = sorted[i] - vmin;
+    if (o < 0 || o >= range) continue;
+    const int32_t d = order[i];
+    const uint32_t off = (uint32_t)fwd_ptr[d];
+    const uint32_t len = (uint32_t)fwd_ptr[d + 1] - off;
+    table[o] = (off << len_bits) | (len < cap ? len : cap);
   }
 }
 
@@ -326,6 +450,16 @@ int bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* 
   return MMJ_OK;
 }
 
+static int launch_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const ListSide& a,
+                               const ListSide& b, int8_t* ans, cudaStream_t st) {
+  // a warp per 32 queries, 16 waves of resident CTAs at most
+  static const bool use_match = getenv("MMJ_BSI_MATCH") && atoi(getenv("MMJ_BSI_MATCH")) != 0;
+  if (use_match) k_bsi_answer_lists<true><<<grid_for(nq, TPB, 16), TPB, 0, st>>>(qa, qb, nq, a, b, ans);
+  else k_bsi_answer_lists<false><<<grid_for(nq, TPB, 16), TPB, 0, st>>>(qa, qb, nq, a, b, ans);
+  MMJ_CHECK_LAUNCH("k_bsi_answer_lists");
+  return MMJ_OK;
+}
+
 int bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* r_sorted,
                      const int32_t* r_order, int64_t r_n, const int32_t* r_table, int64_t r_min, int64_t r_range,
                      const int64_t* s_sorted, const int32_t* s_order, int64_t s_n, const int32_t* s_table,
@@ -336,12 +470,9 @@ int bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const int
     set_error("bsi_answer_lists: both forward CSRs are required");
     return MMJ_ERR_ARG;
   }
-  const IdMap a{r_sorted, r_order, r_n, r_table, r_min, r_range};
-  const IdMap b{s_sorted, s_order, s_n, s_table, s_min, s_range};
-  k_bsi_answer_lists<<<grid_for(nq, TPB, 16), TPB, 0, st>>>(qa, qb, nq, a, b, r_fwd_ptr, r_fwd_idx, s_fwd_ptr,
-                                                             s_fwd_idx, ans);
-  MMJ_CHECK_LAUNCH("k_bsi_answer_lists");
-  return MMJ_OK;
+  const ListSide a{IdMap{r_sorted, r_order, r_n, r_table, r_min, r_range}, nullptr, 0, 0, 0, r_fwd_ptr, 0, r_fwd_idx};
+  const ListSide b{IdMap{s_sorted, s_order, s_n, s_table, s_min, s_range}, nullptr, 0, 0, 0, s_fwd_ptr, 0, s_fwd_idx};
+  return launch_answer_lists(qa, qb, nq, a, b, ans, st);
 }
 
 int bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
@@ -355,6 +486,40 @@ int bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int
   k_direct_table<<<grid_for(n), TPB, 0, st>>>(sorted, order, n, vmin, range, table);
   MMJ_CHECK_LAUNCH("k_direct_table");
   return MMJ_OK;
+}
+
+int bsi_span_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
+                   const int32_t* fwd_ptr, int64_t n_tuples, int len_bits, uint32_t* table, cudaStream_t st) {
+  if (range <= 0 || range >= (1ll << 31)) {
+    set_error("bsi_span_table: range %lld out of (0, 2^31)", (long long)range);
+    return MMJ_ERR_ARG;
+  }
+  if (len_bits < 1 || len_bits > 16 || n_tuples < 0 || n_tuples >= (1ll << (32 - len_bits)) - 1) {
+    set_error("bsi_span_table: %lld tuples do not leave %d length bits in a 32-bit span", (long long)n_tuples,
+              len_bits);
+    return MMJ_ERR_ARG;
+  }
+  MMJ_TRY(cuda_status(cudaMemsetAsync(table, 0xFF, (size_t)range * 4, st), "memset span table"));
+  if (n == 0) return MMJ_OK;
+  k_span_table<<<grid_for(n), TPB, 0, st>>>(sorted, order, n, vmin, range, fwd_ptr, len_bits, table);
+  MMJ_CHECK_LAUNCH("k_span_table");
+  return MMJ_OK;
+}
+
+int bsi_answer_spans(const int64_t* qa, const int64_t* qb, int64_t nq, const uint32_t* r_span, int64_t r_min,
+                     int64_t r_range, int r_len_bits, const int32_t* r_fwd_ptr, int64_t r_dom,
+                     const int32_t* r_fwd_idx, const uint32_t* s_span, int64_t s_min, int64_t s_range, int s_len_bits,
+                     const int32_t* s_fwd_ptr, int64_t s_dom, const int32_t* s_fwd_idx, int8_t* ans,
+                     cudaStream_t st) {
+  if (nq == 0) return MMJ_OK;
+  if (!r_span || !s_span || !r_fwd_ptr || !s_fwd_ptr || r_len_bits < 1 || r_len_bits > 16 || s_len_bits < 1 ||
+      s_len_bits > 16) {
+    set_error("bsi_answer_spans: both span tables (1..16 length bits) and forward CSRs are required");
+    return MMJ_ERR_ARG;
+  }
+  const ListSide a{IdMap{}, r_span, r_min, r_range, r_len_bits, r_fwd_ptr, r_dom, r_fwd_idx};
+  const ListSide b{IdMap{}, s_span, s_min, s_range, s_len_bits, s_fwd_ptr, s_dom, s_fwd_idx};
+  return launch_answer_lists(qa, qb, nq, a, b, ans, st);
 }
 
 int bsi_degree_histogram(const int32_t* rdeg, const int32_t* sdeg, int64_t dom_y, int64_t lo, int64_t hi, int nbins,

@@ -231,6 +231,43 @@ def test_bsi_direct_table_vs_search(oracle, spread, monkeypatch):
         assert np.array_equal(got2, exp)
 
 
+@pytest.mark.parametrize("max_bits", [16, 4])
+def test_bsi_span_tables_vs_id_walk(oracle, max_bits, monkeypatch):
+    """The lists form through the span tables (raw id -> list offset and
+    length in one 32-bit entry) and through the id table + fwd_ptr walk:
+    identical answers, equal to the oracle.  With 4 length bits the lists of
+    15 or more y saturate the length field and take the fwd_ptr search."""
+    from paper_2002_12459_b200 import bsi
+    from paper_2002_12459_b200.apps import bsi_answer_batch_arrays
+    from paper_2002_12459_b200.relation import Relation, build_indexed
+    monkeypatch.setattr(bsi, "SPAN_MAX_LEN_BITS", max_bits)
+    rng = np.random.default_rng(90 + max_bits)
+
+    def side(n_ids, seed):
+        g = np.random.default_rng(seed)
+        # short lists (mean ~3) plus a few ids with exactly 14, 15, 16 and 60 y; id 7 left out
+        lens = g.integers(1, 6, n_ids)
+        lens[[3, 11, 19, 40]] = [14, 15, 16, 60]
+        rows = np.repeat(np.arange(n_ids), lens)
+        ys = np.concatenate([g.choice(500, k, replace=False) for k in lens])
+        keep = rows != 7
+        p = np.stack([rows[keep] + 100, ys[keep]], axis=1)
+        return p[g.permutation(len(p))]
+    rp, sp = side(3000, 1), side(2500, 2)
+    q = rng.integers(95, 3200, (30000, 2))
+    q[:8] = [[103, 103], [111, 111], [119, 119], [140, 140], [111, 140], [107, 103], [103, 107], [3099, 2599]]
+    exp = oracle.bsi(oracle.encode(rp), oracle.encode(sp), q[:, 0], q[:, 1])
+    r = build_indexed(Relation.from_raw_pairs("R", rp))
+    s = build_indexed(Relation.from_raw_pairs("S", sp))
+    sides = bsi.prepare(r, s)
+    assert sides[0].span is not None and sides[1].span is not None and sides[0].span[3] == max_bits
+    for form in ("lists", "walk"):
+        got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], form=form)
+        assert np.array_equal(got, exp), form
+    assert (exp == -1).any() and (exp == 1).any() and (exp == 0).any()
+    assert exp[5] == -1 and exp[6] == -1
+
+
 def test_bsi_tables_abi_errors():
     from paper_2002_12459_b200 import _native as nat
     nat.require_cuda()
@@ -238,6 +275,10 @@ def test_bsi_tables_abi_errors():
     assert lib.mmj_bsi_direct_table(0, 0, 0, 0, 0, 0, 0) == nat.MMJ_ERR_ARG
     assert lib.mmj_bsi_answer(0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 0, 0, 6, 0, 0) == nat.MMJ_ERR_ARG
     assert lib.mmj_bsi_records(0, 0, 1, 0, 12, 0, 0, 0) == nat.MMJ_ERR_ARG
+    # 6 length bits leave 26 offset bits: 2^26 - 1 tuples do not fit
+    assert lib.mmj_bsi_span_table(0, 0, 0, 0, 8, 0, (1 << 26) - 1, 6, 0, 0) == nat.MMJ_ERR_ARG
+    assert lib.mmj_bsi_span_table(0, 0, 0, 0, 8, 0, 10, 0, 0, 0) == nat.MMJ_ERR_ARG
+    assert lib.mmj_bsi_answer_spans(0, 0, 1, 0, 0, 1, 6, 0, 1, 0, 0, 0, 1, 6, 0, 1, 0, 0, 0) == nat.MMJ_ERR_ARG
 
 
 def test_star_golden():

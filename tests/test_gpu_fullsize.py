@@ -211,7 +211,7 @@ def test_cfg5_bsi_full_scale_all_queries(oracle):
     extra[1::4, 1] = -7 - extra[1::4, 1]  # unknown z
     q = np.concatenate([wl.batch, extra])
     exp = oracle.bsi(oracle.encode(wl.relations[0]), oracle.encode(wl.relations[1]), q[:, 0], q[:, 1])
-    for form in ("auto", "records"):      # auto = the bench's "lists" form at cfg5
+    for form in ("auto", "walk", "records"):      # auto = the bench's "lists" form (span tables) at cfg5
         got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], form=form)
         assert np.array_equal(got, exp), form
     assert (exp[-4096:] == -1).sum() >= 2048 and 0.55 < (exp[:-4096] == 1).mean() < 0.7

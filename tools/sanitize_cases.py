@@ -89,12 +89,12 @@ def main():
     print(f"ssj c=3: {'ok' if ok else 'MISMATCH'}", flush=True)
     if not ok:
         bad.append("ssj")
-    # BSI both forms
+    # BSI: span tables, id-table walk, records
     q = rng.integers(-3, 620, (5000, 2))
     expb = o.bsi(o.encode(rp), o.encode(sp), q[:, 0], q[:, 1])
     r0 = build_indexed(Relation.from_raw_pairs("R", rp))
     s0 = build_indexed(Relation.from_raw_pairs("S", sp))
-    for form in ("lists", "records"):
+    for form in ("lists", "walk", "records"):
         got = bsi_answer_batch_arrays(r0, s0, q[:, 0], q[:, 1], form=form)
         ok = np.array_equal(got, expb)
         print(f"bsi {form}: {'ok' if ok else 'MISMATCH'}", flush=True)
