@@ -18,7 +18,6 @@
 //     with its nonzero test, restricted to queried cells; otherwise the two
 //     light lists (sectors prefetched to L1 first) are merge-intersected.
 #include "mmj_common.cuh"
-#include <cstdlib>
 
 namespace mmj {
 namespace {
@@ -199,10 +198,14 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer(const int64_t* __restrict__ 
 // queries, PIPE at a time: lane l loads element l of each list (one coalesced
 // request per list, every sector fetched once, straight into registers), and
 // the two 32-entry chunks are intersected by a shuffle binary search (5
-// steps) + ballot.  Lists longer than 32 take a chunked merge.  The
-// thread-per-query merge this replaces (r3b: 0.48 ms per 4M queries, 0.64 ms
-// before the span tables) ran 0.41 ms at PIPE = 2 (r3d/r3e; PIPE = 1 / 3 / 4 /
-// 8: 0.46 / 0.48 / 0.47 / 0.54 ms -- occupancy beats a deeper pipeline).
+// steps) + ballot.  Lists longer than 32 take a chunked merge.  cfg5, 4M
+// queries: 0.41 ms at PIPE = 2 (r3d/r3e; PIPE = 1 / 3 / 4 / 8: 0.46 / 0.48 /
+// 0.47 / 0.54 ms -- occupancy beats a deeper pipeline) against 0.48 ms for the
+// thread-per-query merge it replaces (r3b; 0.64 ms before the span tables).
+// It is issue-bound (r3f ncu: 76 warp instructions per query, issue slots 71%
+// busy, DRAM 40%); __match_any_sync over both lists in one register row
+// (na + nb <= 32) was slower (0.67 ms, r3h), as was staging 64-byte aligned
+// list copies in shared memory by cp.async and merging per lane (0.44, r3g).
 //
 // Raw id -> list, three ways per side (ListSide):
 //   * span table (mmj_bsi_span_table): table[raw - vmin] = (offset <<
@@ -301,7 +304,6 @@ __device__ __noinline__ bool long_intersect(const int32_t* __restrict__ la, int 
 
 constexpr int PIPE = 2;   // queries whose list loads are in flight together per warp
 
-template <bool MATCH>
 __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restrict__ qa,
                                                           const int64_t* __restrict__ qb, int64_t nq,
                                                           const ListSide sa, const ListSide sb,
@@ -333,25 +335,14 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restr
         na[p] = j[p] >= 0 ? __shfl_sync(FULL, ra.y, src) : 0;
         ob[p] = __shfl_sync(FULL, rb.x, src);
         nb[p] = j[p] >= 0 ? __shfl_sync(FULL, rb.y, src) : 0;
-        if (MATCH && na[p] + nb[p] <= 32) {
-          // both lists in one register row: lanes [0, na) hold A, [na, na + nb) hold B
-          const int32_t* src = lane < na[p] ? sa.lists + oa[p] + lane : sb.lists + ob[p] + (lane - na[p]);
-          a[p] = lane < na[p] + nb[p] ? ld_pol(src, stream) : -1 - lane;
-          b[p] = 0;
-        } else {
-          a[p] = lane < na[p] ? ld_pol(sa.lists + oa[p] + lane, stream) : PAD_Y;
-          b[p] = lane < nb[p] ? ld_pol(sb.lists + ob[p] + lane, stream) : PAD_Y;
-        }
+        a[p] = lane < na[p] ? ld_pol(sa.lists + oa[p] + lane, stream) : PAD_Y;
+        b[p] = lane < nb[p] ? ld_pol(sb.lists + ob[p] + lane, stream) : PAD_Y;
       }
 #pragma unroll
       for (int p = 0; p < PIPE; ++p) {
         if (j[p] < 0) continue;      // warp-uniform
         bool hit;
-        if (MATCH && na[p] + nb[p] <= 32) {
-          // a list holds no value twice, so two equal lanes are one y in both lists
-          const unsigned same = __match_any_sync(FULL, a[p]);
-          hit = __any_sync(FULL, (same & (same - 1)) != 0u);
-        } else if (na[p] <= 32 && nb[p] <= 32) hit = chunk_match(a[p], b[p], na[p], nb[p], lane);
+        if (na[p] <= 32 && nb[p] <= 32) hit = chunk_match(a[p], b[p], na[p], nb[p], lane);
         else hit = long_intersect(sa.lists + oa[p], na[p], sb.lists + ob[p], nb[p], lane);
         if (lane == j[p]) res = hit ? 1 : 0;
       }
@@ -453,9 +444,7 @@ int bsi_answer(const int64_t* qa, const int64_t* qb, int64_t nq, const int64_t* 
 static int launch_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const ListSide& a,
                                const ListSide& b, int8_t* ans, cudaStream_t st) {
   // a warp per 32 queries, 16 waves of resident CTAs at most
-  static const bool use_match = getenv("MMJ_BSI_MATCH") && atoi(getenv("MMJ_BSI_MATCH")) != 0;
-  if (use_match) k_bsi_answer_lists<true><<<grid_for(nq, TPB, 16), TPB, 0, st>>>(qa, qb, nq, a, b, ans);
-  else k_bsi_answer_lists<false><<<grid_for(nq, TPB, 16), TPB, 0, st>>>(qa, qb, nq, a, b, ans);
+  k_bsi_answer_lists<<<grid_for(nq, TPB, 16), TPB, 0, st>>>(qa, qb, nq, a, b, ans);
   MMJ_CHECK_LAUNCH("k_bsi_answer_lists");
   return MMJ_OK;
 }
