@@ -1123,7 +1123,7 @@ def run_reference(args):
     line = {
         "metric": METRIC, "impl": "reference", "value": v, "unit": wl.unit, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(args.steps, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": wl.ref_describe(size, kind) + f", {cores} in parallel per step",
                    "config_name": args.config, "package": "baseline/_ref (mmjoin 0.1.0, pip --target)" if ref
                    else "oracle/mmjoin_oracle.py (numpy port)"},
