@@ -84,6 +84,31 @@ def _device_pairs(eng):
 COMPACT_MAX_KEPT = 0.9
 
 
+def _compact_host_plan(idx, c: int):
+    """Host side of the compaction: (#kept sets, their CSR offsets, their
+    degrees), all read-only.  A function of the family's (frozen) degree
+    vector and c alone, so it is remembered on the index object: repeated
+    joins over one family (batches, shards, bench steps) skip ~0.6 ms of numpy
+    scans while the device compaction itself runs every time."""
+    ldeg = np.asarray(idx.left_deg)
+    memo = getattr(idx, "_mmj_compact_plan", None)
+    if memo is not None and memo[0] == c and memo[1] is idx.left_deg and not ldeg.flags.writeable:
+        return memo[2]
+    keep = ldeg >= c
+    nk = int(keep.sum())
+    hdeg = np.ascontiguousarray(ldeg[keep])
+    ptr = np.concatenate([[0], np.cumsum(hdeg, dtype=np.int64)])
+    for arr in (hdeg, ptr):
+        arr.flags.writeable = False      # engine._host_max memoises read-only degree vectors
+    plan = (nk, ptr, hdeg)
+    if not ldeg.flags.writeable:
+        try:
+            idx._mmj_compact_plan = (c, idx.left_deg, plan)
+        except AttributeError:
+            pass
+    return plan
+
+
 def _compact_family(idx, c: int, ws=None):
     """Sets with fewer than ``c`` elements reach no overlap >= c (the
     ``cnt >= c`` filter of apps.py:61-62), so their rows and columns of the
@@ -99,10 +124,8 @@ def _compact_family(idx, c: int, ws=None):
     from . import _native as nat
     from .device import DeviceRelation, device_relation
     from .ingest import IngestWorkspace
-    ldeg = np.asarray(idx.left_deg)
-    keep = ldeg >= c
-    nk = int(keep.sum())
-    if nk == 0 or nk > COMPACT_MAX_KEPT * len(ldeg):
+    nk, fwd_ptr_host, hdeg = _compact_host_plan(idx, c)
+    if nk == 0 or nk > COMPACT_MAX_KEPT * len(idx.left_deg):
         return None   # nothing to save (or nothing left: the plain engine handles empty outputs)
     dr = device_relation(idx)
     n, dom, dom_y = dr.n, dr.dom_left, dr.dom_right
@@ -130,12 +153,12 @@ def _compact_family(idx, c: int, ws=None):
     # the compacted offsets follow from the host degrees (kept sets keep their
     # order and their whole rows): no device -> host copy, no sync
     dom_c = nk
-    dc.fwd_ptr_host = np.concatenate([[0], np.cumsum(ldeg[keep], dtype=np.int64)])
+    dc.fwd_ptr_host = fwd_ptr_host
     n_c = int(dc.fwd_ptr_host[-1])
     dc.n, dc.dom_left, dc.dom_right, dc.device, dc.h2d_bytes = n_c, dom_c, dom_y, dr.device, 0
     dc.fwd_ptr, dc.left_deg = dc.fwd_ptr[:dom_c + 1], dc.left_deg[:dom_c]
     dc.fwd_idx, dc.fwd_row, dc.rev_idx = dc.fwd_idx[:n_c], dc.fwd_row[:n_c], dc.rev_idx[:n_c]
-    return dc, orig[:dom_c], np.diff(dc.fwd_ptr_host)
+    return dc, orig[:dom_c], hdeg
 
 
 def _decode_compact(codes, dom_c: int, orig, dom: int):

@@ -26,8 +26,8 @@ from .device import Workspace, device_relation
 from .errors import StarResourceError
 
 BK = 128
-LIGHT_RATE = 1.0e10          # light witnesses / s (global atomics)
-MMA_RATE = 2.0e15            # int8 ops / s
+LIGHT_RATE = float(os.environ.get("MMJ_STAR_LIGHT_RATE", 1.0e10))   # light witnesses / s (global atomics)
+MMA_RATE = float(os.environ.get("MMJ_STAR_MMA_RATE", 2.0e15))        # int8 ops / s
 CELL_RATE = 4.0e12           # epilogue floor, output cells / s
 DEFAULT_CHUNK_BYTES = 256 << 20
 
