@@ -26,9 +26,12 @@ from .device import Workspace, device_relation
 from .errors import StarResourceError
 
 BK = 128
-LIGHT_RATE = float(os.environ.get("MMJ_STAR_LIGHT_RATE", 1.0e10))   # light witnesses / s (global atomics)
-MMA_RATE = float(os.environ.get("MMJ_STAR_MMA_RATE", 2.0e15))        # int8 ops / s
-CELL_RATE = 4.0e12           # epilogue floor, output cells / s
+# B200 rates of the star cost model, fitted to cfg3 sweeps (profiles/r3_star_sweep.txt:
+# K = 128 / 256 / 384 / 512 heavy y -> product 16.1 / 21.5 / 25.1 / 31.6 ms, light
+# expansion 22.1 / 5.4 / 3.9 / 3.9 ms for 1.85e9 / 2.6e8 / 8.1e7 / 3.5e7 witnesses)
+LIGHT_RATE = 1.0e11          # light witnesses / s (bitmap atomics), marginal
+MMA_RATE = 7.0e15            # int8 ops / s, marginal per heavy y (z-pair operand: two cells per accumulator)
+CELL_RATE = 1.1e13           # output cells / s of the product's TMEM read-out + bitmap epilogue (K-independent part)
 DEFAULT_CHUNK_BYTES = 256 << 20
 
 
@@ -66,7 +69,7 @@ def choose_threshold(rels) -> float:
     best_t, best_thr = tail[0] / LIGHT_RATE, math.inf                 # no heavy y
     for kk in range(BK, min(len(order), 8192) + BK, BK):
         ke = min(kk, len(order))
-        t = tail[ke] / LIGHT_RATE + max(2.0 * cells * _rup(ke, BK) / MMA_RATE, cells / CELL_RATE)
+        t = tail[ke] / LIGHT_RATE + 2.0 * cells * _rup(ke, BK) / MMA_RATE + cells / CELL_RATE
         if t < best_t:
             best_t, best_thr = t, (float(order[ke]) if ke < len(order) else 0.0)
     return best_thr
@@ -111,6 +114,8 @@ class StarEngine:
         torch = self.torch
         st = nat.stream_handle()
         dom_y = self.dom_y
+        self.nnz.zero_()       # per-run statistics (an engine may run many times)
+        self.wit.zero_()
         rev_ptrs = _ptr_array([nat.ptr(d.rev_ptr) for d in self.dev])
         hflag = self.ws.get("s_hflag", dom_y, torch.uint8)
         lflag = self.ws.get("s_lflag", dom_y, torch.uint8)

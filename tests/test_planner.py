@@ -131,3 +131,53 @@ def test_gpu_plan_is_model_argmin(golden):
     best = min(model(d) for d in cand)
     assert pl.strategy == opt.PARTITIONED and pl.delta2 == 1
     assert math.isclose(pl.total_cost, best, rel_tol=1e-9)
+
+
+def test_star_threshold_is_model_argmin():
+    """star.choose_threshold returns the product-degree cut whose modelled
+    time (light witnesses + per-heavy-y product + K-independent read-out) is
+    smallest among the 128-aligned heavy-y counts; the heavy set it induces
+    has exactly that many y."""
+    import math
+
+    from paper_2002_12459_b200 import star
+    from paper_2002_12459_b200.relation import Relation, build_indexed, semi_join_reduce_many
+    rng = np.random.default_rng(12)
+    raws = []
+    for _ in range(3):
+        y = np.minimum(rng.zipf(1.3, 40000), 3000) - 1
+        raws.append(np.unique(np.stack([rng.integers(0, 400, 40000), y], axis=1), axis=0))
+    idxs = [build_indexed(r) for r in semi_join_reduce_many(
+        [Relation.from_raw_pairs(f"R{j}", p) for j, p in enumerate(raws)])]
+    thr = star.choose_threshold(idxs)
+    prod = np.stack([np.asarray(r.right_deg, dtype=np.float64) for r in idxs]).prod(axis=0)
+    order = np.sort(prod[prod > 0])[::-1]
+    cells = float(math.prod(r.rel.dom_left for r in idxs))
+
+    def model(k):
+        ke = min(k, len(order))
+        return (order[ke:].sum() / star.LIGHT_RATE + 2.0 * cells * (-(-ke // 128) * 128) / star.MMA_RATE
+                + cells / star.CELL_RATE)
+    cands = [order.sum() / star.LIGHT_RATE] + [model(k) for k in range(128, min(len(order), 8192) + 128, 128)]
+    k_chosen = int((prod > thr).sum()) if math.isfinite(thr) else 0
+    t_chosen = model(k_chosen) if k_chosen else order.sum() / star.LIGHT_RATE
+    # y tied with the cut value stay light, so the heavy count may fall a few short of the 128-aligned optimum
+    assert t_chosen <= min(cands) * 1.02
+
+
+def test_ssj_host_compaction_plan_is_remembered():
+    """apps._compact_host_plan: kept-set count, CSR offsets and degrees from
+    the family's frozen degree vector, remembered per (family, c)."""
+    from paper_2002_12459_b200.apps import SetFamily, _compact_host_plan
+    from paper_2002_12459_b200.relation import Relation
+    rng = np.random.default_rng(3)
+    pairs = np.unique(np.stack([np.minimum(rng.zipf(1.5, 5000), 300), rng.integers(0, 200, 5000)], axis=1), axis=0)
+    idx = SetFamily(Relation.from_raw_pairs("sets", pairs)).indexed
+    nk, ptr, hdeg = _compact_host_plan(idx, 3)
+    ldeg = np.asarray(idx.left_deg)
+    assert nk == int((ldeg >= 3).sum()) and np.array_equal(hdeg, ldeg[ldeg >= 3])
+    assert np.array_equal(ptr, np.concatenate([[0], np.cumsum(ldeg[ldeg >= 3])]))
+    assert not ptr.flags.writeable and not hdeg.flags.writeable
+    assert _compact_host_plan(idx, 3)[1] is ptr            # remembered
+    nk5, ptr5, _ = _compact_host_plan(idx, 5)              # another c replaces it
+    assert nk5 == int((ldeg >= 5).sum()) and ptr5 is not ptr
