@@ -677,7 +677,10 @@ class Star:
                 w_mma = 2.0 * rows * eng.kh * eng.dk
                 ops = w_mma / t
                 d.update(achieved=ops / 1e12, unit="TOPS(int8)", frac_datasheet=ops / INT8_DATASHEET_OPS,
-                         w_mma_unpadded=w_mma, note="composite rows (x1,x2) x x3 over heavy y")
+                         w_mma_unpadded=w_mma,
+                         note="composite rows (x1,x2) x x3 over heavy y; K = the heavy-y count that minimises the "
+                              "modelled step (star.choose_threshold; cfg3 sweep in profiles/r3_star_sweep.txt: "
+                              "K = 384 runs this kernel at 0.85 of the datasheet but a 2 ms slower step)")
                 if int8_peak:
                     d.update(frac_measured=ops / int8_peak)
             info[name] = d

@@ -268,6 +268,37 @@ def test_bsi_span_tables_vs_id_walk(oracle, max_bits, monkeypatch):
     assert exp[5] == -1 and exp[6] == -1
 
 
+@pytest.mark.parametrize("form", ["lists", "walk", "records"])
+def test_bsi_long_lists_chunked_merge(oracle, form):
+    """Lists around and beyond the 32-entry chunk of the warp-cooperative
+    intersection (1 .. 257 y per id): disjoint interleaved lists, a single
+    common y at the very end / start / a chunk boundary, and equal lists --
+    every (a, b) combination against the oracle."""
+    from paper_2002_12459_b200.apps import bsi_answer_batch_arrays
+    from paper_2002_12459_b200.relation import Relation, build_indexed
+    lens = [1, 2, 31, 32, 33, 63, 64, 65, 100, 257]
+    rp, sp = [], []
+    for i, n in enumerate(lens):
+        rp += [(i, 2 * k) for k in range(n)]                          # even y: 0, 2, ...
+        sp += [(i, 2 * k + 1) for k in range(n)]                      # odd y: disjoint from every R list
+        sp += [(100 + i, 2 * (n - 1))]                                # + R_i's last y only ...
+        sp += [(100 + i, 2 * k + 1) for k in range(n)]                # ... after n odd ones
+        sp += [(200 + i, 0)] + [(200 + i, 2 * k + 1) for k in range(n)]   # R's first y, then odd ones
+        sp += [(300 + i, 2 * k) for k in range(n)]                    # equal to R_i
+        sp += [(400 + i, 62)] + [(400 + i, 2 * k + 1) for k in range(max(n, 40))]   # y = 62: entry 31 of an R list
+    rp, sp = np.array(rp), np.array(sp)
+    ra = np.arange(len(lens))
+    sb = np.concatenate([base + ra for base in (0, 100, 200, 300, 400)])
+    q = np.array([(a, b) for a in ra for b in sb] + [(99, 0), (0, 99)])
+    exp = oracle.bsi(oracle.encode(rp), oracle.encode(sp), q[:, 0], q[:, 1])
+    r = build_indexed(Relation.from_raw_pairs("R", rp))
+    s = build_indexed(Relation.from_raw_pairs("S", sp))
+    got = bsi_answer_batch_arrays(r, s, q[:, 0], q[:, 1], form=form)
+    assert np.array_equal(got, exp)
+    by_block = exp[:-2].reshape(len(lens), 5, len(lens))      # [a, S block, b]
+    assert (by_block[:, 0, :] == 0).all() and (exp == 1).sum() > 100 and (exp[-2:] == -1).all()
+
+
 def test_bsi_tables_abi_errors():
     from paper_2002_12459_b200 import _native as nat
     nat.require_cuda()
