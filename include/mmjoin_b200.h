@@ -280,18 +280,24 @@ int mmj_bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const
  * binary search; range = max - min + 1 < 2^31) */
 int mmj_bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
                          int32_t* table, void* stream);
-/* span table for dense raw id ranges: table[range] uint32 = (forward-list
- * offset << len_bits) | min(list length, 2^len_bits - 1) of raw value
- * vmin + i, 0xFFFFFFFF where absent; needs n_tuples < 2^(32 - len_bits) - 1.
- * mmj_bsi_answer_spans resolves each query id with that one load (a
- * saturated length falls back to a binary search of the offset in fwd_ptr)
- * and intersects the two forward lists: the left_ids.get() probes and set
+/* span table for dense raw id ranges: table[range] of 8-byte entries, low
+ * word = (forward-list offset << len_bits) | min(list length, 2^len_bits - 1)
+ * of raw value vmin + i (0xFFFFFFFF where absent; needs n_tuples <
+ * 2^(32 - len_bits) - 1), high word = the id's heavy-y signature: bit hpos[y]
+ * for each of its y with 0 <= hpos[y] < 32 (hpos over the shared y space, -1 =
+ * not heavy; hpos NULL = no signatures).  mmj_bsi_answer_spans resolves each
+ * query id with that one load; two ids with a common signature bit share a
+ * heavy y and are answered at once (the heavy part of the reference's
+ * product, joinproject.py:208-216, on the queried cells only), the others
+ * intersect their forward lists (a saturated length falls back to a binary
+ * search of the offset in fwd_ptr): the left_ids.get() probes and set
  * intersection of apps.py:321-350, same answers as mmj_bsi_answer_lists */
 int mmj_bsi_span_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
-                       const int32_t* fwd_ptr, int64_t n_tuples, int len_bits, uint32_t* table, void* stream);
-int mmj_bsi_answer_spans(const int64_t* qa, const int64_t* qb, int64_t nq, const uint32_t* r_span, int64_t r_min,
+                       const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* hpos, int64_t n_tuples,
+                       int len_bits, uint64_t* table, void* stream);
+int mmj_bsi_answer_spans(const int64_t* qa, const int64_t* qb, int64_t nq, const uint64_t* r_span, int64_t r_min,
                          int64_t r_range, int r_len_bits, const int32_t* r_fwd_ptr, int64_t r_dom,
-                         const int32_t* r_fwd_idx, const uint32_t* s_span, int64_t s_min, int64_t s_range,
+                         const int32_t* r_fwd_idx, const uint64_t* s_span, int64_t s_min, int64_t s_range,
                          int s_len_bits, const int32_t* s_fwd_ptr, int64_t s_dom, const int32_t* s_fwd_idx,
                          int8_t* ans, void* stream);
 

@@ -86,7 +86,7 @@ _SIGS = {
     "mmj_bsi_records": (INT, [P, P, I64, P, INT, P, P, P]),
     "mmj_bsi_answer": (INT, [P, P, I64, P, P, I64, P, I64, I64, P, P, I64, P, I64, I64, P, P, P, P, INT, P, P]),
     "mmj_bsi_direct_table": (INT, [P, P, I64, I64, I64, P, P]),
-    "mmj_bsi_span_table": (INT, [P, P, I64, I64, I64, P, I64, INT, P, P]),
+    "mmj_bsi_span_table": (INT, [P, P, I64, I64, I64, P, P, P, I64, INT, P, P]),
     "mmj_bsi_answer_spans": (INT, [P, P, I64, P, I64, I64, INT, P, I64, P, P, I64, I64, INT, P, I64, P, P, P]),
     "mmj_format_keys": (INT, [P, P, I64, INT, P, P, P, P, P, P]),
     "mmj_format_lengths": (INT, [P, P, P, I64, INT, P, P, P, P]),

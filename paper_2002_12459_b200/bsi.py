@@ -28,6 +28,7 @@ from .device import Workspace
 BITS_BLOCK = 128     # bitset width granularity (4 words)
 LIST_MAX_MEAN = 64   # "lists" form when both sides' mean list length is at most this
 DIRECT_SPREAD = 4    # direct id table when max - min + 1 <= 4 x the number of ids
+SIG_BITS = 32          # heavy y per span-table signature (0: no signatures)
 SPAN_MAX_LEN_BITS = 16
 SPAN_MIN_LEN_BITS = 4  # span table only when a 32-bit entry leaves >= 4 length bits ...
 SPAN_MEAN_FRAC = 2     # ... and the mean list is at most half the largest length they hold
@@ -54,7 +55,7 @@ class BsiSide:
     span: object = None       # (span table, vmin, range, len_bits) or None
 
 
-def _attach_table(sd: BsiSide, ends) -> None:
+def _attach_table(sd: BsiSide, ends, hpos=None) -> None:
     """Direct-address raw id -> dense id table when the side's raw ids fill
     at most DIRECT_SPREAD x their count of a value range: each query id then
     resolves with one load instead of a binary search (cfg5: 4M ids in
@@ -76,9 +77,12 @@ def _attach_table(sd: BsiSide, ends) -> None:
     # saturated length costs the query a binary search over fwd_ptr)
     len_bits = min(SPAN_MAX_LEN_BITS, 32 - (sd.n + 1).bit_length())
     if len_bits >= SPAN_MIN_LEN_BITS and sd.n * SPAN_MEAN_FRAC <= ((1 << len_bits) - 1) * sd.dom_left:
-        span = torch.empty(rng, dtype=torch.int32, device="cuda")
+        # 8-byte entries: the span and the id's signature over the SIG_BITS
+        # heaviest y (hpos), which answers most intersecting pairs by itself
+        span = torch.empty(rng, dtype=torch.int64, device="cuda")
         nat.call("mmj_bsi_span_table", nat.ptr(sd.sorted_vals), nat.ptr(sd.order), sd.dom_left, vmin, rng,
-                 nat.ptr(sd.fwd_ptr), sd.n, len_bits, nat.ptr(span), nat.stream_handle())
+                 nat.ptr(sd.fwd_ptr), nat.ptr(sd.fwd_idx), nat.ptr(hpos) if hpos is not None else 0, sd.n, len_bits,
+                 nat.ptr(span), nat.stream_handle())
         sd.span = (span, vmin, rng, len_bits)
 
 
@@ -86,12 +90,29 @@ def _with_tables(sides):
     """Attach the direct id tables of both sides (one device -> host copy of
     their smallest / largest raw ids)."""
     torch = _torch()
-    sR, sS, _ = sides
+    sR, sS, dom_y = sides
     have = [sd for sd in (sR, sS) if sd.sorted_vals is not None and sd.dom_left > 0]
     ends = iter(torch.cat([sd.sorted_vals[[0, sd.dom_left - 1]] for sd in have]).cpu().tolist()) if have else iter(())
+    hpos = _signature_positions(sR, sS, dom_y) if len(have) == 2 else None
     for sd in have:
-        _attach_table(sd, ends)
+        _attach_table(sd, ends, hpos)
     return sides
+
+
+def _signature_positions(sR: BsiSide, sS: BsiSide, dom_y: int):
+    """hpos[y] = rank of y among the SIG_BITS join values shared by the most
+    (a, b) pairs (largest degR(y) * degS(y) > 0), -1 for every other y: the
+    heavy y of the span tables' signatures.  Which y are chosen never changes
+    an answer (a signature bit is exact membership of one y)."""
+    torch = _torch()
+    if dom_y == 0 or SIG_BITS <= 0:
+        return None
+    w = sR.ydeg.to(torch.float64) * sS.ydeg.to(torch.float64)
+    vals, idx = torch.topk(w, min(SIG_BITS, dom_y))
+    idx = idx[vals > 0]
+    hpos = torch.full((dom_y,), -1, dtype=torch.int32, device="cuda")
+    hpos[idx] = torch.arange(idx.numel(), dtype=torch.int32, device="cuda")
+    return hpos
 
 
 def _int_values(vals):

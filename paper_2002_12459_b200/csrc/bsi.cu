@@ -208,17 +208,21 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer(const int64_t* __restrict__ 
 // list copies in shared memory by cp.async and merging per lane (0.44, r3g).
 //
 // Raw id -> list, three ways per side (ListSide):
-//   * span table (mmj_bsi_span_table): table[raw - vmin] = (offset <<
-//     len_bits) | min(length, 2^len_bits - 1), 0xFFFFFFFF for an id the
-//     relation does not hold -- one 4-byte load instead of the id table ->
-//     fwd_ptr[id], fwd_ptr[id + 1] chain (two more DRAM granules per side);
-//     a saturated length field sends the query to a binary search of its
-//     offset in fwd_ptr;
+//   * span table (mmj_bsi_span_table): table[raw - vmin] = {(offset <<
+//     len_bits) | min(length, 2^len_bits - 1), signature}, the first word
+//     0xFFFFFFFF for an id the relation does not hold -- one 8-byte load
+//     instead of the id table -> fwd_ptr[id], fwd_ptr[id + 1] chain (two more
+//     DRAM granules per side); a saturated length field sends the query to a
+//     binary search of its offset in fwd_ptr.  The signature holds one bit
+//     per heaviest join value (up to 32, chosen by the caller): two ids with
+//     a common bit intersect, so that query never touches the lists -- the
+//     heavy part of the reference's product with its nonzero test
+//     (joinproject.py:208-216), restricted to the queried cells;
 //   * direct id table or binary search over the sorted raw ids, then fwd_ptr;
 //   * dense ids already (map all null).
 struct ListSide {
   IdMap map;                // raw id -> dense id (when span == nullptr)
-  const uint32_t* span;     // raw id -> packed (offset, length), or nullptr
+  const uint2* span;        // raw id -> {packed (offset, length), heavy-y signature}, or nullptr
   int64_t vmin, range;      // span table window
   int len_bits;             // length bits of a span entry
   const int32_t* fwd_ptr;   // dom + 1 CSR offsets (searched when a span's length saturates)
@@ -226,19 +230,23 @@ struct ListSide {
   const int32_t* lists;     // fwd_idx
 };
 
-__device__ __forceinline__ uint32_t ld_pol_u32(const uint32_t* p, uint64_t pol) {
-  uint32_t v;
-  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+__device__ __forceinline__ uint2 ld_pol_u32x2(const uint2* p, uint64_t pol) {
+  uint2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.b32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
   return v;
 }
 
-// (first entry index in s.lists, length) of raw id v's list; length -1 for an unknown id
-__device__ __forceinline__ int2 resolve_list(const ListSide& s, int64_t v, uint64_t keep) {
+// (first entry index in s.lists, length) of raw id v's list; length -1 for an
+// unknown id; sig = the id's heavy-y signature (0 without a span table)
+__device__ __forceinline__ int2 resolve_list(const ListSide& s, int64_t v, uint64_t keep, uint32_t& sig) {
+  sig = 0u;
   if (s.span) {
     const int64_t o = v - s.vmin;
     if (o < 0 || o >= s.range) return make_int2(0, -1);
-    const uint32_t e = ld_pol_u32(s.span + o, keep);
+    const uint2 es = ld_pol_u32x2(s.span + o, keep);
+    const uint32_t e = es.x;
     if (e == 0xFFFFFFFFu) return make_int2(0, -1);
+    sig = es.y;
     const uint32_t cap = (1u << s.len_bits) - 1u;
     const int32_t off = (int32_t)(e >> s.len_bits);
     int32_t len = (int32_t)(e & cap);
@@ -317,12 +325,15 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restr
   for (int64_t base = warp * 32; base < nq; base += nwarps * 32) {
     const int64_t q = base + lane;
     int2 ra = make_int2(0, -1), rb = make_int2(0, -1);
+    uint32_t ga = 0u, gb = 0u;
     if (q < nq) {
-      ra = resolve_list(sa, __ldcs(qa + q), keep);
-      rb = resolve_list(sb, __ldcs(qb + q), keep);
+      ra = resolve_list(sa, __ldcs(qa + q), keep, ga);
+      rb = resolve_list(sb, __ldcs(qb + q), keep, gb);
     }
-    int res = (ra.y < 0 || rb.y < 0) ? -1 : 0;
-    unsigned todo = __ballot_sync(FULL, ra.y > 0 && rb.y > 0);
+    // a shared signature bit is a shared heavy y: answered without the lists
+    const bool heavy_hit = (ga & gb) != 0u;
+    int res = (ra.y < 0 || rb.y < 0) ? -1 : (heavy_hit ? 1 : 0);
+    unsigned todo = __ballot_sync(FULL, ra.y > 0 && rb.y > 0 && !heavy_hit);
     while (todo) {
       int j[PIPE], na[PIPE], nb[PIPE], oa[PIPE], ob[PIPE];
       int32_t a[PIPE], b[PIPE];
@@ -351,18 +362,29 @@ __global__ void __launch_bounds__(TPB) k_bsi_answer_lists(const int64_t* __restr
   }
 }
 
-// span entry of every held raw id: (fwd_ptr[dense] << len_bits) | min(length, cap)
+// span entry of every held raw id: {(fwd_ptr[dense] << len_bits) | min(length,
+// cap), signature}: signature bit hpos[y] for each of the id's y with 0 <=
+// hpos[y] < 32 (the heaviest join values: at cfg5's Zipf(1.0) the top 32 y
+// decide ~60% of the queries -- nearly every intersecting pair -- from the
+// two table entries alone)
 __global__ void k_span_table(const int64_t* __restrict__ sorted, const int32_t* __restrict__ order, int64_t n,
-                             int64_t vmin, int64_t range, const int32_t* __restrict__ fwd_ptr, int len_bits,
-                             uint32_t* __restrict__ table) {
+                             int64_t vmin, int64_t range, const int32_t* __restrict__ fwd_ptr,
+                             const int32_t* __restrict__ fwd_idx, const int32_t* __restrict__ hpos, int len_bits,
+                             uint2* __restrict__ table) {
   const uint32_t cap = (1u << len_bits) - 1u;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = sorted[i] - vmin;
     if (o < 0 || o >= range) continue;
     const int32_t d = order[i];
-    const uint32_t off = (uint32_t)fwd_ptr[d];
-    const uint32_t len = (uint32_t)fwd_ptr[d + 1] - off;
-    table[o] = (off << len_bits) | (len < cap ? len : cap);
+    const int32_t p0 = fwd_ptr[d], p1 = fwd_ptr[d + 1];
+    const uint32_t off = (uint32_t)p0, len = (uint32_t)(p1 - p0);
+    uint32_t sig = 0u;
+    if (hpos != nullptr)
+      for (int32_t p = p0; p < p1; ++p) {
+        const int32_t h = __ldg(hpos + __ldg(fwd_idx + p));
+        if (h >= 0 && h < 32) sig |= 1u << h;
+      }
+    table[o] = make_uint2((off << len_bits) | (len < cap ? len : cap), sig);
   }
 }
 
@@ -478,7 +500,8 @@ int bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int
 }
 
 int bsi_span_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
-                   const int32_t* fwd_ptr, int64_t n_tuples, int len_bits, uint32_t* table, cudaStream_t st) {
+                   const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* hpos, int64_t n_tuples,
+                   int len_bits, uint2* table, cudaStream_t st) {
   if (range <= 0 || range >= (1ll << 31)) {
     set_error("bsi_span_table: range %lld out of (0, 2^31)", (long long)range);
     return MMJ_ERR_ARG;
@@ -488,16 +511,16 @@ int bsi_span_table(const int64_t* sorted, const int32_t* order, int64_t n, int64
               len_bits);
     return MMJ_ERR_ARG;
   }
-  MMJ_TRY(cuda_status(cudaMemsetAsync(table, 0xFF, (size_t)range * 4, st), "memset span table"));
+  MMJ_TRY(cuda_status(cudaMemsetAsync(table, 0xFF, (size_t)range * 8, st), "memset span table"));
   if (n == 0) return MMJ_OK;
-  k_span_table<<<grid_for(n), TPB, 0, st>>>(sorted, order, n, vmin, range, fwd_ptr, len_bits, table);
+  k_span_table<<<grid_for(n), TPB, 0, st>>>(sorted, order, n, vmin, range, fwd_ptr, fwd_idx, hpos, len_bits, table);
   MMJ_CHECK_LAUNCH("k_span_table");
   return MMJ_OK;
 }
 
-int bsi_answer_spans(const int64_t* qa, const int64_t* qb, int64_t nq, const uint32_t* r_span, int64_t r_min,
+int bsi_answer_spans(const int64_t* qa, const int64_t* qb, int64_t nq, const uint2* r_span, int64_t r_min,
                      int64_t r_range, int r_len_bits, const int32_t* r_fwd_ptr, int64_t r_dom,
-                     const int32_t* r_fwd_idx, const uint32_t* s_span, int64_t s_min, int64_t s_range, int s_len_bits,
+                     const int32_t* r_fwd_idx, const uint2* s_span, int64_t s_min, int64_t s_range, int s_len_bits,
                      const int32_t* s_fwd_ptr, int64_t s_dom, const int32_t* s_fwd_idx, int8_t* ans,
                      cudaStream_t st) {
   if (nq == 0) return MMJ_OK;

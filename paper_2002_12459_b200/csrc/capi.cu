@@ -54,10 +54,10 @@ int bsi_answer(const int64_t*, const int64_t*, int64_t, const int64_t*, const in
                int64_t, const int64_t*, const int32_t*, int64_t, const int32_t*, int64_t, int64_t, const uint32_t*,
                const int32_t*, const uint32_t*, const int32_t*, int, int8_t*, cudaStream_t);
 int bsi_direct_table(const int64_t*, const int32_t*, int64_t, int64_t, int64_t, int32_t*, cudaStream_t);
-int bsi_span_table(const int64_t*, const int32_t*, int64_t, int64_t, int64_t, const int32_t*, int64_t, int, uint32_t*,
-                   cudaStream_t);
-int bsi_answer_spans(const int64_t*, const int64_t*, int64_t, const uint32_t*, int64_t, int64_t, int, const int32_t*,
-                     int64_t, const int32_t*, const uint32_t*, int64_t, int64_t, int, const int32_t*, int64_t,
+int bsi_span_table(const int64_t*, const int32_t*, int64_t, int64_t, int64_t, const int32_t*, const int32_t*,
+                   const int32_t*, int64_t, int, uint2*, cudaStream_t);
+int bsi_answer_spans(const int64_t*, const int64_t*, int64_t, const uint2*, int64_t, int64_t, int, const int32_t*,
+                     int64_t, const int32_t*, const uint2*, int64_t, int64_t, int, const int32_t*, int64_t,
                      const int32_t*, int8_t*, cudaStream_t);
 int bsi_answer_lists(const int64_t*, const int64_t*, int64_t, const int64_t*, const int32_t*, int64_t, const int32_t*,
                      int64_t, int64_t, const int64_t*, const int32_t*, int64_t, const int32_t*, int64_t, int64_t,
@@ -274,17 +274,20 @@ int mmj_bsi_answer_lists(const int64_t* qa, const int64_t* qb, int64_t nq, const
 }
 
 int mmj_bsi_span_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,
-                       const int32_t* fwd_ptr, int64_t n_tuples, int len_bits, uint32_t* table, void* stream) {
-  return mmj::bsi_span_table(sorted, order, n, vmin, range, fwd_ptr, n_tuples, len_bits, table, ST(stream));
+                       const int32_t* fwd_ptr, const int32_t* fwd_idx, const int32_t* hpos, int64_t n_tuples,
+                       int len_bits, uint64_t* table, void* stream) {
+  return mmj::bsi_span_table(sorted, order, n, vmin, range, fwd_ptr, fwd_idx, hpos, n_tuples, len_bits,
+                             reinterpret_cast<uint2*>(table), ST(stream));
 }
 
-int mmj_bsi_answer_spans(const int64_t* qa, const int64_t* qb, int64_t nq, const uint32_t* r_span, int64_t r_min,
+int mmj_bsi_answer_spans(const int64_t* qa, const int64_t* qb, int64_t nq, const uint64_t* r_span, int64_t r_min,
                          int64_t r_range, int r_len_bits, const int32_t* r_fwd_ptr, int64_t r_dom,
-                         const int32_t* r_fwd_idx, const uint32_t* s_span, int64_t s_min, int64_t s_range,
+                         const int32_t* r_fwd_idx, const uint64_t* s_span, int64_t s_min, int64_t s_range,
                          int s_len_bits, const int32_t* s_fwd_ptr, int64_t s_dom, const int32_t* s_fwd_idx,
                          int8_t* ans, void* stream) {
-  return mmj::bsi_answer_spans(qa, qb, nq, r_span, r_min, r_range, r_len_bits, r_fwd_ptr, r_dom, r_fwd_idx, s_span,
-                               s_min, s_range, s_len_bits, s_fwd_ptr, s_dom, s_fwd_idx, ans, ST(stream));
+  return mmj::bsi_answer_spans(qa, qb, nq, reinterpret_cast<const uint2*>(r_span), r_min, r_range, r_len_bits,
+                               r_fwd_ptr, r_dom, r_fwd_idx, reinterpret_cast<const uint2*>(s_span), s_min, s_range,
+                               s_len_bits, s_fwd_ptr, s_dom, s_fwd_idx, ans, ST(stream));
 }
 
 int mmj_bsi_direct_table(const int64_t* sorted, const int32_t* order, int64_t n, int64_t vmin, int64_t range,

@@ -231,8 +231,8 @@ def test_bsi_direct_table_vs_search(oracle, spread, monkeypatch):
         assert np.array_equal(got2, exp)
 
 
-@pytest.mark.parametrize("max_bits", [16, 4])
-def test_bsi_span_tables_vs_id_walk(oracle, max_bits, monkeypatch):
+@pytest.mark.parametrize("max_bits,sig_bits", [(16, 32), (4, 32), (16, 0), (4, 5)])
+def test_bsi_span_tables_vs_id_walk(oracle, max_bits, sig_bits, monkeypatch):
     """The lists form through the span tables (raw id -> list offset and
     length in one 32-bit entry) and through the id table + fwd_ptr walk:
     identical answers, equal to the oracle.  With 4 length bits the lists of
@@ -241,6 +241,7 @@ def test_bsi_span_tables_vs_id_walk(oracle, max_bits, monkeypatch):
     from paper_2002_12459_b200.apps import bsi_answer_batch_arrays
     from paper_2002_12459_b200.relation import Relation, build_indexed
     monkeypatch.setattr(bsi, "SPAN_MAX_LEN_BITS", max_bits)
+    monkeypatch.setattr(bsi, "SIG_BITS", sig_bits)     # heavy-y signature width (0: lists only)
     rng = np.random.default_rng(90 + max_bits)
 
     def side(n_ids, seed):
@@ -307,8 +308,8 @@ def test_bsi_tables_abi_errors():
     assert lib.mmj_bsi_answer(0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 1, 0, 0, 0, 0, 6, 0, 0) == nat.MMJ_ERR_ARG
     assert lib.mmj_bsi_records(0, 0, 1, 0, 12, 0, 0, 0) == nat.MMJ_ERR_ARG
     # 6 length bits leave 26 offset bits: 2^26 - 1 tuples do not fit
-    assert lib.mmj_bsi_span_table(0, 0, 0, 0, 8, 0, (1 << 26) - 1, 6, 0, 0) == nat.MMJ_ERR_ARG
-    assert lib.mmj_bsi_span_table(0, 0, 0, 0, 8, 0, 10, 0, 0, 0) == nat.MMJ_ERR_ARG
+    assert lib.mmj_bsi_span_table(0, 0, 0, 0, 8, 0, 0, 0, (1 << 26) - 1, 6, 0, 0) == nat.MMJ_ERR_ARG
+    assert lib.mmj_bsi_span_table(0, 0, 0, 0, 8, 0, 0, 0, 10, 0, 0, 0) == nat.MMJ_ERR_ARG
     assert lib.mmj_bsi_answer_spans(0, 0, 1, 0, 0, 1, 6, 0, 1, 0, 0, 0, 1, 6, 0, 1, 0, 0, 0) == nat.MMJ_ERR_ARG
 
 

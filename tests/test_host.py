@@ -212,7 +212,7 @@ def test_capi_new_entry_points_argument_errors_without_gpu():
                               None, 6, None, None) == 1
     assert b"words" in lib.mmj_last_error()
     assert lib.mmj_bsi_record_words(8) == 16 and lib.mmj_bsi_record_words(32) == 48
-    assert lib.mmj_bsi_span_table(None, None, 0, 0, 8, None, (1 << 26) - 1, 6, None, None) == 1
+    assert lib.mmj_bsi_span_table(None, None, 0, 0, 8, None, None, None, (1 << 26) - 1, 6, None, None) == 1
     assert b"length bits" in lib.mmj_last_error()
     assert lib.mmj_bsi_answer_spans(None, None, 1, None, 0, 1, 6, None, 1, None, None, 0, 1, 6, None, 1, None, None,
                                     None) == 1
