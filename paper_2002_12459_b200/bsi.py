@@ -8,8 +8,12 @@ Steps (all kernels of libmmjoin_b200.so), "records" form:
      light lists compacted in place (mmj_bsi_records);
   3. per query: raw id -> dense id through each relation's own (unreduced)
      dictionary, bitset test, light merge intersection (mmj_bsi_answer).
-"lists" form (short lists, BsiEngine): step 3 alone, merging the two ids'
-full forward lists (mmj_bsi_answer_lists).
+"lists" form (short lists, BsiEngine): no per-batch build.  Raw ids resolve
+through span tables (one 8-byte entry per raw id: list offset / length and a
+32-bit signature of the id's heaviest y, built once per relation pair); a
+shared signature bit answers the query, the others intersect the two ids'
+full forward lists (mmj_bsi_answer_spans; mmj_bsi_answer_lists without span
+tables).
 If R and S do not share a right dictionary, their y ids are first mapped to
 a common raw-value space on the host (input preparation, as the reference's
 semi_join_reduce does) -- left ids, hence "known" ids, stay those of the
@@ -257,8 +261,9 @@ class BsiEngine:
                  query with a heavy witness, the light lists the rest -- the
                  heavy part of the reference's product restricted to the
                  queried cells (apps.py:332-350 -> joinproject.py:208-216);
-      "lists"    no index build: the queried ids' forward lists are
-                 merge-intersected (mmj_bsi_answer_lists).
+      "lists"    no per-batch build: span-table signatures of the heaviest y
+                 decide most intersecting pairs, the queried ids' forward
+                 lists the rest (mmj_bsi_answer_spans / mmj_bsi_answer_lists).
     "auto" takes "lists" when both sides' mean list length is at most
     LIST_MAX_MEAN: a record is 64 B, as many DRAM sectors as a 16-entry list,
     so for short lists the records only add their build pass (cfg5: 16 y per
