@@ -972,11 +972,17 @@ class Bsi:
         # once per relation pair, outside the timed steps (like the CSR build
         # of the IndexedRelation inputs): shared y space, direct id tables and
         # span tables with heavy-y signatures; timed here and reported
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        self.sides = prepare(self.r, self.s)
-        torch.cuda.synchronize()
-        self.prepare_ms = 1e3 * (time.perf_counter() - t0)
+        # (the first call also loads torch's topk / sort kernels: timed twice)
+        self.prepare_first_ms = self.prepare_ms = 0.0
+        for k in range(2):
+            self.r._mmj_bsi_cache = None
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            self.sides = prepare(self.r, self.s)
+            torch.cuda.synchronize()
+            self.prepare_ms = 1e3 * (time.perf_counter() - t0)
+            if k == 0:
+                self.prepare_first_ms = self.prepare_ms
         nq = len(wl.batch)
         self.qlo, self.qhi = batch_slice(nq, self.rank, self.world)
         q = wl.batch[self.qlo:self.qhi]
@@ -1039,6 +1045,7 @@ class Bsi:
                         "heavy-y signatures; per batch and inside the step: nothing to build in the lists form "
                         "(records form: heavy-y split + records)",
                "prepare_ms_once_per_relation_pair": round(self.prepare_ms, 3),
+               "prepare_ms_first_call_in_process": round(self.prepare_first_ms, 3),
                "answers_per_s_one_batch_with_prepare": self.nq / (t_step + 1e-3 * self.prepare_ms),
                "span_tables": bool(self.sides[0].span and self.sides[1].span),
                "l2": "256 MiB L2 flush before every timed step"}
